@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 GPU replica step (Hogbatch / Adaptive Hogbatch MLP worker).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config w8a] [--impl ours|reference]
+
+One "step" = one replica SGD step (forward, fused softmax-CE, backward, fused
+SGD update) over one batch of the named BASELINE.json configuration.  The
+default workload is configs[1], the w8a-shaped sparse MLP 300-512-512-512-2
+at GPU batch 8192 (BASELINE.json).  N>1 (torchrun) runs one GPU worker per
+rank on its own batch stream (weak scaling) and averages the replicas with
+NCCL allreduce every step (the GPU-replica merge).
+
+Prints ONE JSON line (rank 0).  `value` is device-timed throughput with the
+epoch resident in HBM; `e2e` is the same metric through the drop-in replica
+call (host float64 model snapshot H2D, CSR batch H2D from host memory, the
+gradient D2H and float64 stale merge on the host, loss D2H) -- the exact
+semantics of the reference's execute_batch_replica.  `--impl reference` times
+the reference algorithm's CPU implementation (the float64 NumPy port in
+oracle/, OpenBLAS on all host cores) on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MLP train samples/sec"
+UNIT = "samples/s"
+
+# BASELINE.json configs
+CONFIGS = {
+    "covtype": dict(sizes=(54, 512, 512, 512, 2), n=581012, kind="dense", classes=2, batch=512, eta=0.5,
+                    desc="covtype-shaped synthetic dense 581012x54, MLP 54-512-512-512-2, b=512"),
+    "w8a": dict(sizes=(300, 512, 512, 512, 2), n=64700, kind="csr", nnz=12, binary=True, normalize=False,
+                classes=2, batch=8192, eta=0.5,
+                desc="w8a-shaped synthetic sparse 64700x300 (12 nnz/row, ~4%), MLP 300-512-512-512-2, GPU batch 8192"),
+    "delicious": dict(sizes=(500, 1024, 1024, 983), n=16105, kind="dense", classes=983, batch=8192, eta=0.5,
+                      desc="delicious-shaped synthetic dense 16105x500, 983 labels, MLP 500-1024-1024-983, GPU batch 8192"),
+    "realsim": dict(sizes=(20958, 1024, 1024, 2), n=72309, kind="csr", nnz=52, binary=False, normalize=True,
+                    classes=2, batch=8192, eta=0.5,
+                    desc="real-sim-shaped synthetic sparse 72309x20958 (52 nnz/row), MLP 20958-1024-1024-2, GPU batch 8192"),
+    "scaled": dict(sizes=(1024, 4096, 4096, 4096, 1000), n=131072, kind="dense", classes=1000, batch=8192, eta=0.1,
+                   desc="scaled synthetic dense 1024-d (131072 staged rows of the 10M-row set), "
+                        "MLP 1024-4096-4096-4096-1000, GPU batch 8192"),
+}
+
+
+def dense_flops_per_sample(sizes, sparse_first):
+    """6*sum(d_l d_{l+1}) - 2 d_0 d_1 (no dX for layer 0); the sparse first layer
+    is counted as bytes instead."""
+    pairs = list(zip(sizes[:-1], sizes[1:]))
+    tot = sum(6 * a * b for a, b in pairs) - 2 * sizes[0] * sizes[1]
+    if sparse_first:
+        tot -= 4 * sizes[0] * sizes[1]  # the dense-equivalent fwd+dW of layer 0
+    return tot
+
+
+def make_data(cfg, seed, rank=0):
+    import paper_2004_08771_b200 as hb
+
+    if cfg["kind"] == "csr":
+        return hb.synthetic_csr(cfg["n"], cfg["sizes"][0], cfg["nnz"], cfg["classes"], seed=seed + rank,
+                                binary=cfg["binary"], normalize=cfg["normalize"])
+    return hb.synthetic_blobs(cfg["n"], cfg["sizes"][0], cfg["classes"], 2.5, seed=seed + rank)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+def kernel_work(name, cfg, rows, dw_splits=None):
+    """Algorithmic work of one launch of kernel `name` at `rows` batch rows:
+    ("tensor", flops) for GEMMs, ("hbm", bytes) for the memory-bound kernels."""
+    sizes = cfg["sizes"]
+    base, _, l = name.rpartition("_l")
+    l = int(l)
+    if base.startswith("gemm_fwd"):
+        return "tensor", 2.0 * rows * sizes[l + 1] * sizes[l]
+    if base.startswith("gemm_dx"):
+        return "tensor", 2.0 * rows * sizes[l + 1] * sizes[l]
+    if base.startswith("gemm_dw"):
+        return "tensor", 2.0 * rows * sizes[l + 1] * sizes[l]
+    if base == "spmm_sigmoid":
+        nnz = cfg.get("nnz", 0)
+        # gathered W0^T rows (unique rows touched ~ d_in at these batch sizes) + CSR + output write
+        return "hbm", rows * (nnz * 8.0) + min(rows * nnz, sizes[0]) * sizes[1] * 4.0 + rows * sizes[1] * 4.0
+    if base == "sparse_dw_sgd":
+        nnz = cfg.get("nnz", 0)
+        touched = min(rows * nnz, sizes[0])
+        return "hbm", rows * sizes[1] * 4.0 + rows * nnz * 8.0 + 2.0 * touched * sizes[1] * 4.0
+    if base == "head_small":
+        d = sizes[-2]
+        return "hbm", rows * d * 4.0 * 2 + rows * 8.0
+    if base == "reduce_sgd":
+        return "hbm", 3.0 * sizes[l + 1] * sizes[l] * 4.0 * (dw_splits or 1)
+    return "hbm", 0.0
+
+
+def run_ours(args, cfg, rank, world, local_rank, dist):
+    import paper_2004_08771_b200 as hb
+    from paper_2004_08771_b200.nn import Architecture, init_model
+
+    device = local_rank
+    sizes = cfg["sizes"]
+    b = cfg["batch"]
+    sparse = cfg["kind"] == "csr"
+    data = make_data(cfg, args.seed, rank)
+    n = data.n_examples
+    model = init_model(Architecture(sizes), seed=args.seed)
+    ctx = hb.GpuReplica(sizes, b, device=device, sparse=sparse, precision=args.precision)
+    ctx.set_weights(model.weights)
+    if sparse:
+        ctx.stage(data)
+    else:
+        ctx.stage(data.features.astype(np.float32), data.labels)
+    if world > 1:
+        uid = hb.GpuReplica.nccl_unique_id() if rank == 0 else bytes(128)
+        import torch
+
+        t = torch.tensor(list(uid), dtype=torch.uint8)
+        dist.broadcast(t, 0)
+        ctx.comm_init(bytes(t.tolist()), world, rank)
+    n_batches = max(1, (n - b) // b + 1)
+    starts = [(i % n_batches) * b for i in range(args.warmup + args.steps)]
+
+    import torch
+
+    torch.cuda.set_device(device)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{device}")
+
+    def l2_flush():
+        flush.zero_()
+        torch.cuda.synchronize(device)
+
+    for i in range(args.warmup):
+        ctx.step(starts[i], b, cfg["eta"], timed=True)
+        if world > 1:
+            ctx.merge_allreduce()
+    # ---------------------------------------------------------- timed region
+    ctx.profile(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    step_ms, merge_ms, launches = [], [], 0
+    with ClockSampler(device) as clocks:
+        for i in range(args.warmup, args.warmup + args.steps):
+            l2_flush()
+            ctx.step(starts[i], b, cfg["eta"], timed=True)
+            step_ms.append(ctx.last_step_ms)
+            launches += ctx.last_step_launches
+            if world > 1:
+                t0 = time.perf_counter()
+                ctx.merge_allreduce()
+                merge_ms.append((time.perf_counter() - t0) * 1000.0)
+        torch.cuda.synchronize(device)
+    if world > 1:
+        dist.barrier()
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    total_ms = sum(step_ms) + sum(merge_ms)
+    if world > 1:
+        tt = torch.tensor([total_ms], dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    value = world * args.steps * b / (total_ms / 1000.0)
+
+    # ---------------------------------------------------------- e2e (drop-in replica semantics)
+    e2e = None
+    if not args.skip_e2e:
+        host_batches = []
+        for i in range(args.steps):
+            s = starts[i]
+            if sparse:
+                sub = data.rows(s, s + b)
+                sub.val = sub.val.astype(np.float32)
+                host_batches.append((sub, None))
+            else:
+                host_batches.append((np.ascontiguousarray(data.features[s:s + b], dtype=np.float32),
+                                     data.labels[s:s + b].copy()))
+        host_model = [w.copy() for w in model.weights]
+        h2d = sum(w.nbytes for w in host_model)
+        d2h = sum(w.size * 4 for w in host_model) + 8
+        bb = host_batches[0][0]
+        if sparse:
+            h2d += bb.rowptr.nbytes + (sizes[0] + 1) * 8 + bb.labels.nbytes + 2 * bb.col.nbytes + 2 * bb.nnz * 4
+        else:
+            h2d += bb.nbytes + host_batches[0][1].nbytes
+        for i in range(min(2, args.warmup)):  # warm the host path
+            ctx.set_weights(host_model)
+            ctx.step_host(host_batches[i % len(host_batches)][0], host_batches[i % len(host_batches)][1],
+                          cfg["eta"], emit_grad=True)
+            ctx.merge_grads_into(host_model, cfg["eta"])
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            xb, yb = host_batches[i]
+            ctx.set_weights(host_model)  # snapshot of the shared host model (workers.py:132)
+            ctx.step_host(xb, yb, cfg["eta"], emit_grad=True, want_loss=True)  # batch H2D, loss D2H
+            ctx.merge_grads_into(host_model, cfg["eta"])  # stale merge (workers.py:135)
+        el = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([el], dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            el = float(tt.item())
+        e2e = {"value": world * args.steps * b / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h),
+               "path": "execute_gpu_replica semantics via the C ABI: f64 model snapshot H2D + host batch H2D "
+                       "+ step + grad D2H + f64 stale merge + loss D2H"}
+    ctx.close()
+
+    # ---------------------------------------------------------- roofline of the dominant kernel
+    hbm_peak, bf16_peak, peak_src = measured_peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1][0]) if prof else None
+    roofline = None
+    kernels = {}
+    if prof:
+        step_total = sum(v[0] for v in prof.values())
+        for name, (ms, cnt) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
+            kernels[name] = {"avg_us": round(1000.0 * ms / cnt, 2), "launches": cnt,
+                             "share": round(ms / step_total, 4)}
+        name, (ms, cnt) = dom
+        bound, work = kernel_work(name, cfg, b)
+        avg_s = ms / cnt / 1000.0
+        if bound == "tensor":
+            tf32 = bf16_peak / 2.0
+            peak = tf32 / (3.0 if args.precision == "3xtf32" else 1.0)
+            roofline = {"bound": "tensor", "kernel": name, "achieved": round(work / avg_s / 1e12, 2),
+                        "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(work / avg_s / 1e12 / peak, 4),
+                        "traffic": None,
+                        "peak_basis": f"{'3xTF32-effective = ' if args.precision == '3xtf32' else ''}"
+                                      f"TF32 dense = bf16/2 of {bf16_peak} TF/s {peak_src}",
+                        "work_per_launch": work, "avg_launch_us": round(avg_s * 1e6, 2)}
+        else:
+            roofline = {"bound": "hbm", "kernel": name, "achieved": round(work / avg_s / 1e9, 1),
+                        "peak": hbm_peak, "unit": "GB/s", "frac": round(work / avg_s / 1e9 / hbm_peak, 4),
+                        "traffic": None, "peak_basis": peak_src, "work_per_launch": work,
+                        "avg_launch_us": round(avg_s * 1e6, 2)}
+    return dict(value=value, total_ms=total_ms, e2e=e2e, roofline=roofline, kernels=kernels,
+                clocks=clocks.summary(), launches=launches, merge_ms=sum(merge_ms))
+
+
+def cpu_reference_rate(cfg, seed, budget_s, max_steps):
+    """The reference algorithm's CPU step (execute_batch_replica: deep copy,
+    forward, backward, stale merge; float64 NumPy + OpenBLAS, all host cores)
+    on the dense twin of the same batches -- the oracle port."""
+    from oracle import ref_nn
+
+    sizes, b = cfg["sizes"], cfg["batch"]
+    data = make_data(dict(cfg, n=min(cfg["n"], 4 * b)), seed)
+    w = ref_nn.init_weights(sizes, seed)
+    nrow = data.n_examples
+
+    def batch(i):
+        s = (i * b) % max(1, nrow - b + 1)
+        if cfg["kind"] == "csr":
+            return data.dense(s, s + b), data.labels[s:s + b]
+        return data.features[s:s + b], data.labels[s:s + b]
+
+    x, y = batch(0)
+    t0 = time.perf_counter()
+    ref_nn.replica_step(w, x, y, cfg["eta"])  # warm-up + time estimate
+    one = time.perf_counter() - t0
+    rows = b
+    if one * max_steps > budget_s:  # bounded sample: shrink the rows per step, same shapes otherwise
+        rows = max(64, int(b * budget_s / (one * max_steps)))
+    steps, t_total = 0, 0.0
+    for i in range(max_steps):
+        x, y = batch(i + 1)
+        t0 = time.perf_counter()
+        ref_nn.replica_step(w, x[:rows], y[:rows], cfg["eta"])
+        t_total += time.perf_counter() - t0
+        steps += 1
+        if t_total > budget_s:
+            break
+    cores = os.cpu_count() or 1
+    try:
+        from threadpoolctl import threadpool_info
+
+        blas = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
+        if blas:
+            cores = int(blas[0])
+    except Exception:
+        pass
+    return dict(value=steps * rows / t_total, unit=UNIT, cores=cores, kind="port",
+                sample=f"{steps} replica steps x {rows} rows of the {cfg['desc']} workload "
+                       f"(float64 NumPy port of workers.py:126-138, oracle/ref_nn.py)",
+                seconds=round(t_total, 2))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="w8a", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "tf32"])
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    config = {"workload": cfg["desc"], "config": args.config, "arch": "-".join(map(str, cfg["sizes"])),
+              "batch_per_gpu": cfg["batch"], "global_batch": cfg["batch"] * world, "precision": args.precision,
+              "parallelism": f"dp{world}" + (" (NCCL replica averaging every step)" if world > 1 else ""),
+              "l2": "flushed between timed steps (256 MiB write)", "data": "synthetic, resident in HBM"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cpu = cpu_reference_rate(cfg, args.seed, budget_s=min(120.0, 6.0 * args.steps), max_steps=args.steps)
+        line = {"impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * cfg["batch"] / cpu["value"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": config,
+                "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    res = run_ours(args, cfg, rank, world, local_rank, dist)
+    if rank == 0:
+        cpu = None
+        if world == 1:
+            cpu = cpu_reference_rate(cfg, args.seed, budget_s=args.cpu_budget_s, max_steps=10)
+        line = {
+            "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["total_ms"] / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05)" if args.precision == "3xtf32"
+            else "f32 (TF32 tcgen05)", "data": "synthetic", "config": config,
+            "e2e": res["e2e"], "roofline": res["roofline"],
+            "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "clocks": res["clocks"], "gpu_launches": res["launches"], "kernels": res["kernels"],
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,141 @@
+/*
+ * hogbatch_b200.h -- C ABI of the B200-native GPU replica worker for the
+ * heterogeneous CPU+GPU Hogbatch / Adaptive Hogbatch SGD of
+ * arXiv:2004.08771 (reference package: /root/reference/pkg, `hogtrain`).
+ *
+ * The reference's GPU worker is `execute_batch_replica(model, batch, eta,
+ * speed_factor)` (pkg/src/hogtrain/workers.py:126-138), called from
+ * `WorkerThread._execute` (workers.py:193-210), plus the evaluation call
+ * `loss_sum(eval_model, x, y)` (nn.py:139-146, from workers.py:212-222).
+ * Everything below is what a binding of that seam needs: a device context
+ * per (worker, device), the model layout of nn.py:63-78, the batch layout of
+ * data.py:30-79, one training step, the stale merge back into the host
+ * model, loss evaluation, device timing for the batch-size controller
+ * (policies.py:84-129 fed from engine.py:318-328), and the NCCL merge between
+ * GPU replicas.
+ *
+ * Conventions
+ *  - Every function returns HB_OK (0) or an HB_E* code; hb_last_error()
+ *    returns a thread-local message for the last failure on the calling
+ *    thread.  Argument/shape errors are HB_EINVAL (the reference raises
+ *    ValueError there: linalg.py:40-44, nn.py:110-113); CUDA/NCCL failures
+ *    are HB_ECUDA / HB_ENCCL.
+ *  - Plain pointers and sizes only.  "host" pointers are ordinary (pageable
+ *    or pinned) CPU memory; nothing here retains a host pointer after return.
+ *  - A context is affine to one device and must be used from one thread at a
+ *    time (the reference's worker thread).  Calls block until the device work
+ *    they enqueue is complete unless stated otherwise.
+ *  - Layer l weight: row-major (d_{l+1}, d_l) float64 on the host, exactly
+ *    `Model.weights[l]` (nn.py:75).  The device keeps an fp32 mirror; for a
+ *    sparse first layer it stores W_0 transposed, which is invisible here.
+ */
+#ifndef HOGBATCH_B200_H
+#define HOGBATCH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HB_OK 0
+#define HB_EINVAL 1
+#define HB_ECUDA 2
+#define HB_ENCCL 3
+#define HB_ESTATE 4
+
+/* hb_ctx_create flags */
+#define HB_SPARSE_INPUT 1u  /* first layer consumes CSR input (CSR-gather SpMM) */
+#define HB_PRECISION_TF32 2u /* 1-pass TF32 GEMMs (fast mode); default is 3xTF32 */
+
+/* hb_train_step flags */
+#define HB_STEP_EMIT_GRAD 1u /* keep the raw mean gradient of every layer (for the host merge / parity) */
+#define HB_STEP_TIMED 2u     /* bracket the step with CUDA events (hb_last_step_ms) */
+#define HB_STEP_ASYNC 4u     /* return once the step is enqueued (no out_loss); hb_synchronize() waits */
+
+typedef struct hb_ctx hb_ctx;
+
+/* Thread-local message describing the last error on this thread. */
+const char* hb_last_error(void);
+/* Library build identification (arch, precision modes). */
+const char* hb_version(void);
+int hb_device_count(int* out);
+
+/* Device context for one GPU replica worker.  Replaces the per-call
+ * deep_copy + numpy state of execute_batch_replica (workers.py:131-135) with
+ * resident device buffers.  layer_sizes[0..n_layers] as Architecture.layer_sizes
+ * (nn.py:38-60).  max_batch bounds every step's row count (WorkerConfig.max_batch,
+ * workers.py:61-62). */
+int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* layer_sizes, int max_batch, uint32_t flags);
+int hb_ctx_destroy(hb_ctx* ctx);
+
+/* Model snapshot H2D (deep_copy, nn.py:182-184): host float64 (d_{l+1}, d_l). */
+int hb_set_weights_f64(hb_ctx* ctx, int layer, const double* w);
+/* Device model D2H into host float64 (d_{l+1}, d_l). */
+int hb_get_weights_f64(hb_ctx* ctx, int layer, double* w);
+int hb_get_weights_f32(hb_ctx* ctx, int layer, float* w);
+
+/* Stale merge (workers.py:135 -> nn.py:174-179 -> linalg.py:70-79):
+ * host_w -= eta * g_l for the gradient kept by the last HB_STEP_EMIT_GRAD
+ * step, element by element with aligned 8-byte stores.  */
+int hb_merge_grad_into_f64(hb_ctx* ctx, int layer, double* host_w, double eta);
+/* Raw mean gradient of the last HB_STEP_EMIT_GRAD step, (d_{l+1}, d_l) fp32. */
+int hb_get_grad_f32(hb_ctx* ctx, int layer, float* g);
+
+/* Stage one epoch's (or any dataset's) rows on the device so steps can index
+ * them by (start, rows) -- the per-epoch shuffled copy that BatchRef views
+ * (engine.py:214-221, data.py:57-79).  Dense: features (n_rows, n_cols) with
+ * row stride ld (elements); labels int64 class indices. */
+int hb_stage_dense_f64(hb_ctx* ctx, const double* x, int64_t n_rows, int64_t ld, const int64_t* labels);
+int hb_stage_dense_f32(hb_ctx* ctx, const float* x, int64_t n_rows, int64_t ld, const int64_t* labels);
+/* Sparse (HB_SPARSE_INPUT contexts): CSR with int64 row pointer (n_rows+1),
+ * int32 0-based column ids, fp32 values.  The column-sorted (CSC) copy used
+ * by the sparse dW kernel is built once here. */
+int hb_stage_csr(hb_ctx* ctx, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n_rows,
+                 const int64_t* labels);
+int64_t hb_staged_rows(hb_ctx* ctx);
+
+/* One replica SGD step over staged rows [start, start+rows): forward
+ * (nn.py:108-121), fused softmax/CE error (nn.py:162-164), backward
+ * (nn.py:149-171) and the SGD update W -= eta * g fused into the dW epilogues
+ * (nn.py:174-179), all on the device.  out_loss (nullable) receives the mean
+ * training cross-entropy of the batch (nn.py:124-136), a by-product. */
+int hb_train_step(hb_ctx* ctx, int64_t start, int rows, double eta, uint32_t flags, double* out_loss);
+/* Same step on a batch held in host memory (copied H2D inside the call):
+ * dense (rows, d0) with row stride ld, or CSR (rows+1 row pointer starting at 0). */
+int hb_train_step_host_dense(hb_ctx* ctx, const float* x, int64_t ld, const int64_t* labels, int rows, double eta,
+                             uint32_t flags, double* out_loss);
+int hb_train_step_host_csr(hb_ctx* ctx, const int64_t* rowptr, const int32_t* col, const float* val,
+                           const int64_t* labels, int rows, double eta, uint32_t flags, double* out_loss);
+
+/* Sum over staged rows [start, start+rows) of -log max(p_y, 1e-12)
+ * (loss_sum, nn.py:139-146), evaluated in chunks of at most max_batch rows. */
+int hb_eval_loss_sum(hb_ctx* ctx, int64_t start, int64_t rows, double* out_sum);
+
+/* Forward only over staged rows (tests): then read layer activations
+ * A_l (rows, d_l), l = 1..n_layers-1, or the output probabilities. */
+int hb_forward(hb_ctx* ctx, int64_t start, int rows);
+int hb_get_activation_f32(hb_ctx* ctx, int layer, int rows, float* out);
+
+/* Device time of the last HB_STEP_TIMED step (CUDA events on the step stream). */
+int hb_last_step_ms(hb_ctx* ctx, float* ms);
+/* Kernel launches issued by the last step. */
+int hb_last_step_launches(hb_ctx* ctx, int* n);
+int hb_synchronize(hb_ctx* ctx);
+/* Per-launch CUDA-event profiling on the step stream (off by default):
+ * enable, run steps, then read per-kernel totals.  names receives
+ * max_entries NUL-terminated 64-byte slots ("gemm_fwd_sigmoid_l1", ...). */
+int hb_profile_enable(hb_ctx* ctx, int on);
+int hb_profile_read(hb_ctx* ctx, int max_entries, char* names, double* total_ms, int* counts, int* n_out);
+
+/* NCCL merge between GPU replicas (one communicator per process/device). */
+int hb_nccl_unique_id(void* out_128_bytes);
+int hb_comm_init(hb_ctx* ctx, const void* id_128_bytes, int nranks, int rank);
+/* Average the device models of all ranks in place (allreduce-sum / nranks). */
+int hb_merge_allreduce(hb_ctx* ctx);
+int hb_comm_destroy(hb_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOGBATCH_B200_H */

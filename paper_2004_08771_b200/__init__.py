@@ -1,0 +1,57 @@
+"""B200-native GPU replica worker for heterogeneous CPU+GPU (Adaptive) Hogbatch SGD.
+
+The hot path of arXiv:2004.08771's GPU worker -- the large-batch synchronous
+MLP step `execute_batch_replica` of the reference package `hogtrain`
+(pkg/src/hogtrain/workers.py:126-138) and its loss evaluation
+(nn.py:139-146) -- rebuilt as hand-written sm_100a CUDA (TMA + tcgen05/TMEM
+GEMMs with fused epilogues, CSR-gather SpMM first layer) behind a C ABI
+(include/hogbatch_b200.h), bound here with ctypes.
+
+Drop-in: `execute_gpu_replica` / `gpu_loss_sum` have the reference's
+signatures; `install()` rebinds them into a live `hogtrain`.
+"""
+
+from ._native import device_count, load as load_library
+from .data import (
+    BatchRef,
+    CsrBatchRef,
+    CsrDataset,
+    Dataset,
+    epoch_shuffle_seed,
+    reorder,
+    shuffle_epoch,
+    synthetic_blobs,
+    synthetic_csr,
+)
+from .nn import Architecture, InitScheme, Model, deep_copy, init_model
+from .policies import (
+    AdaptiveHogbatch,
+    AdaptiveState,
+    DeviceSpeedFeed,
+    FixedHeterogeneous,
+    PolicyDecision,
+    UniformHogbatch,
+    adaptive_update,
+)
+from .replica import GpuReplica
+from .trainer import TrainResult, train_gpu
+from .workers import (
+    WorkerConfig,
+    WorkerMode,
+    execute_gpu_replica,
+    gpu_loss_sum,
+    install,
+    last_device_ms,
+    set_worker_device,
+)
+
+__all__ = [
+    "AdaptiveHogbatch", "AdaptiveState", "Architecture", "BatchRef", "CsrBatchRef", "CsrDataset", "Dataset",
+    "DeviceSpeedFeed", "FixedHeterogeneous", "GpuReplica", "InitScheme", "Model", "PolicyDecision",
+    "TrainResult", "UniformHogbatch", "WorkerConfig", "WorkerMode", "adaptive_update", "deep_copy",
+    "device_count", "epoch_shuffle_seed", "execute_gpu_replica", "gpu_loss_sum", "init_model", "install",
+    "last_device_ms", "load_library", "reorder", "set_worker_device", "shuffle_epoch", "synthetic_blobs",
+    "synthetic_csr", "train_gpu",
+]
+
+__version__ = "0.1.0"

@@ -1,0 +1,1220 @@
+// hb_capi.cu -- device context and the C ABI of include/hogbatch_b200.h.
+//
+// A context owns, on one B200:
+//   * the fp32 model mirror W_l (row-major (d_{l+1}, d_l), W_0 transposed for
+//     sparse input), laid out with 16-byte-aligned row strides for TMA;
+//   * the activation tape A_l and error signals D_l for up to max_batch rows;
+//   * the staged epoch (dense fp32 rows or CSR + its column-sorted twin);
+//   * split-K / per-block reduction workspaces, TMA tensor maps, one stream.
+// A training step is a fixed sequence of kernel launches on that stream:
+//   forward  : [SpMM+sigmoid | GEMM+sigmoid] per hidden layer
+//   head     : fused small softmax-CE head (classes <= 4) or
+//              GEMM logits -> softmax_delta (wide heads)
+//   backward : per layer dX GEMM (x s(1-s) epilogue) then dW GEMM whose
+//              epilogue applies W -= eta*g (split-K: deterministic reduce+SGD)
+//   sparse L0: CSC-slice gather dW + in-place update of active rows
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hogbatch_b200.h"
+#include "hb_gemm.cuh"
+#include "hb_kernels.cuh"
+
+using namespace hb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define HB_CUDA(expr)                                                                                   \
+  do {                                                                                                  \
+    cudaError_t e_ = (expr);                                                                            \
+    if (e_ != cudaSuccess) return fail(HB_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                             \
+  } while (0)
+#define HB_TRY(expr)          \
+  do {                        \
+    int r_ = (expr);          \
+    if (r_ != HB_OK) return r_; \
+  } while (0)
+
+inline long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
+inline int cdiv(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+// ---------------------------------------------------------------- TMA maps
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled g_encode = nullptr;
+
+int get_encoder() {
+  if (g_encode) return HB_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  HB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (fn == nullptr || q != cudaDriverEntryPointSuccess) return fail(HB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  g_encode = reinterpret_cast<PFN_encodeTiled>(fn);
+  return HB_OK;
+}
+
+// fp32 2-D map over (rows, inner) with row stride ld (elements).
+//   K-major operand tiles: box {32, box_rows}, SWIZZLE_128B.
+//   MN-major operand tiles: box {32, 32}, SWIZZLE_128B_ATOM_32B.
+int make_map(CUtensorMap* m, const float* base, long long inner, long long rows, long long ld, int box_rows,
+             bool mn_major) {
+  HB_TRY(get_encoder());
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(std::max<long long>(rows, 1))};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  cuuint32_t box[2] = {32, static_cast<cuuint32_t>(mn_major ? 32 : box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(HB_ECUDA, "cuTensorMapEncodeTiled failed (%d): inner=%lld rows=%lld ld=%lld box_rows=%d mn=%d",
+                static_cast<int>(r), inner, rows, ld, box_rows, static_cast<int>(mn_major));
+  return HB_OK;
+}
+
+// ------------------------------------------------------------ GEMM launch
+template <int BN, bool A_MN, bool B_MN, int EPI, int PASSES>
+int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int m_tiles, int n_tiles,
+                  int splits, cudaStream_t st) {
+  using C = GemmCfg<BN, PASSES>;
+  auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, EPI, PASSES>;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    HB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    configured = true;
+  }
+  dim3 grid(n_tiles, m_tiles, splits);
+  kern<<<grid, C::THREADS, C::SMEM, st>>>(ta, tb, a);
+  HB_CUDA(cudaGetLastError());
+  return HB_OK;
+}
+
+enum GemmKind { G_FWD = 0, G_DX = 1, G_DW = 2 };
+
+template <int PASSES>
+int launch_gemm_p(GemmKind kind, int epi, int bn, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+                  int m_tiles, int n_tiles, int splits, cudaStream_t st) {
+#define HB_L(BN_, AMN_, BMN_, EPI_) \
+  return launch_gemm_t<BN_, AMN_, BMN_, EPI_, PASSES>(ta, tb, a, m_tiles, n_tiles, splits, st)
+  if (kind == G_FWD) {
+    if (epi == EPI_SIGMOID) {
+      if (bn == 256) HB_L(256, false, false, EPI_SIGMOID);
+      HB_L(128, false, false, EPI_SIGMOID);
+    }
+    if (bn == 256) HB_L(256, false, false, EPI_STORE);
+    HB_L(128, false, false, EPI_STORE);
+  }
+  if (kind == G_DX) {
+    if (bn == 256) HB_L(256, false, true, EPI_DSIG);
+    HB_L(128, false, true, EPI_DSIG);
+  }
+  if (epi == EPI_SGD) {
+    if (bn == 256) HB_L(256, true, true, EPI_SGD);
+    HB_L(128, true, true, EPI_SGD);
+  }
+  if (bn == 256) HB_L(256, true, true, EPI_PARTIAL);
+  HB_L(128, true, true, EPI_PARTIAL);
+#undef HB_L
+}
+
+int launch_gemm(int passes, GemmKind kind, int epi, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
+                const GemmArgs& a, int m_tiles, int n_tiles, int splits, cudaStream_t st) {
+  if (passes == 3) return launch_gemm_p<3>(kind, epi, bn, ta, tb, a, m_tiles, n_tiles, splits, st);
+  return launch_gemm_p<1>(kind, epi, bn, ta, tb, a, m_tiles, n_tiles, splits, st);
+}
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+typedef struct {
+  char internal[128];
+} nccl_uid_t;
+typedef void* nccl_comm_t;
+struct NcclApi {
+  void* h = nullptr;
+  int (*getUniqueId)(nccl_uid_t*) = nullptr;
+  int (*commInitRank)(nccl_comm_t*, int, nccl_uid_t, int) = nullptr;
+  int (*allReduce)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+  int (*commDestroy)(nccl_comm_t) = nullptr;
+  const char* (*errStr)(int) = nullptr;
+};
+NcclApi g_nccl;
+int load_nccl() {
+  if (g_nccl.h) return HB_OK;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return fail(HB_ENCCL, "cannot dlopen libnccl.so.2: %s", dlerror());
+  g_nccl.getUniqueId = reinterpret_cast<int (*)(nccl_uid_t*)>(dlsym(h, "ncclGetUniqueId"));
+  g_nccl.commInitRank = reinterpret_cast<int (*)(nccl_comm_t*, int, nccl_uid_t, int)>(dlsym(h, "ncclCommInitRank"));
+  g_nccl.allReduce =
+      reinterpret_cast<int (*)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t)>(dlsym(h, "ncclAllReduce"));
+  g_nccl.commDestroy = reinterpret_cast<int (*)(nccl_comm_t)>(dlsym(h, "ncclCommDestroy"));
+  g_nccl.errStr = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
+  if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.allReduce || !g_nccl.commDestroy)
+    return fail(HB_ENCCL, "libnccl is missing required symbols");
+  g_nccl.h = h;
+  return HB_OK;
+}
+constexpr int kNcclFloat32 = 7;  // ncclFloat32
+constexpr int kNcclSum = 0;      // ncclSum
+
+}  // namespace
+
+// ======================================================================
+struct DataView {
+  // dense
+  const float* x = nullptr;
+  long long ldx = 0;
+  long long n_rows = 0;
+  CUtensorMap tm_fwd;  // K-major A operand of the first forward GEMM
+  CUtensorMap tm_dw;   // MN-major B operand of the first dW GEMM
+  // sparse
+  const int64_t* rowptr = nullptr;
+  const int32_t* col = nullptr;
+  const float* val = nullptr;
+  const int64_t* colptr = nullptr;
+  const int32_t* rowidx = nullptr;
+  const float* cval = nullptr;
+  const int64_t* labels = nullptr;
+};
+
+struct hb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int L = 0;
+  std::vector<int> d;          // layer sizes, L+1 entries
+  std::vector<long long> ld;   // padded row stride of a width-d_l buffer
+  int cap = 0;                 // row capacity (max_batch rounded up to 128)
+  int max_batch = 0;
+  bool sparse = false;
+  int passes = 3;
+  bool small_head = false;
+  int head_nct = 0, head_maxt = 0;
+
+  std::vector<float*> W, G;    // W[l]; G[l] raw gradient (EMIT_GRAD)
+  std::vector<long long> ldw;  // row stride of W[l] (in its device layout)
+  std::vector<float*> A;       // A[l] l=1..L-1 activations (cap, ld[l])
+  std::vector<float*> D;       // D[l] error at the output of layer l (cap, ld[l+1])
+  std::vector<int> bn_fwd, bn_dx, bn_dw;
+  std::vector<CUtensorMap> tmW_k, tmW_mn, tmA_k, tmA_mn, tmD_k, tmD_mn;
+
+  // staged epoch / host batch slot
+  float* ex = nullptr;
+  int64_t* elabels = nullptr;
+  int64_t *erowptr = nullptr, *ecolptr = nullptr;
+  int32_t *ecol = nullptr, *erowidx = nullptr;
+  float *eval_ = nullptr, *ecval = nullptr;
+  long long e_rows = 0, e_nnz = 0;
+  DataView epoch;
+  bool staged = false;
+
+  float* bx = nullptr;  // batch slot (dense rows) for host-buffer steps
+  int64_t* blabels = nullptr;
+  int64_t *browptr = nullptr, *bcolptr = nullptr;
+  int32_t *bcol = nullptr, *browidx = nullptr;
+  float *bval = nullptr, *bcval = nullptr;
+  long long b_nnz_cap = 0;
+  DataView batch;
+  std::vector<int64_t> h_colptr;  // host scratch for the per-batch CSC
+  std::vector<int32_t> h_rowidx;
+  std::vector<float> h_cval;
+  void* pinned = nullptr;  // pinned host staging
+  size_t pinned_bytes = 0;
+
+  float* ws = nullptr;  // split-K partials / head partials
+  size_t ws_floats = 0;
+  double* ws_loss = nullptr;
+  int ws_loss_n = 0;
+  double* d_loss = nullptr;
+  double* stage64 = nullptr;  // f64 staging for the weight exchange
+  size_t stage64_n = 0;
+  float* stage32 = nullptr;  // fp32 staging (grad transpose)
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  float last_ms = 0.f;
+  int last_launches = 0;
+  bool grads_valid = false;
+  // per-launch CUDA-event profiling (bench.py reads it live; off by default)
+  bool prof_on = false;
+  std::vector<cudaEvent_t> evpool;
+  size_t ev_used = 0;
+  std::vector<std::pair<std::string, size_t>> marks;
+  void* comm = nullptr;
+  int nranks = 1;
+  float* flat = nullptr;  // contiguous model copy for allreduce
+  size_t n_params = 0;
+};
+
+namespace {
+
+int ctx_check(hb_ctx* c) {
+  if (c == nullptr) return fail(HB_EINVAL, "null context");
+  HB_CUDA(cudaSetDevice(c->device));
+  return HB_OK;
+}
+
+void prof_begin(hb_ctx* c) {
+  if (!c->prof_on) return;
+  while (c->evpool.size() < c->ev_used + 2) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) {
+      c->prof_on = false;
+      return;
+    }
+    c->evpool.push_back(e);
+  }
+  cudaEventRecord(c->evpool[c->ev_used], c->stream);
+}
+void prof_end(hb_ctx* c, const char* kind, int layer) {
+  if (!c->prof_on) return;
+  cudaEventRecord(c->evpool[c->ev_used + 1], c->stream);
+  char name[64];
+  if (layer >= 0)
+    snprintf(name, sizeof name, "%s_l%d", kind, layer);
+  else
+    snprintf(name, sizeof name, "%s", kind);
+  c->marks.emplace_back(name, c->ev_used);
+  c->ev_used += 2;
+}
+
+int build_data_maps(hb_ctx* c, DataView& v) {
+  if (c->sparse) return HB_OK;
+  HB_TRY(make_map(&v.tm_fwd, v.x, c->d[0], v.n_rows, v.ldx, 128, false));
+  HB_TRY(make_map(&v.tm_dw, v.x, c->d[0], v.n_rows, v.ldx, 32, true));
+  return HB_OK;
+}
+
+int choose_bn(long long m_tiles, long long n) {
+  if (n <= 128) return 128;
+  if (m_tiles * cdiv(n, 256) >= 120) return 256;
+  return 128;
+}
+
+// split-K plan for the dW GEMM of layer l at `rows` batch rows
+void dw_plan(const hb_ctx* c, int l, int rows, int* splits, int* kb_per, int* kb_total) {
+  const int M = c->d[l + 1], N = c->d[l];
+  const int tiles = cdiv(M, kBM) * cdiv(N, c->bn_dw[l]);
+  *kb_total = std::max(1, cdiv(rows, kBK));
+  int want = std::max(1, (148 * 3 / 2 + tiles - 1) / tiles);
+  want = std::min(want, *kb_total);
+  *kb_per = cdiv(*kb_total, want);
+  *splits = cdiv(*kb_total, *kb_per);
+}
+
+int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool train, uint32_t flags, double eta) {
+  cudaStream_t st = c->stream;
+  const int L = c->L;
+  const int m_tiles = cdiv(rows, kBM);
+  const int zrows = std::min<long long>(round_up(rows, kBM), c->cap);
+  // hidden layers
+  for (int l = 0; l < L - 1; ++l) {
+    if (l == 0 && c->sparse) {
+      SpmmArgs p{v.rowptr, v.col, v.val, start, rows, c->W[0], c->ldw[0], c->d[1], c->A[1], c->ld[1]};
+      const int blocks = cdiv(static_cast<long long>(rows) * 32, 256);
+      prof_begin(c);
+      if (c->d[1] % 128 == 0)
+        spmm_sigmoid_kernel<true><<<blocks, 256, 0, st>>>(p);
+      else
+        spmm_sigmoid_kernel<false><<<blocks, 256, 0, st>>>(p);
+      HB_CUDA(cudaGetLastError());
+      prof_end(c, "spmm_sigmoid", 0);
+      c->last_launches++;
+      continue;
+    }
+    GemmArgs a{};
+    a.M = rows;
+    a.N = c->d[l + 1];
+    a.a_off = l == 0 ? static_cast<int>(start) : 0;
+    a.kb_total = cdiv(c->d[l], kBK);
+    a.kb_per_split = a.kb_total;
+    a.out = c->A[l + 1];
+    a.ldo = c->ld[l + 1];
+    const CUtensorMap& ta = l == 0 ? v.tm_fwd : c->tmA_k[l];
+    prof_begin(c);
+    HB_TRY(launch_gemm(c->passes, G_FWD, EPI_SIGMOID, c->bn_fwd[l], ta, c->tmW_k[l], a, m_tiles,
+                       cdiv(a.N, c->bn_fwd[l]), 1, st));
+    prof_end(c, "gemm_fwd_sigmoid", l);
+    c->last_launches++;
+  }
+  // output layer
+  const int l = L - 1;
+  const float inv_n = 1.0f / static_cast<float>(rows);
+  const int64_t* labels = v.labels + start;
+  if (c->small_head) {
+    HeadArgs h{};
+    if (L == 1) {
+      h.a = v.x + start * v.ldx;
+      h.lda = v.ldx;
+    } else {
+      h.a = c->A[L - 1];
+      h.lda = c->ld[L - 1];
+    }
+    h.w = c->W[l];
+    h.ldw = c->ldw[l];
+    h.labels = labels;
+    h.rows = rows;
+    h.d = c->d[l];
+    h.nc = c->d[L];
+    h.zero_rows = zrows;
+    h.inv_n = inv_n;
+    h.train = train ? 1 : 0;
+    h.delta_prev = (train && L >= 2) ? c->D[L - 2] : nullptr;
+    h.ld_dp = L >= 2 ? c->ld[L - 1] : 0;
+    h.delta_out = nullptr;
+    h.ws_dw = c->ws;
+    h.ws_loss = c->ws_loss;
+    const int grid = cdiv(rows, kHeadRowsPerBlock);
+    const int threads = kHeadWarps * 32;
+    prof_begin(c);
+    if (c->head_nct == 2) {
+      if (c->head_maxt == 8)
+        head_small_kernel<2, 8><<<grid, threads, 0, st>>>(h);
+      else
+        head_small_kernel<2, 32><<<grid, threads, 0, st>>>(h);
+    } else {
+      if (c->head_maxt == 8)
+        head_small_kernel<4, 8><<<grid, threads, 0, st>>>(h);
+      else
+        head_small_kernel<4, 32><<<grid, threads, 0, st>>>(h);
+    }
+    HB_CUDA(cudaGetLastError());
+    prof_end(c, "head_small", l);
+    loss_reduce_kernel<<<1, 32, 0, st>>>(c->ws_loss, grid, c->d_loss, 0);
+    HB_CUDA(cudaGetLastError());
+    c->last_launches += 2;
+    if (train) {
+      const long long n = static_cast<long long>(c->d[L]) * c->d[l];
+      prof_begin(c);
+      reduce_sgd_kernel<<<std::min<long long>(cdiv(n, 256), 4096), 256, 0, st>>>(
+          c->W[l], c->ldw[l], c->ws, grid, n, c->d[L], c->d[l], static_cast<float>(eta),
+          (flags & HB_STEP_EMIT_GRAD) ? c->G[l] : nullptr, c->d[l]);
+      HB_CUDA(cudaGetLastError());
+      prof_end(c, "reduce_sgd", l);
+      c->last_launches++;
+    }
+    return HB_OK;
+  }
+  // wide head: logits GEMM then softmax -> delta in place
+  GemmArgs a{};
+  a.M = rows;
+  a.N = c->d[L];
+  a.a_off = l == 0 ? static_cast<int>(start) : 0;
+  a.kb_total = cdiv(c->d[l], kBK);
+  a.kb_per_split = a.kb_total;
+  a.out = c->D[l];
+  a.ldo = c->ld[L];
+  const CUtensorMap& ta = l == 0 ? v.tm_fwd : c->tmA_k[l];
+  prof_begin(c);
+  HB_TRY(launch_gemm(c->passes, G_FWD, EPI_STORE, c->bn_fwd[l], ta, c->tmW_k[l], a, m_tiles, cdiv(a.N, c->bn_fwd[l]),
+                     1, st));
+  prof_end(c, "gemm_fwd_logits", l);
+  SoftmaxArgs s{c->D[l], c->ld[L], labels, rows, c->d[L], zrows, inv_n, train ? 1 : 0, c->ws_loss};
+  const int grid = cdiv(std::max(rows, zrows), 8);
+  prof_begin(c);
+  softmax_delta_kernel<<<grid, 256, 0, st>>>(s);
+  HB_CUDA(cudaGetLastError());
+  prof_end(c, "softmax_delta", l);
+  loss_reduce_kernel<<<1, 32, 0, st>>>(c->ws_loss, grid, c->d_loss, 0);
+  HB_CUDA(cudaGetLastError());
+  c->last_launches += 3;
+  return HB_OK;
+}
+
+int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32_t flags, double eta) {
+  cudaStream_t st = c->stream;
+  const int L = c->L;
+  const int m_tiles = cdiv(rows, kBM);
+  const int zrows = std::min<long long>(round_up(rows, kBM), c->cap);
+  const bool emit = (flags & HB_STEP_EMIT_GRAD) != 0;
+  // with the small head the output layer is already done (dW + delta_{L-2})
+  const int top = c->small_head ? L - 2 : L - 1;
+  for (int l = top; l >= 0; --l) {
+    // dX: D[l-1] = (D[l] . W[l]) * A[l] (1 - A[l])   -- must precede W[l]'s update
+    if (l >= 1) {
+      GemmArgs a{};
+      a.M = rows;
+      a.N = c->d[l];
+      a.m_zero_rows = zrows;
+      a.kb_total = cdiv(c->d[l + 1], kBK);
+      a.kb_per_split = a.kb_total;
+      a.out = c->D[l - 1];
+      a.ldo = c->ld[l];
+      a.aux = c->A[l];
+      a.ld_aux = c->ld[l];
+      prof_begin(c);
+      HB_TRY(launch_gemm(c->passes, G_DX, EPI_DSIG, c->bn_dx[l], c->tmD_k[l], c->tmW_mn[l], a,
+                         cdiv(zrows, kBM), cdiv(a.N, c->bn_dx[l]), 1, st));
+      prof_end(c, "gemm_dx_dsig", l);
+      c->last_launches++;
+    }
+    // dW + SGD
+    if (l == 0 && c->sparse) {
+      SparseDwArgs p{v.colptr, v.rowidx, v.cval, start, rows, c->d[0], c->d[1], c->D[0], c->ld[1],
+                     c->W[0], c->ldw[0], static_cast<float>(eta), emit ? c->G[0] : nullptr, c->ldw[0]};
+      const int blocks = cdiv(static_cast<long long>(c->d[0]) * 32, 256);
+      prof_begin(c);
+      if (c->d[1] % 128 == 0)
+        sparse_dw_kernel<true><<<blocks, 256, 0, st>>>(p);
+      else
+        sparse_dw_kernel<false><<<blocks, 256, 0, st>>>(p);
+      HB_CUDA(cudaGetLastError());
+      prof_end(c, "sparse_dw_sgd", 0);
+      c->last_launches++;
+      continue;
+    }
+    int splits, kb_per, kb_total;
+    dw_plan(c, l, rows, &splits, &kb_per, &kb_total);
+    GemmArgs a{};
+    a.M = c->d[l + 1];
+    a.N = c->d[l];
+    a.b_off = l == 0 ? static_cast<int>(start) : 0;
+    a.kb_total = kb_total;
+    a.kb_per_split = kb_per;
+    a.eta = static_cast<float>(eta);
+    const CUtensorMap& tb = l == 0 ? v.tm_dw : c->tmA_mn[l];
+    const int mt = cdiv(a.M, kBM), nt = cdiv(a.N, c->bn_dw[l]);
+    if (splits == 1) {
+      a.out = c->W[l];
+      a.ldo = c->ldw[l];
+      a.grad = emit ? c->G[l] : nullptr;
+      a.ld_grad = c->d[l];
+      prof_begin(c);
+      HB_TRY(launch_gemm(c->passes, G_DW, EPI_SGD, c->bn_dw[l], c->tmD_mn[l], tb, a, mt, nt, 1, st));
+      prof_end(c, "gemm_dw_sgd", l);
+      c->last_launches++;
+    } else {
+      const long long slab = static_cast<long long>(a.M) * a.N;
+      a.out = c->ws;
+      a.ldo = a.N;
+      a.split_stride = slab;
+      prof_begin(c);
+      HB_TRY(launch_gemm(c->passes, G_DW, EPI_PARTIAL, c->bn_dw[l], c->tmD_mn[l], tb, a, mt, nt, splits, st));
+      prof_end(c, "gemm_dw_partial", l);
+      prof_begin(c);
+      reduce_sgd_kernel<<<std::min<long long>(cdiv(slab, 256), 4096), 256, 0, st>>>(
+          c->W[l], c->ldw[l], c->ws, splits, slab, a.M, a.N, static_cast<float>(eta), emit ? c->G[l] : nullptr,
+          c->d[l]);
+      HB_CUDA(cudaGetLastError());
+      prof_end(c, "reduce_sgd", l);
+      c->last_launches += 2;
+    }
+  }
+  return HB_OK;
+}
+
+int do_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta, uint32_t flags, double* out_loss) {
+  if (rows < 1 || rows > c->max_batch) return fail(HB_EINVAL, "rows=%d outside [1, %d]", rows, c->max_batch);
+  c->last_launches = 0;
+  const bool timed = (flags & HB_STEP_TIMED) != 0;
+  if (timed) HB_CUDA(cudaEventRecord(c->ev0, c->stream));
+  HB_TRY(run_forward(c, v, start, rows, true, flags, eta));
+  HB_TRY(run_backward(c, v, start, rows, flags, eta));
+  if (timed) HB_CUDA(cudaEventRecord(c->ev1, c->stream));
+  c->grads_valid = (flags & HB_STEP_EMIT_GRAD) != 0;
+  if (out_loss != nullptr) {
+    double s = 0.0;
+    HB_CUDA(cudaMemcpyAsync(&s, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    HB_CUDA(cudaStreamSynchronize(c->stream));
+    *out_loss = s / rows;
+  } else if (!(flags & HB_STEP_ASYNC)) {
+    HB_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  if (timed) {
+    HB_CUDA(cudaEventSynchronize(c->ev1));
+    HB_CUDA(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+  }
+  return HB_OK;
+}
+
+// stable counting sort of CSR entries by column -> CSC with ascending rows
+void build_csc(const int64_t* rowptr, const int32_t* col, const float* val, long long n_rows, int n_cols,
+               std::vector<int64_t>& colptr, std::vector<int32_t>& rowidx, std::vector<float>& cval,
+               long long row_base) {
+  const long long nnz = rowptr[n_rows] - rowptr[0];
+  colptr.assign(n_cols + 1, 0);
+  for (long long e = rowptr[0]; e < rowptr[n_rows]; ++e) colptr[col[e] + 1]++;
+  for (int j = 0; j < n_cols; ++j) colptr[j + 1] += colptr[j];
+  rowidx.resize(nnz);
+  cval.resize(nnz);
+  std::vector<int64_t> cur(colptr.begin(), colptr.end() - 1);
+  for (long long r = 0; r < n_rows; ++r)
+    for (long long e = rowptr[r]; e < rowptr[r + 1]; ++e) {
+      const long long k = cur[col[e]]++;
+      rowidx[k] = static_cast<int32_t>(r + row_base);
+      cval[k] = val[e];
+    }
+}
+
+int ensure_pinned(hb_ctx* c, size_t bytes) {
+  if (c->pinned_bytes >= bytes) return HB_OK;
+  if (c->pinned) cudaFreeHost(c->pinned);
+  c->pinned = nullptr;
+  HB_CUDA(cudaMallocHost(&c->pinned, bytes));
+  c->pinned_bytes = bytes;
+  return HB_OK;
+}
+
+int free_epoch(hb_ctx* c) {
+  cudaFree(c->ex);
+  cudaFree(c->elabels);
+  cudaFree(c->erowptr);
+  cudaFree(c->ecol);
+  cudaFree(c->eval_);
+  cudaFree(c->ecolptr);
+  cudaFree(c->erowidx);
+  cudaFree(c->ecval);
+  c->ex = nullptr;
+  c->elabels = nullptr;
+  c->erowptr = nullptr;
+  c->ecol = nullptr;
+  c->eval_ = nullptr;
+  c->ecolptr = nullptr;
+  c->erowidx = nullptr;
+  c->ecval = nullptr;
+  c->staged = false;
+  c->e_rows = 0;
+  return HB_OK;
+}
+
+size_t layer_elems(const hb_ctx* c, int l) { return static_cast<size_t>(c->d[l + 1]) * c->ldw[l]; }
+
+}  // namespace
+
+// ======================================================================
+extern "C" {
+
+const char* hb_last_error(void) { return g_err.c_str(); }
+
+const char* hb_version(void) {
+  return "hogbatch_b200 0.1 sm_100a tcgen05 kind::tf32 (3xTF32 / TF32), TMA SW128, CSR SpMM";
+}
+
+int hb_device_count(int* out) {
+  if (!out) return fail(HB_EINVAL, "null out");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) n = 0;
+  *out = n;
+  return HB_OK;
+}
+
+int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int max_batch, uint32_t flags) {
+  if (!out || !sizes) return fail(HB_EINVAL, "null argument");
+  *out = nullptr;
+  if (n_layers < 1) return fail(HB_EINVAL, "architecture needs at least input and output layers");
+  for (int i = 0; i <= n_layers; ++i)
+    if (sizes[i] < 1) return fail(HB_EINVAL, "layer sizes must be >= 1, got %d at %d", sizes[i], i);
+  if (sizes[n_layers] < 2) return fail(HB_EINVAL, "softmax output needs >= 2 classes");
+  if (max_batch < 1) return fail(HB_EINVAL, "max_batch must be >= 1");
+  if ((flags & HB_SPARSE_INPUT) && n_layers < 2)
+    return fail(HB_EINVAL, "sparse input needs at least one hidden layer");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(HB_ECUDA, "no CUDA device available");
+  if (device < 0 || device >= ndev) return fail(HB_EINVAL, "device %d out of range [0, %d)", device, ndev);
+  HB_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  HB_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(HB_ECUDA, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor);
+
+  hb_ctx* c = new hb_ctx();
+  c->device = device;
+  c->L = n_layers;
+  c->d.assign(sizes, sizes + n_layers + 1);
+  c->sparse = (flags & HB_SPARSE_INPUT) != 0;
+  c->passes = (flags & HB_PRECISION_TF32) ? 1 : 3;
+  c->max_batch = max_batch;
+  c->cap = static_cast<int>(round_up(max_batch, kBM));
+  const int L = c->L;
+  c->ld.resize(L + 1);
+  for (int l = 0; l <= L; ++l) c->ld[l] = round_up(c->d[l], 4);
+  const int nc = c->d[L], dlast = c->d[L - 1];
+  c->small_head = nc <= 4 && dlast <= 1024 && !(c->sparse && L == 1);
+  if (c->small_head) {
+    c->head_nct = nc <= 2 ? 2 : 4;
+    c->head_maxt = dlast <= 256 ? 8 : 32;
+  }
+  auto bail = [&](int code) {
+    hb_ctx_destroy(c);
+    return code;
+  };
+#define HB_CK(expr)                                                                                       \
+  do {                                                                                                    \
+    cudaError_t e_ = (expr);                                                                              \
+    if (e_ != cudaSuccess) return bail(fail(HB_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(e_))); \
+  } while (0)
+  HB_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  HB_CK(cudaEventCreate(&c->ev0));
+  HB_CK(cudaEventCreate(&c->ev1));
+  c->W.assign(L, nullptr);
+  c->G.assign(L, nullptr);
+  c->ldw.assign(L, 0);
+  c->A.assign(L + 1, nullptr);
+  c->D.assign(L, nullptr);
+  c->bn_fwd.assign(L, 128);
+  c->bn_dx.assign(L, 128);
+  c->bn_dw.assign(L, 128);
+  const int m_tiles = cdiv(c->cap, kBM);
+  size_t n_params = 0;
+  for (int l = 0; l < L; ++l) {
+    const bool tr = (l == 0 && c->sparse);
+    c->ldw[l] = tr ? c->ld[1] : c->ld[l];
+    const long long rows = tr ? c->d[0] : c->d[l + 1];
+    HB_CK(cudaMalloc(&c->W[l], rows * c->ldw[l] * sizeof(float)));
+    HB_CK(cudaMemset(c->W[l], 0, rows * c->ldw[l] * sizeof(float)));
+    HB_CK(cudaMalloc(&c->G[l], static_cast<size_t>(c->d[l + 1]) * c->d[l] * sizeof(float)));
+    HB_CK(cudaMalloc(&c->D[l], static_cast<size_t>(c->cap) * c->ld[l + 1] * sizeof(float)));
+    HB_CK(cudaMemset(c->D[l], 0, static_cast<size_t>(c->cap) * c->ld[l + 1] * sizeof(float)));
+    c->bn_fwd[l] = choose_bn(m_tiles, c->d[l + 1]);
+    c->bn_dx[l] = choose_bn(m_tiles, c->d[l]);
+    c->bn_dw[l] = choose_bn(cdiv(c->d[l + 1], kBM), c->d[l]);
+    n_params += static_cast<size_t>(c->d[l + 1]) * c->d[l];
+  }
+  c->n_params = n_params;
+  for (int l = 1; l < L; ++l) {
+    HB_CK(cudaMalloc(&c->A[l], static_cast<size_t>(c->cap) * c->ld[l] * sizeof(float)));
+    HB_CK(cudaMemset(c->A[l], 0, static_cast<size_t>(c->cap) * c->ld[l] * sizeof(float)));
+  }
+  // tensor maps
+  c->tmW_k.resize(L);
+  c->tmW_mn.resize(L);
+  c->tmA_k.resize(L + 1);
+  c->tmA_mn.resize(L + 1);
+  c->tmD_k.resize(L);
+  c->tmD_mn.resize(L);
+  int rc = HB_OK;
+  for (int l = 0; l < L && rc == HB_OK; ++l) {
+    if (!(l == 0 && c->sparse)) {
+      rc = make_map(&c->tmW_k[l], c->W[l], c->d[l], c->d[l + 1], c->ldw[l], c->bn_fwd[l], false);
+      if (rc == HB_OK) rc = make_map(&c->tmW_mn[l], c->W[l], c->d[l], c->d[l + 1], c->ldw[l], 32, true);
+    }
+    if (rc == HB_OK) rc = make_map(&c->tmD_k[l], c->D[l], c->d[l + 1], c->cap, c->ld[l + 1], 128, false);
+    if (rc == HB_OK) rc = make_map(&c->tmD_mn[l], c->D[l], c->d[l + 1], c->cap, c->ld[l + 1], 32, true);
+  }
+  for (int l = 1; l < L && rc == HB_OK; ++l) {
+    rc = make_map(&c->tmA_k[l], c->A[l], c->d[l], c->cap, c->ld[l], 128, false);
+    if (rc == HB_OK) rc = make_map(&c->tmA_mn[l], c->A[l], c->d[l], c->cap, c->ld[l], 32, true);
+  }
+  if (rc != HB_OK) return bail(rc);
+  // workspaces: split-K partial slabs and head partials
+  size_t ws = 0;
+  for (int l = 0; l < L; ++l) {
+    int splits, kb_per, kb_total;
+    dw_plan(c, l, c->cap, &splits, &kb_per, &kb_total);
+    if (splits > 1) ws = std::max(ws, static_cast<size_t>(splits) * c->d[l + 1] * c->d[l]);
+  }
+  if (c->small_head) ws = std::max(ws, static_cast<size_t>(cdiv(c->cap, kHeadRowsPerBlock)) * nc * dlast);
+  c->ws_floats = std::max<size_t>(ws, 1);
+  HB_CK(cudaMalloc(&c->ws, c->ws_floats * sizeof(float)));
+  c->ws_loss_n = std::max(cdiv(c->cap, kHeadRowsPerBlock), cdiv(c->cap, 8)) + 1;
+  HB_CK(cudaMalloc(&c->ws_loss, c->ws_loss_n * sizeof(double)));
+  HB_CK(cudaMalloc(&c->d_loss, sizeof(double)));
+  size_t maxw = 0;
+  for (int l = 0; l < L; ++l) maxw = std::max(maxw, static_cast<size_t>(c->d[l + 1]) * c->d[l]);
+  c->stage64_n = std::max<size_t>(maxw, size_t(4) << 20);
+  HB_CK(cudaMalloc(&c->stage64, c->stage64_n * sizeof(double)));
+  HB_CK(cudaMalloc(&c->stage32, maxw * sizeof(float)));
+  // batch slot for host-buffer steps
+  HB_CK(cudaMalloc(&c->blabels, static_cast<size_t>(c->cap) * sizeof(int64_t)));
+  if (c->sparse) {
+    HB_CK(cudaMalloc(&c->browptr, static_cast<size_t>(c->cap + 1) * sizeof(int64_t)));
+    HB_CK(cudaMalloc(&c->bcolptr, static_cast<size_t>(c->d[0] + 1) * sizeof(int64_t)));
+  } else {
+    HB_CK(cudaMalloc(&c->bx, static_cast<size_t>(c->cap) * c->ld[0] * sizeof(float)));
+    HB_CK(cudaMemset(c->bx, 0, static_cast<size_t>(c->cap) * c->ld[0] * sizeof(float)));
+    c->batch.x = c->bx;
+    c->batch.ldx = c->ld[0];
+    c->batch.n_rows = c->cap;
+    rc = build_data_maps(c, c->batch);
+    if (rc != HB_OK) return bail(rc);
+  }
+  c->batch.labels = c->blabels;
+#undef HB_CK
+  *out = c;
+  return HB_OK;
+}
+
+int hb_ctx_destroy(hb_ctx* c) {
+  if (!c) return HB_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  hb_comm_destroy(c);
+  for (auto p : c->W) cudaFree(p);
+  for (auto p : c->G) cudaFree(p);
+  for (auto p : c->A) cudaFree(p);
+  for (auto p : c->D) cudaFree(p);
+  free_epoch(c);
+  cudaFree(c->bx);
+  cudaFree(c->blabels);
+  cudaFree(c->browptr);
+  cudaFree(c->bcol);
+  cudaFree(c->bval);
+  cudaFree(c->bcolptr);
+  cudaFree(c->browidx);
+  cudaFree(c->bcval);
+  cudaFree(c->ws);
+  cudaFree(c->ws_loss);
+  cudaFree(c->d_loss);
+  cudaFree(c->stage64);
+  cudaFree(c->stage32);
+  cudaFree(c->flat);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  for (auto e : c->evpool) cudaEventDestroy(e);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return HB_OK;
+}
+
+int hb_set_weights_f64(hb_ctx* c, int layer, const double* w) {
+  HB_TRY(ctx_check(c));
+  if (layer < 0 || layer >= c->L || !w) return fail(HB_EINVAL, "bad layer %d or null weights", layer);
+  const int rows = c->d[layer + 1], cols = c->d[layer];
+  const size_t n = static_cast<size_t>(rows) * cols;
+  HB_CUDA(cudaMemcpyAsync(c->stage64, w, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 4096));
+  if (layer == 0 && c->sparse)
+    f64_to_f32_kernel<true><<<blocks, 256, 0, c->stream>>>(c->W[0], c->ldw[0], c->stage64, cols, rows, cols);
+  else
+    f64_to_f32_kernel<false><<<blocks, 256, 0, c->stream>>>(c->W[layer], c->ldw[layer], c->stage64, cols, rows, cols);
+  HB_CUDA(cudaGetLastError());
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  return HB_OK;
+}
+
+int hb_get_weights_f64(hb_ctx* c, int layer, double* w) {
+  HB_TRY(ctx_check(c));
+  if (layer < 0 || layer >= c->L || !w) return fail(HB_EINVAL, "bad layer %d or null output", layer);
+  const int rows = c->d[layer + 1], cols = c->d[layer];
+  const size_t n = static_cast<size_t>(rows) * cols;
+  const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 4096));
+  if (layer == 0 && c->sparse)
+    f32_to_f64_kernel<true><<<blocks, 256, 0, c->stream>>>(c->stage64, cols, c->W[0], c->ldw[0], rows, cols);
+  else
+    f32_to_f64_kernel<false><<<blocks, 256, 0, c->stream>>>(c->stage64, cols, c->W[layer], c->ldw[layer], rows, cols);
+  HB_CUDA(cudaGetLastError());
+  HB_CUDA(cudaMemcpyAsync(w, c->stage64, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  return HB_OK;
+}
+
+int hb_get_weights_f32(hb_ctx* c, int layer, float* w) {
+  HB_TRY(ctx_check(c));
+  if (layer < 0 || layer >= c->L || !w) return fail(HB_EINVAL, "bad layer %d or null output", layer);
+  const int rows = c->d[layer + 1], cols = c->d[layer];
+  if (layer == 0 && c->sparse) {
+    std::vector<double> tmp(static_cast<size_t>(rows) * cols);
+    HB_TRY(hb_get_weights_f64(c, layer, tmp.data()));
+    for (size_t i = 0; i < tmp.size(); ++i) w[i] = static_cast<float>(tmp[i]);
+    return HB_OK;
+  }
+  HB_CUDA(cudaMemcpy2DAsync(w, cols * sizeof(float), c->W[layer], c->ldw[layer] * sizeof(float), cols * sizeof(float),
+                            rows, cudaMemcpyDeviceToHost, c->stream));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  return HB_OK;
+}
+
+int hb_get_grad_f32(hb_ctx* c, int layer, float* g) {
+  HB_TRY(ctx_check(c));
+  if (layer < 0 || layer >= c->L || !g) return fail(HB_EINVAL, "bad layer %d or null output", layer);
+  if (!c->grads_valid) return fail(HB_ESTATE, "no gradient kept: run a step with HB_STEP_EMIT_GRAD first");
+  const int rows = c->d[layer + 1], cols = c->d[layer];
+  const size_t n = static_cast<size_t>(rows) * cols;
+  if (layer == 0 && c->sparse) {
+    // G[0] holds the transposed (d_in, d_out) gradient with row stride ldw[0]
+    std::vector<float> t(static_cast<size_t>(cols) * c->ldw[0]);
+    HB_CUDA(cudaMemcpyAsync(t.data(), c->G[0], t.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    HB_CUDA(cudaStreamSynchronize(c->stream));
+    for (int r = 0; r < rows; ++r)
+      for (int k = 0; k < cols; ++k) g[static_cast<size_t>(r) * cols + k] = t[static_cast<size_t>(k) * c->ldw[0] + r];
+    return HB_OK;
+  }
+  HB_CUDA(cudaMemcpyAsync(g, c->G[layer], n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  return HB_OK;
+}
+
+int hb_merge_grad_into_f64(hb_ctx* c, int layer, double* host_w, double eta) {
+  HB_TRY(ctx_check(c));
+  if (layer < 0 || layer >= c->L || !host_w) return fail(HB_EINVAL, "bad layer %d or null weights", layer);
+  const int rows = c->d[layer + 1], cols = c->d[layer];
+  const size_t n = static_cast<size_t>(rows) * cols;
+  HB_TRY(ensure_pinned(c, n * sizeof(float) + (layer == 0 && c->sparse ? n * sizeof(float) : 0)));
+  float* g = static_cast<float*>(c->pinned);
+  HB_TRY(hb_get_grad_f32(c, layer, g));
+  // linalg.py:79 np.add(target, scale*source, out=target), scale = -eta
+  const double scale = -eta;
+  for (size_t i = 0; i < n; ++i) host_w[i] += scale * static_cast<double>(g[i]);
+  return HB_OK;
+}
+
+static int stage_dense_common(hb_ctx* c, int64_t n_rows, const int64_t* labels) {
+  if (c->sparse) return fail(HB_EINVAL, "context was created for sparse (CSR) input");
+  if (n_rows < 1 || !labels) return fail(HB_EINVAL, "need n_rows >= 1 and labels");
+  HB_TRY(free_epoch(c));
+  HB_CUDA(cudaMalloc(&c->ex, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
+  HB_CUDA(cudaMalloc(&c->elabels, static_cast<size_t>(n_rows) * sizeof(int64_t)));
+  HB_CUDA(cudaMemcpyAsync(c->elabels, labels, n_rows * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+  c->e_rows = n_rows;
+  return HB_OK;
+}
+
+static int finish_dense_stage(hb_ctx* c) {
+  c->epoch = DataView();
+  c->epoch.x = c->ex;
+  c->epoch.ldx = c->ld[0];
+  c->epoch.n_rows = c->e_rows;
+  c->epoch.labels = c->elabels;
+  HB_TRY(build_data_maps(c, c->epoch));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  c->staged = true;
+  return HB_OK;
+}
+
+int hb_stage_dense_f64(hb_ctx* c, const double* x, int64_t n_rows, int64_t ld, const int64_t* labels) {
+  HB_TRY(ctx_check(c));
+  if (!x || ld < c->d[0]) return fail(HB_EINVAL, "null features or ld < %d", c->d[0]);
+  HB_TRY(stage_dense_common(c, n_rows, labels));
+  // chunked H2D of float64 rows through the f64 staging buffer, converted on device
+  const long long chunk = std::max<long long>(1, static_cast<long long>(c->stage64_n) / ld);
+  for (long long r0 = 0; r0 < n_rows; r0 += chunk) {
+    const long long nr = std::min<long long>(chunk, n_rows - r0);
+    HB_CUDA(cudaMemcpyAsync(c->stage64, x + r0 * ld, nr * ld * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    const long long n = nr * c->d[0];
+    f64_to_f32_kernel<false><<<static_cast<int>(std::min<long long>((n + 255) / 256, 4096)), 256, 0, c->stream>>>(
+        c->ex + r0 * c->ld[0], c->ld[0], c->stage64, ld, static_cast<int>(nr), c->d[0]);
+    HB_CUDA(cudaGetLastError());
+    HB_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  return finish_dense_stage(c);
+}
+
+int hb_stage_dense_f32(hb_ctx* c, const float* x, int64_t n_rows, int64_t ld, const int64_t* labels) {
+  HB_TRY(ctx_check(c));
+  if (!x || ld < c->d[0]) return fail(HB_EINVAL, "null features or ld < %d", c->d[0]);
+  HB_TRY(stage_dense_common(c, n_rows, labels));
+  HB_CUDA(cudaMemcpy2DAsync(c->ex, c->ld[0] * sizeof(float), x, ld * sizeof(float), c->d[0] * sizeof(float), n_rows,
+                            cudaMemcpyHostToDevice, c->stream));
+  return finish_dense_stage(c);
+}
+
+int hb_stage_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n_rows,
+                 const int64_t* labels) {
+  HB_TRY(ctx_check(c));
+  if (!c->sparse) return fail(HB_EINVAL, "context was created for dense input");
+  if (!rowptr || !labels || n_rows < 1) return fail(HB_EINVAL, "null CSR arrays or n_rows < 1");
+  if (rowptr[0] != 0) return fail(HB_EINVAL, "rowptr[0] must be 0");
+  const long long nnz = rowptr[n_rows];
+  for (long long r = 0; r < n_rows; ++r)
+    if (rowptr[r + 1] < rowptr[r]) return fail(HB_EINVAL, "rowptr not non-decreasing at row %lld", r);
+  for (long long e = 0; e < nnz; ++e)
+    if (col[e] < 0 || col[e] >= c->d[0])
+      return fail(HB_EINVAL, "feature index %d outside [0, %d) at nnz %lld", col[e], c->d[0], e);
+  HB_TRY(free_epoch(c));
+  std::vector<int64_t> colptr;
+  std::vector<int32_t> rowidx;
+  std::vector<float> cval;
+  build_csc(rowptr, col, val, n_rows, c->d[0], colptr, rowidx, cval, 0);
+  const size_t nz = std::max<long long>(nnz, 1);
+  HB_CUDA(cudaMalloc(&c->erowptr, (n_rows + 1) * sizeof(int64_t)));
+  HB_CUDA(cudaMalloc(&c->ecol, nz * sizeof(int32_t)));
+  HB_CUDA(cudaMalloc(&c->eval_, nz * sizeof(float)));
+  HB_CUDA(cudaMalloc(&c->ecolptr, (c->d[0] + 1) * sizeof(int64_t)));
+  HB_CUDA(cudaMalloc(&c->erowidx, nz * sizeof(int32_t)));
+  HB_CUDA(cudaMalloc(&c->ecval, nz * sizeof(float)));
+  HB_CUDA(cudaMalloc(&c->elabels, n_rows * sizeof(int64_t)));
+  HB_CUDA(cudaMemcpy(c->erowptr, rowptr, (n_rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  if (nnz > 0) {
+    HB_CUDA(cudaMemcpy(c->ecol, col, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
+    HB_CUDA(cudaMemcpy(c->eval_, val, nnz * sizeof(float), cudaMemcpyHostToDevice));
+    HB_CUDA(cudaMemcpy(c->erowidx, rowidx.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
+    HB_CUDA(cudaMemcpy(c->ecval, cval.data(), nnz * sizeof(float), cudaMemcpyHostToDevice));
+  }
+  HB_CUDA(cudaMemcpy(c->ecolptr, colptr.data(), (c->d[0] + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  HB_CUDA(cudaMemcpy(c->elabels, labels, n_rows * sizeof(int64_t), cudaMemcpyHostToDevice));
+  c->e_rows = n_rows;
+  c->e_nnz = nnz;
+  c->epoch = DataView();
+  c->epoch.rowptr = c->erowptr;
+  c->epoch.col = c->ecol;
+  c->epoch.val = c->eval_;
+  c->epoch.colptr = c->ecolptr;
+  c->epoch.rowidx = c->erowidx;
+  c->epoch.cval = c->ecval;
+  c->epoch.labels = c->elabels;
+  c->epoch.n_rows = n_rows;
+  c->staged = true;
+  return HB_OK;
+}
+
+int64_t hb_staged_rows(hb_ctx* c) { return c ? c->e_rows : 0; }
+
+static int check_labels(const int64_t* y, long long n, int nc) {
+  for (long long i = 0; i < n; ++i)
+    if (y[i] < 0 || y[i] >= nc) return fail(HB_EINVAL, "labels must lie in [0, %d), got %lld", nc, (long long)y[i]);
+  return HB_OK;
+}
+
+int hb_train_step(hb_ctx* c, int64_t start, int rows, double eta, uint32_t flags, double* out_loss) {
+  HB_TRY(ctx_check(c));
+  if (!c->staged) return fail(HB_ESTATE, "no data staged");
+  if (start < 0 || rows < 1 || start + rows > c->e_rows)
+    return fail(HB_EINVAL, "batch range [%lld, %lld) out of bounds for %lld rows", (long long)start,
+                (long long)(start + rows), (long long)c->e_rows);
+  return do_step(c, c->epoch, start, rows, eta, flags, out_loss);
+}
+
+int hb_train_step_host_dense(hb_ctx* c, const float* x, int64_t ld, const int64_t* labels, int rows, double eta,
+                             uint32_t flags, double* out_loss) {
+  HB_TRY(ctx_check(c));
+  if (c->sparse) return fail(HB_EINVAL, "context was created for sparse (CSR) input");
+  if (!x || !labels || ld < c->d[0]) return fail(HB_EINVAL, "null batch or ld < %d", c->d[0]);
+  if (rows < 1 || rows > c->max_batch) return fail(HB_EINVAL, "rows=%d outside [1, %d]", rows, c->max_batch);
+  HB_TRY(check_labels(labels, rows, c->d[c->L]));
+  HB_CUDA(cudaMemcpy2DAsync(c->bx, c->ld[0] * sizeof(float), x, ld * sizeof(float), c->d[0] * sizeof(float), rows,
+                            cudaMemcpyHostToDevice, c->stream));
+  HB_CUDA(cudaMemcpyAsync(c->blabels, labels, rows * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+  return do_step(c, c->batch, 0, rows, eta, flags, out_loss);
+}
+
+int hb_train_step_host_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col, const float* val,
+                           const int64_t* labels, int rows, double eta, uint32_t flags, double* out_loss) {
+  HB_TRY(ctx_check(c));
+  if (!c->sparse) return fail(HB_EINVAL, "context was created for dense input");
+  if (!rowptr || !labels) return fail(HB_EINVAL, "null batch");
+  if (rows < 1 || rows > c->max_batch) return fail(HB_EINVAL, "rows=%d outside [1, %d]", rows, c->max_batch);
+  if (rowptr[0] != 0) return fail(HB_EINVAL, "rowptr[0] must be 0");
+  HB_TRY(check_labels(labels, rows, c->d[c->L]));
+  const long long nnz = rowptr[rows];
+  for (long long e = 0; e < nnz; ++e)
+    if (col[e] < 0 || col[e] >= c->d[0]) return fail(HB_EINVAL, "feature index %d outside [0, %d)", col[e], c->d[0]);
+  if (nnz > c->b_nnz_cap) {
+    cudaFree(c->bcol);
+    cudaFree(c->bval);
+    cudaFree(c->browidx);
+    cudaFree(c->bcval);
+    const long long cap = std::max<long long>(nnz, 1) * 3 / 2 + 64;
+    HB_CUDA(cudaMalloc(&c->bcol, cap * sizeof(int32_t)));
+    HB_CUDA(cudaMalloc(&c->bval, cap * sizeof(float)));
+    HB_CUDA(cudaMalloc(&c->browidx, cap * sizeof(int32_t)));
+    HB_CUDA(cudaMalloc(&c->bcval, cap * sizeof(float)));
+    c->b_nnz_cap = cap;
+  }
+  build_csc(rowptr, col, val, rows, c->d[0], c->h_colptr, c->h_rowidx, c->h_cval, 0);
+  // one pinned buffer carries the whole batch: rowptr | colptr | labels | col | rowidx | val | cval
+  const size_t b_rowptr = (rows + 1) * sizeof(int64_t), b_colptr = (c->d[0] + 1) * sizeof(int64_t),
+               b_lab = rows * sizeof(int64_t), b_i32 = nnz * sizeof(int32_t), b_f32 = nnz * sizeof(float);
+  HB_TRY(ensure_pinned(c, b_rowptr + b_colptr + b_lab + 2 * b_i32 + 2 * b_f32 + 64));
+  char* p = static_cast<char*>(c->pinned);
+  std::memcpy(p, rowptr, b_rowptr);
+  std::memcpy(p + b_rowptr, c->h_colptr.data(), b_colptr);
+  std::memcpy(p + b_rowptr + b_colptr, labels, b_lab);
+  char* q = p + b_rowptr + b_colptr + b_lab;
+  std::memcpy(q, col, b_i32);
+  std::memcpy(q + b_i32, c->h_rowidx.data(), b_i32);
+  std::memcpy(q + 2 * b_i32, val, b_f32);
+  std::memcpy(q + 2 * b_i32 + b_f32, c->h_cval.data(), b_f32);
+  cudaStream_t st = c->stream;
+  HB_CUDA(cudaMemcpyAsync(c->browptr, p, b_rowptr, cudaMemcpyHostToDevice, st));
+  HB_CUDA(cudaMemcpyAsync(c->bcolptr, p + b_rowptr, b_colptr, cudaMemcpyHostToDevice, st));
+  HB_CUDA(cudaMemcpyAsync(c->blabels, p + b_rowptr + b_colptr, b_lab, cudaMemcpyHostToDevice, st));
+  if (nnz > 0) {
+    HB_CUDA(cudaMemcpyAsync(c->bcol, q, b_i32, cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemcpyAsync(c->browidx, q + b_i32, b_i32, cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemcpyAsync(c->bval, q + 2 * b_i32, b_f32, cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemcpyAsync(c->bcval, q + 2 * b_i32 + b_f32, b_f32, cudaMemcpyHostToDevice, st));
+  }
+  DataView v;
+  v.rowptr = c->browptr;
+  v.col = c->bcol;
+  v.val = c->bval;
+  v.colptr = c->bcolptr;
+  v.rowidx = c->browidx;
+  v.cval = c->bcval;
+  v.labels = c->blabels;
+  v.n_rows = rows;
+  return do_step(c, v, 0, rows, eta, flags, out_loss);
+}
+
+int hb_forward(hb_ctx* c, int64_t start, int rows) {
+  HB_TRY(ctx_check(c));
+  if (!c->staged) return fail(HB_ESTATE, "no data staged");
+  if (start < 0 || rows < 1 || rows > c->max_batch || start + rows > c->e_rows)
+    return fail(HB_EINVAL, "batch range out of bounds");
+  c->last_launches = 0;
+  HB_TRY(run_forward(c, c->epoch, start, rows, false, 0, 0.0));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  return HB_OK;
+}
+
+int hb_get_activation_f32(hb_ctx* c, int layer, int rows, float* out) {
+  HB_TRY(ctx_check(c));
+  if (layer < 1 || layer >= c->L || !out || rows < 1 || rows > c->cap)
+    return fail(HB_EINVAL, "activation layer must be in [1, %d)", c->L);
+  HB_CUDA(cudaMemcpy2DAsync(out, c->d[layer] * sizeof(float), c->A[layer], c->ld[layer] * sizeof(float),
+                            c->d[layer] * sizeof(float), rows, cudaMemcpyDeviceToHost, c->stream));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  return HB_OK;
+}
+
+int hb_eval_loss_sum(hb_ctx* c, int64_t start, int64_t rows, double* out_sum) {
+  HB_TRY(ctx_check(c));
+  if (!out_sum) return fail(HB_EINVAL, "null output");
+  if (!c->staged) return fail(HB_ESTATE, "no data staged");
+  if (start < 0 || rows < 1 || start + rows > c->e_rows) return fail(HB_EINVAL, "eval range out of bounds");
+  double total = 0.0;
+  for (long long s = start; s < start + rows; s += c->max_batch) {
+    const int n = static_cast<int>(std::min<long long>(c->max_batch, start + rows - s));
+    HB_TRY(run_forward(c, c->epoch, s, n, false, 0, 0.0));
+    double part = 0.0;
+    HB_CUDA(cudaMemcpyAsync(&part, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    HB_CUDA(cudaStreamSynchronize(c->stream));
+    total += part;
+  }
+  *out_sum = total;
+  return HB_OK;
+}
+
+int hb_last_step_ms(hb_ctx* c, float* ms) {
+  if (!c || !ms) return fail(HB_EINVAL, "null argument");
+  *ms = c->last_ms;
+  return HB_OK;
+}
+
+int hb_last_step_launches(hb_ctx* c, int* n) {
+  if (!c || !n) return fail(HB_EINVAL, "null argument");
+  *n = c->last_launches;
+  return HB_OK;
+}
+
+int hb_profile_enable(hb_ctx* c, int on) {
+  HB_TRY(ctx_check(c));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  c->prof_on = on != 0;
+  c->ev_used = 0;
+  c->marks.clear();
+  return HB_OK;
+}
+
+int hb_profile_read(hb_ctx* c, int max_entries, char* names, double* total_ms, int* counts, int* n_out) {
+  HB_TRY(ctx_check(c));
+  if (!n_out) return fail(HB_EINVAL, "null n_out");
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<std::string> keys;
+  std::vector<double> tot;
+  std::vector<int> cnt;
+  for (auto& m : c->marks) {
+    float ms = 0.f;
+    HB_CUDA(cudaEventElapsedTime(&ms, c->evpool[m.second], c->evpool[m.second + 1]));
+    size_t k = 0;
+    while (k < keys.size() && keys[k] != m.first) ++k;
+    if (k == keys.size()) {
+      keys.push_back(m.first);
+      tot.push_back(0.0);
+      cnt.push_back(0);
+    }
+    tot[k] += ms;
+    cnt[k] += 1;
+  }
+  const int n = static_cast<int>(std::min<size_t>(keys.size(), static_cast<size_t>(std::max(max_entries, 0))));
+  for (int i = 0; i < n; ++i) {
+    if (names) {
+      std::memset(names + 64 * i, 0, 64);
+      std::strncpy(names + 64 * i, keys[i].c_str(), 63);
+    }
+    if (total_ms) total_ms[i] = tot[i];
+    if (counts) counts[i] = cnt[i];
+  }
+  *n_out = n;
+  c->ev_used = 0;
+  c->marks.clear();
+  return HB_OK;
+}
+
+int hb_synchronize(hb_ctx* c) {
+  HB_TRY(ctx_check(c));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  return HB_OK;
+}
+
+int hb_nccl_unique_id(void* out) {
+  if (!out) return fail(HB_EINVAL, "null output");
+  HB_TRY(load_nccl());
+  nccl_uid_t id;
+  int r = g_nccl.getUniqueId(&id);
+  if (r != 0) return fail(HB_ENCCL, "ncclGetUniqueId: %s", g_nccl.errStr ? g_nccl.errStr(r) : "error");
+  std::memcpy(out, &id, sizeof id);
+  return HB_OK;
+}
+
+int hb_comm_init(hb_ctx* c, const void* id_bytes, int nranks, int rank) {
+  HB_TRY(ctx_check(c));
+  if (!id_bytes || nranks < 1 || rank < 0 || rank >= nranks) return fail(HB_EINVAL, "bad communicator arguments");
+  HB_TRY(load_nccl());
+  nccl_uid_t id;
+  std::memcpy(&id, id_bytes, sizeof id);
+  nccl_comm_t comm = nullptr;
+  int r = g_nccl.commInitRank(&comm, nranks, id, rank);
+  if (r != 0) return fail(HB_ENCCL, "ncclCommInitRank: %s", g_nccl.errStr ? g_nccl.errStr(r) : "error");
+  c->comm = comm;
+  c->nranks = nranks;
+  if (!c->flat) HB_CUDA(cudaMalloc(&c->flat, c->n_params * sizeof(float)));
+  return HB_OK;
+}
+
+int hb_merge_allreduce(hb_ctx* c) {
+  HB_TRY(ctx_check(c));
+  if (!c->comm) return fail(HB_ESTATE, "communicator not initialised");
+  // pack (W_l rows are padded) -> allreduce(sum) -> unpack scaled by 1/nranks
+  size_t off = 0;
+  for (int l = 0; l < c->L; ++l) {
+    const bool tr = l == 0 && c->sparse;
+    const long long rows = tr ? c->d[0] : c->d[l + 1], cols = tr ? c->d[1] : c->d[l];
+    HB_CUDA(cudaMemcpy2DAsync(c->flat + off, cols * sizeof(float), c->W[l], c->ldw[l] * sizeof(float),
+                              cols * sizeof(float), rows, cudaMemcpyDeviceToDevice, c->stream));
+    off += rows * cols;
+  }
+  int r = g_nccl.allReduce(c->flat, c->flat, c->n_params, kNcclFloat32, kNcclSum, c->comm, c->stream);
+  if (r != 0) return fail(HB_ENCCL, "ncclAllReduce: %s", g_nccl.errStr ? g_nccl.errStr(r) : "error");
+  off = 0;
+  const float inv = 1.0f / static_cast<float>(c->nranks);
+  for (int l = 0; l < c->L; ++l) {
+    const bool tr = l == 0 && c->sparse;
+    const long long rows = tr ? c->d[0] : c->d[l + 1], cols = tr ? c->d[1] : c->d[l];
+    unpack_scale_kernel<<<static_cast<int>(std::min<long long>(cdiv(rows * cols, 256), 4096)), 256, 0, c->stream>>>(
+        c->W[l], c->ldw[l], c->flat + off, static_cast<int>(rows), static_cast<int>(cols), inv);
+    HB_CUDA(cudaGetLastError());
+    off += rows * cols;
+  }
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  return HB_OK;
+}
+
+int hb_comm_destroy(hb_ctx* c) {
+  if (!c || !c->comm) return HB_OK;
+  if (g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+  c->comm = nullptr;
+  return HB_OK;
+}
+
+}  // extern "C"

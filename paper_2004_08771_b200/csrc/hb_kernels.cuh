@@ -1,0 +1,478 @@
+// hb_kernels.cuh -- the non-GEMM kernels of the Hogbatch replica step:
+// the fused small softmax/cross-entropy head, the wide-head softmax->delta
+// pass, deterministic SGD reductions, the CSR-gather SpMM first layer and
+// its sparse dW + update, precision conversion for the host exchange.
+//
+// Every reduction here runs in a fixed order (no float atomics), so a step is
+// bit-reproducible run to run.
+#pragma once
+#include <cstdint>
+
+#include "hb_ptx.cuh"
+
+namespace hb {
+
+constexpr float kProbFloor = 1e-12f;  // nn.py:26
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// ------------------------------------------------------------------------
+// Fused small head (classes <= NCT, hidden width d <= 32*MAXT):
+//   z = a . W^T, p = softmax(z)                               (nn.py:118-119)
+//   loss_i = -log max(p_y, 1e-12)                              (nn.py:124-136)
+//   delta = (p - onehot(y)) / n                                (nn.py:162-164)
+//   delta_prev = (delta . W) * a (1 - a)                       (nn.py:170)
+//   dW partial per block = sum_rows delta^T a                  (nn.py:168)
+// One warp per row; lanes own columns j = lane + 32 t (coalesced).  A block
+// owns HEAD_ROWS_PER_BLOCK consecutive rows and reduces its 8 warps' dW
+// partials in warp order, so the result is deterministic.
+constexpr int kHeadWarps = 8;
+constexpr int kHeadRowsPerBlock = 32;
+
+struct HeadArgs {
+  const float* a;          // (rows, d) last hidden activation
+  long long lda;
+  const float* w;          // (nc, d) output weights
+  long long ldw;
+  const int64_t* labels;   // already offset to the batch start
+  int rows, d, nc;
+  int zero_rows;           // delta_prev rows [rows, zero_rows) are zeroed
+  float inv_n;             // 1 / batch size
+  int train;               // 0 = loss only (evaluation)
+  float* delta_prev;       // (zero_rows, d) or null
+  long long ld_dp;
+  float* delta_out;        // (rows, nc) or null (tests)
+  long long ld_do;
+  float* ws_dw;            // [grid][nc][d] partials
+  double* ws_loss;         // [grid] per-block loss sums
+};
+
+template <int NCT, int MAXT>
+__global__ void __launch_bounds__(kHeadWarps * 32) head_small_kernel(const HeadArgs p) {
+  __shared__ float sW[NCT * 32 * MAXT];
+  __shared__ double sLoss[kHeadWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = (p.d + 31) / 32;
+  for (int i = threadIdx.x; i < NCT * 32 * MAXT; i += blockDim.x) {
+    const int c = i / (32 * MAXT), j = i % (32 * MAXT);
+    sW[i] = (c < p.nc && j < p.d) ? p.w[c * p.ldw + j] : 0.f;
+  }
+  __syncthreads();
+
+  float acc[NCT][MAXT];
+#pragma unroll
+  for (int c = 0; c < NCT; ++c)
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) acc[c][t] = 0.f;
+  double loss = 0.0;
+
+  const int row0 = blockIdx.x * kHeadRowsPerBlock;
+  for (int rr = warp; rr < kHeadRowsPerBlock; rr += kHeadWarps) {
+    const int row = row0 + rr;
+    if (row >= p.rows) {
+      if (p.train && p.delta_prev != nullptr && row < p.zero_rows) {
+        for (int t = 0; t < T; ++t) {
+          const int j = lane + 32 * t;
+          if (j < p.d) p.delta_prev[row * p.ld_dp + j] = 0.f;
+        }
+      }
+      continue;
+    }
+    float av[MAXT];
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) {
+      const int j = lane + 32 * t;
+      av[t] = (t < T && j < p.d) ? p.a[row * p.lda + j] : 0.f;
+    }
+    float z[NCT];
+#pragma unroll
+    for (int c = 0; c < NCT; ++c) {
+      float s = 0.f;
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t) s = fmaf(av[t], sW[c * 32 * MAXT + lane + 32 * t], s);
+      z[c] = warp_sum(s);
+    }
+    float zmax = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < NCT; ++c)
+      if (c < p.nc) zmax = fmaxf(zmax, z[c]);
+    float e[NCT], esum = 0.f;
+#pragma unroll
+    for (int c = 0; c < NCT; ++c) {
+      e[c] = c < p.nc ? expf(z[c] - zmax) : 0.f;
+      esum += e[c];
+    }
+    const int y = static_cast<int>(p.labels[row]);
+    float py = 0.f;
+#pragma unroll
+    for (int c = 0; c < NCT; ++c)
+      if (c == y) py = e[c] / esum;
+    loss += -log(fmax(static_cast<double>(py), 1e-12));
+    if (!p.train) continue;
+    float dl[NCT];
+#pragma unroll
+    for (int c = 0; c < NCT; ++c) dl[c] = c < p.nc ? (e[c] / esum - (c == y ? 1.f : 0.f)) * p.inv_n : 0.f;
+    if (p.delta_out != nullptr && lane < p.nc) {
+#pragma unroll
+      for (int c = 0; c < NCT; ++c)
+        if (c == lane) p.delta_out[row * p.ld_do + c] = dl[c];
+    }
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) {
+      const int j = lane + 32 * t;
+      float g = 0.f;
+#pragma unroll
+      for (int c = 0; c < NCT; ++c) {
+        g = fmaf(dl[c], sW[c * 32 * MAXT + j], g);
+        acc[c][t] = fmaf(dl[c], av[t], acc[c][t]);
+      }
+      if (p.delta_prev != nullptr && t < T && j < p.d) p.delta_prev[row * p.ld_dp + j] = g * (av[t] * (1.f - av[t]));
+    }
+  }
+
+  // deterministic block reduction of the loss
+  if (lane == 0) sLoss[warp] = loss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kHeadWarps; ++w) s += sLoss[w];
+    p.ws_loss[blockIdx.x] = s;
+  }
+  if (!p.train) return;
+  // deterministic block reduction of the dW partials, one class at a time:
+  // warps add into a shared row in warp order (sW is free after the row loop).
+  for (int c = 0; c < NCT && c < p.nc; ++c) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < 32 * MAXT; j += blockDim.x) sW[j] = 0.f;
+    __syncthreads();
+    for (int w = 0; w < kHeadWarps; ++w) {
+      if (warp == w) {
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) {
+          const int j = lane + 32 * t;
+          if (t < T && j < p.d) sW[j] += acc[c][t];
+        }
+      }
+      __syncthreads();
+    }
+    for (int j = threadIdx.x; j < p.d; j += blockDim.x)
+      p.ws_dw[(static_cast<long long>(blockIdx.x) * p.nc + c) * p.d + j] = sW[j];
+  }
+}
+
+// ------------------------------------------------------------------------
+// Wide head second pass: logits (rows, nc) -> delta in place + per-row loss.
+// One warp per row, row max shift as linalg.py:63-67.
+struct SoftmaxArgs {
+  float* z;  // (zero_rows, nc) logits in, delta out
+  long long ldz;
+  const int64_t* labels;
+  int rows, nc, zero_rows;
+  float inv_n;
+  int train;
+  double* ws_loss;  // [grid]
+};
+
+__global__ void __launch_bounds__(256) softmax_delta_kernel(const SoftmaxArgs p) {
+  __shared__ double sLoss[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + warp;
+  double loss = 0.0;
+  if (row < p.rows) {
+    float* zr = p.z + row * p.ldz;
+    float m = -INFINITY;
+    for (int j = lane; j < p.nc; j += 32) m = fmaxf(m, zr[j]);
+    m = warp_max(m);
+    float s = 0.f;
+    for (int j = lane; j < p.nc; j += 32) s += expf(zr[j] - m);
+    s = warp_sum(s);
+    const int y = static_cast<int>(p.labels[row]);
+    if (lane == 0) {
+      const float py = expf(zr[y] - m) / s;
+      loss = -log(fmax(static_cast<double>(py), 1e-12));
+    }
+    if (p.train) {
+      __syncwarp();
+      for (int j = lane; j < p.nc; j += 32) {
+        const float pj = expf(zr[j] - m) / s;
+        zr[j] = (pj - (j == y ? 1.f : 0.f)) * p.inv_n;
+      }
+    }
+  } else if (p.train && row < p.zero_rows) {
+    for (int j = lane; j < p.nc; j += 32) p.z[row * p.ldz + j] = 0.f;
+  }
+  if (lane == 0) sLoss[warp] = loss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += sLoss[w];
+    p.ws_loss[blockIdx.x] = t;
+  }
+}
+
+// Fixed-order sum of per-block loss partials (one thread; tiny).
+__global__ void loss_reduce_kernel(const double* ws, int n, double* out, int accumulate) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += ws[i];
+    *out = accumulate ? *out + s : s;
+  }
+}
+
+// ------------------------------------------------------------------------
+// W (rows, cols, ldw) -= eta * sum_{s<S} P[s] (rows, cols, dense), in place.
+// The split-K / per-block partials are summed in slab order -> deterministic.
+__global__ void __launch_bounds__(256) reduce_sgd_kernel(float* w, long long ldw, const float* part, int S,
+                                                           long long slab, int rows, int cols, float eta,
+                                                           float* grad, long long ldg) {
+  const long long total = static_cast<long long>(rows) * cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / cols), c = static_cast<int>(i % cols);
+    float g = 0.f;
+    for (int s = 0; s < S; ++s) g += part[s * slab + i];
+    w[r * ldw + c] -= eta * g;
+    if (grad != nullptr) grad[r * ldg + c] = g;
+  }
+}
+
+// ------------------------------------------------------------------------
+// CSR-gather SpMM first layer: A1[i, :] = sigmoid(sum_k val_k * W0T[col_k, :])
+// for batch rows i in [0, rows) of the staged CSR starting at row `start`.
+// W0 is held transposed, (d_in, d_out) row-major, so each nonzero gathers one
+// contiguous d_out-long row.  One warp per example row; VEC = float4 columns.
+struct SpmmArgs {
+  const int64_t* rowptr;  // epoch CSR row pointer (n_rows + 1)
+  const int32_t* col;
+  const float* val;
+  long long start;
+  int rows;
+  const float* w0t;  // (d_in, d_out)
+  long long ldw;
+  int d_out;
+  float* out;  // (rows, d_out)
+  long long ldo;
+};
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) spmm_sigmoid_kernel(const SpmmArgs p) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= p.rows) return;
+  const long long r = p.start + warp;
+  const long long e0 = p.rowptr[r], e1 = p.rowptr[r + 1];
+  float* o = p.out + warp * p.ldo;
+  if (VEC) {
+    // d_out % 128 == 0: lane owns float4 columns 4*lane + 128*t
+    for (int base = 0; base < p.d_out; base += 128 * 8) {
+      float4 acc[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (long long e = e0; e < e1; ++e) {
+        const float v = __ldg(p.val + e);
+        const float4* wr = reinterpret_cast<const float4*>(p.w0t + static_cast<long long>(__ldg(p.col + e)) * p.ldw);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int j = base + 4 * lane + 128 * t;
+          if (j < p.d_out) {
+            const float4 w = __ldg(wr + j / 4);
+            acc[t].x = fmaf(v, w.x, acc[t].x);
+            acc[t].y = fmaf(v, w.y, acc[t].y);
+            acc[t].z = fmaf(v, w.z, acc[t].z);
+            acc[t].w = fmaf(v, w.w, acc[t].w);
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int j = base + 4 * lane + 128 * t;
+        if (j < p.d_out)
+          reinterpret_cast<float4*>(o)[j / 4] = make_float4(sigmoidf_stable(acc[t].x), sigmoidf_stable(acc[t].y),
+                                                            sigmoidf_stable(acc[t].z), sigmoidf_stable(acc[t].w));
+      }
+    }
+  } else {
+    for (int base = 0; base < p.d_out; base += 32 * 8) {
+      float acc[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc[t] = 0.f;
+      for (long long e = e0; e < e1; ++e) {
+        const float v = __ldg(p.val + e);
+        const float* wr = p.w0t + static_cast<long long>(__ldg(p.col + e)) * p.ldw;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int j = base + lane + 32 * t;
+          if (j < p.d_out) acc[t] = fmaf(v, __ldg(wr + j), acc[t]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int j = base + lane + 32 * t;
+        if (j < p.d_out) o[j] = sigmoidf_stable(acc[t]);
+      }
+    }
+  }
+}
+
+// Sparse dW0 + fused SGD update on the active feature rows only:
+//   W0T[f, :] -= eta * sum_{i in batch, x_if != 0} x_if * delta0[i, :]
+// using the epoch CSC (column pointer, ascending row index within a column).
+// The batch [start, start+rows) is a contiguous row range of the epoch
+// (engine.py:298-299), so its entries in column f are one contiguous slice
+// found by binary search -- no per-batch transpose, fixed summation order.
+struct SparseDwArgs {
+  const int64_t* colptr;  // (d_in + 1)
+  const int32_t* rowidx;  // ascending within each column (epoch row ids)
+  const float* cval;
+  long long start;
+  int rows;
+  int d_in, d_out;
+  const float* delta0;  // (rows, d_out)
+  long long ldd;
+  float* w0t;  // (d_in, d_out), updated in place
+  long long ldw;
+  float eta;
+  float* grad;  // optional (d_in, d_out) raw gradient (transposed layout)
+  long long ldg;
+};
+
+__device__ __forceinline__ long long lower_bound_i32(const int32_t* a, long long lo, long long hi, long long key) {
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (static_cast<long long>(a[mid]) < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) sparse_dw_kernel(const SparseDwArgs p) {
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (f >= p.d_in) return;
+  const long long c0 = p.colptr[f], c1 = p.colptr[f + 1];
+  long long lo = 0, hi = 0;
+  if (lane == 0) {
+    lo = lower_bound_i32(p.rowidx, c0, c1, p.start);
+    hi = lower_bound_i32(p.rowidx, lo, c1, p.start + p.rows);
+  }
+  lo = __shfl_sync(0xffffffffu, lo, 0);
+  hi = __shfl_sync(0xffffffffu, hi, 0);
+  float* wrow = p.w0t + static_cast<long long>(f) * p.ldw;
+  float* grow = p.grad != nullptr ? p.grad + static_cast<long long>(f) * p.ldg : nullptr;
+  if (lo == hi) {
+    if (grow != nullptr)
+      for (int j = lane; j < p.d_out; j += 32) grow[j] = 0.f;
+    return;
+  }
+  if (VEC) {
+    for (int base = 0; base < p.d_out; base += 128 * 8) {
+      float4 acc[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (long long e = lo; e < hi; ++e) {
+        const float v = __ldg(p.cval + e);
+        const float4* dr =
+            reinterpret_cast<const float4*>(p.delta0 + (static_cast<long long>(__ldg(p.rowidx + e)) - p.start) * p.ldd);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int j = base + 4 * lane + 128 * t;
+          if (j < p.d_out) {
+            const float4 d = __ldg(dr + j / 4);
+            acc[t].x = fmaf(v, d.x, acc[t].x);
+            acc[t].y = fmaf(v, d.y, acc[t].y);
+            acc[t].z = fmaf(v, d.z, acc[t].z);
+            acc[t].w = fmaf(v, d.w, acc[t].w);
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int j = base + 4 * lane + 128 * t;
+        if (j < p.d_out) {
+          float4 w = reinterpret_cast<float4*>(wrow)[j / 4];
+          w.x -= p.eta * acc[t].x;
+          w.y -= p.eta * acc[t].y;
+          w.z -= p.eta * acc[t].z;
+          w.w -= p.eta * acc[t].w;
+          reinterpret_cast<float4*>(wrow)[j / 4] = w;
+          if (grow != nullptr) reinterpret_cast<float4*>(grow)[j / 4] = acc[t];
+        }
+      }
+    }
+  } else {
+    for (int base = 0; base < p.d_out; base += 32 * 8) {
+      float acc[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc[t] = 0.f;
+      for (long long e = lo; e < hi; ++e) {
+        const float v = __ldg(p.cval + e);
+        const float* dr = p.delta0 + (static_cast<long long>(__ldg(p.rowidx + e)) - p.start) * p.ldd;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int j = base + lane + 32 * t;
+          if (j < p.d_out) acc[t] = fmaf(v, __ldg(dr + j), acc[t]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int j = base + lane + 32 * t;
+        if (j < p.d_out) {
+          wrow[j] -= p.eta * acc[t];
+          if (grow != nullptr) grow[j] = acc[t];
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------
+// Precision conversion / layout for the host <-> device model exchange.
+// dst (rows, cols, ldd) fp32 <- src (rows, cols, lds) fp64; TRANSPOSE writes
+// dst[c, r] (used for the transposed sparse first-layer weight).
+template <bool TRANSPOSE>
+__global__ void f64_to_f32_kernel(float* dst, long long ldd, const double* src, long long lds, int rows, int cols) {
+  const long long total = static_cast<long long>(rows) * cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / cols, c = i % cols;
+    const float v = static_cast<float>(src[r * lds + c]);
+    if (TRANSPOSE)
+      dst[c * ldd + r] = v;
+    else
+      dst[r * ldd + c] = v;
+  }
+}
+template <bool TRANSPOSE>
+__global__ void f32_to_f64_kernel(double* dst, long long ldd, const float* src, long long lds, int rows, int cols) {
+  const long long total = static_cast<long long>(rows) * cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / cols, c = i % cols;
+    dst[r * ldd + c] = static_cast<double>(TRANSPOSE ? src[c * lds + r] : src[r * lds + c]);
+  }
+}
+
+// dst (rows, cols, ldd) = scale * src (rows, cols, dense): unpack of the
+// allreduced flat model (replica averaging).
+__global__ void unpack_scale_kernel(float* dst, long long ldd, const float* src, int rows, int cols, float scale) {
+  const long long total = static_cast<long long>(rows) * cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / cols, c = i % cols;
+    dst[r * ldd + c] = src[i] * scale;
+  }
+}
+
+}  // namespace hb

@@ -1,0 +1,238 @@
+"""GpuReplica: one device context of the C library, owned by one worker thread.
+
+This is the B200 replacement for the state `execute_batch_replica` rebuilds
+on every call (workers.py:126-138): instead of `deep_copy` + NumPy tape, the
+context keeps the fp32 model mirror, the activation tape, the staged epoch
+and TMA descriptors resident on the GPU, and exchanges only the model
+snapshot (H2D) and the gradient for the stale merge (D2H).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+
+import numpy as np
+
+from . import _native as N
+from .data import CsrDataset
+
+
+class GpuReplica:
+    """Device context for layer sizes `sizes` and batches of <= max_batch rows."""
+
+    def __init__(self, sizes, max_batch: int, device: int = 0, sparse: bool = False, precision: str = "3xtf32"):
+        self._lib = N.load()
+        self.sizes = tuple(int(s) for s in sizes)
+        self.depth = len(self.sizes) - 1
+        self.max_batch = int(max_batch)
+        self.device = int(device)
+        self.sparse = bool(sparse)
+        if precision not in ("3xtf32", "tf32"):
+            raise ValueError(f"precision must be '3xtf32' or 'tf32', got {precision!r}")
+        self.precision = precision
+        flags = (N.HB_SPARSE_INPUT if sparse else 0) | (N.HB_PRECISION_TF32 if precision == "tf32" else 0)
+        arr = (C.c_int * len(self.sizes))(*self.sizes)
+        h = C.c_void_p()
+        N.check(self._lib.hb_ctx_create(C.byref(h), self.device, self.depth, arr, self.max_batch, flags))
+        self._h = h
+        self._staged_key = None
+        self._staged_ref = None
+        self._keep = None
+        self._fin = weakref.finalize(self, GpuReplica._destroy, self._lib, h)
+
+    @staticmethod
+    def _destroy(lib, h):
+        if h:
+            lib.hb_ctx_destroy(h)
+
+    def close(self):
+        self._fin()
+
+    # ----------------------------------------------------------- model
+    def set_weights(self, weights) -> None:
+        """Snapshot a host float64 model into the device mirror (deep_copy, nn.py:182)."""
+        if len(weights) != self.depth:
+            raise ValueError("weight count does not match architecture")
+        for l, w in enumerate(weights):
+            want = (self.sizes[l + 1], self.sizes[l])
+            if w.shape != want:
+                raise ValueError(f"weights[{l}] has shape {w.shape}, expected {want}")
+            w64 = np.ascontiguousarray(w, dtype=np.float64)
+            N.check(self._lib.hb_set_weights_f64(self._h, l, N.ptr(w64, C.c_double)))
+
+    def get_weights(self) -> list:
+        out = []
+        for l in range(self.depth):
+            w = np.empty((self.sizes[l + 1], self.sizes[l]), dtype=np.float64)
+            N.check(self._lib.hb_get_weights_f64(self._h, l, N.ptr(w, C.c_double)))
+            out.append(w)
+        return out
+
+    def write_weights_into(self, weights) -> None:
+        """Copy the device model into existing host float64 arrays in place."""
+        for l, w in enumerate(self.get_weights()):
+            np.copyto(weights[l], w)
+
+    def grads(self) -> list:
+        """Raw mean gradients of the last step run with emit_grad=True."""
+        out = []
+        for l in range(self.depth):
+            g = np.empty((self.sizes[l + 1], self.sizes[l]), dtype=np.float32)
+            N.check(self._lib.hb_get_grad_f32(self._h, l, N.ptr(g, C.c_float)))
+            out.append(g)
+        return out
+
+    def merge_grads_into(self, weights, eta: float) -> None:
+        """Stale merge W_global -= eta * g (workers.py:135 -> linalg.py:79) with
+        the gradient of the last emit_grad step, in place on host float64 arrays."""
+        for l, w in enumerate(weights):
+            if not (w.flags.c_contiguous and w.dtype == np.float64):
+                raise ValueError("host weights must be C-contiguous float64 (Model layout, nn.py:75)")
+            N.check(self._lib.hb_merge_grad_into_f64(self._h, l, N.ptr(w, C.c_double), float(eta)))
+
+    # ------------------------------------------------------------ data
+    @staticmethod
+    def key_of(data) -> tuple:
+        """Identity of a host dataset: its buffer address and shape.  The
+        staged array is kept referenced, so the address cannot be recycled by
+        a different array while it is staged."""
+        if isinstance(data, CsrDataset):
+            return ("csr", data.rowptr.__array_interface__["data"][0], data.col.__array_interface__["data"][0],
+                    data.n_examples)
+        return ("dense", data.__array_interface__["data"][0], data.shape, data.dtype.str)
+
+    def stage(self, data, labels=None) -> None:
+        """Stage a dataset (dense (N, d) float array + labels, or CsrDataset) on
+        the device; steps then index it by (start, rows)."""
+        key = self.key_of(data)
+        if isinstance(data, CsrDataset):
+            if not self.sparse:
+                raise ValueError("dense context cannot stage CSR data")
+            if data.n_cols != self.sizes[0]:
+                raise ValueError(f"CSR has {data.n_cols} columns, model input is {self.sizes[0]}")
+            val32 = np.ascontiguousarray(data.val, dtype=np.float32)
+            N.check(self._lib.hb_stage_csr(self._h, N.ptr(data.rowptr, C.c_int64), N.ptr(data.col, C.c_int32),
+                                           N.ptr(val32, C.c_float), data.n_examples, N.ptr(data.labels, C.c_int64)))
+            self._staged_key = key
+            self._keep = data
+            return
+        x = data
+        if self.sparse:
+            raise ValueError("sparse context needs a CsrDataset")
+        if x.ndim != 2 or x.shape[1] != self.sizes[0]:
+            raise ValueError(f"batch shape {x.shape} incompatible with input dim {self.sizes[0]}")
+        y = np.ascontiguousarray(labels, dtype=np.int64)
+        if y.shape != (x.shape[0],):
+            raise ValueError("labels length must equal the number of feature rows")
+        if x.dtype == np.float32 and x.strides[1] == 4:
+            N.check(self._lib.hb_stage_dense_f32(self._h, N.ptr(x, C.c_float), x.shape[0], x.strides[0] // 4,
+                                                 N.ptr(y, C.c_int64)))
+        else:
+            x = x if (x.dtype == np.float64 and x.strides[1] == 8) else np.ascontiguousarray(x, dtype=np.float64)
+            N.check(self._lib.hb_stage_dense_f64(self._h, N.ptr(x, C.c_double), x.shape[0], x.strides[0] // 8,
+                                                 N.ptr(y, C.c_int64)))
+        self._staged_key = key
+        self._keep = (data, x, y)
+
+    def is_staged(self, key) -> bool:
+        return self._staged_key == key
+
+    @property
+    def staged_rows(self) -> int:
+        return int(self._lib.hb_staged_rows(self._h))
+
+    # ------------------------------------------------------------ steps
+    def step(self, start: int, rows: int, eta: float, emit_grad: bool = False, timed: bool = False,
+             want_loss: bool = False, blocking: bool = True):
+        """One SGD step on staged rows [start, start+rows); returns the mean
+        training loss of the batch when want_loss.  blocking=False returns as
+        soon as the step is enqueued (synchronize() waits)."""
+        flags = (N.HB_STEP_EMIT_GRAD if emit_grad else 0) | (N.HB_STEP_TIMED if timed else 0)
+        if not blocking and not want_loss:
+            flags |= N.HB_STEP_ASYNC
+        loss = C.c_double(0.0)
+        N.check(self._lib.hb_train_step(self._h, int(start), int(rows), float(eta), flags,
+                                        C.byref(loss) if want_loss else None))
+        return loss.value if want_loss else None
+
+    def step_host(self, batch, labels, eta: float, emit_grad: bool = False, timed: bool = False,
+                  want_loss: bool = True):
+        """One SGD step on a batch held in host memory (copied H2D in the call).
+        batch: float32 (rows, d) array, or a CsrDataset of the batch rows."""
+        flags = (N.HB_STEP_EMIT_GRAD if emit_grad else 0) | (N.HB_STEP_TIMED if timed else 0)
+        loss = C.c_double(0.0)
+        lp = C.byref(loss) if want_loss else None
+        if isinstance(batch, CsrDataset):
+            val32 = batch.val if batch.val.dtype == np.float32 else np.ascontiguousarray(batch.val, dtype=np.float32)
+            y = batch.labels if labels is None else np.ascontiguousarray(labels, dtype=np.int64)
+            N.check(self._lib.hb_train_step_host_csr(self._h, N.ptr(batch.rowptr, C.c_int64),
+                                                     N.ptr(batch.col, C.c_int32), N.ptr(val32, C.c_float),
+                                                     N.ptr(y, C.c_int64), batch.n_examples, float(eta), flags, lp))
+        else:
+            x = batch if (batch.dtype == np.float32 and batch.strides[1] == 4) else np.ascontiguousarray(
+                batch, dtype=np.float32)
+            y = np.ascontiguousarray(labels, dtype=np.int64)
+            N.check(self._lib.hb_train_step_host_dense(self._h, N.ptr(x, C.c_float), x.strides[0] // 4,
+                                                       N.ptr(y, C.c_int64), x.shape[0], float(eta), flags, lp))
+        return loss.value if want_loss else None
+
+    def eval_loss_sum(self, start: int, rows: int) -> float:
+        """Sum of per-example cross-entropy over staged rows (loss_sum, nn.py:139-146)."""
+        out = C.c_double(0.0)
+        N.check(self._lib.hb_eval_loss_sum(self._h, int(start), int(rows), C.byref(out)))
+        return out.value
+
+    def forward(self, start: int, rows: int) -> None:
+        N.check(self._lib.hb_forward(self._h, int(start), int(rows)))
+
+    def activation(self, layer: int, rows: int) -> np.ndarray:
+        out = np.empty((rows, self.sizes[layer]), dtype=np.float32)
+        N.check(self._lib.hb_get_activation_f32(self._h, int(layer), int(rows), N.ptr(out, C.c_float)))
+        return out
+
+    @property
+    def last_step_ms(self) -> float:
+        v = C.c_float(0.0)
+        N.check(self._lib.hb_last_step_ms(self._h, C.byref(v)))
+        return float(v.value)
+
+    @property
+    def last_step_launches(self) -> int:
+        v = C.c_int(0)
+        N.check(self._lib.hb_last_step_launches(self._h, C.byref(v)))
+        return int(v.value)
+
+    def profile(self, on: bool) -> None:
+        """Bracket every kernel launch with CUDA events on the step stream."""
+        N.check(self._lib.hb_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self) -> dict:
+        """{kernel name: (total ms, launches)} since profile(True) / the last read."""
+        cap = 256
+        names = C.create_string_buffer(64 * cap)
+        tot = (C.c_double * cap)()
+        cnt = (C.c_int * cap)()
+        n = C.c_int(0)
+        N.check(self._lib.hb_profile_read(self._h, cap, names, tot, cnt, C.byref(n)))
+        raw = names.raw
+        return {raw[64 * i: 64 * i + 64].split(b"\0")[0].decode(): (tot[i], cnt[i]) for i in range(n.value)}
+
+    def synchronize(self) -> None:
+        N.check(self._lib.hb_synchronize(self._h))
+
+    # ------------------------------------------------- multi-GPU merge
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        lib = N.load()
+        buf = (C.c_char * 128)()
+        N.check(lib.hb_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def comm_init(self, uid: bytes, nranks: int, rank: int) -> None:
+        buf = (C.c_char * 128).from_buffer_copy(uid)
+        N.check(self._lib.hb_comm_init(self._h, buf, int(nranks), int(rank)))
+
+    def merge_allreduce(self) -> None:
+        """Average the device models of all ranks (NCCL allreduce over NVLink)."""
+        N.check(self._lib.hb_merge_allreduce(self._h))

@@ -1,0 +1,179 @@
+"""The GPU replica worker behind the reference's own worker interface.
+
+Drop-in seam: the reference's `WorkerThread._execute` calls
+the module-global `execute_batch_replica(model, batch, eta, speed_factor)`
+(pkg/src/hogtrain/workers.py:204-206) and `_evaluate` calls
+`loss_sum(eval_model, x, y)` (workers.py:214).  `execute_gpu_replica` and
+`gpu_loss_sum` here have exactly those signatures and semantics and run the
+whole step on a B200; `install()` rebinds them into a live `hogtrain` module
+(the reference's own injection mechanism, test_engine_modes.py:59).
+
+`WorkerMode.GPU_REPLICA` / `WorkerConfig(device=...)` extend the reference's
+config surface (workers.py:38-77; harness.py:153-177 reads `worker.N.mode`)
+for rosters that name the GPU worker explicitly.
+"""
+
+from __future__ import annotations
+
+import threading
+import time
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+
+from .data import CsrBatchRef, CsrDataset
+from .nn import layer_sizes_of
+from .replica import GpuReplica
+
+
+class WorkerMode(Enum):  # workers.py:38-40 plus the B200 worker
+    HOGWILD_SHARDED = "hogwild_sharded"
+    BATCH_REPLICA = "batch_replica"
+    GPU_REPLICA = "gpu_replica"
+
+
+class ReplicaMode(Enum):  # workers.py:43-45
+    REFERENCE = "reference"
+    DEEP_COPY = "deep_copy"
+
+
+_REQUIRED_REPLICA = {  # workers.py:48-51
+    WorkerMode.HOGWILD_SHARDED: ReplicaMode.REFERENCE,
+    WorkerMode.BATCH_REPLICA: ReplicaMode.DEEP_COPY,
+    WorkerMode.GPU_REPLICA: ReplicaMode.DEEP_COPY,
+}
+
+
+@dataclass(frozen=True)
+class WorkerConfig:  # workers.py:54-77, plus device / precision / sync_every for GPU workers
+    worker_id: str
+    mode: WorkerMode
+    threads: int = 1
+    replica_mode: ReplicaMode | None = None
+    speed_factor: float = 0.0
+    min_batch: int = 1
+    max_batch: int = 1
+    device: int = 0
+    precision: str = "3xtf32"
+
+    def __post_init__(self):
+        if self.threads < 1:
+            raise ValueError("threads must be >= 1")
+        if self.speed_factor < 0:
+            raise ValueError("speed_factor must be >= 0")
+        if not (1 <= self.min_batch <= self.max_batch):
+            raise ValueError(f"need 1 <= min_batch <= max_batch, got [{self.min_batch}, {self.max_batch}]")
+        if self.device < 0:
+            raise ValueError("device must be >= 0")
+        required = _REQUIRED_REPLICA[self.mode]
+        if self.replica_mode is None:
+            object.__setattr__(self, "replica_mode", required)
+        elif self.replica_mode is not required:
+            raise ValueError(f"{self.mode.value} workers require replica_mode={required.value}")
+
+
+# ------------------------------------------------------------------------
+# Per-thread device contexts: a context is affine to the worker thread that
+# created it (include/hogbatch_b200.h "Conventions").
+_tls = threading.local()
+_DEFAULT_MAX_BATCH = 8192
+
+
+def set_worker_device(device: int, max_batch: int | None = None, precision: str = "3xtf32") -> None:
+    """Select the GPU (and batch capacity / precision) for replica calls made on this thread."""
+    _tls.device = int(device)
+    _tls.precision = precision
+    if max_batch is not None:
+        _tls.max_batch = int(max_batch)
+
+
+def _replica(sizes, rows: int, sparse: bool, purpose: str) -> GpuReplica:
+    cache = getattr(_tls, "contexts", None)
+    if cache is None:
+        cache = _tls.contexts = {}
+    device = getattr(_tls, "device", 0)
+    precision = getattr(_tls, "precision", "3xtf32")
+    key = (purpose, device, sizes, sparse, precision)
+    ctx = cache.get(key)
+    want = max(rows, getattr(_tls, "max_batch", _DEFAULT_MAX_BATCH))
+    if ctx is None or ctx.max_batch < rows:
+        if ctx is not None:
+            ctx.close()
+        ctx = cache[key] = GpuReplica(sizes, want, device=device, sparse=sparse, precision=precision)
+    return ctx
+
+
+def release_thread_contexts() -> None:
+    for ctx in getattr(_tls, "contexts", {}).values():
+        ctx.close()
+    _tls.contexts = {}
+
+
+def _stage_for(ctx: GpuReplica, batch) -> None:
+    """Stage the array a BatchRef views (the epoch copy) once; later batches of
+    the same epoch only pass (start, length)."""
+    if isinstance(batch, CsrBatchRef):
+        if not ctx.is_staged(GpuReplica.key_of(batch.data)):
+            ctx.stage(batch.data)
+        return
+    if not ctx.is_staged(GpuReplica.key_of(batch.features)):
+        ctx.stage(batch.features, batch.labels)
+
+
+def execute_gpu_replica(model, batch, eta: float, speed_factor: float = 0.0) -> float:
+    """GPU version of execute_batch_replica (workers.py:126-138).
+
+    Gradient on a snapshot of the *current* shared model, then a stale merge
+    of that gradient into whatever the shared model holds at merge time:
+      snapshot  host float64 model -> device fp32 mirror     (deep_copy, :132)
+      step      forward/backward on the device              (:133-134)
+      merge     W_host -= eta * g, float64, in place         (apply_update, :135)
+    Returns the update-count delta 1.0.  `speed_factor` keeps the reference's
+    emulation contract (sleep speed_factor x elapsed); real devices pass 0."""
+    start_t = time.perf_counter()
+    sizes = layer_sizes_of(model)
+    sparse = isinstance(batch, CsrBatchRef)
+    ctx = _replica(sizes, batch.length, sparse, "train")
+    _stage_for(ctx, batch)
+    ctx.set_weights(model.weights)
+    ctx.step(batch.start, batch.length, eta, emit_grad=True, timed=True)
+    ctx.merge_grads_into(model.weights, eta)
+    _tls.last_device_ms = ctx.last_step_ms
+    if speed_factor > 0:
+        time.sleep(speed_factor * (time.perf_counter() - start_t))
+    return 1.0
+
+
+def last_device_ms() -> float:
+    """CUDA-event time of the last replica step on this thread (controller feed)."""
+    return float(getattr(_tls, "last_device_ms", 0.0))
+
+
+def gpu_loss_sum(model, features, labels, chunk: int = 4096) -> float:
+    """GPU version of loss_sum (nn.py:139-146): sum over rows of
+    -log max(p_y, 1e-12) of `model` on (features, labels)."""
+    sizes = layer_sizes_of(model)
+    if isinstance(features, CsrDataset):
+        ctx = _replica(sizes, chunk, True, "eval")
+        if not ctx.is_staged(GpuReplica.key_of(features)):
+            ctx.stage(features)
+        n = features.n_examples
+    else:
+        if features.ndim != 2 or features.shape[1] != sizes[0]:
+            raise ValueError(f"batch shape {features.shape} incompatible with input dim {sizes[0]}")
+        ctx = _replica(sizes, chunk, False, "eval")
+        if not ctx.is_staged(GpuReplica.key_of(features)):
+            ctx.stage(features, np.asarray(labels, dtype=np.int64))
+        n = features.shape[0]
+    ctx.set_weights(model.weights)
+    return ctx.eval_loss_sum(0, n)
+
+
+def install(hogtrain_module=None) -> None:
+    """Route the reference's BATCH_REPLICA workers to the B200 path by
+    rebinding `hogtrain.workers.execute_batch_replica` and `loss_sum`."""
+    if hogtrain_module is None:
+        import hogtrain.workers as hogtrain_module  # noqa: F811  (reference package, if present)
+    hogtrain_module.execute_batch_replica = execute_gpu_replica
+    hogtrain_module.loss_sum = gpu_loss_sum

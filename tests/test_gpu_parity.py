@@ -1,0 +1,220 @@
+"""Parity of the B200 replica step (through the C ABI) with the reference.
+
+Bar (BASELINE.json north_star): per-step gradients and updated weights
+within 1e-4 relative under the reference's own floored metric
+(pkg/tests/helpers.py:29-35); loss curves within 1% at equal sample counts.
+Sources of truth: golden vectors produced by the reference itself
+(tests/golden/*.npz) and, at larger shapes, the float64 oracle (oracle/).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_runs, max_relative_error
+from oracle import ref_nn
+
+pytestmark = pytest.mark.gpu
+
+STEP_TOL = 1e-4  # north_star: per-step gradients and weights within 1e-4 relative
+CURVE_TOL = 0.01  # north_star: loss curves within 1%
+
+
+@pytest.fixture(scope="module")
+def hb():
+    import paper_2004_08771_b200 as hb
+
+    if hb.device_count() < 1:
+        pytest.fail("GPU tests need a CUDA device")
+    return hb
+
+
+def to_csr(hb, x, y):
+    rows, cols = np.nonzero(x)
+    rowptr = np.zeros(x.shape[0] + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=x.shape[0]), out=rowptr[1:])
+    return hb.CsrDataset(rowptr, cols.astype(np.int32), x[rows, cols], np.asarray(y, dtype=np.int64), x.shape[1])
+
+
+def run_step(hb, sizes, w, x, y, eta, sparse=False, precision="3xtf32"):
+    ctx = hb.GpuReplica(sizes, x.shape[0], sparse=sparse, precision=precision)
+    try:
+        ctx.set_weights(w)
+        if sparse:
+            ctx.stage(to_csr(hb, x, y))
+        else:
+            ctx.stage(x, y)
+        acts = []
+        if len(sizes) > 2:
+            ctx.forward(0, x.shape[0])
+            acts = [ctx.activation(l, x.shape[0]) for l in range(1, len(sizes) - 1)]
+        loss = ctx.step(0, x.shape[0], eta, emit_grad=True, want_loss=True)
+        return dict(grads=ctx.grads(), weights=ctx.get_weights(), loss=loss, acts=acts)
+    finally:
+        ctx.close()
+
+
+class TestGoldenStep:
+    """Every reference-generated case: activations, gradients, merged weights."""
+
+    def test_cases(self, hb, golden_cases):
+        for c in golden_cases:
+            out = run_step(hb, c["sizes"], c["w"], c["x"], c["y"], c["eta"])
+            for l, a in enumerate(out["acts"]):
+                assert np.abs(a - c["a"][l]).max() <= 1e-5, (c["name"], "act", l)
+            eg = max_relative_error(out["grads"], c["g"])
+            ew = max_relative_error(out["weights"], c["u"])
+            assert eg <= STEP_TOL, (c["name"], "grad", eg)
+            assert ew <= STEP_TOL, (c["name"], "weights", ew)
+            assert out["loss"] == pytest.approx(c["ce"], rel=1e-5, abs=1e-6), c["name"]
+
+    def test_sparse_case_through_csr(self, hb, golden_cases):
+        c = next(c for c in golden_cases if c["name"] == "sparse_w8a_like")
+        out = run_step(hb, c["sizes"], c["w"], c["x"], c["y"], c["eta"], sparse=True)
+        assert max_relative_error(out["grads"], c["g"]) <= STEP_TOL
+        assert max_relative_error(out["weights"], c["u"]) <= STEP_TOL
+
+    def test_eval_loss_sum(self, hb, golden_cases):
+        for c in golden_cases:
+            ctx = hb.GpuReplica(c["sizes"], 64)
+            ctx.set_weights(c["w"])
+            ctx.stage(c["x"], c["y"])
+            got = ctx.eval_loss_sum(0, c["x"].shape[0])
+            ctx.close()
+            assert got == pytest.approx(c["loss_sum"], rel=1e-5, abs=1e-6), c["name"]
+
+
+def oracle_case(sizes, b, seed, sparse_nnz=None):
+    rng = np.random.default_rng(seed)
+    w = ref_nn.init_weights(sizes, seed)
+    if sparse_nnz:
+        x = np.zeros((b, sizes[0]))
+        for r in range(b):
+            x[r, rng.choice(sizes[0], size=sparse_nnz, replace=False)] = rng.random(sparse_nnz) + 0.5
+    else:
+        x, _ = ref_nn.synthetic_blobs(b, sizes[0], 2, 2.5, seed)
+    y = rng.integers(0, sizes[-1], size=b)
+    return w, x, y
+
+
+@pytest.mark.parametrize(
+    "sizes,b,sparse_nnz,eta",
+    [
+        ((300, 512, 512, 512, 2), 1024, 12, 0.5),  # w8a-shaped (sparse first layer)
+        ((54, 512, 512, 512, 2), 512, None, 0.5),  # covtype-shaped (K = 54 tail)
+        ((500, 1024, 1024, 983), 300, None, 1.0),  # delicious-shaped (wide softmax, M tail)
+        ((2000, 256, 256, 2), 777, 52, 0.3),  # real-sim-shaped, scaled down
+        ((1024, 512, 512, 1000), 256, None, 0.2),  # scaled-shaped, narrowed
+        ((37, 96, 3), 129, None, 0.1),  # odd widths, 3 classes
+    ],
+)
+def test_oracle_step_at_shape(hb, sizes, b, sparse_nnz, eta):
+    w, x, y = oracle_case(sizes, b, seed=sum(sizes) + b, sparse_nnz=sparse_nnz)
+    tape = ref_nn.forward(w, x)
+    grads = ref_nn.backward(w, tape, y)
+    upd = ref_nn.deep_copy(w)
+    ref_nn.apply_update(upd, grads, eta)
+    out = run_step(hb, sizes, w, x, y, eta, sparse=bool(sparse_nnz))
+    eg = max_relative_error(out["grads"], grads)
+    ew = max_relative_error(out["weights"], upd)
+    assert eg <= STEP_TOL, eg
+    assert ew <= STEP_TOL, ew
+    assert out["loss"] == pytest.approx(ref_nn.cross_entropy_loss(tape, y), rel=1e-5)
+
+
+def test_tf32_mode_is_less_precise_but_close(hb):
+    sizes, b = (256, 512, 512, 2), 512
+    w, x, y = oracle_case(sizes, b, seed=3)
+    grads = ref_nn.backward(w, ref_nn.forward(w, x), y)
+    e3 = max_relative_error(run_step(hb, sizes, w, x, y, 0.1)["grads"], grads)
+    e1 = max_relative_error(run_step(hb, sizes, w, x, y, 0.1, precision="tf32")["grads"], grads)
+    assert e3 <= STEP_TOL
+    assert e3 < e1 < 0.5
+
+
+def test_step_is_bit_reproducible(hb):
+    sizes, b = (300, 512, 512, 2), 700
+    w, x, y = oracle_case(sizes, b, seed=9, sparse_nnz=12)
+    a = run_step(hb, sizes, w, x, y, 0.5, sparse=True)
+    c = run_step(hb, sizes, w, x, y, 0.5, sparse=True)
+    for p, q in zip(a["weights"], c["weights"]):
+        assert np.array_equal(p, q)
+
+
+def test_host_buffer_steps_match_staged(hb):
+    for sparse in (False, True):
+        sizes, b = (300, 256, 256, 2), 333
+        w, x, y = oracle_case(sizes, b, seed=11, sparse_nnz=12 if sparse else None)
+        staged = run_step(hb, sizes, w, x, y, 0.4, sparse=sparse)
+        ctx = hb.GpuReplica(sizes, 512, sparse=sparse)
+        ctx.set_weights(w)
+        batch = to_csr(hb, x, y) if sparse else x.astype(np.float32)
+        loss = ctx.step_host(batch, y, 0.4, emit_grad=True)
+        got = ctx.get_weights()
+        ctx.close()
+        assert loss == pytest.approx(staged["loss"], rel=1e-6)
+        for p, q in zip(got, staged["weights"]):
+            assert np.array_equal(p, q)
+
+
+def test_batches_inside_staged_epoch(hb):
+    """(start, rows) indexing of the staged epoch equals staging the batch alone."""
+    sizes = (54, 128, 128, 2)
+    w, x, y = oracle_case(sizes, 1000, seed=5)
+    ctx = hb.GpuReplica(sizes, 300)
+    ctx.set_weights(w)
+    ctx.stage(x, y)
+    ctx.step(417, 300, 0.3, emit_grad=True)
+    g = ctx.grads()
+    ctx.close()
+    ref = ref_nn.backward(w, ref_nn.forward(w, x[417:717]), y[417:717])
+    assert max_relative_error(g, ref) <= STEP_TOL
+
+
+def test_execute_gpu_replica_stale_merge(hb):
+    """workers.py:126-138: gradient on the snapshot, merged into the model."""
+    from paper_2004_08771_b200 import BatchRef, Model, Architecture, execute_gpu_replica
+
+    sizes = (20, 64, 64, 3)
+    w, x, y = oracle_case(sizes, 200, seed=21)
+    model = Model(Architecture(sizes), [a.copy() for a in w])
+    batch = BatchRef(x, y, 50, 100)
+    assert execute_gpu_replica(model, batch, 0.25) == 1.0
+    g = ref_nn.backward(w, ref_nn.forward(w, x[50:150]), y[50:150])
+    want = ref_nn.deep_copy(w)
+    ref_nn.apply_update(want, g, 0.25)
+    assert max_relative_error(model.weights, want) <= STEP_TOL
+    # two gradients from one snapshot applied in turn (test_engine.py:74-89)
+    model2 = Model(Architecture(sizes), [a.copy() for a in w])
+    snap = [a.copy() for a in w]
+    execute_gpu_replica(model2, BatchRef(x, y, 0, 100), 0.1)
+    g1 = ref_nn.backward(snap, ref_nn.forward(snap, x[:100]), y[:100])
+    assert max_relative_error(model2.weights, [s - 0.1 * a for s, a in zip(snap, g1)]) <= STEP_TOL
+
+
+def test_argument_errors(hb):
+    ctx = hb.GpuReplica((10, 16, 2), 64)
+    with pytest.raises(ValueError):
+        ctx.set_weights([np.zeros((16, 11)), np.zeros((2, 16))])
+    x = np.zeros((100, 10))
+    ctx.stage(x, np.zeros(100, dtype=np.int64))
+    with pytest.raises(ValueError):
+        ctx.step(0, 65, 0.1)  # above max_batch
+    with pytest.raises(ValueError):
+        ctx.step(90, 20, 0.1)  # past the staged rows
+    with pytest.raises(ValueError):
+        ctx.step_host(np.zeros((4, 10), np.float32), np.array([0, 1, 2, 0]), 0.1)  # label 2 >= classes
+    with pytest.raises(RuntimeError):
+        ctx.grads()  # no emit_grad step yet
+    ctx.close()
+
+
+def test_sequential_curves_match_reference(hb):
+    """Loss-vs-epoch curves of the deterministic single-worker schedule."""
+    for r in load_runs():
+        model = hb.Model(hb.Architecture(r["sizes"]), [w.copy() for w in r["w"]])
+        ds = hb.Dataset(r["x"], r["y"])
+        res = hb.train_gpu(ds, model, r["batch"], r["eta"], r["epochs"], r["seed"])
+        curve = np.array(res.curve)
+        rel = np.abs(curve - r["curve"]) / np.abs(r["curve"])
+        assert rel.max() <= CURVE_TOL, (r["name"], rel.max())
+        assert res.examples == r["epochs"] * r["x"].shape[0]

@@ -119,24 +119,21 @@ int launch_gemm_p(GemmKind kind, int epi, int bn, const CUtensorMap& ta, const C
                   int m_tiles, int n_tiles, int splits, cudaStream_t st) {
 #define HB_L(BN_, AMN_, BMN_, EPI_) \
   return launch_gemm_t<BN_, AMN_, BMN_, EPI_, PASSES>(ta, tb, a, m_tiles, n_tiles, splits, st)
+#define HB_BN(AMN_, BMN_, EPI_)                    \
+  do {                                             \
+    if (bn == 32) HB_L(32, AMN_, BMN_, EPI_);      \
+    if (bn == 64) HB_L(64, AMN_, BMN_, EPI_);      \
+    if (bn == 256) HB_L(256, AMN_, BMN_, EPI_);    \
+    HB_L(128, AMN_, BMN_, EPI_);                   \
+  } while (0)
   if (kind == G_FWD) {
-    if (epi == EPI_SIGMOID) {
-      if (bn == 256) HB_L(256, false, false, EPI_SIGMOID);
-      HB_L(128, false, false, EPI_SIGMOID);
-    }
-    if (bn == 256) HB_L(256, false, false, EPI_STORE);
-    HB_L(128, false, false, EPI_STORE);
+    if (epi == EPI_SIGMOID) HB_BN(false, false, EPI_SIGMOID);
+    HB_BN(false, false, EPI_STORE);
   }
-  if (kind == G_DX) {
-    if (bn == 256) HB_L(256, false, true, EPI_DSIG);
-    HB_L(128, false, true, EPI_DSIG);
-  }
-  if (epi == EPI_SGD) {
-    if (bn == 256) HB_L(256, true, true, EPI_SGD);
-    HB_L(128, true, true, EPI_SGD);
-  }
-  if (bn == 256) HB_L(256, true, true, EPI_PARTIAL);
-  HB_L(128, true, true, EPI_PARTIAL);
+  if (kind == G_DX) HB_BN(false, true, EPI_DSIG);
+  if (epi == EPI_SGD) HB_BN(true, true, EPI_SGD);
+  HB_BN(true, true, EPI_PARTIAL);
+#undef HB_BN
 #undef HB_L
 }
 
@@ -305,6 +302,10 @@ int build_data_maps(hb_ctx* c, DataView& v) {
 }
 
 int choose_bn(long long m_tiles, long long n) {
+  // narrow outputs get narrow tiles: less wasted MMA work and more TMEM
+  // accumulators to rotate over (hb_gemm.cuh, GemmCfg::NBIG)
+  if (n <= 32) return 32;
+  if (n <= 64) return 64;
   if (n <= 128) return 128;
   if (m_tiles * cdiv(n, 256) >= 120) return 256;
   return 128;

@@ -62,6 +62,17 @@ struct GemmCfg {
   static constexpr int STAGES_RAW = BUDGET / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
   static constexpr int THREADS = PASSES == 3 ? 384 : 256;
+  // TMEM accumulators: the tensor core's fp32 accumulation error grows with
+  // the number of MMAs chained into one accumulator, so 3xTF32 keeps the two
+  // small cross terms in their own accumulator and rotates the hi*hi term over
+  // NBIG accumulators by k-block; the epilogue sums them in fp32 registers.
+  static constexpr int NBIG_RAW = PASSES == 3 ? 512 / BN - 1 : 1;
+  static constexpr int NBIG = NBIG_RAW > 15 ? 15 : (NBIG_RAW < 1 ? 1 : NBIG_RAW);
+  static constexpr int NACC = PASSES == 3 ? NBIG + 1 : 1;
+  static constexpr int TMEM_COLS_RAW = NACC * BN;
+  static constexpr int TMEM_COLS = TMEM_COLS_RAW <= 32 ? 32 : TMEM_COLS_RAW <= 64 ? 64 : TMEM_COLS_RAW <= 128 ? 128
+                                   : TMEM_COLS_RAW <= 256 ? 256 : 512;
+  static_assert(TMEM_COLS_RAW <= 512, "TMEM holds 512 fp32 columns");
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
   static_assert(STAGES >= 2, "need at least double buffering");
 };
@@ -108,7 +119,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
     fence_barrier_init();
   }
   if (warp == 2) {
-    tmem_alloc(tmem_slot, BN < 32 ? 32 : BN);
+    tmem_alloc(tmem_slot, C::TMEM_COLS);
     tmem_relinquish();
   }
   tc_fence_before();
@@ -154,17 +165,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
         const uint32_t bHi = aHi + C::A_BYTES;
 #pragma unroll
         for (int kk = 0; kk < kBK / 8; ++kk) {
-          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
           const uint64_t ah = op_desc(aHi, kk, A_MN);
           const uint64_t bh = op_desc(bHi, kk, B_MN);
           if (PASSES == 3) {
             const uint64_t al = op_desc(aHi + C::OP_BYTES, kk, A_MN);
             const uint64_t bl = op_desc(bHi + C::OP_BYTES, kk, B_MN);
-            mma_tf32(tmem_base, al, bh, idesc, acc);  // small terms first
-            mma_tf32(tmem_base, ah, bl, idesc, 1u);
-            mma_tf32(tmem_base, ah, bh, idesc, 1u);
+            const uint32_t t_small = tmem_base + C::NBIG * BN;
+            const uint32_t t_big = tmem_base + (i % C::NBIG) * BN;
+            mma_tf32(t_small, al, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+            mma_tf32(t_small, ah, bl, idesc, 1u);
+            mma_tf32(t_big, ah, bh, idesc, (i >= C::NBIG || kk > 0) ? 1u : 0u);
           } else {
-            mma_tf32(tmem_base, ah, bh, idesc, acc);
+            mma_tf32(tmem_base, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
           }
         }
         mma_commit(&empty[s]);  // frees the smem stage once these MMAs retire
@@ -179,14 +191,30 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
     const int row = m0 + q * 32 + lane;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c, r);
-      tmem_ld_wait();
+      const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c;
+      float v[32];
+      {
+        uint32_t r[32];
+        // small-term accumulator first, then the hi*hi accumulators (only those
+        // the k loop actually wrote)
+        tmem_ld_32x32b_x32(lane_addr + (C::NACC - 1) * BN, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = nkb > 0 ? __uint_as_float(r[j]) : 0.f;
+        if (C::NACC > 1) {
+#pragma unroll 1
+          for (int a = 0; a < C::NBIG; ++a) {
+            tmem_ld_32x32b_x32(lane_addr + a * BN, r);
+            tmem_ld_wait();
+            if (a < nkb) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += __uint_as_float(r[j]);
+            }
+          }
+        }
+      }
       const int n = n0 + c;
       if (n >= args.N) continue;
-      float v[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = nkb > 0 ? __uint_as_float(r[j]) : 0.f;
       const int ncols = min(32, args.N - n);
       if (EPI == EPI_SIGMOID || EPI == EPI_STORE) {
         if (row < args.M) {
@@ -245,7 +273,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
 #pragma unroll 4
       for (int j = t; j < C::OP_BYTES / 16; j += 128) {
         uint4 x = hi[j];
-        uint4 h = make_uint4(x.x & 0xFFFFE000u, x.y & 0xFFFFE000u, x.z & 0xFFFFE000u, x.w & 0xFFFFE000u);
+        uint4 h = make_uint4(to_tf32_rna(x.x), to_tf32_rna(x.y), to_tf32_rna(x.z), to_tf32_rna(x.w));
         lo[j] = make_float4(__uint_as_float(x.x) - __uint_as_float(h.x), __uint_as_float(x.y) - __uint_as_float(h.y),
                             __uint_as_float(x.z) - __uint_as_float(h.z), __uint_as_float(x.w) - __uint_as_float(h.w));
         hi[j] = h;
@@ -259,7 +287,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, BN < 32 ? 32 : BN);
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
 }
 

@@ -143,6 +143,14 @@ __host__ __device__ constexpr uint32_t make_idesc_tf32(int M, int N, bool a_mn, 
          ((static_cast<uint32_t>(N) >> 3) << 17) | ((static_cast<uint32_t>(M) >> 4) << 24);
 }
 
+// fp32 -> tf32 (round to nearest, ties away), low 13 bits zero.  x - tf32(x)
+// is then exact in fp32 and |x - tf32(x)| <= 2^-11 |x|.
+__device__ __forceinline__ uint32_t to_tf32_rna(uint32_t bits) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(__uint_as_float(bits)));
+  return r;
+}
+
 // --------------------------------------------------------------- misc
 __device__ __forceinline__ float sigmoidf_stable(float z) {
   // Two-branch form of linalg.py:48-55; IEEE expf (no fast-math) so that

@@ -47,12 +47,15 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out=None) -> Path:
+    """Compile the library; `defines` (e.g. ["HB_SPLIT_WARPS=8"]) and `out`
+    build experimental variants next to the default library."""
+    lib = Path(out) if out else LIB
+    if not force and not defines and out is None and not needs_build():
         return LIB
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), *map(str, SOURCES), "-o", str(tmp),
-           "-lcudart", "-ldl"]
+    tmp = lib.with_suffix(".so.tmp")
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"), *map(str, SOURCES),
+           "-o", str(tmp), "-lcudart", "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
@@ -61,16 +64,18 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr[-8000:]}")
     if verbose:
         print(res.stderr, file=sys.stderr)
-    tmp.replace(LIB)
-    return LIB
+    tmp.replace(lib)
+    return lib
 
 
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("-D", "--define", action="append", default=[])
+    ap.add_argument("--out")
     a = ap.parse_args(argv)
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, defines=a.define, out=a.out))
 
 
 if __name__ == "__main__":

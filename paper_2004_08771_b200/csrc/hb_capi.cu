@@ -387,17 +387,33 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     const int grid = cdiv(rows, kHeadRowsPerBlock);
     const int threads = kHeadWarps * 32;
     prof_begin(c);
-    if (c->head_nct == 2) {
+#define HB_HEAD(NCT_, MAXT_) head_small_kernel<NCT_, MAXT_><<<grid, threads, 0, st>>>(h)
+#define HB_HEADV(NCT_, VPL_) head_small_vec_kernel<NCT_, VPL_><<<grid, threads, 0, st>>>(h)
+    const bool vec = (h.d % 4 == 0) && (h.lda % 4 == 0) && (h.ld_dp % 4 == 0);
+    if (vec && (h.d <= 1024 && (c->head_nct == 2 || h.d <= 512))) {
+      const int vpl = h.d <= 256 ? 2 : (h.d <= 512 ? 4 : 8);
+      if (c->head_nct == 2) {
+        if (vpl == 2) HB_HEADV(2, 2); else if (vpl == 4) HB_HEADV(2, 4); else HB_HEADV(2, 8);
+      } else {
+        if (vpl == 2) HB_HEADV(4, 2); else HB_HEADV(4, 4);
+      }
+    } else if (c->head_nct == 2) {
       if (c->head_maxt == 8)
-        head_small_kernel<2, 8><<<grid, threads, 0, st>>>(h);
+        HB_HEAD(2, 8);
+      else if (c->head_maxt == 16)
+        HB_HEAD(2, 16);
       else
-        head_small_kernel<2, 32><<<grid, threads, 0, st>>>(h);
+        HB_HEAD(2, 32);
     } else {
       if (c->head_maxt == 8)
-        head_small_kernel<4, 8><<<grid, threads, 0, st>>>(h);
+        HB_HEAD(4, 8);
+      else if (c->head_maxt == 16)
+        HB_HEAD(4, 16);
       else
-        head_small_kernel<4, 32><<<grid, threads, 0, st>>>(h);
+        HB_HEAD(4, 32);
     }
+#undef HB_HEAD
+#undef HB_HEADV
     HB_CUDA(cudaGetLastError());
     prof_end(c, "head_small", l);
     loss_reduce_kernel<<<1, 32, 0, st>>>(c->ws_loss, grid, c->d_loss, 0);
@@ -406,7 +422,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     if (train) {
       const long long n = static_cast<long long>(c->d[L]) * c->d[l];
       prof_begin(c);
-      reduce_sgd_kernel<<<std::min<long long>(cdiv(n, 256), 4096), 256, 0, st>>>(
+      reduce_sgd_kernel<<<cdiv(n, 32), 256, 0, st>>>(
           c->W[l], c->ldw[l], c->ws, grid, n, c->d[L], c->d[l], static_cast<float>(eta),
           (flags & HB_STEP_EMIT_GRAD) ? c->G[l] : nullptr, c->d[l]);
       HB_CUDA(cudaGetLastError());
@@ -472,9 +488,9 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
     if (l == 0 && c->sparse) {
       SparseDwArgs p{v.colptr, v.rowidx, v.cval, start, rows, c->d[0], c->d[1], c->D[0], c->ld[1],
                      c->W[0], c->ldw[0], static_cast<float>(eta), emit ? c->G[0] : nullptr, c->ldw[0]};
-      const int blocks = cdiv(static_cast<long long>(c->d[0]) * 32, 256);
+      const dim3 blocks(c->d[0], cdiv(c->d[1], 128));
       prof_begin(c);
-      if (c->d[1] % 128 == 0)
+      if (c->d[1] % 4 == 0)
         sparse_dw_kernel<true><<<blocks, 256, 0, st>>>(p);
       else
         sparse_dw_kernel<false><<<blocks, 256, 0, st>>>(p);
@@ -512,7 +528,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       HB_TRY(launch_gemm(c->passes, G_DW, EPI_PARTIAL, c->bn_dw[l], c->tmD_mn[l], tb, a, mt, nt, splits, st));
       prof_end(c, "gemm_dw_partial", l);
       prof_begin(c);
-      reduce_sgd_kernel<<<std::min<long long>(cdiv(slab, 256), 4096), 256, 0, st>>>(
+      reduce_sgd_kernel<<<cdiv(slab, 32), 256, 0, st>>>(
           c->W[l], c->ldw[l], c->ws, splits, slab, a.M, a.N, static_cast<float>(eta), emit ? c->G[l] : nullptr,
           c->d[l]);
       HB_CUDA(cudaGetLastError());
@@ -652,7 +668,7 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
   c->small_head = nc <= 4 && dlast <= 1024 && !(c->sparse && L == 1);
   if (c->small_head) {
     c->head_nct = nc <= 2 ? 2 : 4;
-    c->head_maxt = dlast <= 256 ? 8 : 32;
+    c->head_maxt = dlast <= 256 ? 8 : (dlast <= 512 ? 16 : 32);
   }
   auto bail = [&](int code) {
     hb_ctx_destroy(c);
@@ -1151,6 +1167,18 @@ int hb_profile_read(hb_ctx* c, int max_entries, char* names, double* total_ms, i
   c->marks.clear();
   return HB_OK;
 }
+
+#ifdef HB_TRACE
+// debug builds only: copy the pipeline timeline of the last traced GEMM
+extern "C" int hb_trace_read(unsigned long long* out, int n) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, hb::hb_trace_buf, sizeof(unsigned long long) * std::min(n, 4096));
+  cudaMemset(reinterpret_cast<void*>(0), 0, 0);
+  unsigned long long zeros[4096] = {0};
+  cudaMemcpyToSymbol(hb::hb_trace_buf, zeros, sizeof zeros);
+  return HB_OK;
+}
+#endif
 
 int hb_synchronize(hb_ctx* c) {
   HB_TRY(ctx_check(c));

@@ -24,8 +24,9 @@
 //   warp 0        TMA producer (one elected lane)
 //   warp 1        MMA issuer   (one elected lane)
 //   warp 2        TMEM allocator
-//   warps 4..7    epilogue: tcgen05.ld TMEM -> registers -> fused op -> global
-//   warps 8..11   (PASSES == 3) hi/lo splitter
+//   warps 4..11   epilogue: tcgen05.ld TMEM -> registers -> smem transpose -> fused op ->
+//                 coalesced float4 global traffic (2 warps per TMEM lane quarter)
+//   warps 12..    (PASSES == 3) hi/lo splitter (HB_SPLIT_WARPS warps)
 #pragma once
 #include "hb_ptx.cuh"
 
@@ -49,6 +50,38 @@ struct GemmArgs {
   float eta;
 };
 
+// 3xTF32 split variants (compile-time):
+//   HB_SPLIT_HI_RAW 0: hi = cvt.rna.tf32(x) written back, lo = x - hi
+//   HB_SPLIT_HI_RAW 1: hi = x consumed raw by the tensor core, which truncates
+//                      fp32 operands to their top 19 bits (verified by the GPU
+//                      parity tests: with RN the lo term would be off by up to
+//                      2^-11 |x|), lo = x - trunc_tf32(x); saves the hi store.
+//                      Default.
+#ifndef HB_SPLIT_HI_RAW
+#define HB_SPLIT_HI_RAW 1
+#endif
+#ifndef HB_SPLIT_WARPS
+#define HB_SPLIT_WARPS 4
+#endif
+
+// Optional pipeline timeline (debug builds, -DHB_TRACE): CTA (0,0,0) records
+// globaltimer stamps per role and k-block into hb_trace_buf.
+#ifdef HB_TRACE
+__device__ unsigned long long hb_trace_buf[4096];
+#define HB_STAMP(slot)                                                                   \
+  do {                                                                                   \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (slot) < 4096) {        \
+      unsigned long long t_;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
+      hb_trace_buf[(slot)] = t_;                                                         \
+    }                                                                                    \
+  } while (0)
+#else
+#define HB_STAMP(slot) \
+  do {                 \
+  } while (0)
+#endif
+
 constexpr int kBM = 128;
 constexpr int kBK = 32;  // 32 fp32 = one 128-byte swizzle row
 
@@ -61,7 +94,10 @@ struct GemmCfg {
   static constexpr int BUDGET = 200 * 1024;
   static constexpr int STAGES_RAW = BUDGET / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
-  static constexpr int THREADS = PASSES == 3 ? 384 : 256;
+  static constexpr int SPLIT_THREADS = PASSES == 3 ? 32 * HB_SPLIT_WARPS : 0;
+  static constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, alternating 32-column chunks
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS + SPLIT_THREADS;
+  static constexpr int SPLIT_BASE = 128 + 32 * EPI_WARPS;
   // TMEM accumulators: the tensor core's fp32 accumulation error grows with
   // the number of MMAs chained into one accumulator, so 3xTF32 keeps the two
   // small cross terms in their own accumulator and rotates the hi*hi term over
@@ -101,6 +137,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) HB_STAMP(6 * 512 + 2);  // CTA start
   const int n0 = blockIdx.x * BN;
   const int m0 = blockIdx.y * kBM;
   const int kb_begin = blockIdx.z * args.kb_per_split;
@@ -112,7 +149,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&ready[s], 128);
+      mbar_init(&ready[s], C::SPLIT_THREADS > 0 ? C::SPLIT_THREADS : 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
@@ -134,6 +171,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
         mbar_wait(&empty[s], ph ^ 1);
+        HB_STAMP(0 * 512 + i);  // producer: stage free, issuing TMA
         uint8_t* sA = smem + s * C::STAGE_BYTES;
         uint8_t* sB = sA + C::A_BYTES;
         mbar_arrive_expect_tx(&full[s], C::OP_BYTES);
@@ -160,6 +198,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
         mbar_wait(PASSES == 3 ? &ready[s] : &full[s], ph);
+        HB_STAMP(1 * 512 + i);  // MMA: operands ready, issuing
         tc_fence_after();
         const uint32_t aHi = smem_u32(smem + s * C::STAGE_BYTES);
         const uint32_t bHi = aHi + C::A_BYTES;
@@ -180,17 +219,30 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
           }
         }
         mma_commit(&empty[s]);  // frees the smem stage once these MMAs retire
+        HB_STAMP(2 * 512 + i);  // MMA: issue done
       }
       mma_commit(tmem_full);  // accumulator complete (immediate if nkb == 0)
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 4 && warp < 4 + C::EPI_WARPS) {
     // ---------------------------------------------------------- epilogue
-    const int q = warp - 4;  // TMEM lane quarter owned by this warp
+    // TMEM -> registers (thread = row) -> per-warp smem transpose -> coalesced
+    // float4 global traffic (8 lanes per 128-byte row segment).  The mainloop
+    // is finished once tmem_full fires, so stage 0 is reused as staging space.
+    const int ew = warp - 4;
+    const int q = ew & 3;          // TMEM lane quarter owned by this warp (warp % 4)
+    const int half = ew >> 2;      // which alternating 32-column chunks
     mbar_wait(tmem_full, 0);
+    if (threadIdx.x == 128) HB_STAMP(6 * 512 + 0);  // epilogue start
     tc_fence_after();
-    const int row = m0 + q * 32 + lane;
+    constexpr int TP = 36;  // padded tile row (floats): conflict-free v4 in and out
+    float* tile = reinterpret_cast<float*>(smem) + ew * 32 * TP;
+    const bool vec_out = (args.ldo & 3) == 0;
+    const bool vec_aux = (args.ld_aux & 3) == 0;
+    const bool vec_grad = (args.ld_grad & 3) == 0;
+    const int sub_r = lane >> 3;       // row within a group of 4
+    const int sub_c = (lane & 7) * 4;  // column quad within the 32-column chunk
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = 32 * half; c < BN; c += 32 * (C::EPI_WARPS / 4)) {
       const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c;
       float v[32];
       {
@@ -214,77 +266,125 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
         }
       }
       const int n = n0 + c;
-      if (n >= args.N) continue;
-      const int ncols = min(32, args.N - n);
-      if (EPI == EPI_SIGMOID || EPI == EPI_STORE) {
-        if (row < args.M) {
-          float* o = args.out + static_cast<long long>(row) * args.ldo + n;
+      if (n >= args.N) continue;  // warp-uniform
+#ifdef HB_DEBUG_NO_EPI_STORE
+      if (v[0] == 12345.f) args.out[0] = v[1];  // timing experiment only: keep the TMEM loads alive
+      continue;
+#endif
+      __syncwarp();
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < ncols) o[j] = (EPI == EPI_SIGMOID) ? sigmoidf_stable(v[j]) : v[j];
-        }
-      } else if (EPI == EPI_DSIG) {
-        if (row < args.M) {
-          float* o = args.out + static_cast<long long>(row) * args.ldo + n;
-          const float* a = args.aux + static_cast<long long>(row) * args.ld_aux + n;
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(tile + lane * TP + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      __syncwarp();
+      const int gn = n + sub_c;
+      const int nleft = args.N - gn;  // columns of this quad still inside N
+#pragma unroll 2
+      for (int rr = 0; rr < 32; rr += 4) {
+        const int tr = rr + sub_r;
+        const long long grow = static_cast<long long>(m0) + q * 32 + tr;
+        const float4 acc = *reinterpret_cast<const float4*>(tile + tr * TP + sub_c);
+        if (nleft <= 0) continue;
+        float o[4] = {acc.x, acc.y, acc.z, acc.w};
+        bool write = grow < args.M;
+        if (EPI == EPI_SIGMOID) {
+#ifndef HB_DEBUG_EPI_NO_SIGMOID
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < ncols) {
-              const float s = a[j];
-              o[j] = v[j] * (s * (1.f - s));
+          for (int k = 0; k < 4; ++k) o[k] = sigmoidf_fast(o[k]);
+#endif
+        } else if (EPI == EPI_DSIG) {
+          if (write) {
+            const float* ap = args.aux + grow * args.ld_aux + gn;
+            float av[4];
+            if (vec_aux && nleft >= 4) {
+              const float4 t4 = *reinterpret_cast<const float4*>(ap);
+              av[0] = t4.x; av[1] = t4.y; av[2] = t4.z; av[3] = t4.w;
+            } else {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) av[k] = k < nleft ? ap[k] : 0.f;
             }
-        } else if (row < args.m_zero_rows) {
-          float* o = args.out + static_cast<long long>(row) * args.ldo + n;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < ncols) o[j] = 0.f;
+            for (int k = 0; k < 4; ++k) o[k] = o[k] * (av[k] * (1.f - av[k]));
+          } else if (grow < args.m_zero_rows) {
+            write = true;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) o[k] = 0.f;
+          }
         }
-      } else if (EPI == EPI_PARTIAL) {
-        if (row < args.M) {
-          float* o = args.out + blockIdx.z * args.split_stride + static_cast<long long>(row) * args.ldo + n;
+        if (!write) continue;
+#ifdef HB_DEBUG_EPI_NO_GLOBAL
+        if (o[0] == 12345.f) args.out[0] = o[1];
+        continue;
+#endif
+        if (EPI == EPI_SGD) {
+          float* wp = args.out + grow * args.ldo + gn;
+          if (vec_out && nleft >= 4) {
+            float4 w4 = *reinterpret_cast<float4*>(wp);
+            w4.x -= args.eta * o[0];
+            w4.y -= args.eta * o[1];
+            w4.z -= args.eta * o[2];
+            w4.w -= args.eta * o[3];
+            *reinterpret_cast<float4*>(wp) = w4;
+          } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < ncols) o[j] = v[j];
-        }
-      } else {  // EPI_SGD
-        if (row < args.M) {
-          float* w = args.out + static_cast<long long>(row) * args.ldo + n;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < ncols) w[j] = w[j] - args.eta * v[j];
+            for (int k = 0; k < 4; ++k)
+              if (k < nleft) wp[k] -= args.eta * o[k];
+          }
           if (args.grad != nullptr) {
-            float* g = args.grad + static_cast<long long>(row) * args.ld_grad + n;
+            float* gp = args.grad + grow * args.ld_grad + gn;
+            if (vec_grad && nleft >= 4) {
+              *reinterpret_cast<float4*>(gp) = make_float4(o[0], o[1], o[2], o[3]);
+            } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (j < ncols) g[j] = v[j];
+              for (int k = 0; k < 4; ++k)
+                if (k < nleft) gp[k] = o[k];
+            }
+          }
+        } else {
+          float* op = args.out + (EPI == EPI_PARTIAL ? static_cast<long long>(blockIdx.z) * args.split_stride : 0LL) +
+                      grow * args.ldo + gn;
+          if (vec_out && nleft >= 4) {
+            *reinterpret_cast<float4*>(op) = make_float4(o[0], o[1], o[2], o[3]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (k < nleft) op[k] = o[k];
           }
         }
       }
     }
-  } else if (PASSES == 3 && warp >= 8) {
+  } else if (PASSES == 3 && threadIdx.x >= C::SPLIT_BASE) {
     // ------------------------------------------------- hi/lo splitter
-    const int t = threadIdx.x - 256;
+    const int t = threadIdx.x - C::SPLIT_BASE;
     for (int i = 0; i < nkb; ++i) {
       const int s = i % STAGES;
       const uint32_t ph = (i / STAGES) & 1;
       mbar_wait(&full[s], ph);
-      uint4* hi = reinterpret_cast<uint4*>(smem + s * C::STAGE_BYTES);
-      float4* lo = reinterpret_cast<float4*>(smem + s * C::STAGE_BYTES + C::OP_BYTES);
+      if (t == 0) HB_STAMP(3 * 512 + i);  // split: TMA landed
+      const uint32_t hi = smem_u32(smem + s * C::STAGE_BYTES);
+      const uint32_t lo = hi + C::OP_BYTES;
 #pragma unroll 4
-      for (int j = t; j < C::OP_BYTES / 16; j += 128) {
-        uint4 x = hi[j];
-        uint4 h = make_uint4(to_tf32_rna(x.x), to_tf32_rna(x.y), to_tf32_rna(x.z), to_tf32_rna(x.w));
-        lo[j] = make_float4(__uint_as_float(x.x) - __uint_as_float(h.x), __uint_as_float(x.y) - __uint_as_float(h.y),
-                            __uint_as_float(x.z) - __uint_as_float(h.z), __uint_as_float(x.w) - __uint_as_float(h.w));
-        hi[j] = h;
+      for (int j = t; j < C::OP_BYTES / 16; j += C::SPLIT_THREADS) {
+        uint32_t x0, x1, x2, x3;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3) : "r"(hi + 16 * j));
+#if HB_SPLIT_HI_RAW
+        const uint32_t h0 = x0 & 0xFFFFE000u, h1 = x1 & 0xFFFFE000u, h2 = x2 & 0xFFFFE000u, h3 = x3 & 0xFFFFE000u;
+#else
+        const uint32_t h0 = to_tf32_rna(x0), h1 = to_tf32_rna(x1), h2 = to_tf32_rna(x2), h3 = to_tf32_rna(x3);
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(hi + 16 * j), "r"(h0), "r"(h1), "r"(h2), "r"(h3));
+#endif
+        const float l0 = __uint_as_float(x0) - __uint_as_float(h0), l1 = __uint_as_float(x1) - __uint_as_float(h1),
+                    l2 = __uint_as_float(x2) - __uint_as_float(h2), l3 = __uint_as_float(x3) - __uint_as_float(h3);
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lo + 16 * j), "f"(l0), "f"(l1), "f"(l2), "f"(l3));
       }
       fence_proxy_async_smem();
       mbar_arrive(&ready[s]);
+      if (t == 0) HB_STAMP(4 * 512 + i);  // split: done
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) HB_STAMP(6 * 512 + 1);  // CTA end
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);

@@ -36,7 +36,7 @@ __device__ __forceinline__ float warp_max(float v) {
 // owns HEAD_ROWS_PER_BLOCK consecutive rows and reduces its 8 warps' dW
 // partials in warp order, so the result is deterministic.
 constexpr int kHeadWarps = 8;
-constexpr int kHeadRowsPerBlock = 32;
+constexpr int kHeadRowsPerBlock = 16;
 
 struct HeadArgs {
   const float* a;          // (rows, d) last hidden activation
@@ -57,7 +57,7 @@ struct HeadArgs {
 };
 
 template <int NCT, int MAXT>
-__global__ void __launch_bounds__(kHeadWarps * 32) head_small_kernel(const HeadArgs p) {
+__global__ void __launch_bounds__(kHeadWarps * 32, (MAXT <= 16 && NCT <= 2) ? 2 : 1) head_small_kernel(const HeadArgs p) {
   __shared__ float sW[NCT * 32 * MAXT];
   __shared__ double sLoss[kHeadWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -169,6 +169,150 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_small_kernel(const HeadA
   }
 }
 
+// Vectorised variant for d % 4 == 0 (all padded row strides are multiples of
+// 4 floats): lanes own float4 column groups 4*lane + 128*t, t < VPL, and each
+// warp keeps its two rows' loads in flight together.  Same math and the same
+// fixed reduction order (per-warp row order, then warps in order).
+template <int NCT, int VPL>
+__global__ void __launch_bounds__(kHeadWarps * 32) head_small_vec_kernel(const HeadArgs p) {
+  __shared__ __align__(16) float sW[NCT * 128 * VPL];
+  __shared__ double sLoss[kHeadWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int D = 128 * VPL;
+  for (int i = threadIdx.x; i < NCT * D; i += blockDim.x) {
+    const int c = i / D, j = i % D;
+    sW[i] = (c < p.nc && j < p.d) ? p.w[c * p.ldw + j] : 0.f;
+  }
+  __syncthreads();
+  float4 acc[NCT][VPL];
+#pragma unroll
+  for (int c = 0; c < NCT; ++c)
+#pragma unroll
+    for (int t = 0; t < VPL; ++t) acc[c][t] = make_float4(0.f, 0.f, 0.f, 0.f);
+  double loss = 0.0;
+  constexpr int RPW = kHeadRowsPerBlock / kHeadWarps;  // rows per warp (2)
+  const int rbase = blockIdx.x * kHeadRowsPerBlock + warp * RPW;
+  float4 av[RPW][VPL];
+#pragma unroll
+  for (int k = 0; k < RPW; ++k)
+#pragma unroll
+    for (int t = 0; t < VPL; ++t) {
+      const int j = 4 * lane + 128 * t;
+      const int row = rbase + k;
+      av[k][t] = (row < p.rows && j < p.d) ? *reinterpret_cast<const float4*>(p.a + row * p.lda + j)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  float z[RPW][NCT];
+#pragma unroll
+  for (int k = 0; k < RPW; ++k)
+#pragma unroll
+    for (int c = 0; c < NCT; ++c) {
+      float sacc = 0.f;
+#pragma unroll
+      for (int t = 0; t < VPL; ++t) {
+        const float4 w4 = *reinterpret_cast<const float4*>(&sW[c * D + 4 * lane + 128 * t]);
+        sacc = fmaf(av[k][t].x, w4.x, sacc);
+        sacc = fmaf(av[k][t].y, w4.y, sacc);
+        sacc = fmaf(av[k][t].z, w4.z, sacc);
+        sacc = fmaf(av[k][t].w, w4.w, sacc);
+      }
+      z[k][c] = sacc;
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < RPW; ++k)
+#pragma unroll
+      for (int c = 0; c < NCT; ++c) z[k][c] += __shfl_xor_sync(0xffffffffu, z[k][c], o);
+#pragma unroll
+  for (int k = 0; k < RPW; ++k) {
+    const int row = rbase + k;
+    if (row >= p.rows) {
+      if (p.train && p.delta_prev != nullptr && row < p.zero_rows) {
+#pragma unroll
+        for (int t = 0; t < VPL; ++t) {
+          const int j = 4 * lane + 128 * t;
+          if (j < p.d) *reinterpret_cast<float4*>(p.delta_prev + row * p.ld_dp + j) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      continue;
+    }
+    float zmax = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < NCT; ++c)
+      if (c < p.nc) zmax = fmaxf(zmax, z[k][c]);
+    float e[NCT], esum = 0.f;
+#pragma unroll
+    for (int c = 0; c < NCT; ++c) {
+      e[c] = c < p.nc ? expf(z[k][c] - zmax) : 0.f;
+      esum += e[c];
+    }
+    const int y = static_cast<int>(p.labels[row]);
+    float py = 0.f;
+#pragma unroll
+    for (int c = 0; c < NCT; ++c)
+      if (c == y) py = e[c] / esum;
+    loss += -log(fmax(static_cast<double>(py), 1e-12));
+    if (!p.train) continue;
+    float dl[NCT];
+#pragma unroll
+    for (int c = 0; c < NCT; ++c) dl[c] = c < p.nc ? (e[c] / esum - (c == y ? 1.f : 0.f)) * p.inv_n : 0.f;
+#pragma unroll
+    for (int t = 0; t < VPL; ++t) {
+      const int j = 4 * lane + 128 * t;
+      float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < NCT; ++c) {
+        const float4 w4 = *reinterpret_cast<const float4*>(&sW[c * D + j]);
+        g.x = fmaf(dl[c], w4.x, g.x);
+        g.y = fmaf(dl[c], w4.y, g.y);
+        g.z = fmaf(dl[c], w4.z, g.z);
+        g.w = fmaf(dl[c], w4.w, g.w);
+        acc[c][t].x = fmaf(dl[c], av[k][t].x, acc[c][t].x);
+        acc[c][t].y = fmaf(dl[c], av[k][t].y, acc[c][t].y);
+        acc[c][t].z = fmaf(dl[c], av[k][t].z, acc[c][t].z);
+        acc[c][t].w = fmaf(dl[c], av[k][t].w, acc[c][t].w);
+      }
+      if (p.delta_prev != nullptr && j < p.d) {
+        const float4 a4 = av[k][t];
+        *reinterpret_cast<float4*>(p.delta_prev + row * p.ld_dp + j) =
+            make_float4(g.x * (a4.x * (1.f - a4.x)), g.y * (a4.y * (1.f - a4.y)), g.z * (a4.z * (1.f - a4.z)),
+                        g.w * (a4.w * (1.f - a4.w)));
+      }
+    }
+  }
+  if (lane == 0) sLoss[warp] = loss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kHeadWarps; ++w) t += sLoss[w];
+    p.ws_loss[blockIdx.x] = t;
+  }
+  if (!p.train) return;
+  for (int c = 0; c < NCT && c < p.nc; ++c) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < D; j += blockDim.x) sW[j] = 0.f;
+    __syncthreads();
+    for (int w = 0; w < kHeadWarps; ++w) {
+      if (warp == w) {
+#pragma unroll
+        for (int t = 0; t < VPL; ++t) {
+          float4* sp = reinterpret_cast<float4*>(&sW[4 * lane + 128 * t]);
+          float4 v = *sp;
+          v.x += acc[c][t].x;
+          v.y += acc[c][t].y;
+          v.z += acc[c][t].z;
+          v.w += acc[c][t].w;
+          *sp = v;
+        }
+      }
+      __syncthreads();
+    }
+    for (int j = threadIdx.x; j < p.d; j += blockDim.x)
+      p.ws_dw[(static_cast<long long>(blockIdx.x) * p.nc + c) * p.d + j] = sW[j];
+  }
+}
+
 // ------------------------------------------------------------------------
 // Wide head second pass: logits (rows, nc) -> delta in place + per-row loss.
 // One warp per row, row max shift as linalg.py:63-67.
@@ -219,27 +363,52 @@ __global__ void __launch_bounds__(256) softmax_delta_kernel(const SoftmaxArgs p)
   }
 }
 
-// Fixed-order sum of per-block loss partials (one thread; tiny).
+// Fixed-order sum of per-block loss partials: one warp, lane-strided partial
+// sums then a fixed shuffle tree (deterministic).
 __global__ void loss_reduce_kernel(const double* ws, int n, double* out, int accumulate) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < n; ++i) s += ws[i];
-    *out = accumulate ? *out + s : s;
-  }
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int i = lane; i < n; i += 32) s += ws[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) *out = accumulate ? *out + s : s;
 }
 
 // ------------------------------------------------------------------------
 // W (rows, cols, ldw) -= eta * sum_{s<S} P[s] (rows, cols, dense), in place.
 // The split-K / per-block partials are summed in slab order -> deterministic.
+// Launch with one block of 256 threads per 32 consecutive elements: the 8
+// warps split the slabs (warp w takes s = w, w+8, ...), then warp 0 adds the
+// 8 warp sums in order -- a fixed summation order for every element.
 __global__ void __launch_bounds__(256) reduce_sgd_kernel(float* w, long long ldw, const float* part, int S,
                                                            long long slab, int rows, int cols, float eta,
                                                            float* grad, long long ldg) {
+  __shared__ float red[8][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long i = blockIdx.x * 32LL + lane;
   const long long total = static_cast<long long>(rows) * cols;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(i / cols), c = static_cast<int>(i % cols);
+  // warp w sums slabs s = w, w+8, w+16, ... as four interleaved chains
+  // (fixed order: chain k takes every fourth of the warp's slabs)
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  if (i < total) {
+    int s = warp;
+    for (; s + 24 < S; s += 32) {
+      s0 += __ldcs(part + s * slab + i);
+      s1 += __ldcs(part + (s + 8) * slab + i);
+      s2 += __ldcs(part + (s + 16) * slab + i);
+      s3 += __ldcs(part + (s + 24) * slab + i);
+    }
+    if (s < S) s0 += __ldcs(part + s * slab + i);
+    if (s + 8 < S) s1 += __ldcs(part + (s + 8) * slab + i);
+    if (s + 16 < S) s2 += __ldcs(part + (s + 16) * slab + i);
+  }
+  red[warp][lane] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (warp == 0 && i < total) {
     float g = 0.f;
-    for (int s = 0; s < S; ++s) g += part[s * slab + i];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) g += red[k][lane];
+    const long long r = i / cols, c = i % cols;
     w[r * ldw + c] -= eta * g;
     if (grad != nullptr) grad[r * ldg + c] = g;
   }
@@ -356,84 +525,78 @@ __device__ __forceinline__ long long lower_bound_i32(const int32_t* a, long long
   return lo;
 }
 
+// One block (8 warps) per (input feature f, 128-column chunk): the warps
+// split the feature's batch entries round-robin (entry e -> warp (e-lo) % 8,
+// four entries in flight per warp), each lane owns one float4 of the chunk;
+// the 8 partial rows are added in warp order in shared memory and applied to
+// W0T[f, chunk] in place (gradient optionally kept).  Fixed summation order.
 template <bool VEC>
 __global__ void __launch_bounds__(256) sparse_dw_kernel(const SparseDwArgs p) {
-  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (f >= p.d_in) return;
-  const long long c0 = p.colptr[f], c1 = p.colptr[f + 1];
-  long long lo = 0, hi = 0;
-  if (lane == 0) {
-    lo = lower_bound_i32(p.rowidx, c0, c1, p.start);
-    hi = lower_bound_i32(p.rowidx, lo, c1, p.start + p.rows);
+  __shared__ float red[8][128];
+  __shared__ long long s_rng[2];
+  const int f = blockIdx.x;
+  const int base = blockIdx.y * 128;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    const long long c0 = p.colptr[f], c1 = p.colptr[f + 1];
+    const long long lo = lower_bound_i32(p.rowidx, c0, c1, p.start);
+    s_rng[0] = lo;
+    s_rng[1] = lower_bound_i32(p.rowidx, lo, c1, p.start + p.rows);
   }
-  lo = __shfl_sync(0xffffffffu, lo, 0);
-  hi = __shfl_sync(0xffffffffu, hi, 0);
-  float* wrow = p.w0t + static_cast<long long>(f) * p.ldw;
-  float* grow = p.grad != nullptr ? p.grad + static_cast<long long>(f) * p.ldg : nullptr;
+  __syncthreads();
+  const long long lo = s_rng[0], hi = s_rng[1];
+  const int width = min(128, p.d_out - base);
+  float* wrow = p.w0t + static_cast<long long>(f) * p.ldw + base;
+  float* grow = p.grad != nullptr ? p.grad + static_cast<long long>(f) * p.ldg + base : nullptr;
   if (lo == hi) {
-    if (grow != nullptr)
-      for (int j = lane; j < p.d_out; j += 32) grow[j] = 0.f;
+    if (grow != nullptr && threadIdx.x < width) grow[threadIdx.x] = 0.f;
     return;
   }
   if (VEC) {
-    for (int base = 0; base < p.d_out; base += 128 * 8) {
-      float4 acc[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (long long e = lo; e < hi; ++e) {
-        const float v = __ldg(p.cval + e);
-        const float4* dr =
-            reinterpret_cast<const float4*>(p.delta0 + (static_cast<long long>(__ldg(p.rowidx + e)) - p.start) * p.ldd);
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const int j = base + 4 * lane + 128 * t;
-          if (j < p.d_out) {
-            const float4 d = __ldg(dr + j / 4);
-            acc[t].x = fmaf(v, d.x, acc[t].x);
-            acc[t].y = fmaf(v, d.y, acc[t].y);
-            acc[t].z = fmaf(v, d.z, acc[t].z);
-            acc[t].w = fmaf(v, d.w, acc[t].w);
-          }
-        }
+    const int j = 4 * lane;
+    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+    if (j < width) {
+      long long e = lo + warp;
+      for (; e + 8 < hi; e += 16) {
+        const float v0 = __ldg(p.cval + e), v1 = __ldg(p.cval + e + 8);
+        const float4 d0 = __ldg(reinterpret_cast<const float4*>(
+            p.delta0 + (static_cast<long long>(__ldg(p.rowidx + e)) - p.start) * p.ldd + base + j));
+        const float4 d1 = __ldg(reinterpret_cast<const float4*>(
+            p.delta0 + (static_cast<long long>(__ldg(p.rowidx + e + 8)) - p.start) * p.ldd + base + j));
+        a0.x = fmaf(v0, d0.x, a0.x); a0.y = fmaf(v0, d0.y, a0.y); a0.z = fmaf(v0, d0.z, a0.z); a0.w = fmaf(v0, d0.w, a0.w);
+        a1.x = fmaf(v1, d1.x, a1.x); a1.y = fmaf(v1, d1.y, a1.y); a1.z = fmaf(v1, d1.z, a1.z); a1.w = fmaf(v1, d1.w, a1.w);
       }
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const int j = base + 4 * lane + 128 * t;
-        if (j < p.d_out) {
-          float4 w = reinterpret_cast<float4*>(wrow)[j / 4];
-          w.x -= p.eta * acc[t].x;
-          w.y -= p.eta * acc[t].y;
-          w.z -= p.eta * acc[t].z;
-          w.w -= p.eta * acc[t].w;
-          reinterpret_cast<float4*>(wrow)[j / 4] = w;
-          if (grow != nullptr) reinterpret_cast<float4*>(grow)[j / 4] = acc[t];
-        }
+      if (e < hi) {
+        const float v0 = __ldg(p.cval + e);
+        const float4 d0 = __ldg(reinterpret_cast<const float4*>(
+            p.delta0 + (static_cast<long long>(__ldg(p.rowidx + e)) - p.start) * p.ldd + base + j));
+        a0.x = fmaf(v0, d0.x, a0.x); a0.y = fmaf(v0, d0.y, a0.y); a0.z = fmaf(v0, d0.z, a0.z); a0.w = fmaf(v0, d0.w, a0.w);
       }
+      *reinterpret_cast<float4*>(&red[warp][j]) =
+          make_float4(a0.x + a1.x, a0.y + a1.y, a0.z + a1.z, a0.w + a1.w);
     }
   } else {
-    for (int base = 0; base < p.d_out; base += 32 * 8) {
-      float acc[8];
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (long long e = lo + warp; e < hi; e += 8) {
+      const float v = __ldg(p.cval + e);
+      const float* dr = p.delta0 + (static_cast<long long>(__ldg(p.rowidx + e)) - p.start) * p.ldd + base;
 #pragma unroll
-      for (int t = 0; t < 8; ++t) acc[t] = 0.f;
-      for (long long e = lo; e < hi; ++e) {
-        const float v = __ldg(p.cval + e);
-        const float* dr = p.delta0 + (static_cast<long long>(__ldg(p.rowidx + e)) - p.start) * p.ldd;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const int j = base + lane + 32 * t;
-          if (j < p.d_out) acc[t] = fmaf(v, __ldg(dr + j), acc[t]);
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const int j = base + lane + 32 * t;
-        if (j < p.d_out) {
-          wrow[j] -= p.eta * acc[t];
-          if (grow != nullptr) grow[j] = acc[t];
-        }
+      for (int t = 0; t < 4; ++t) {
+        const int j = lane + 32 * t;
+        if (j < width) acc[t] = fmaf(v, __ldg(dr + j), acc[t]);
       }
     }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) red[warp][lane + 32 * t] = acc[t];
+  }
+  __syncthreads();
+  if (threadIdx.x < width) {
+    const int j = threadIdx.x;
+    float g = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) g += (lo + k < hi) ? red[k][j] : 0.f;
+    wrow[j] -= p.eta * g;
+    if (grow != nullptr) grow[j] = g;
   }
 }
 

@@ -36,6 +36,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+from paper_2004_08771_b200.parallel import batch_starts, init_replica_comm, max_over_ranks, shard_seed  # noqa: E402
+
 METRIC = "MLP train samples/sec"
 UNIT = "samples/s"
 
@@ -70,10 +72,11 @@ def dense_flops_per_sample(sizes, sparse_first):
 def make_data(cfg, seed, rank=0):
     import paper_2004_08771_b200 as hb
 
+    s = shard_seed(seed, rank)
     if cfg["kind"] == "csr":
-        return hb.synthetic_csr(cfg["n"], cfg["sizes"][0], cfg["nnz"], cfg["classes"], seed=seed + rank,
+        return hb.synthetic_csr(cfg["n"], cfg["sizes"][0], cfg["nnz"], cfg["classes"], seed=s,
                                 binary=cfg["binary"], normalize=cfg["normalize"])
-    return hb.synthetic_blobs(cfg["n"], cfg["sizes"][0], cfg["classes"], 2.5, seed=seed + rank)
+    return hb.synthetic_blobs(cfg["n"], cfg["sizes"][0], cfg["classes"], 2.5, seed=s)
 
 
 class ClockSampler:
@@ -188,14 +191,8 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
     else:
         ctx.stage(data.features.astype(np.float32), data.labels)
     if world > 1:
-        uid = hb.GpuReplica.nccl_unique_id() if rank == 0 else bytes(128)
-        import torch
-
-        t = torch.tensor(list(uid), dtype=torch.uint8)
-        dist.broadcast(t, 0)
-        ctx.comm_init(bytes(t.tolist()), world, rank)
-    n_batches = max(1, (n - b) // b + 1)
-    starts = [(i % n_batches) * b for i in range(args.warmup + args.steps)]
+        init_replica_comm(ctx, dist, rank, world)
+    starts = batch_starts(n, b, args.warmup + args.steps)
 
     import torch
 
@@ -233,9 +230,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
     ctx.profile(False)
     total_ms = sum(step_ms) + sum(merge_ms)
     if world > 1:
-        tt = torch.tensor([total_ms], dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
+        total_ms = max_over_ranks(dist, total_ms)
     value = world * args.steps * b / (total_ms / 1000.0)
 
     # ---------------------------------------------------------- e2e (drop-in replica semantics)
@@ -274,9 +269,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
             ctx.merge_grads_into(host_model, cfg["eta"])  # stale merge (workers.py:135)
         el = time.perf_counter() - t0
         if world > 1:
-            tt = torch.tensor([el], dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            el = float(tt.item())
+            el = max_over_ranks(dist, el)
         e2e = {"value": world * args.steps * b / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
                "path": "execute_gpu_replica semantics via the C ABI: f64 model snapshot H2D + host batch H2D "

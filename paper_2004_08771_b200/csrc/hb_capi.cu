@@ -21,7 +21,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/hogbatch_b200.h"
@@ -196,6 +198,17 @@ struct DataView {
   const int64_t* labels = nullptr;
 };
 
+struct Mark {
+  std::string name;
+  cudaEvent_t e0, e1;
+};
+struct StepGraph {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<Mark> marks;
+  std::vector<cudaEvent_t> events;
+  int launches = 0;
+};
+
 struct hb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -255,7 +268,17 @@ struct hb_ctx {
   bool prof_on = false;
   std::vector<cudaEvent_t> evpool;
   size_t ev_used = 0;
-  std::vector<std::pair<std::string, size_t>> marks;
+  std::pair<cudaEvent_t, cudaEvent_t> pending;
+  std::vector<Mark> step_marks;
+  std::map<std::string, std::pair<double, int>> prof_acc;
+  // CUDA graphs of the step, one per (rows, flags, data view generation)
+  bool use_graphs = true;
+  bool capturing = false;
+  std::vector<cudaEvent_t> cap_events;
+  std::map<std::tuple<int, uint32_t, long long, bool>, StepGraph> graphs;
+  std::map<std::tuple<int, uint32_t, long long, bool>, int> graph_seen;
+  DevStep* d_step = nullptr;  // device copy of the per-step scalars
+  long long view_gen = 1;     // bumped whenever staged buffers / maps change
   void* comm = nullptr;
   int nranks = 1;
   float* flat = nullptr;  // contiguous model copy for allreduce
@@ -270,28 +293,57 @@ int ctx_check(hb_ctx* c) {
   return HB_OK;
 }
 
+// Profiling marks: (kernel name, begin event, end event) on the step stream.
+// Eager steps take events from a reusable pool; a captured graph owns its
+// events (they become event-record nodes) and re-reads them after every launch.
 void prof_begin(hb_ctx* c) {
   if (!c->prof_on) return;
-  while (c->evpool.size() < c->ev_used + 2) {
-    cudaEvent_t e;
-    if (cudaEventCreate(&e) != cudaSuccess) {
-      c->prof_on = false;
-      return;
+  cudaEvent_t e0, e1;
+  if (c->capturing) {
+    if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return;
+    c->cap_events.push_back(e0);
+    c->cap_events.push_back(e1);
+  } else {
+    while (c->evpool.size() < c->ev_used + 2) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return;
+      c->evpool.push_back(e);
     }
-    c->evpool.push_back(e);
+    e0 = c->evpool[c->ev_used];
+    e1 = c->evpool[c->ev_used + 1];
+    c->ev_used += 2;
   }
-  cudaEventRecord(c->evpool[c->ev_used], c->stream);
+  c->pending = {e0, e1};
+  // inside stream capture a plain record is only a dependency marker; the
+  // External flag makes it a real event-record node of the graph
+  if (c->capturing)
+    cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e0, c->stream);
 }
 void prof_end(hb_ctx* c, const char* kind, int layer) {
   if (!c->prof_on) return;
-  cudaEventRecord(c->evpool[c->ev_used + 1], c->stream);
+  if (c->capturing)
+    cudaEventRecordWithFlags(c->pending.second, c->stream, cudaEventRecordExternal);
+  else
+    cudaEventRecord(c->pending.second, c->stream);
   char name[64];
   if (layer >= 0)
     snprintf(name, sizeof name, "%s_l%d", kind, layer);
   else
     snprintf(name, sizeof name, "%s", kind);
-  c->marks.emplace_back(name, c->ev_used);
-  c->ev_used += 2;
+  c->step_marks.push_back({name, c->pending.first, c->pending.second});
+}
+// fold the marks of a completed step into the per-kernel totals
+int prof_resolve(hb_ctx* c, const std::vector<Mark>& marks) {
+  for (auto& m : marks) {
+    float ms = 0.f;
+    HB_CUDA(cudaEventElapsedTime(&ms, m.e0, m.e1));
+    auto& acc = c->prof_acc[m.name];
+    acc.first += ms;
+    acc.second += 1;
+  }
+  return HB_OK;
 }
 
 int build_data_maps(hb_ctx* c, DataView& v) {
@@ -322,7 +374,10 @@ void dw_plan(const hb_ctx* c, int l, int rows, int* splits, int* kb_per, int* kb
   *splits = cdiv(*kb_total, *kb_per);
 }
 
-int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool train, uint32_t flags, double eta) {
+// `ds` != null: graph mode -- kernels read the batch start and eta from
+// device memory (the by-value start/eta are then 0 and ignored).
+int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool train, uint32_t flags, double eta,
+                const DevStep* ds) {
   cudaStream_t st = c->stream;
   const int L = c->L;
   const int m_tiles = cdiv(rows, kBM);
@@ -330,7 +385,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   // hidden layers
   for (int l = 0; l < L - 1; ++l) {
     if (l == 0 && c->sparse) {
-      SpmmArgs p{v.rowptr, v.col, v.val, start, rows, c->W[0], c->ldw[0], c->d[1], c->A[1], c->ld[1]};
+      SpmmArgs p{v.rowptr, v.col, v.val, ds, start, rows, c->W[0], c->ldw[0], c->d[1], c->A[1], c->ld[1]};
       const int blocks = cdiv(static_cast<long long>(rows) * 32, 256);
       prof_begin(c);
       if (c->d[1] % 128 == 0)
@@ -346,6 +401,8 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     a.M = rows;
     a.N = c->d[l + 1];
     a.a_off = l == 0 ? static_cast<int>(start) : 0;
+    a.a_start = (l == 0) ? 1 : 0;
+    a.ds = ds;
     a.kb_total = cdiv(c->d[l], kBK);
     a.kb_per_split = a.kb_total;
     a.out = c->A[l + 1];
@@ -360,19 +417,21 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   // output layer
   const int l = L - 1;
   const float inv_n = 1.0f / static_cast<float>(rows);
-  const int64_t* labels = v.labels + start;
   if (c->small_head) {
     HeadArgs h{};
     if (L == 1) {
-      h.a = v.x + start * v.ldx;
+      h.a = v.x;
       h.lda = v.ldx;
+      h.a_input = 1;
     } else {
       h.a = c->A[L - 1];
       h.lda = c->ld[L - 1];
     }
     h.w = c->W[l];
     h.ldw = c->ldw[l];
-    h.labels = labels;
+    h.labels = v.labels;
+    h.start = start;
+    h.ds = ds;
     h.rows = rows;
     h.d = c->d[l];
     h.nc = c->d[L];
@@ -422,9 +481,9 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     if (train) {
       const long long n = static_cast<long long>(c->d[L]) * c->d[l];
       prof_begin(c);
-      reduce_sgd_kernel<<<cdiv(n, 32), 256, 0, st>>>(
-          c->W[l], c->ldw[l], c->ws, grid, n, c->d[L], c->d[l], static_cast<float>(eta),
-          (flags & HB_STEP_EMIT_GRAD) ? c->G[l] : nullptr, c->d[l]);
+      reduce_sgd_kernel<<<cdiv(n, 32), 256, 0, st>>>(c->W[l], c->ldw[l], c->ws, grid, n, c->d[L], c->d[l],
+                                                     static_cast<float>(eta),
+                                                     (flags & HB_STEP_EMIT_GRAD) ? c->G[l] : nullptr, c->d[l], ds);
       HB_CUDA(cudaGetLastError());
       prof_end(c, "reduce_sgd", l);
       c->last_launches++;
@@ -436,6 +495,8 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   a.M = rows;
   a.N = c->d[L];
   a.a_off = l == 0 ? static_cast<int>(start) : 0;
+  a.a_start = (l == 0) ? 1 : 0;
+  a.ds = ds;
   a.kb_total = cdiv(c->d[l], kBK);
   a.kb_per_split = a.kb_total;
   a.out = c->D[l];
@@ -445,10 +506,10 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   HB_TRY(launch_gemm(c->passes, G_FWD, EPI_STORE, c->bn_fwd[l], ta, c->tmW_k[l], a, m_tiles, cdiv(a.N, c->bn_fwd[l]),
                      1, st));
   prof_end(c, "gemm_fwd_logits", l);
-  SoftmaxArgs s{c->D[l], c->ld[L], labels, rows, c->d[L], zrows, inv_n, train ? 1 : 0, c->ws_loss};
+  SoftmaxArgs sm{c->D[l], c->ld[L], v.labels, start, ds, rows, c->d[L], zrows, inv_n, train ? 1 : 0, c->ws_loss};
   const int grid = cdiv(std::max(rows, zrows), 8);
   prof_begin(c);
-  softmax_delta_kernel<<<grid, 256, 0, st>>>(s);
+  softmax_delta_kernel<<<grid, 256, 0, st>>>(sm);
   HB_CUDA(cudaGetLastError());
   prof_end(c, "softmax_delta", l);
   loss_reduce_kernel<<<1, 32, 0, st>>>(c->ws_loss, grid, c->d_loss, 0);
@@ -457,10 +518,10 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   return HB_OK;
 }
 
-int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32_t flags, double eta) {
+int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32_t flags, double eta,
+                 const DevStep* ds) {
   cudaStream_t st = c->stream;
   const int L = c->L;
-  const int m_tiles = cdiv(rows, kBM);
   const int zrows = std::min<long long>(round_up(rows, kBM), c->cap);
   const bool emit = (flags & HB_STEP_EMIT_GRAD) != 0;
   // with the small head the output layer is already done (dW + delta_{L-2})
@@ -478,6 +539,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       a.ldo = c->ld[l];
       a.aux = c->A[l];
       a.ld_aux = c->ld[l];
+      a.ds = ds;
       prof_begin(c);
       HB_TRY(launch_gemm(c->passes, G_DX, EPI_DSIG, c->bn_dx[l], c->tmD_k[l], c->tmW_mn[l], a,
                          cdiv(zrows, kBM), cdiv(a.N, c->bn_dx[l]), 1, st));
@@ -486,7 +548,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
     }
     // dW + SGD
     if (l == 0 && c->sparse) {
-      SparseDwArgs p{v.colptr, v.rowidx, v.cval, start, rows, c->d[0], c->d[1], c->D[0], c->ld[1],
+      SparseDwArgs p{v.colptr, v.rowidx, v.cval, ds, start, rows, c->d[0], c->d[1], c->D[0], c->ld[1],
                      c->W[0], c->ldw[0], static_cast<float>(eta), emit ? c->G[0] : nullptr, c->ldw[0]};
       const dim3 blocks(c->d[0], cdiv(c->d[1], 128));
       prof_begin(c);
@@ -505,6 +567,8 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
     a.M = c->d[l + 1];
     a.N = c->d[l];
     a.b_off = l == 0 ? static_cast<int>(start) : 0;
+    a.b_start = (l == 0) ? 1 : 0;
+    a.ds = ds;
     a.kb_total = kb_total;
     a.kb_per_split = kb_per;
     a.eta = static_cast<float>(eta);
@@ -528,9 +592,9 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       HB_TRY(launch_gemm(c->passes, G_DW, EPI_PARTIAL, c->bn_dw[l], c->tmD_mn[l], tb, a, mt, nt, splits, st));
       prof_end(c, "gemm_dw_partial", l);
       prof_begin(c);
-      reduce_sgd_kernel<<<cdiv(slab, 32), 256, 0, st>>>(
-          c->W[l], c->ldw[l], c->ws, splits, slab, a.M, a.N, static_cast<float>(eta), emit ? c->G[l] : nullptr,
-          c->d[l]);
+      reduce_sgd_kernel<<<cdiv(slab, 32), 256, 0, st>>>(c->W[l], c->ldw[l], c->ws, splits, slab, a.M, a.N,
+                                                        static_cast<float>(eta), emit ? c->G[l] : nullptr, c->d[l],
+                                                        ds);
       HB_CUDA(cudaGetLastError());
       prof_end(c, "reduce_sgd", l);
       c->last_launches += 2;
@@ -539,13 +603,73 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
   return HB_OK;
 }
 
-int do_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta, uint32_t flags, double* out_loss) {
+// Enqueue one step.  Eager the first time a (rows, flags, data view) shape is
+// seen; from the second time on, the whole step is a captured CUDA graph that
+// reads (start, eta) from c->d_step, so a step costs one graph launch.
+int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta, uint32_t flags, bool graph_ok) {
+  const uint32_t gflags = flags & HB_STEP_EMIT_GRAD;
+  const bool view_epoch = (&v == &c->epoch);
+  if (!c->use_graphs || !graph_ok) {
+    HB_TRY(run_forward(c, v, start, rows, true, flags, eta, nullptr));
+    return run_backward(c, v, start, rows, flags, eta, nullptr);
+  }
+  const auto key = std::make_tuple(rows, gflags, view_epoch ? c->view_gen : -c->view_gen, c->prof_on);
+  DevStep hs{start, static_cast<float>(eta), 0};
+  auto it = c->graphs.find(key);
+  if (it == c->graphs.end()) {
+    if (c->graph_seen[key]++ == 0) {  // first sighting: run eagerly (also configures kernel attributes)
+      HB_TRY(run_forward(c, v, start, rows, true, flags, eta, nullptr));
+      return run_backward(c, v, start, rows, flags, eta, nullptr);
+    }
+    StepGraph g;
+    c->capturing = true;
+    c->cap_events.clear();
+    c->step_marks.clear();
+    HB_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const int launches0 = c->last_launches;
+    int rc = run_forward(c, v, 0, rows, true, flags, 0.0, c->d_step);
+    if (rc == HB_OK) rc = run_backward(c, v, 0, rows, flags, 0.0, c->d_step);
+    cudaGraph_t graph = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
+    c->capturing = false;
+    if (rc != HB_OK) return rc;
+    if (ce != cudaSuccess) return fail(HB_ECUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+    ce = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) return fail(HB_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(ce));
+    g.marks = c->step_marks;
+    g.events = c->cap_events;
+    g.launches = c->last_launches - launches0;
+    c->step_marks.clear();
+    c->cap_events.clear();
+    it = c->graphs.emplace(key, std::move(g)).first;
+    c->last_launches = 0;
+  }
+  HB_CUDA(cudaMemcpyAsync(c->d_step, &hs, sizeof hs, cudaMemcpyHostToDevice, c->stream));
+  HB_CUDA(cudaGraphLaunch(it->second.exec, c->stream));
+  c->last_launches += it->second.launches;
+  if (c->prof_on) c->step_marks = it->second.marks;
+  return HB_OK;
+}
+
+void drop_graphs(hb_ctx* c) {
+  for (auto& kv : c->graphs) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    for (auto e : kv.second.events) cudaEventDestroy(e);
+  }
+  c->graphs.clear();
+  c->graph_seen.clear();
+}
+
+int do_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta, uint32_t flags, double* out_loss,
+            bool graph_ok = true) {
   if (rows < 1 || rows > c->max_batch) return fail(HB_EINVAL, "rows=%d outside [1, %d]", rows, c->max_batch);
   c->last_launches = 0;
+  c->ev_used = 0;
+  c->step_marks.clear();
   const bool timed = (flags & HB_STEP_TIMED) != 0;
   if (timed) HB_CUDA(cudaEventRecord(c->ev0, c->stream));
-  HB_TRY(run_forward(c, v, start, rows, true, flags, eta));
-  HB_TRY(run_backward(c, v, start, rows, flags, eta));
+  HB_TRY(enqueue_step(c, v, start, rows, eta, flags, graph_ok));
   if (timed) HB_CUDA(cudaEventRecord(c->ev1, c->stream));
   c->grads_valid = (flags & HB_STEP_EMIT_GRAD) != 0;
   if (out_loss != nullptr) {
@@ -553,12 +677,16 @@ int do_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta,
     HB_CUDA(cudaMemcpyAsync(&s, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     HB_CUDA(cudaStreamSynchronize(c->stream));
     *out_loss = s / rows;
-  } else if (!(flags & HB_STEP_ASYNC)) {
+  } else if (!(flags & HB_STEP_ASYNC) || c->prof_on) {
     HB_CUDA(cudaStreamSynchronize(c->stream));
   }
   if (timed) {
     HB_CUDA(cudaEventSynchronize(c->ev1));
     HB_CUDA(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+  }
+  if (c->prof_on) {
+    HB_TRY(prof_resolve(c, c->step_marks));
+    c->step_marks.clear();
   }
   return HB_OK;
 }
@@ -610,6 +738,7 @@ int free_epoch(hb_ctx* c) {
   c->ecval = nullptr;
   c->staged = false;
   c->e_rows = 0;
+  c->view_gen++;  // captured graphs baked the old buffers / tensor maps
   return HB_OK;
 }
 
@@ -745,6 +874,9 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
   c->ws_loss_n = std::max(cdiv(c->cap, kHeadRowsPerBlock), cdiv(c->cap, 8)) + 1;
   HB_CK(cudaMalloc(&c->ws_loss, c->ws_loss_n * sizeof(double)));
   HB_CK(cudaMalloc(&c->d_loss, sizeof(double)));
+  HB_CK(cudaMalloc(&c->d_step, sizeof(DevStep)));
+  HB_CK(cudaMemset(c->d_step, 0, sizeof(DevStep)));
+  if (const char* g = getenv("HB_NO_GRAPHS")) c->use_graphs = g[0] == '0';
   size_t maxw = 0;
   for (int l = 0; l < L; ++l) maxw = std::max(maxw, static_cast<size_t>(c->d[l + 1]) * c->d[l]);
   c->stage64_n = std::max<size_t>(maxw, size_t(4) << 20);
@@ -775,6 +907,8 @@ int hb_ctx_destroy(hb_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   hb_comm_destroy(c);
+  drop_graphs(c);
+  cudaFree(c->d_step);
   for (auto p : c->W) cudaFree(p);
   for (auto p : c->G) cudaFree(p);
   for (auto p : c->A) cudaFree(p);
@@ -1036,6 +1170,7 @@ int hb_train_step_host_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col,
     HB_CUDA(cudaMalloc(&c->browidx, cap * sizeof(int32_t)));
     HB_CUDA(cudaMalloc(&c->bcval, cap * sizeof(float)));
     c->b_nnz_cap = cap;
+    c->view_gen++;
   }
   build_csc(rowptr, col, val, rows, c->d[0], c->h_colptr, c->h_rowidx, c->h_cval, 0);
   // one pinned buffer carries the whole batch: rowptr | colptr | labels | col | rowidx | val | cval
@@ -1079,7 +1214,7 @@ int hb_forward(hb_ctx* c, int64_t start, int rows) {
   if (start < 0 || rows < 1 || rows > c->max_batch || start + rows > c->e_rows)
     return fail(HB_EINVAL, "batch range out of bounds");
   c->last_launches = 0;
-  HB_TRY(run_forward(c, c->epoch, start, rows, false, 0, 0.0));
+  HB_TRY(run_forward(c, c->epoch, start, rows, false, 0, 0.0, nullptr));
   HB_CUDA(cudaStreamSynchronize(c->stream));
   return HB_OK;
 }
@@ -1102,7 +1237,7 @@ int hb_eval_loss_sum(hb_ctx* c, int64_t start, int64_t rows, double* out_sum) {
   double total = 0.0;
   for (long long s = start; s < start + rows; s += c->max_batch) {
     const int n = static_cast<int>(std::min<long long>(c->max_batch, start + rows - s));
-    HB_TRY(run_forward(c, c->epoch, s, n, false, 0, 0.0));
+    HB_TRY(run_forward(c, c->epoch, s, n, false, 0, 0.0, nullptr));
     double part = 0.0;
     HB_CUDA(cudaMemcpyAsync(&part, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     HB_CUDA(cudaStreamSynchronize(c->stream));
@@ -1129,7 +1264,8 @@ int hb_profile_enable(hb_ctx* c, int on) {
   HB_CUDA(cudaStreamSynchronize(c->stream));
   c->prof_on = on != 0;
   c->ev_used = 0;
-  c->marks.clear();
+  c->step_marks.clear();
+  c->prof_acc.clear();
   return HB_OK;
 }
 
@@ -1137,34 +1273,19 @@ int hb_profile_read(hb_ctx* c, int max_entries, char* names, double* total_ms, i
   HB_TRY(ctx_check(c));
   if (!n_out) return fail(HB_EINVAL, "null n_out");
   HB_CUDA(cudaStreamSynchronize(c->stream));
-  std::vector<std::string> keys;
-  std::vector<double> tot;
-  std::vector<int> cnt;
-  for (auto& m : c->marks) {
-    float ms = 0.f;
-    HB_CUDA(cudaEventElapsedTime(&ms, c->evpool[m.second], c->evpool[m.second + 1]));
-    size_t k = 0;
-    while (k < keys.size() && keys[k] != m.first) ++k;
-    if (k == keys.size()) {
-      keys.push_back(m.first);
-      tot.push_back(0.0);
-      cnt.push_back(0);
-    }
-    tot[k] += ms;
-    cnt[k] += 1;
-  }
-  const int n = static_cast<int>(std::min<size_t>(keys.size(), static_cast<size_t>(std::max(max_entries, 0))));
-  for (int i = 0; i < n; ++i) {
+  int i = 0;
+  for (auto& kv : c->prof_acc) {
+    if (i >= max_entries) break;
     if (names) {
       std::memset(names + 64 * i, 0, 64);
-      std::strncpy(names + 64 * i, keys[i].c_str(), 63);
+      std::strncpy(names + 64 * i, kv.first.c_str(), 63);
     }
-    if (total_ms) total_ms[i] = tot[i];
-    if (counts) counts[i] = cnt[i];
+    if (total_ms) total_ms[i] = kv.second.first;
+    if (counts) counts[i] = kv.second.second;
+    ++i;
   }
-  *n_out = n;
-  c->ev_used = 0;
-  c->marks.clear();
+  *n_out = i;
+  c->prof_acc.clear();
   return HB_OK;
 }
 

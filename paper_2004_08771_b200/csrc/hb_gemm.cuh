@@ -28,6 +28,7 @@
 //                 coalesced float4 global traffic (2 warps per TMEM lane quarter)
 //   warps 12..    (PASSES == 3) hi/lo splitter (HB_SPLIT_WARPS warps)
 #pragma once
+#include "hb_kernels.cuh"
 #include "hb_ptx.cuh"
 
 namespace hb {
@@ -48,6 +49,8 @@ struct GemmArgs {
   float* grad;            // EPI_SGD: optional raw gradient output
   long long ld_grad;
   float eta;
+  const DevStep* ds;      // graph launches: start / eta from device memory
+  int a_start, b_start;   // add ds->start to a_off / b_off (staged-input operands)
 };
 
 // 3xTF32 split variants (compile-time):
@@ -124,8 +127,14 @@ __device__ __forceinline__ uint64_t op_desc(uint32_t tile, int kk, bool mn_major
 template <int BN, bool A_MN, bool B_MN, int EPI, int PASSES>
 __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const GemmArgs args) {
+                     GemmArgs args) {
   using C = GemmCfg<BN, PASSES>;
+  if (args.ds != nullptr) {
+    const int st = static_cast<int>(args.ds->start);
+    if (args.a_start) args.a_off += st;
+    if (args.b_start) args.b_off += st;
+    args.eta = args.ds->eta;
+  }
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));

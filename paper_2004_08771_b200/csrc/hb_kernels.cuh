@@ -14,6 +14,19 @@ namespace hb {
 
 constexpr float kProbFloor = 1e-12f;  // nn.py:26
 
+// Per-step scalars read from device memory, so that one captured CUDA graph
+// serves every batch of the same size: the batch's first row in the staged
+// epoch and the learning rate (the coordinator's EXECUTE_WORK payload,
+// messaging.py:91-96).  Kernels fall back to their by-value fields when the
+// pointer is null (eager launches).
+struct DevStep {
+  long long start;
+  float eta;
+  int pad;
+};
+__device__ __forceinline__ long long step_start(const DevStep* ds, long long s) { return ds ? ds->start : s; }
+__device__ __forceinline__ float step_eta(const DevStep* ds, float e) { return ds ? ds->eta : e; }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -43,7 +56,10 @@ struct HeadArgs {
   long long lda;
   const float* w;          // (nc, d) output weights
   long long ldw;
-  const int64_t* labels;   // already offset to the batch start
+  const int64_t* labels;   // label array of the staged data (indexed from start)
+  long long start;         // first batch row (ds->start when ds != null)
+  int a_input;             // 1: `a` is the staged input itself (depth-1 nets), offset by start
+  const DevStep* ds;
   int rows, d, nc;
   int zero_rows;           // delta_prev rows [rows, zero_rows) are zeroed
   float inv_n;             // 1 / batch size
@@ -57,8 +73,13 @@ struct HeadArgs {
 };
 
 template <int NCT, int MAXT>
-__global__ void __launch_bounds__(kHeadWarps * 32, (MAXT <= 16 && NCT <= 2) ? 2 : 1) head_small_kernel(const HeadArgs p) {
+__global__ void __launch_bounds__(kHeadWarps * 32, (MAXT <= 16 && NCT <= 2) ? 2 : 1) head_small_kernel(HeadArgs p) {
   __shared__ float sW[NCT * 32 * MAXT];
+  {
+    const long long st = step_start(p.ds, p.start);
+    p.labels += st;
+    if (p.a_input) p.a += st * p.lda;
+  }
   __shared__ double sLoss[kHeadWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = (p.d + 31) / 32;
@@ -174,8 +195,13 @@ __global__ void __launch_bounds__(kHeadWarps * 32, (MAXT <= 16 && NCT <= 2) ? 2 
 // warp keeps its two rows' loads in flight together.  Same math and the same
 // fixed reduction order (per-warp row order, then warps in order).
 template <int NCT, int VPL>
-__global__ void __launch_bounds__(kHeadWarps * 32) head_small_vec_kernel(const HeadArgs p) {
+__global__ void __launch_bounds__(kHeadWarps * 32) head_small_vec_kernel(HeadArgs p) {
   __shared__ __align__(16) float sW[NCT * 128 * VPL];
+  {
+    const long long st = step_start(p.ds, p.start);
+    p.labels += st;
+    if (p.a_input) p.a += st * p.lda;
+  }
   __shared__ double sLoss[kHeadWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int D = 128 * VPL;
@@ -319,15 +345,18 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_small_vec_kernel(const H
 struct SoftmaxArgs {
   float* z;  // (zero_rows, nc) logits in, delta out
   long long ldz;
-  const int64_t* labels;
+  const int64_t* labels;  // staged label array, indexed from start
+  long long start;
+  const DevStep* ds;
   int rows, nc, zero_rows;
   float inv_n;
   int train;
   double* ws_loss;  // [grid]
 };
 
-__global__ void __launch_bounds__(256) softmax_delta_kernel(const SoftmaxArgs p) {
+__global__ void __launch_bounds__(256) softmax_delta_kernel(SoftmaxArgs p) {
   __shared__ double sLoss[8];
+  p.labels += step_start(p.ds, p.start);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + warp;
   double loss = 0.0;
@@ -382,8 +411,9 @@ __global__ void loss_reduce_kernel(const double* ws, int n, double* out, int acc
 // 8 warp sums in order -- a fixed summation order for every element.
 __global__ void __launch_bounds__(256) reduce_sgd_kernel(float* w, long long ldw, const float* part, int S,
                                                            long long slab, int rows, int cols, float eta,
-                                                           float* grad, long long ldg) {
+                                                           float* grad, long long ldg, const DevStep* ds) {
   __shared__ float red[8][33];
+  eta = step_eta(ds, eta);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long i = blockIdx.x * 32LL + lane;
   const long long total = static_cast<long long>(rows) * cols;
@@ -423,6 +453,7 @@ struct SpmmArgs {
   const int64_t* rowptr;  // epoch CSR row pointer (n_rows + 1)
   const int32_t* col;
   const float* val;
+  const DevStep* ds;
   long long start;
   int rows;
   const float* w0t;  // (d_in, d_out)
@@ -433,7 +464,8 @@ struct SpmmArgs {
 };
 
 template <bool VEC>
-__global__ void __launch_bounds__(256) spmm_sigmoid_kernel(const SpmmArgs p) {
+__global__ void __launch_bounds__(256) spmm_sigmoid_kernel(SpmmArgs p) {
+  p.start = step_start(p.ds, p.start);
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= p.rows) return;
@@ -502,6 +534,7 @@ struct SparseDwArgs {
   const int64_t* colptr;  // (d_in + 1)
   const int32_t* rowidx;  // ascending within each column (epoch row ids)
   const float* cval;
+  const DevStep* ds;
   long long start;
   int rows;
   int d_in, d_out;
@@ -531,8 +564,10 @@ __device__ __forceinline__ long long lower_bound_i32(const int32_t* a, long long
 // the 8 partial rows are added in warp order in shared memory and applied to
 // W0T[f, chunk] in place (gradient optionally kept).  Fixed summation order.
 template <bool VEC>
-__global__ void __launch_bounds__(256) sparse_dw_kernel(const SparseDwArgs p) {
+__global__ void __launch_bounds__(256) sparse_dw_kernel(SparseDwArgs p) {
   __shared__ float red[8][128];
+  p.start = step_start(p.ds, p.start);
+  p.eta = step_eta(p.ds, p.eta);
   __shared__ long long s_rng[2];
   const int f = blockIdx.x;
   const int base = blockIdx.y * 128;

@@ -252,6 +252,8 @@ struct hb_ctx {
   void* pinned = nullptr;  // pinned host staging
   size_t pinned_bytes = 0;
 
+  long long *csc_lo = nullptr, *csc_hi = nullptr;  // per-feature batch slices (sparse dW)
+  double nnz_per_row = 0.0;
   float* ws = nullptr;  // split-K partials / head partials
   size_t ws_floats = 0;
   double* ws_loss = nullptr;
@@ -549,14 +551,24 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
     // dW + SGD
     if (l == 0 && c->sparse) {
       SparseDwArgs p{v.colptr, v.rowidx, v.cval, ds, start, rows, c->d[0], c->d[1], c->D[0], c->ld[1],
-                     c->W[0], c->ldw[0], static_cast<float>(eta), emit ? c->G[0] : nullptr, c->ldw[0]};
-      const dim3 blocks(c->d[0], cdiv(c->d[1], 128));
+                     c->W[0], c->ldw[0], static_cast<float>(eta), emit ? c->G[0] : nullptr, c->ldw[0],
+                     c->csc_lo, c->csc_hi};
       prof_begin(c);
-      if (c->d[1] % 4 == 0)
-        sparse_dw_kernel<true><<<blocks, 256, 0, st>>>(p);
-      else
-        sparse_dw_kernel<false><<<blocks, 256, 0, st>>>(p);
+      csc_batch_ranges_kernel<<<cdiv(c->d[0], 256), 256, 0, st>>>(v.colptr, v.rowidx, c->d[0], start, rows, ds,
+                                                                  c->csc_lo, c->csc_hi);
+      // batch entries per feature decide the parallelisation
+      const double per_feature = static_cast<double>(rows) * c->nnz_per_row / std::max(1, c->d[0]);
+      if (per_feature < 48.0 && c->d[1] % 4 == 0) {
+        sparse_dw_warp_kernel<<<cdiv(static_cast<long long>(c->d[0]) * 32, 256), 256, 0, st>>>(p);
+      } else {
+        const dim3 blocks(c->d[0], cdiv(c->d[1], 128));
+        if (c->d[1] % 4 == 0)
+          sparse_dw_kernel<true><<<blocks, 256, 0, st>>>(p);
+        else
+          sparse_dw_kernel<false><<<blocks, 256, 0, st>>>(p);
+      }
       HB_CUDA(cudaGetLastError());
+      c->last_launches++;
       prof_end(c, "sparse_dw_sgd", 0);
       c->last_launches++;
       continue;
@@ -592,9 +604,14 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       HB_TRY(launch_gemm(c->passes, G_DW, EPI_PARTIAL, c->bn_dw[l], c->tmD_mn[l], tb, a, mt, nt, splits, st));
       prof_end(c, "gemm_dw_partial", l);
       prof_begin(c);
-      reduce_sgd_kernel<<<cdiv(slab, 32), 256, 0, st>>>(c->W[l], c->ldw[l], c->ws, splits, slab, a.M, a.N,
-                                                        static_cast<float>(eta), emit ? c->G[l] : nullptr, c->d[l],
-                                                        ds);
+      if (a.N % 4 == 0 && c->ldw[l] % 4 == 0 && (slab / 4) >= 148 * 256)
+        reduce_sgd_vec_kernel<<<static_cast<int>(std::min<long long>(cdiv(slab / 4, 256), 148 * 8)), 256, 0, st>>>(
+            c->W[l], c->ldw[l], c->ws, splits, slab, a.M, a.N, static_cast<float>(eta), emit ? c->G[l] : nullptr,
+            c->d[l], ds);
+      else
+        reduce_sgd_kernel<<<cdiv(slab, 32), 256, 0, st>>>(c->W[l], c->ldw[l], c->ws, splits, slab, a.M, a.N,
+                                                          static_cast<float>(eta), emit ? c->G[l] : nullptr, c->d[l],
+                                                          ds);
       HB_CUDA(cudaGetLastError());
       prof_end(c, "reduce_sgd", l);
       c->last_launches += 2;
@@ -875,6 +892,10 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
   HB_CK(cudaMalloc(&c->ws_loss, c->ws_loss_n * sizeof(double)));
   HB_CK(cudaMalloc(&c->d_loss, sizeof(double)));
   HB_CK(cudaMalloc(&c->d_step, sizeof(DevStep)));
+  if (c->sparse) {
+    HB_CK(cudaMalloc(&c->csc_lo, static_cast<size_t>(c->d[0]) * sizeof(long long)));
+    HB_CK(cudaMalloc(&c->csc_hi, static_cast<size_t>(c->d[0]) * sizeof(long long)));
+  }
   HB_CK(cudaMemset(c->d_step, 0, sizeof(DevStep)));
   if (const char* g = getenv("HB_NO_GRAPHS")) c->use_graphs = g[0] == '0';
   size_t maxw = 0;
@@ -909,6 +930,8 @@ int hb_ctx_destroy(hb_ctx* c) {
   hb_comm_destroy(c);
   drop_graphs(c);
   cudaFree(c->d_step);
+  cudaFree(c->csc_lo);
+  cudaFree(c->csc_hi);
   for (auto p : c->W) cudaFree(p);
   for (auto p : c->G) cudaFree(p);
   for (auto p : c->A) cudaFree(p);
@@ -1105,6 +1128,7 @@ int hb_stage_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col, const flo
   HB_CUDA(cudaMemcpy(c->elabels, labels, n_rows * sizeof(int64_t), cudaMemcpyHostToDevice));
   c->e_rows = n_rows;
   c->e_nnz = nnz;
+  c->nnz_per_row = static_cast<double>(nnz) / static_cast<double>(n_rows);
   c->epoch = DataView();
   c->epoch.rowptr = c->erowptr;
   c->epoch.col = c->ecol;
@@ -1173,6 +1197,7 @@ int hb_train_step_host_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col,
     c->view_gen++;
   }
   build_csc(rowptr, col, val, rows, c->d[0], c->h_colptr, c->h_rowidx, c->h_cval, 0);
+  c->nnz_per_row = static_cast<double>(nnz) / rows;
   // one pinned buffer carries the whole batch: rowptr | colptr | labels | col | rowidx | val | cval
   const size_t b_rowptr = (rows + 1) * sizeof(int64_t), b_colptr = (c->d[0] + 1) * sizeof(int64_t),
                b_lab = rows * sizeof(int64_t), b_i32 = nnz * sizeof(int32_t), b_f32 = nnz * sizeof(float);

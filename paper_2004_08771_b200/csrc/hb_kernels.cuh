@@ -444,6 +444,38 @@ __global__ void __launch_bounds__(256) reduce_sgd_kernel(float* w, long long ldw
   }
 }
 
+// Element-parallel variant for few slabs and many elements (split-K partials
+// of large dW GEMMs): a grid-stride loop over float4 groups, every thread sums
+// its 4 elements over the S slabs in slab order.  Needs cols % 4 == 0 and
+// 16-byte-aligned rows of w / grad.
+__global__ void __launch_bounds__(256) reduce_sgd_vec_kernel(float* w, long long ldw, const float* part, int S,
+                                                               long long slab, int rows, int cols, float eta,
+                                                               float* grad, long long ldg, const DevStep* ds) {
+  eta = step_eta(ds, eta);
+  const long long quads = static_cast<long long>(rows) * cols / 4;
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < quads;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = 4 * q;
+    float4 g = __ldcs(reinterpret_cast<const float4*>(part + i));
+    for (int s = 1; s < S; ++s) {
+      const float4 t = __ldcs(reinterpret_cast<const float4*>(part + s * slab + i));
+      g.x += t.x;
+      g.y += t.y;
+      g.z += t.z;
+      g.w += t.w;
+    }
+    const long long r = i / cols, c = i % cols;
+    float4* wp = reinterpret_cast<float4*>(w + r * ldw + c);
+    float4 wv = *wp;
+    wv.x -= eta * g.x;
+    wv.y -= eta * g.y;
+    wv.z -= eta * g.z;
+    wv.w -= eta * g.w;
+    *wp = wv;
+    if (grad != nullptr) *reinterpret_cast<float4*>(grad + r * ldg + c) = g;
+  }
+}
+
 // ------------------------------------------------------------------------
 // CSR-gather SpMM first layer: A1[i, :] = sigmoid(sum_k val_k * W0T[col_k, :])
 // for batch rows i in [0, rows) of the staged CSR starting at row `start`.
@@ -545,6 +577,8 @@ struct SparseDwArgs {
   float eta;
   float* grad;  // optional (d_in, d_out) raw gradient (transposed layout)
   long long ldg;
+  const long long* lo_arr;  // per-feature batch slice of the CSC (csc_batch_ranges_kernel)
+  const long long* hi_arr;
 };
 
 __device__ __forceinline__ long long lower_bound_i32(const int32_t* a, long long lo, long long hi, long long key) {
@@ -568,18 +602,10 @@ __global__ void __launch_bounds__(256) sparse_dw_kernel(SparseDwArgs p) {
   __shared__ float red[8][128];
   p.start = step_start(p.ds, p.start);
   p.eta = step_eta(p.ds, p.eta);
-  __shared__ long long s_rng[2];
   const int f = blockIdx.x;
   const int base = blockIdx.y * 128;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    const long long c0 = p.colptr[f], c1 = p.colptr[f + 1];
-    const long long lo = lower_bound_i32(p.rowidx, c0, c1, p.start);
-    s_rng[0] = lo;
-    s_rng[1] = lower_bound_i32(p.rowidx, lo, c1, p.start + p.rows);
-  }
-  __syncthreads();
-  const long long lo = s_rng[0], hi = s_rng[1];
+  const long long lo = p.lo_arr[f], hi = p.hi_arr[f];
   const int width = min(128, p.d_out - base);
   float* wrow = p.w0t + static_cast<long long>(f) * p.ldw + base;
   float* grow = p.grad != nullptr ? p.grad + static_cast<long long>(f) * p.ldg + base : nullptr;
@@ -632,6 +658,72 @@ __global__ void __launch_bounds__(256) sparse_dw_kernel(SparseDwArgs p) {
     for (int k = 0; k < 8; ++k) g += (lo + k < hi) ? red[k][j] : 0.f;
     wrow[j] -= p.eta * g;
     if (grow != nullptr) grow[j] = g;
+  }
+}
+
+// Per-feature slice [lo, hi) of the epoch CSC that falls in the batch rows
+// [start, start+rows): one thread per feature, two binary searches.
+__global__ void csc_batch_ranges_kernel(const int64_t* colptr, const int32_t* rowidx, int d_in, long long start,
+                                        int rows, const DevStep* ds, long long* lo_out, long long* hi_out) {
+  start = step_start(ds, start);
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < d_in; f += gridDim.x * blockDim.x) {
+    const long long c0 = colptr[f], c1 = colptr[f + 1];
+    const long long lo = lower_bound_i32(rowidx, c0, c1, start);
+    lo_out[f] = lo;
+    hi_out[f] = lower_bound_i32(rowidx, lo, c1, start + rows);
+  }
+}
+
+// Sparse-feature regime (few batch entries per feature, e.g. real-sim's
+// 20958 columns x ~20 entries): one warp per feature covering all d_out
+// columns (float4 per lane, 1024-column chunks), entries in CSC order.
+// Needs d_out % 4 == 0.
+__global__ void __launch_bounds__(256) sparse_dw_warp_kernel(SparseDwArgs p) {
+  p.start = step_start(p.ds, p.start);
+  p.eta = step_eta(p.ds, p.eta);
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (f >= p.d_in) return;
+  const long long lo = p.lo_arr[f], hi = p.hi_arr[f];
+  float* wrow = p.w0t + static_cast<long long>(f) * p.ldw;
+  float* grow = p.grad != nullptr ? p.grad + static_cast<long long>(f) * p.ldg : nullptr;
+  if (lo == hi) {
+    if (grow != nullptr)
+      for (int j = lane * 4; j < p.d_out; j += 128) *reinterpret_cast<float4*>(grow + j) = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  for (int base = 0; base < p.d_out; base += 1024) {
+    float4 acc[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (long long e = lo; e < hi; ++e) {
+      const float v = __ldg(p.cval + e);
+      const float* dr = p.delta0 + (static_cast<long long>(__ldg(p.rowidx + e)) - p.start) * p.ldd + base;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int j = 4 * lane + 128 * t;
+        if (base + j < p.d_out) {
+          const float4 d = __ldg(reinterpret_cast<const float4*>(dr + j));
+          acc[t].x = fmaf(v, d.x, acc[t].x);
+          acc[t].y = fmaf(v, d.y, acc[t].y);
+          acc[t].z = fmaf(v, d.z, acc[t].z);
+          acc[t].w = fmaf(v, d.w, acc[t].w);
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int j = base + 4 * lane + 128 * t;
+      if (j < p.d_out) {
+        float4 w = *reinterpret_cast<float4*>(wrow + j);
+        w.x -= p.eta * acc[t].x;
+        w.y -= p.eta * acc[t].y;
+        w.z -= p.eta * acc[t].z;
+        w.w -= p.eta * acc[t].w;
+        *reinterpret_cast<float4*>(wrow + j) = w;
+        if (grow != nullptr) *reinterpret_cast<float4*>(grow + j) = acc[t];
+      }
+    }
   }
 }
 

@@ -98,9 +98,16 @@ int make_map(CUtensorMap* m, const float* base, long long inner, long long rows,
 }
 
 // ------------------------------------------------------------ GEMM launch
+int g_trace_launch_no = 0;  // HB_TRACE builds: index of the GEMM launch being issued
+// A GEMM operand: the fp32 tensor's map and its 3xTF32 lo twin's map.
+struct Operand {
+  const CUtensorMap* hi;
+  const CUtensorMap* lo;
+};
+
 template <int BN, bool A_MN, bool B_MN, int EPI, int PASSES>
-int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int m_tiles, int n_tiles,
-                  int splits, cudaStream_t st) {
+int launch_gemm_t(const Operand& ta, const Operand& tb, const GemmArgs& a, int m_tiles, int n_tiles, int splits,
+                  cudaStream_t st) {
   using C = GemmCfg<BN, PASSES>;
   auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, EPI, PASSES>;
   static bool configured = false;  // per instantiation
@@ -108,16 +115,39 @@ int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& 
     HB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     configured = true;
   }
-  dim3 grid(n_tiles, m_tiles, splits);
-  kern<<<grid, C::THREADS, C::SMEM, st>>>(ta, tb, a);
-  HB_CUDA(cudaGetLastError());
+  // CTA pairs (cta_group::2) along M for the 3xTF32 kernels: grid.y padded to even
+#ifdef HB_TRACE
+  {
+    const int target = getenv("HB_TRACE_LAUNCH") ? atoi(getenv("HB_TRACE_LAUNCH")) : -1;
+    const_cast<GemmArgs&>(a).trace = (target < 0 || g_trace_launch_no == target) ? 1 : 0;
+    ++g_trace_launch_no;
+  }
+#endif
+  const int cm = C::PAIR ? 2 : 1;
+  const int gy = (m_tiles + cm - 1) / cm * cm;  // M tiles (padded to whole pairs) along grid.x
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(gy, n_tiles, splits);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cm;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t le = cudaLaunchKernelEx(&cfg, kern, *ta.hi, *tb.hi, *ta.lo, *tb.lo, a);
+  if (le != cudaSuccess)
+    return fail(HB_ECUDA, "gemm launch failed: %s (BN=%d pair=%d passes=%d grid=%d,%d,%d smem=%d)",
+                cudaGetErrorString(le), BN, static_cast<int>(C::PAIR), PASSES, gy, n_tiles, splits, C::SMEM);
   return HB_OK;
 }
 
 enum GemmKind { G_FWD = 0, G_DX = 1, G_DW = 2 };
 
 template <int PASSES>
-int launch_gemm_p(GemmKind kind, int epi, int bn, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+int launch_gemm_p(GemmKind kind, int epi, int bn, const Operand& ta, const Operand& tb, const GemmArgs& a,
                   int m_tiles, int n_tiles, int splits, cudaStream_t st) {
 #define HB_L(BN_, AMN_, BMN_, EPI_) \
   return launch_gemm_t<BN_, AMN_, BMN_, EPI_, PASSES>(ta, tb, a, m_tiles, n_tiles, splits, st)
@@ -139,7 +169,7 @@ int launch_gemm_p(GemmKind kind, int epi, int bn, const CUtensorMap& ta, const C
 #undef HB_L
 }
 
-int launch_gemm(int passes, GemmKind kind, int epi, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
+int launch_gemm(int passes, GemmKind kind, int epi, int bn, const Operand& ta, const Operand& tb,
                 const GemmArgs& a, int m_tiles, int n_tiles, int splits, cudaStream_t st) {
   if (passes == 3) return launch_gemm_p<3>(kind, epi, bn, ta, tb, a, m_tiles, n_tiles, splits, st);
   return launch_gemm_p<1>(kind, epi, bn, ta, tb, a, m_tiles, n_tiles, splits, st);
@@ -186,8 +216,11 @@ struct DataView {
   const float* x = nullptr;
   long long ldx = 0;
   long long n_rows = 0;
-  CUtensorMap tm_fwd;  // K-major A operand of the first forward GEMM
-  CUtensorMap tm_dw;   // MN-major B operand of the first dW GEMM
+  const float* x_lo = nullptr;  // 3xTF32 lo twin of x (same layout)
+  CUtensorMap tm_fwd, tm_fwd_lo;  // K-major A operand of the first forward GEMM
+  CUtensorMap tm_dw, tm_dw_lo;    // MN-major B operand of the first dW GEMM
+  Operand fwd() const { return {&tm_fwd, x_lo ? &tm_fwd_lo : &tm_fwd}; }
+  Operand dw() const { return {&tm_dw, x_lo ? &tm_dw_lo : &tm_dw}; }
   // sparse
   const int64_t* rowptr = nullptr;
   const int32_t* col = nullptr;
@@ -223,14 +256,24 @@ struct hb_ctx {
   int head_nct = 0, head_maxt = 0;
 
   std::vector<float*> W, G;    // W[l]; G[l] raw gradient (EMIT_GRAD)
+  std::vector<float*> W_lo, A_lo, D_lo;  // 3xTF32 lo twins of the GEMM operands (3-pass only)
   std::vector<long long> ldw;  // row stride of W[l] (in its device layout)
   std::vector<float*> A;       // A[l] l=1..L-1 activations (cap, ld[l])
   std::vector<float*> D;       // D[l] error at the output of layer l (cap, ld[l+1])
   std::vector<int> bn_fwd, bn_dx, bn_dw;
   std::vector<CUtensorMap> tmW_k, tmW_mn, tmA_k, tmA_mn, tmD_k, tmD_mn;
+  std::vector<CUtensorMap> tmW_k_lo, tmW_mn_lo, tmA_k_lo, tmA_mn_lo, tmD_k_lo, tmD_mn_lo;
+  bool need_lo() const { return passes == 3; }
+  Operand opW_k(int l) const { return {&tmW_k[l], need_lo() ? &tmW_k_lo[l] : &tmW_k[l]}; }
+  Operand opW_mn(int l) const { return {&tmW_mn[l], need_lo() ? &tmW_mn_lo[l] : &tmW_mn[l]}; }
+  Operand opA_k(int l) const { return {&tmA_k[l], need_lo() ? &tmA_k_lo[l] : &tmA_k[l]}; }
+  Operand opA_mn(int l) const { return {&tmA_mn[l], need_lo() ? &tmA_mn_lo[l] : &tmA_mn[l]}; }
+  Operand opD_k(int l) const { return {&tmD_k[l], need_lo() ? &tmD_k_lo[l] : &tmD_k[l]}; }
+  Operand opD_mn(int l) const { return {&tmD_mn[l], need_lo() ? &tmD_mn_lo[l] : &tmD_mn[l]}; }
 
   // staged epoch / host batch slot
   float* ex = nullptr;
+  float* ex_lo = nullptr;
   int64_t* elabels = nullptr;
   int64_t *erowptr = nullptr, *ecolptr = nullptr;
   int32_t *ecol = nullptr, *erowidx = nullptr;
@@ -240,6 +283,7 @@ struct hb_ctx {
   bool staged = false;
 
   float* bx = nullptr;  // batch slot (dense rows) for host-buffer steps
+  float* bx_lo = nullptr;
   int64_t* blabels = nullptr;
   int64_t *browptr = nullptr, *bcolptr = nullptr;
   int32_t *bcol = nullptr, *browidx = nullptr;
@@ -352,6 +396,10 @@ int build_data_maps(hb_ctx* c, DataView& v) {
   if (c->sparse) return HB_OK;
   HB_TRY(make_map(&v.tm_fwd, v.x, c->d[0], v.n_rows, v.ldx, 128, false));
   HB_TRY(make_map(&v.tm_dw, v.x, c->d[0], v.n_rows, v.ldx, 32, true));
+  if (v.x_lo != nullptr) {
+    HB_TRY(make_map(&v.tm_fwd_lo, v.x_lo, c->d[0], v.n_rows, v.ldx, 128, false));
+    HB_TRY(make_map(&v.tm_dw_lo, v.x_lo, c->d[0], v.n_rows, v.ldx, 32, true));
+  }
   return HB_OK;
 }
 
@@ -387,7 +435,8 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   // hidden layers
   for (int l = 0; l < L - 1; ++l) {
     if (l == 0 && c->sparse) {
-      SpmmArgs p{v.rowptr, v.col, v.val, ds, start, rows, c->W[0], c->ldw[0], c->d[1], c->A[1], c->ld[1]};
+      SpmmArgs p{v.rowptr, v.col, v.val, ds, start, rows, c->W[0], c->ldw[0], c->d[1], c->A[1], c->ld[1],
+                 c->need_lo() ? c->A_lo[1] : nullptr};
       const int blocks = cdiv(static_cast<long long>(rows) * 32, 256);
       prof_begin(c);
       if (c->d[1] % 128 == 0)
@@ -408,10 +457,11 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     a.kb_total = cdiv(c->d[l], kBK);
     a.kb_per_split = a.kb_total;
     a.out = c->A[l + 1];
+    a.out_lo = c->need_lo() ? c->A_lo[l + 1] : nullptr;
     a.ldo = c->ld[l + 1];
-    const CUtensorMap& ta = l == 0 ? v.tm_fwd : c->tmA_k[l];
+    const Operand ta = l == 0 ? v.fwd() : c->opA_k(l);
     prof_begin(c);
-    HB_TRY(launch_gemm(c->passes, G_FWD, EPI_SIGMOID, c->bn_fwd[l], ta, c->tmW_k[l], a, m_tiles,
+    HB_TRY(launch_gemm(c->passes, G_FWD, EPI_SIGMOID, c->bn_fwd[l], ta, c->opW_k(l), a, m_tiles,
                        cdiv(a.N, c->bn_fwd[l]), 1, st));
     prof_end(c, "gemm_fwd_sigmoid", l);
     c->last_launches++;
@@ -441,6 +491,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     h.inv_n = inv_n;
     h.train = train ? 1 : 0;
     h.delta_prev = (train && L >= 2) ? c->D[L - 2] : nullptr;
+    h.delta_prev_lo = (train && L >= 2 && c->need_lo()) ? c->D_lo[L - 2] : nullptr;
     h.ld_dp = L >= 2 ? c->ld[L - 1] : 0;
     h.delta_out = nullptr;
     h.ws_dw = c->ws;
@@ -485,7 +536,8 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
       prof_begin(c);
       reduce_sgd_kernel<<<cdiv(n, 32), 256, 0, st>>>(c->W[l], c->ldw[l], c->ws, grid, n, c->d[L], c->d[l],
                                                      static_cast<float>(eta),
-                                                     (flags & HB_STEP_EMIT_GRAD) ? c->G[l] : nullptr, c->d[l], ds);
+                                                     (flags & HB_STEP_EMIT_GRAD) ? c->G[l] : nullptr, c->d[l], ds,
+                                                     c->need_lo() ? c->W_lo[l] : nullptr);
       HB_CUDA(cudaGetLastError());
       prof_end(c, "reduce_sgd", l);
       c->last_launches++;
@@ -503,12 +555,13 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   a.kb_per_split = a.kb_total;
   a.out = c->D[l];
   a.ldo = c->ld[L];
-  const CUtensorMap& ta = l == 0 ? v.tm_fwd : c->tmA_k[l];
+  const Operand ta = l == 0 ? v.fwd() : c->opA_k(l);
   prof_begin(c);
-  HB_TRY(launch_gemm(c->passes, G_FWD, EPI_STORE, c->bn_fwd[l], ta, c->tmW_k[l], a, m_tiles, cdiv(a.N, c->bn_fwd[l]),
+  HB_TRY(launch_gemm(c->passes, G_FWD, EPI_STORE, c->bn_fwd[l], ta, c->opW_k(l), a, m_tiles, cdiv(a.N, c->bn_fwd[l]),
                      1, st));
   prof_end(c, "gemm_fwd_logits", l);
-  SoftmaxArgs sm{c->D[l], c->ld[L], v.labels, start, ds, rows, c->d[L], zrows, inv_n, train ? 1 : 0, c->ws_loss};
+  SoftmaxArgs sm{c->D[l], c->need_lo() ? c->D_lo[l] : nullptr, c->ld[L], v.labels, start, ds, rows, c->d[L],
+                 zrows, inv_n, train ? 1 : 0, c->ws_loss};
   const int grid = cdiv(std::max(rows, zrows), 8);
   prof_begin(c);
   softmax_delta_kernel<<<grid, 256, 0, st>>>(sm);
@@ -538,12 +591,13 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       a.kb_total = cdiv(c->d[l + 1], kBK);
       a.kb_per_split = a.kb_total;
       a.out = c->D[l - 1];
+      a.out_lo = c->need_lo() ? c->D_lo[l - 1] : nullptr;
       a.ldo = c->ld[l];
       a.aux = c->A[l];
       a.ld_aux = c->ld[l];
       a.ds = ds;
       prof_begin(c);
-      HB_TRY(launch_gemm(c->passes, G_DX, EPI_DSIG, c->bn_dx[l], c->tmD_k[l], c->tmW_mn[l], a,
+      HB_TRY(launch_gemm(c->passes, G_DX, EPI_DSIG, c->bn_dx[l], c->opD_k(l), c->opW_mn(l), a,
                          cdiv(zrows, kBM), cdiv(a.N, c->bn_dx[l]), 1, st));
       prof_end(c, "gemm_dx_dsig", l);
       c->last_launches++;
@@ -584,15 +638,16 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
     a.kb_total = kb_total;
     a.kb_per_split = kb_per;
     a.eta = static_cast<float>(eta);
-    const CUtensorMap& tb = l == 0 ? v.tm_dw : c->tmA_mn[l];
+    const Operand tb = l == 0 ? v.dw() : c->opA_mn(l);
     const int mt = cdiv(a.M, kBM), nt = cdiv(a.N, c->bn_dw[l]);
     if (splits == 1) {
       a.out = c->W[l];
+      a.out_lo = c->need_lo() ? c->W_lo[l] : nullptr;
       a.ldo = c->ldw[l];
       a.grad = emit ? c->G[l] : nullptr;
       a.ld_grad = c->d[l];
       prof_begin(c);
-      HB_TRY(launch_gemm(c->passes, G_DW, EPI_SGD, c->bn_dw[l], c->tmD_mn[l], tb, a, mt, nt, 1, st));
+      HB_TRY(launch_gemm(c->passes, G_DW, EPI_SGD, c->bn_dw[l], c->opD_mn(l), tb, a, mt, nt, 1, st));
       prof_end(c, "gemm_dw_sgd", l);
       c->last_launches++;
     } else {
@@ -601,17 +656,17 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       a.ldo = a.N;
       a.split_stride = slab;
       prof_begin(c);
-      HB_TRY(launch_gemm(c->passes, G_DW, EPI_PARTIAL, c->bn_dw[l], c->tmD_mn[l], tb, a, mt, nt, splits, st));
+      HB_TRY(launch_gemm(c->passes, G_DW, EPI_PARTIAL, c->bn_dw[l], c->opD_mn(l), tb, a, mt, nt, splits, st));
       prof_end(c, "gemm_dw_partial", l);
       prof_begin(c);
       if (a.N % 4 == 0 && c->ldw[l] % 4 == 0 && (slab / 4) >= 148 * 256)
         reduce_sgd_vec_kernel<<<static_cast<int>(std::min<long long>(cdiv(slab / 4, 256), 148 * 8)), 256, 0, st>>>(
             c->W[l], c->ldw[l], c->ws, splits, slab, a.M, a.N, static_cast<float>(eta), emit ? c->G[l] : nullptr,
-            c->d[l], ds);
+            c->d[l], ds, c->need_lo() ? c->W_lo[l] : nullptr);
       else
         reduce_sgd_kernel<<<cdiv(slab, 32), 256, 0, st>>>(c->W[l], c->ldw[l], c->ws, splits, slab, a.M, a.N,
                                                           static_cast<float>(eta), emit ? c->G[l] : nullptr, c->d[l],
-                                                          ds);
+                                                          ds, c->need_lo() ? c->W_lo[l] : nullptr);
       HB_CUDA(cudaGetLastError());
       prof_end(c, "reduce_sgd", l);
       c->last_launches += 2;
@@ -738,6 +793,8 @@ int ensure_pinned(hb_ctx* c, size_t bytes) {
 
 int free_epoch(hb_ctx* c) {
   cudaFree(c->ex);
+  cudaFree(c->ex_lo);
+  c->ex_lo = nullptr;
   cudaFree(c->elabels);
   cudaFree(c->erowptr);
   cudaFree(c->ecol);
@@ -833,6 +890,10 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
   c->ldw.assign(L, 0);
   c->A.assign(L + 1, nullptr);
   c->D.assign(L, nullptr);
+  c->W_lo.assign(L, nullptr);
+  c->A_lo.assign(L + 1, nullptr);
+  c->D_lo.assign(L, nullptr);
+  const bool lo = c->need_lo();
   c->bn_fwd.assign(L, 128);
   c->bn_dx.assign(L, 128);
   c->bn_dw.assign(L, 128);
@@ -847,6 +908,14 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
     HB_CK(cudaMalloc(&c->G[l], static_cast<size_t>(c->d[l + 1]) * c->d[l] * sizeof(float)));
     HB_CK(cudaMalloc(&c->D[l], static_cast<size_t>(c->cap) * c->ld[l + 1] * sizeof(float)));
     HB_CK(cudaMemset(c->D[l], 0, static_cast<size_t>(c->cap) * c->ld[l + 1] * sizeof(float)));
+    if (lo) {
+      if (!tr) {
+        HB_CK(cudaMalloc(&c->W_lo[l], rows * c->ldw[l] * sizeof(float)));
+        HB_CK(cudaMemset(c->W_lo[l], 0, rows * c->ldw[l] * sizeof(float)));
+      }
+      HB_CK(cudaMalloc(&c->D_lo[l], static_cast<size_t>(c->cap) * c->ld[l + 1] * sizeof(float)));
+      HB_CK(cudaMemset(c->D_lo[l], 0, static_cast<size_t>(c->cap) * c->ld[l + 1] * sizeof(float)));
+    }
     c->bn_fwd[l] = choose_bn(m_tiles, c->d[l + 1]);
     c->bn_dx[l] = choose_bn(m_tiles, c->d[l]);
     c->bn_dw[l] = choose_bn(cdiv(c->d[l + 1], kBM), c->d[l]);
@@ -856,6 +925,10 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
   for (int l = 1; l < L; ++l) {
     HB_CK(cudaMalloc(&c->A[l], static_cast<size_t>(c->cap) * c->ld[l] * sizeof(float)));
     HB_CK(cudaMemset(c->A[l], 0, static_cast<size_t>(c->cap) * c->ld[l] * sizeof(float)));
+    if (lo) {
+      HB_CK(cudaMalloc(&c->A_lo[l], static_cast<size_t>(c->cap) * c->ld[l] * sizeof(float)));
+      HB_CK(cudaMemset(c->A_lo[l], 0, static_cast<size_t>(c->cap) * c->ld[l] * sizeof(float)));
+    }
   }
   // tensor maps
   c->tmW_k.resize(L);
@@ -864,18 +937,34 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
   c->tmA_mn.resize(L + 1);
   c->tmD_k.resize(L);
   c->tmD_mn.resize(L);
+  c->tmW_k_lo.resize(L);
+  c->tmW_mn_lo.resize(L);
+  c->tmA_k_lo.resize(L + 1);
+  c->tmA_mn_lo.resize(L + 1);
+  c->tmD_k_lo.resize(L);
+  c->tmD_mn_lo.resize(L);
   int rc = HB_OK;
   for (int l = 0; l < L && rc == HB_OK; ++l) {
-    if (!(l == 0 && c->sparse)) {
-      rc = make_map(&c->tmW_k[l], c->W[l], c->d[l], c->d[l + 1], c->ldw[l], c->bn_fwd[l], false);
-      if (rc == HB_OK) rc = make_map(&c->tmW_mn[l], c->W[l], c->d[l], c->d[l + 1], c->ldw[l], 32, true);
+    for (int h = 0; h < (lo ? 2 : 1) && rc == HB_OK; ++h) {
+      if (!(l == 0 && c->sparse)) {
+        float* w = h ? c->W_lo[l] : c->W[l];
+        rc = make_map(h ? &c->tmW_k_lo[l] : &c->tmW_k[l], w, c->d[l], c->d[l + 1], c->ldw[l], 32, false);
+        if (rc == HB_OK)
+          rc = make_map(h ? &c->tmW_mn_lo[l] : &c->tmW_mn[l], w, c->d[l], c->d[l + 1], c->ldw[l], 32, true);
+      }
+      float* dd = h ? c->D_lo[l] : c->D[l];
+      if (rc == HB_OK)
+        rc = make_map(h ? &c->tmD_k_lo[l] : &c->tmD_k[l], dd, c->d[l + 1], c->cap, c->ld[l + 1], 128, false);
+      if (rc == HB_OK)
+        rc = make_map(h ? &c->tmD_mn_lo[l] : &c->tmD_mn[l], dd, c->d[l + 1], c->cap, c->ld[l + 1], 32, true);
     }
-    if (rc == HB_OK) rc = make_map(&c->tmD_k[l], c->D[l], c->d[l + 1], c->cap, c->ld[l + 1], 128, false);
-    if (rc == HB_OK) rc = make_map(&c->tmD_mn[l], c->D[l], c->d[l + 1], c->cap, c->ld[l + 1], 32, true);
   }
   for (int l = 1; l < L && rc == HB_OK; ++l) {
-    rc = make_map(&c->tmA_k[l], c->A[l], c->d[l], c->cap, c->ld[l], 128, false);
-    if (rc == HB_OK) rc = make_map(&c->tmA_mn[l], c->A[l], c->d[l], c->cap, c->ld[l], 32, true);
+    for (int h = 0; h < (lo ? 2 : 1) && rc == HB_OK; ++h) {
+      float* aa = h ? c->A_lo[l] : c->A[l];
+      rc = make_map(h ? &c->tmA_k_lo[l] : &c->tmA_k[l], aa, c->d[l], c->cap, c->ld[l], 128, false);
+      if (rc == HB_OK) rc = make_map(h ? &c->tmA_mn_lo[l] : &c->tmA_mn[l], aa, c->d[l], c->cap, c->ld[l], 32, true);
+    }
   }
   if (rc != HB_OK) return bail(rc);
   // workspaces: split-K partial slabs and head partials
@@ -911,7 +1000,12 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
   } else {
     HB_CK(cudaMalloc(&c->bx, static_cast<size_t>(c->cap) * c->ld[0] * sizeof(float)));
     HB_CK(cudaMemset(c->bx, 0, static_cast<size_t>(c->cap) * c->ld[0] * sizeof(float)));
+    if (lo) {
+      HB_CK(cudaMalloc(&c->bx_lo, static_cast<size_t>(c->cap) * c->ld[0] * sizeof(float)));
+      HB_CK(cudaMemset(c->bx_lo, 0, static_cast<size_t>(c->cap) * c->ld[0] * sizeof(float)));
+    }
     c->batch.x = c->bx;
+    c->batch.x_lo = c->bx_lo;
     c->batch.ldx = c->ld[0];
     c->batch.n_rows = c->cap;
     rc = build_data_maps(c, c->batch);
@@ -936,6 +1030,10 @@ int hb_ctx_destroy(hb_ctx* c) {
   for (auto p : c->G) cudaFree(p);
   for (auto p : c->A) cudaFree(p);
   for (auto p : c->D) cudaFree(p);
+  for (auto p : c->W_lo) cudaFree(p);
+  for (auto p : c->A_lo) cudaFree(p);
+  for (auto p : c->D_lo) cudaFree(p);
+  cudaFree(c->bx_lo);
   free_epoch(c);
   cudaFree(c->bx);
   cudaFree(c->blabels);
@@ -968,9 +1066,11 @@ int hb_set_weights_f64(hb_ctx* c, int layer, const double* w) {
   HB_CUDA(cudaMemcpyAsync(c->stage64, w, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 4096));
   if (layer == 0 && c->sparse)
-    f64_to_f32_kernel<true><<<blocks, 256, 0, c->stream>>>(c->W[0], c->ldw[0], c->stage64, cols, rows, cols);
+    f64_to_f32_kernel<true><<<blocks, 256, 0, c->stream>>>(c->W[0], c->ldw[0], c->stage64, cols, rows, cols,
+                                                           nullptr);
   else
-    f64_to_f32_kernel<false><<<blocks, 256, 0, c->stream>>>(c->W[layer], c->ldw[layer], c->stage64, cols, rows, cols);
+    f64_to_f32_kernel<false><<<blocks, 256, 0, c->stream>>>(c->W[layer], c->ldw[layer], c->stage64, cols, rows, cols,
+                                                            c->need_lo() ? c->W_lo[layer] : nullptr);
   HB_CUDA(cudaGetLastError());
   HB_CUDA(cudaStreamSynchronize(c->stream));
   return HB_OK;
@@ -1047,6 +1147,7 @@ static int stage_dense_common(hb_ctx* c, int64_t n_rows, const int64_t* labels) 
   if (n_rows < 1 || !labels) return fail(HB_EINVAL, "need n_rows >= 1 and labels");
   HB_TRY(free_epoch(c));
   HB_CUDA(cudaMalloc(&c->ex, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
+  if (c->need_lo()) HB_CUDA(cudaMalloc(&c->ex_lo, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
   HB_CUDA(cudaMalloc(&c->elabels, static_cast<size_t>(n_rows) * sizeof(int64_t)));
   HB_CUDA(cudaMemcpyAsync(c->elabels, labels, n_rows * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
   c->e_rows = n_rows;
@@ -1056,6 +1157,7 @@ static int stage_dense_common(hb_ctx* c, int64_t n_rows, const int64_t* labels) 
 static int finish_dense_stage(hb_ctx* c) {
   c->epoch = DataView();
   c->epoch.x = c->ex;
+  c->epoch.x_lo = c->ex_lo;
   c->epoch.ldx = c->ld[0];
   c->epoch.n_rows = c->e_rows;
   c->epoch.labels = c->elabels;
@@ -1076,7 +1178,8 @@ int hb_stage_dense_f64(hb_ctx* c, const double* x, int64_t n_rows, int64_t ld, c
     HB_CUDA(cudaMemcpyAsync(c->stage64, x + r0 * ld, nr * ld * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     const long long n = nr * c->d[0];
     f64_to_f32_kernel<false><<<static_cast<int>(std::min<long long>((n + 255) / 256, 4096)), 256, 0, c->stream>>>(
-        c->ex + r0 * c->ld[0], c->ld[0], c->stage64, ld, static_cast<int>(nr), c->d[0]);
+        c->ex + r0 * c->ld[0], c->ld[0], c->stage64, ld, static_cast<int>(nr), c->d[0],
+        c->ex_lo ? c->ex_lo + r0 * c->ld[0] : nullptr);
     HB_CUDA(cudaGetLastError());
     HB_CUDA(cudaStreamSynchronize(c->stream));
   }
@@ -1089,6 +1192,11 @@ int hb_stage_dense_f32(hb_ctx* c, const float* x, int64_t n_rows, int64_t ld, co
   HB_TRY(stage_dense_common(c, n_rows, labels));
   HB_CUDA(cudaMemcpy2DAsync(c->ex, c->ld[0] * sizeof(float), x, ld * sizeof(float), c->d[0] * sizeof(float), n_rows,
                             cudaMemcpyHostToDevice, c->stream));
+  if (c->ex_lo) {
+    split_lo_kernel<<<static_cast<int>(std::min<long long>(cdiv(n_rows * c->d[0], 256), 148 * 16)), 256, 0,
+                      c->stream>>>(c->ex, c->ex_lo, c->ld[0], n_rows, c->d[0]);
+    HB_CUDA(cudaGetLastError());
+  }
   return finish_dense_stage(c);
 }
 
@@ -1168,6 +1276,11 @@ int hb_train_step_host_dense(hb_ctx* c, const float* x, int64_t ld, const int64_
   HB_TRY(check_labels(labels, rows, c->d[c->L]));
   HB_CUDA(cudaMemcpy2DAsync(c->bx, c->ld[0] * sizeof(float), x, ld * sizeof(float), c->d[0] * sizeof(float), rows,
                             cudaMemcpyHostToDevice, c->stream));
+  if (c->bx_lo) {
+    split_lo_kernel<<<std::min(cdiv(static_cast<long long>(rows) * c->d[0], 256), 148 * 16), 256, 0, c->stream>>>(
+        c->bx, c->bx_lo, c->ld[0], rows, c->d[0]);
+    HB_CUDA(cudaGetLastError());
+  }
   HB_CUDA(cudaMemcpyAsync(c->blabels, labels, rows * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
   return do_step(c, c->batch, 0, rows, eta, flags, out_loss);
 }
@@ -1377,7 +1490,8 @@ int hb_merge_allreduce(hb_ctx* c) {
     const bool tr = l == 0 && c->sparse;
     const long long rows = tr ? c->d[0] : c->d[l + 1], cols = tr ? c->d[1] : c->d[l];
     unpack_scale_kernel<<<static_cast<int>(std::min<long long>(cdiv(rows * cols, 256), 4096)), 256, 0, c->stream>>>(
-        c->W[l], c->ldw[l], c->flat + off, static_cast<int>(rows), static_cast<int>(cols), inv);
+        c->W[l], c->ldw[l], c->flat + off, static_cast<int>(rows), static_cast<int>(cols), inv,
+        c->need_lo() ? c->W_lo[l] : nullptr);
     HB_CUDA(cudaGetLastError());
     off += rows * cols;
   }

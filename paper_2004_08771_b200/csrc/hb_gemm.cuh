@@ -13,20 +13,22 @@
 //   EPI_SGD      W_l -= eta * G in place (+ optional raw G) (nn.py:174-179)
 //
 // Precision: fp32 data; PASSES == 3 runs the 3xTF32 split
-//   x = hi + lo, hi = x with the low 13 mantissa bits cleared,
+//   x = hi + lo, hi = trunc_tf32(x) (what the tensor core reads from raw fp32),
+//   lo = x - hi (exact in fp32), every operand tensor keeps its lo twin in HBM
+//   (written by the kernel that produced it),
 //   A.B ~= A_lo.B_hi + A_hi.B_lo + A_hi.B_hi   (fp32 accumulate in TMEM)
 // which meets the reference's per-step 1e-4 bar (SURVEY §7 hard part 1);
-// PASSES == 1 is plain TF32.  The hi/lo split is done in shared memory by a
-// dedicated warpgroup right after TMA lands each stage, so HBM/L2 traffic is
-// the same as a plain fp32 GEMM.
+// PASSES == 1 is plain TF32.  Pre-split twins cost one extra TMA load per
+// operand but keep the in-CTA shared-memory traffic to TMA writes + MMA reads
+// (an in-smem splitter made the kernel smem-bandwidth bound).
 //
 // Warp roles (one CTA = one 128 x BN output tile, one split of K):
 //   warp 0        TMA producer (one elected lane)
 //   warp 1        MMA issuer   (one elected lane)
 //   warp 2        TMEM allocator
 //   warps 4..11   epilogue: tcgen05.ld TMEM -> registers -> smem transpose -> fused op ->
-//                 coalesced float4 global traffic (2 warps per TMEM lane quarter)
-//   warps 12..    (PASSES == 3) hi/lo splitter (HB_SPLIT_WARPS warps)
+//                 coalesced float4 global traffic (2 warps per TMEM lane quarter);
+//                 operand-producing epilogues also write the lo twin
 #pragma once
 #include "hb_kernels.cuh"
 #include "hb_ptx.cuh"
@@ -49,23 +51,12 @@ struct GemmArgs {
   float* grad;            // EPI_SGD: optional raw gradient output
   long long ld_grad;
   float eta;
+  float* out_lo;          // lo twin of the output (EPI_SIGMOID / EPI_DSIG: same indexing as out;
+                          // EPI_SGD: lo twin of W), or null
   const DevStep* ds;      // graph launches: start / eta from device memory
   int a_start, b_start;   // add ds->start to a_off / b_off (staged-input operands)
+  int trace;              // HB_TRACE builds: record this launch's pipeline timeline
 };
-
-// 3xTF32 split variants (compile-time):
-//   HB_SPLIT_HI_RAW 0: hi = cvt.rna.tf32(x) written back, lo = x - hi
-//   HB_SPLIT_HI_RAW 1: hi = x consumed raw by the tensor core, which truncates
-//                      fp32 operands to their top 19 bits (verified by the GPU
-//                      parity tests: with RN the lo term would be off by up to
-//                      2^-11 |x|), lo = x - trunc_tf32(x); saves the hi store.
-//                      Default.
-#ifndef HB_SPLIT_HI_RAW
-#define HB_SPLIT_HI_RAW 1
-#endif
-#ifndef HB_SPLIT_WARPS
-#define HB_SPLIT_WARPS 4
-#endif
 
 // Optional pipeline timeline (debug builds, -DHB_TRACE): CTA (0,0,0) records
 // globaltimer stamps per role and k-block into hb_trace_buf.
@@ -73,7 +64,7 @@ struct GemmArgs {
 __device__ unsigned long long hb_trace_buf[4096];
 #define HB_STAMP(slot)                                                                   \
   do {                                                                                   \
-    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (slot) < 4096) {        \
+    if (args.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (slot) < 4096) { \
       unsigned long long t_;                                                             \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
       hb_trace_buf[(slot)] = t_;                                                         \
@@ -88,19 +79,25 @@ __device__ unsigned long long hb_trace_buf[4096];
 constexpr int kBM = 128;
 constexpr int kBK = 32;  // 32 fp32 = one 128-byte swizzle row
 
+// PAIR: 2-CTA tcgen05 (cta_group::2).  The two CTAs of a cluster pair compute a
+// 256 x BN tile: each loads its own 128 rows of A and HALF of the B tile (so
+// per-SM TMA ingest and shared-memory operand reads for B halve -- with fp32
+// operands and 3xTF32 lo twins the single-CTA kernel was bound by per-SM TMA
+// ingest, ~96 KB per k-block), the even CTA issues M=256 MMAs that read both
+// CTAs' shared memory and write each CTA's own TMEM lanes.
 template <int BN, int PASSES>
 struct GemmCfg {
+  static constexpr bool PAIR = (PASSES == 3) && (BN >= 64);
+  static constexpr int BNL = PAIR ? BN / 2 : BN;  // B rows (K-major) / columns (MN-major) held per CTA
   static constexpr int A_BYTES = kBM * kBK * 4;
-  static constexpr int B_BYTES = BN * kBK * 4;
+  static constexpr int B_BYTES = BNL * kBK * 4;
   static constexpr int OP_BYTES = A_BYTES + B_BYTES;  // raw (hi) operands of one stage
   static constexpr int STAGE_BYTES = OP_BYTES * (PASSES == 3 ? 2 : 1);
   static constexpr int BUDGET = 200 * 1024;
   static constexpr int STAGES_RAW = BUDGET / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
-  static constexpr int SPLIT_THREADS = PASSES == 3 ? 32 * HB_SPLIT_WARPS : 0;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, alternating 32-column chunks
-  static constexpr int THREADS = 128 + 32 * EPI_WARPS + SPLIT_THREADS;
-  static constexpr int SPLIT_BASE = 128 + 32 * EPI_WARPS;
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   // TMEM accumulators: the tensor core's fp32 accumulation error grows with
   // the number of MMAs chained into one accumulator, so 3xTF32 keeps the two
   // small cross terms in their own accumulator and rotates the hi*hi term over
@@ -127,8 +124,10 @@ __device__ __forceinline__ uint64_t op_desc(uint32_t tile, int kk, bool mn_major
 template <int BN, bool A_MN, bool B_MN, int EPI, int PASSES>
 __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmA_lo, const __grid_constant__ CUtensorMap tmB_lo,
                      GemmArgs args) {
   using C = GemmCfg<BN, PASSES>;
+  constexpr bool PAIR = C::PAIR;
   if (args.ds != nullptr) {
     const int st = static_cast<int>(args.ds->start);
     if (args.a_start) args.a_off += st;
@@ -139,16 +138,19 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
-  uint64_t* ready = full + STAGES;
-  uint64_t* empty = ready + STAGES;
+  uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) HB_STAMP(6 * 512 + 2);  // CTA start
-  const int n0 = blockIdx.x * BN;
-  const int m0 = blockIdx.y * kBM;
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0u;  // 0: MMA-issuing CTA of the pair
+  const bool leader = crank == 0;
+  // grid: x = M tiles (CTA pairs are x-adjacent: cluster (2,1,1)), y = N tiles, z = K splits
+  const int n0 = blockIdx.y * BN;
+  const int m0 = blockIdx.x * kBM;
+  const int nl0 = n0 + static_cast<int>(crank) * C::BNL;  // this CTA's B slice
   const int kb_begin = blockIdx.z * args.kb_per_split;
   const int kb_end = min(kb_begin + args.kb_per_split, args.kb_total);
   const int nkb = max(kb_end - kb_begin, 0);
@@ -156,26 +158,39 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (PASSES == 3) {
+      tma_prefetch_desc(&tmA_lo);
+      tma_prefetch_desc(&tmB_lo);
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&ready[s], C::SPLIT_THREADS > 0 ? C::SPLIT_THREADS : 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
     fence_barrier_init();
   }
   if (warp == 2) {
-    tmem_alloc(tmem_slot, C::TMEM_COLS);
-    tmem_relinquish();
+    if (PAIR) {
+      tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+      tmem_relinquish_pair();
+    } else {
+      tmem_alloc(tmem_slot, C::TMEM_COLS);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync_all();  // the peer's barriers / TMEM must exist before any cross-CTA traffic
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
     if (lane == 0) {
+      // completion of both CTAs' loads is counted on the leader's full barrier
+      const uint32_t full_leader0 = PAIR ? mapa_shared(smem_u32(&full[0]), 0) : smem_u32(&full[0]);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
@@ -183,30 +198,40 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
         HB_STAMP(0 * 512 + i);  // producer: stage free, issuing TMA
         uint8_t* sA = smem + s * C::STAGE_BYTES;
         uint8_t* sB = sA + C::A_BYTES;
-        mbar_arrive_expect_tx(&full[s], C::OP_BYTES);
+        const uint32_t fb = full_leader0 + 8u * s;
+        if (leader) mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * C::STAGE_BYTES);
         const int k0 = (kb_begin + i) * kBK;
-        if (!A_MN) {
-          tma_load_2d(sA, &tmA, &full[s], k0, m0 + args.a_off);
-        } else {
 #pragma unroll
-          for (int j = 0; j < kBM / 32; ++j) tma_load_2d(sA + j * 4096, &tmA, &full[s], m0 + 32 * j, k0 + args.a_off);
-        }
-        if (!B_MN) {
-          tma_load_2d(sB, &tmB, &full[s], k0, n0 + args.b_off);
-        } else {
+        for (int h = 0; h < (PASSES == 3 ? 2 : 1); ++h) {
+          const CUtensorMap* ma = h ? &tmA_lo : &tmA;
+          const CUtensorMap* mb = h ? &tmB_lo : &tmB;
+          uint8_t* dA = sA + h * C::OP_BYTES;
+          uint8_t* dB = sB + h * C::OP_BYTES;
+          if (!A_MN) {
+            tma_load_2d_to(dA, ma, fb, k0, m0 + args.a_off, PAIR);
+          } else {
 #pragma unroll
-          for (int j = 0; j < BN / 32; ++j) tma_load_2d(sB + j * 4096, &tmB, &full[s], n0 + 32 * j, k0 + args.b_off);
+            for (int j = 0; j < kBM / 32; ++j) tma_load_2d_to(dA + j * 4096, ma, fb, m0 + 32 * j, k0 + args.a_off, PAIR);
+          }
+          // this CTA's half of B in 32-wide slices (4 KB: 32 K-major rows, or
+          // 32 MN columns x 32 K-lines)
+#pragma unroll
+          for (int j = 0; j < C::BNL / 32; ++j) {
+            const int c0 = B_MN ? nl0 + 32 * j : k0;
+            const int c1 = B_MN ? k0 + args.b_off : nl0 + 32 * j + args.b_off;
+            tma_load_2d_to(dB + j * 4096, mb, fb, c0, c1, PAIR);
+          }
         }
       }
     }
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc_tf32(kBM, BN, A_MN, B_MN);
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = make_idesc_tf32(PAIR ? 2 * kBM : kBM, BN, A_MN, B_MN);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(PASSES == 3 ? &ready[s] : &full[s], ph);
+        mbar_wait(&full[s], ph);
         HB_STAMP(1 * 512 + i);  // MMA: operands ready, issuing
         tc_fence_after();
         const uint32_t aHi = smem_u32(smem + s * C::STAGE_BYTES);
@@ -220,17 +245,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
             const uint64_t bl = op_desc(bHi + C::OP_BYTES, kk, B_MN);
             const uint32_t t_small = tmem_base + C::NBIG * BN;
             const uint32_t t_big = tmem_base + (i % C::NBIG) * BN;
-            mma_tf32(t_small, al, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
-            mma_tf32(t_small, ah, bl, idesc, 1u);
-            mma_tf32(t_big, ah, bh, idesc, (i >= C::NBIG || kk > 0) ? 1u : 0u);
+            mma_tf32_cg(t_small, al, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u, PAIR);
+            mma_tf32_cg(t_small, ah, bl, idesc, 1u, PAIR);
+            mma_tf32_cg(t_big, ah, bh, idesc, (i >= C::NBIG || kk > 0) ? 1u : 0u, PAIR);
           } else {
-            mma_tf32(tmem_base, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+            mma_tf32_cg(tmem_base, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u, PAIR);
           }
         }
-        mma_commit(&empty[s]);  // frees the smem stage once these MMAs retire
+        // frees the smem stage of both CTAs once these MMAs retire
+        mma_commit_cg(&empty[s], PAIR);
         HB_STAMP(2 * 512 + i);  // MMA: issue done
       }
-      mma_commit(tmem_full);  // accumulator complete (immediate if nkb == 0)
+      mma_commit_cg(tmem_full, PAIR);  // accumulators complete (immediate if nkb == 0)
     }
   } else if (warp >= 4 && warp < 4 + C::EPI_WARPS) {
     // ---------------------------------------------------------- epilogue
@@ -240,18 +266,49 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
     const int ew = warp - 4;
     const int q = ew & 3;          // TMEM lane quarter owned by this warp (warp % 4)
     const int half = ew >> 2;      // which alternating 32-column chunks
+    constexpr int CSTEP = 32 * (C::EPI_WARPS / 4);
+    // The epilogue's second operand (A_l for dX, W for the SGD update) does not
+    // depend on the accumulator: it is loaded for a whole chunk at once (the
+    // first chunk while the mainloop is still running) so its HBM latency is
+    // paid once per chunk instead of once per 4-row group.
+    constexpr bool HAS_PRE = (EPI == EPI_DSIG || EPI == EPI_SGD);
+    float4 pre[8];
+    auto load_pre = [&](int cc, float4(&dst)[8]) {
+#pragma unroll
+      for (int g = 0; g < 8; ++g) dst[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (!HAS_PRE) return;
+      const int gnn = n0 + cc + (lane & 7) * 4;
+      const int left = args.N - gnn;
+      if (cc >= BN || left <= 0) return;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const long long gr = static_cast<long long>(m0) + q * 32 + 4 * g + (lane >> 3);
+        if (gr >= args.M) continue;
+        const float* ptr = (EPI == EPI_DSIG) ? args.aux + gr * args.ld_aux + gnn : args.out + gr * args.ldo + gnn;
+        const bool vec = (EPI == EPI_DSIG) ? ((args.ld_aux & 3) == 0) : ((args.ldo & 3) == 0);
+        if (vec && left >= 4) {
+          dst[g] = *reinterpret_cast<const float4*>(ptr);
+        } else {
+          dst[g].x = ptr[0];
+          if (left > 1) dst[g].y = ptr[1];
+          if (left > 2) dst[g].z = ptr[2];
+          if (left > 3) dst[g].w = ptr[3];
+        }
+      }
+    };
+    load_pre(32 * half, pre);
     mbar_wait(tmem_full, 0);
     if (threadIdx.x == 128) HB_STAMP(6 * 512 + 0);  // epilogue start
     tc_fence_after();
     constexpr int TP = 36;  // padded tile row (floats): conflict-free v4 in and out
     float* tile = reinterpret_cast<float*>(smem) + ew * 32 * TP;
     const bool vec_out = (args.ldo & 3) == 0;
-    const bool vec_aux = (args.ld_aux & 3) == 0;
     const bool vec_grad = (args.ld_grad & 3) == 0;
     const int sub_r = lane >> 3;       // row within a group of 4
     const int sub_c = (lane & 7) * 4;  // column quad within the 32-column chunk
 #pragma unroll 1
-    for (int c = 32 * half; c < BN; c += 32 * (C::EPI_WARPS / 4)) {
+    for (int c = 32 * half; c < BN; c += CSTEP) {
+      if (c != 32 * half) load_pre(c, pre);  // one latency per chunk, overlapping the TMEM loads
       const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c;
       float v[32];
       {
@@ -275,7 +332,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
         }
       }
       const int n = n0 + c;
-      if (n >= args.N) continue;  // warp-uniform
+      if (n >= args.N) continue;  // warp-uniform (and then so are all later chunks)
 #ifdef HB_DEBUG_NO_EPI_STORE
       if (v[0] == 12345.f) args.out[0] = v[1];  // timing experiment only: keep the TMEM loads alive
       continue;
@@ -287,7 +344,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
       __syncwarp();
       const int gn = n + sub_c;
       const int nleft = args.N - gn;  // columns of this quad still inside N
-#pragma unroll 2
+#pragma unroll
       for (int rr = 0; rr < 32; rr += 4) {
         const int tr = rr + sub_r;
         const long long grow = static_cast<long long>(m0) + q * 32 + tr;
@@ -302,15 +359,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
 #endif
         } else if (EPI == EPI_DSIG) {
           if (write) {
-            const float* ap = args.aux + grow * args.ld_aux + gn;
-            float av[4];
-            if (vec_aux && nleft >= 4) {
-              const float4 t4 = *reinterpret_cast<const float4*>(ap);
-              av[0] = t4.x; av[1] = t4.y; av[2] = t4.z; av[3] = t4.w;
-            } else {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) av[k] = k < nleft ? ap[k] : 0.f;
-            }
+            const float4 t4 = pre[rr / 4];
+            const float av[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
             for (int k = 0; k < 4; ++k) o[k] = o[k] * (av[k] * (1.f - av[k]));
           } else if (grow < args.m_zero_rows) {
@@ -326,17 +376,24 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
 #endif
         if (EPI == EPI_SGD) {
           float* wp = args.out + grow * args.ldo + gn;
+          float* lp = args.out_lo != nullptr ? args.out_lo + grow * args.ldo + gn : nullptr;
           if (vec_out && nleft >= 4) {
-            float4 w4 = *reinterpret_cast<float4*>(wp);
+            float4 w4 = pre[rr / 4];
             w4.x -= args.eta * o[0];
             w4.y -= args.eta * o[1];
             w4.z -= args.eta * o[2];
             w4.w -= args.eta * o[3];
             *reinterpret_cast<float4*>(wp) = w4;
+            if (lp != nullptr) *reinterpret_cast<float4*>(lp) = lo4(w4);
           } else {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              if (k < nleft) wp[k] -= args.eta * o[k];
+              if (k < nleft) {
+                const float prev = k == 0 ? pre[rr / 4].x : k == 1 ? pre[rr / 4].y : k == 2 ? pre[rr / 4].z : pre[rr / 4].w;
+                const float nw = prev - args.eta * o[k];
+                wp[k] = nw;
+                if (lp != nullptr) lp[k] = tf32_lo(nw);
+              }
           }
           if (args.grad != nullptr) {
             float* gp = args.grad + grow * args.ld_grad + gn;
@@ -351,52 +408,36 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
         } else {
           float* op = args.out + (EPI == EPI_PARTIAL ? static_cast<long long>(blockIdx.z) * args.split_stride : 0LL) +
                       grow * args.ldo + gn;
+          float* lp = (EPI != EPI_PARTIAL && args.out_lo != nullptr) ? args.out_lo + grow * args.ldo + gn : nullptr;
           if (vec_out && nleft >= 4) {
-            *reinterpret_cast<float4*>(op) = make_float4(o[0], o[1], o[2], o[3]);
+            const float4 v4 = make_float4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<float4*>(op) = v4;
+            if (lp != nullptr) *reinterpret_cast<float4*>(lp) = lo4(v4);
           } else {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              if (k < nleft) op[k] = o[k];
+              if (k < nleft) {
+                op[k] = o[k];
+                if (lp != nullptr) lp[k] = tf32_lo(o[k]);
+              }
           }
         }
       }
     }
-  } else if (PASSES == 3 && threadIdx.x >= C::SPLIT_BASE) {
-    // ------------------------------------------------- hi/lo splitter
-    const int t = threadIdx.x - C::SPLIT_BASE;
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % STAGES;
-      const uint32_t ph = (i / STAGES) & 1;
-      mbar_wait(&full[s], ph);
-      if (t == 0) HB_STAMP(3 * 512 + i);  // split: TMA landed
-      const uint32_t hi = smem_u32(smem + s * C::STAGE_BYTES);
-      const uint32_t lo = hi + C::OP_BYTES;
-#pragma unroll 4
-      for (int j = t; j < C::OP_BYTES / 16; j += C::SPLIT_THREADS) {
-        uint32_t x0, x1, x2, x3;
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3) : "r"(hi + 16 * j));
-#if HB_SPLIT_HI_RAW
-        const uint32_t h0 = x0 & 0xFFFFE000u, h1 = x1 & 0xFFFFE000u, h2 = x2 & 0xFFFFE000u, h3 = x3 & 0xFFFFE000u;
-#else
-        const uint32_t h0 = to_tf32_rna(x0), h1 = to_tf32_rna(x1), h2 = to_tf32_rna(x2), h3 = to_tf32_rna(x3);
-        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(hi + 16 * j), "r"(h0), "r"(h1), "r"(h2), "r"(h3));
-#endif
-        const float l0 = __uint_as_float(x0) - __uint_as_float(h0), l1 = __uint_as_float(x1) - __uint_as_float(h1),
-                    l2 = __uint_as_float(x2) - __uint_as_float(h2), l3 = __uint_as_float(x3) - __uint_as_float(h3);
-        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lo + 16 * j), "f"(l0), "f"(l1), "f"(l2), "f"(l3));
-      }
-      fence_proxy_async_smem();
-      mbar_arrive(&ready[s]);
-      if (t == 0) HB_STAMP(4 * 512 + i);  // split: done
-    }
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync_all();  // no CTA may exit while its peer can still touch its smem / barriers
+  else
+    __syncthreads();
   if (threadIdx.x == 0) HB_STAMP(6 * 512 + 1);  // CTA end
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, C::TMEM_COLS);
+    if (PAIR)
+      tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+    else
+      tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
 }
 

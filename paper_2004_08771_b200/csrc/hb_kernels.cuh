@@ -65,6 +65,7 @@ struct HeadArgs {
   float inv_n;             // 1 / batch size
   int train;               // 0 = loss only (evaluation)
   float* delta_prev;       // (zero_rows, d) or null
+  float* delta_prev_lo;    // its 3xTF32 lo twin (same layout) or null
   long long ld_dp;
   float* delta_out;        // (rows, nc) or null (tests)
   long long ld_do;
@@ -103,7 +104,10 @@ __global__ void __launch_bounds__(kHeadWarps * 32, (MAXT <= 16 && NCT <= 2) ? 2 
       if (p.train && p.delta_prev != nullptr && row < p.zero_rows) {
         for (int t = 0; t < T; ++t) {
           const int j = lane + 32 * t;
-          if (j < p.d) p.delta_prev[row * p.ld_dp + j] = 0.f;
+          if (j < p.d) {
+            p.delta_prev[row * p.ld_dp + j] = 0.f;
+            if (p.delta_prev_lo != nullptr) p.delta_prev_lo[row * p.ld_dp + j] = 0.f;
+          }
         }
       }
       continue;
@@ -156,7 +160,11 @@ __global__ void __launch_bounds__(kHeadWarps * 32, (MAXT <= 16 && NCT <= 2) ? 2 
         g = fmaf(dl[c], sW[c * 32 * MAXT + j], g);
         acc[c][t] = fmaf(dl[c], av[t], acc[c][t]);
       }
-      if (p.delta_prev != nullptr && t < T && j < p.d) p.delta_prev[row * p.ld_dp + j] = g * (av[t] * (1.f - av[t]));
+      if (p.delta_prev != nullptr && t < T && j < p.d) {
+        const float dv = g * (av[t] * (1.f - av[t]));
+        p.delta_prev[row * p.ld_dp + j] = dv;
+        if (p.delta_prev_lo != nullptr) p.delta_prev_lo[row * p.ld_dp + j] = tf32_lo(dv);
+      }
     }
   }
 
@@ -258,7 +266,11 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_small_vec_kernel(HeadArg
 #pragma unroll
         for (int t = 0; t < VPL; ++t) {
           const int j = 4 * lane + 128 * t;
-          if (j < p.d) *reinterpret_cast<float4*>(p.delta_prev + row * p.ld_dp + j) = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (j < p.d) {
+            *reinterpret_cast<float4*>(p.delta_prev + row * p.ld_dp + j) = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (p.delta_prev_lo != nullptr)
+              *reinterpret_cast<float4*>(p.delta_prev_lo + row * p.ld_dp + j) = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
         }
       }
       continue;
@@ -301,9 +313,10 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_small_vec_kernel(HeadArg
       }
       if (p.delta_prev != nullptr && j < p.d) {
         const float4 a4 = av[k][t];
-        *reinterpret_cast<float4*>(p.delta_prev + row * p.ld_dp + j) =
-            make_float4(g.x * (a4.x * (1.f - a4.x)), g.y * (a4.y * (1.f - a4.y)), g.z * (a4.z * (1.f - a4.z)),
-                        g.w * (a4.w * (1.f - a4.w)));
+        const float4 dv = make_float4(g.x * (a4.x * (1.f - a4.x)), g.y * (a4.y * (1.f - a4.y)),
+                                      g.z * (a4.z * (1.f - a4.z)), g.w * (a4.w * (1.f - a4.w)));
+        *reinterpret_cast<float4*>(p.delta_prev + row * p.ld_dp + j) = dv;
+        if (p.delta_prev_lo != nullptr) *reinterpret_cast<float4*>(p.delta_prev_lo + row * p.ld_dp + j) = lo4(dv);
       }
     }
   }
@@ -344,6 +357,7 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_small_vec_kernel(HeadArg
 // One warp per row, row max shift as linalg.py:63-67.
 struct SoftmaxArgs {
   float* z;  // (zero_rows, nc) logits in, delta out
+  float* z_lo;  // lo twin of delta (or null)
   long long ldz;
   const int64_t* labels;  // staged label array, indexed from start
   long long start;
@@ -377,11 +391,16 @@ __global__ void __launch_bounds__(256) softmax_delta_kernel(SoftmaxArgs p) {
       __syncwarp();
       for (int j = lane; j < p.nc; j += 32) {
         const float pj = expf(zr[j] - m) / s;
-        zr[j] = (pj - (j == y ? 1.f : 0.f)) * p.inv_n;
+        const float dv = (pj - (j == y ? 1.f : 0.f)) * p.inv_n;
+        zr[j] = dv;
+        if (p.z_lo != nullptr) p.z_lo[row * p.ldz + j] = tf32_lo(dv);
       }
     }
   } else if (p.train && row < p.zero_rows) {
-    for (int j = lane; j < p.nc; j += 32) p.z[row * p.ldz + j] = 0.f;
+    for (int j = lane; j < p.nc; j += 32) {
+      p.z[row * p.ldz + j] = 0.f;
+      if (p.z_lo != nullptr) p.z_lo[row * p.ldz + j] = 0.f;
+    }
   }
   if (lane == 0) sLoss[warp] = loss;
   __syncthreads();
@@ -411,7 +430,8 @@ __global__ void loss_reduce_kernel(const double* ws, int n, double* out, int acc
 // 8 warp sums in order -- a fixed summation order for every element.
 __global__ void __launch_bounds__(256) reduce_sgd_kernel(float* w, long long ldw, const float* part, int S,
                                                            long long slab, int rows, int cols, float eta,
-                                                           float* grad, long long ldg, const DevStep* ds) {
+                                                           float* grad, long long ldg, const DevStep* ds,
+                                                           float* w_lo) {
   __shared__ float red[8][33];
   eta = step_eta(ds, eta);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -439,7 +459,9 @@ __global__ void __launch_bounds__(256) reduce_sgd_kernel(float* w, long long ldw
 #pragma unroll
     for (int k = 0; k < 8; ++k) g += red[k][lane];
     const long long r = i / cols, c = i % cols;
-    w[r * ldw + c] -= eta * g;
+    const float nw = w[r * ldw + c] - eta * g;
+    w[r * ldw + c] = nw;
+    if (w_lo != nullptr) w_lo[r * ldw + c] = tf32_lo(nw);
     if (grad != nullptr) grad[r * ldg + c] = g;
   }
 }
@@ -450,7 +472,8 @@ __global__ void __launch_bounds__(256) reduce_sgd_kernel(float* w, long long ldw
 // 16-byte-aligned rows of w / grad.
 __global__ void __launch_bounds__(256) reduce_sgd_vec_kernel(float* w, long long ldw, const float* part, int S,
                                                                long long slab, int rows, int cols, float eta,
-                                                               float* grad, long long ldg, const DevStep* ds) {
+                                                               float* grad, long long ldg, const DevStep* ds,
+                                                               float* w_lo) {
   eta = step_eta(ds, eta);
   const long long quads = static_cast<long long>(rows) * cols / 4;
   for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < quads;
@@ -472,6 +495,7 @@ __global__ void __launch_bounds__(256) reduce_sgd_vec_kernel(float* w, long long
     wv.z -= eta * g.z;
     wv.w -= eta * g.w;
     *wp = wv;
+    if (w_lo != nullptr) *reinterpret_cast<float4*>(w_lo + r * ldw + c) = lo4(wv);
     if (grad != nullptr) *reinterpret_cast<float4*>(grad + r * ldg + c) = g;
   }
 }
@@ -493,6 +517,7 @@ struct SpmmArgs {
   int d_out;
   float* out;  // (rows, d_out)
   long long ldo;
+  float* out_lo;  // lo twin of out (or null)
 };
 
 template <bool VEC>
@@ -528,9 +553,12 @@ __global__ void __launch_bounds__(256) spmm_sigmoid_kernel(SpmmArgs p) {
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const int j = base + 4 * lane + 128 * t;
-        if (j < p.d_out)
-          reinterpret_cast<float4*>(o)[j / 4] = make_float4(sigmoidf_stable(acc[t].x), sigmoidf_stable(acc[t].y),
-                                                            sigmoidf_stable(acc[t].z), sigmoidf_stable(acc[t].w));
+        if (j < p.d_out) {
+          const float4 sv = make_float4(sigmoidf_stable(acc[t].x), sigmoidf_stable(acc[t].y),
+                                        sigmoidf_stable(acc[t].z), sigmoidf_stable(acc[t].w));
+          reinterpret_cast<float4*>(o)[j / 4] = sv;
+          if (p.out_lo != nullptr) reinterpret_cast<float4*>(p.out_lo + warp * p.ldo)[j / 4] = lo4(sv);
+        }
       }
     }
   } else {
@@ -550,7 +578,11 @@ __global__ void __launch_bounds__(256) spmm_sigmoid_kernel(SpmmArgs p) {
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const int j = base + lane + 32 * t;
-        if (j < p.d_out) o[j] = sigmoidf_stable(acc[t]);
+        if (j < p.d_out) {
+          const float sv = sigmoidf_stable(acc[t]);
+          o[j] = sv;
+          if (p.out_lo != nullptr) p.out_lo[warp * p.ldo + j] = tf32_lo(sv);
+        }
       }
     }
   }
@@ -732,16 +764,16 @@ __global__ void __launch_bounds__(256) sparse_dw_warp_kernel(SparseDwArgs p) {
 // dst (rows, cols, ldd) fp32 <- src (rows, cols, lds) fp64; TRANSPOSE writes
 // dst[c, r] (used for the transposed sparse first-layer weight).
 template <bool TRANSPOSE>
-__global__ void f64_to_f32_kernel(float* dst, long long ldd, const double* src, long long lds, int rows, int cols) {
+__global__ void f64_to_f32_kernel(float* dst, long long ldd, const double* src, long long lds, int rows, int cols,
+                                  float* dst_lo) {
   const long long total = static_cast<long long>(rows) * cols;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long r = i / cols, c = i % cols;
     const float v = static_cast<float>(src[r * lds + c]);
-    if (TRANSPOSE)
-      dst[c * ldd + r] = v;
-    else
-      dst[r * ldd + c] = v;
+    const long long o = TRANSPOSE ? c * ldd + r : r * ldd + c;
+    dst[o] = v;
+    if (dst_lo != nullptr) dst_lo[o] = tf32_lo(v);
   }
 }
 template <bool TRANSPOSE>
@@ -754,14 +786,27 @@ __global__ void f32_to_f64_kernel(double* dst, long long ldd, const float* src, 
   }
 }
 
+// lo (rows, cols, ld) = x - trunc_tf32(x): the 3xTF32 twin of a staged input.
+__global__ void split_lo_kernel(const float* x, float* lo, long long ld, long long rows, int cols) {
+  const long long total = rows * cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / cols, c = i % cols;
+    lo[r * ld + c] = tf32_lo(x[r * ld + c]);
+  }
+}
+
 // dst (rows, cols, ldd) = scale * src (rows, cols, dense): unpack of the
 // allreduced flat model (replica averaging).
-__global__ void unpack_scale_kernel(float* dst, long long ldd, const float* src, int rows, int cols, float scale) {
+__global__ void unpack_scale_kernel(float* dst, long long ldd, const float* src, int rows, int cols, float scale,
+                                    float* dst_lo) {
   const long long total = static_cast<long long>(rows) * cols;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long r = i / cols, c = i % cols;
-    dst[r * ldd + c] = src[i] * scale;
+    const float v = src[i] * scale;
+    dst[r * ldd + c] = v;
+    if (dst_lo != nullptr) dst_lo[r * ldd + c] = tf32_lo(v);
   }
 }
 

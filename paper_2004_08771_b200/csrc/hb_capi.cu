@@ -297,6 +297,9 @@ struct hb_ctx {
   size_t pinned_bytes = 0;
 
   long long *csc_lo = nullptr, *csc_hi = nullptr;  // per-feature batch slices (sparse dW)
+  bool sdw_narrow = false;                         // sparse dW via smem slices (small d_in)
+  bool sparse_smem = false;                        // experimental smem-sliced sparse kernels
+  size_t sdw_smem = 0;
   double nnz_per_row = 0.0;
   float* ws = nullptr;  // split-K partials / head partials
   size_t ws_floats = 0;
@@ -416,9 +419,12 @@ int choose_bn(long long m_tiles, long long n) {
 // split-K plan for the dW GEMM of layer l at `rows` batch rows
 void dw_plan(const hb_ctx* c, int l, int rows, int* splits, int* kb_per, int* kb_total) {
   const int M = c->d[l + 1], N = c->d[l];
-  const int tiles = cdiv(M, kBM) * cdiv(N, c->bn_dw[l]);
+  // CTAs per split: M tiles padded to whole CTA pairs (3xTF32 kernels run in pairs)
+  const int mt = cdiv(M, kBM);
+  const int tiles = (c->passes == 3 && c->bn_dw[l] >= 64 ? (mt + 1) / 2 * 2 : mt) * cdiv(N, c->bn_dw[l]);
   *kb_total = std::max(1, cdiv(rows, kBK));
-  int want = std::max(1, (148 * 3 / 2 + tiles - 1) / tiles);
+  // one wave: as many K splits as fit on the 148 SMs (1 CTA / SM)
+  int want = std::max(1, 148 / tiles);
   want = std::min(want, *kb_total);
   *kb_per = cdiv(*kb_total, want);
   *splits = cdiv(*kb_total, *kb_per);
@@ -435,14 +441,30 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   // hidden layers
   for (int l = 0; l < L - 1; ++l) {
     if (l == 0 && c->sparse) {
-      SpmmArgs p{v.rowptr, v.col, v.val, ds, start, rows, c->W[0], c->ldw[0], c->d[1], c->A[1], c->ld[1],
+      SpmmArgs p{v.rowptr, v.col, v.val, ds, start, rows, c->W[0], c->ldw[0], c->d[0], c->d[1], c->A[1], c->ld[1],
                  c->need_lo() ? c->A_lo[1] : nullptr};
-      const int blocks = cdiv(static_cast<long long>(rows) * 32, 256);
       prof_begin(c);
-      if (c->d[1] % 128 == 0)
-        spmm_sigmoid_kernel<true><<<blocks, 256, 0, st>>>(p);
-      else
-        spmm_sigmoid_kernel<false><<<blocks, 256, 0, st>>>(p);
+      const size_t slice_smem = static_cast<size_t>(c->d[0]) * kSpmmSliceCols * sizeof(float) +
+                                kCsrChunkEntries * 8 + (kCsrChunkRows + 1) * 4;
+      if (c->sparse_smem && c->d[1] % 4 == 0 && slice_smem <= 200 * 1024) {
+        // narrow input: W0^T column slices staged in shared memory
+        static bool configured = false;
+        if (!configured) {
+          HB_CUDA(cudaFuncSetAttribute(spmm_sigmoid_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       200 * 1024));
+          configured = true;
+        }
+        const int col_slices = cdiv(c->d[1], kSpmmSliceCols);
+        const int row_blocks = std::max(1, std::min(cdiv(rows, 16), 148 / std::max(1, col_slices)));
+        const int rpb = cdiv(rows, row_blocks);
+        spmm_sigmoid_smem_kernel<<<dim3(col_slices, cdiv(rows, rpb)), 512, slice_smem, st>>>(p, rpb);
+      } else {
+        const int blocks = cdiv(static_cast<long long>(rows) * 32, 256);
+        if (c->d[1] % 128 == 0)
+          spmm_sigmoid_kernel<true><<<blocks, 256, 0, st>>>(p);
+        else
+          spmm_sigmoid_kernel<false><<<blocks, 256, 0, st>>>(p);
+      }
       HB_CUDA(cudaGetLastError());
       prof_end(c, "spmm_sigmoid", 0);
       c->last_launches++;
@@ -608,6 +630,34 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
                      c->W[0], c->ldw[0], static_cast<float>(eta), emit ? c->G[0] : nullptr, c->ldw[0],
                      c->csc_lo, c->csc_hi};
       prof_begin(c);
+      if (c->sdw_narrow) {
+        // narrow input: smem dW0^T slices per row block, then fixed-order reduce + SGD
+        const int col_slices = cdiv(c->d[1], kSdwSliceCols);
+        const int row_blocks = std::max(1, std::min(cdiv(rows, 64), 148 / std::max(1, col_slices)));
+        SparseDwSmemArgs q{v.rowptr, v.col, v.val, ds, start, rows, c->d[0], c->d[1], c->D[0], c->ld[1], c->ws,
+                           cdiv(rows, row_blocks)};
+        static bool configured = false;
+        if (!configured) {
+          HB_CUDA(cudaFuncSetAttribute(sparse_dw_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       200 * 1024));
+          configured = true;
+        }
+        sparse_dw_smem_kernel<<<dim3(col_slices, row_blocks), 512, c->sdw_smem, st>>>(q);
+        HB_CUDA(cudaGetLastError());
+        const long long slab = static_cast<long long>(c->d[0]) * c->d[1];
+        if (c->d[1] % 4 == 0 && (slab / 4) >= 148 * 256)
+          reduce_sgd_vec_kernel<<<static_cast<int>(std::min<long long>(cdiv(slab / 4, 256), 148 * 8)), 256, 0, st>>>(
+              c->W[0], c->ldw[0], c->ws, row_blocks, slab, c->d[0], c->d[1], static_cast<float>(eta),
+              emit ? c->G[0] : nullptr, c->ldw[0], ds, nullptr);
+        else
+          reduce_sgd_kernel<<<cdiv(slab, 32), 256, 0, st>>>(c->W[0], c->ldw[0], c->ws, row_blocks, slab, c->d[0],
+                                                            c->d[1], static_cast<float>(eta),
+                                                            emit ? c->G[0] : nullptr, c->ldw[0], ds, nullptr);
+        HB_CUDA(cudaGetLastError());
+        prof_end(c, "sparse_dw_sgd", 0);
+        c->last_launches += 2;
+        continue;
+      }
       csc_batch_ranges_kernel<<<cdiv(c->d[0], 256), 256, 0, st>>>(v.colptr, v.rowidx, c->d[0], start, rows, ds,
                                                                   c->csc_lo, c->csc_hi);
       // batch entries per feature decide the parallelisation
@@ -975,6 +1025,19 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
     if (splits > 1) ws = std::max(ws, static_cast<size_t>(splits) * c->d[l + 1] * c->d[l]);
   }
   if (c->small_head) ws = std::max(ws, static_cast<size_t>(cdiv(c->cap, kHeadRowsPerBlock)) * nc * dlast);
+  if (c->sparse) {
+    c->sdw_smem = (static_cast<size_t>(c->d[0]) * kSdwSliceCols + static_cast<size_t>(kCsrChunkRows) * kSdwSliceCols) *
+                      sizeof(float) +
+                  static_cast<size_t>(kCsrChunkEntries) * 12;
+    // experimental (HB_SPARSE_SMEM=1): slower than the CSC-slice kernel at w8a shapes so far
+    c->sparse_smem = getenv("HB_SPARSE_SMEM") && getenv("HB_SPARSE_SMEM")[0] == '1';
+    c->sdw_narrow = c->sparse_smem && c->d[0] <= kCsrChunkEntries && c->sdw_smem <= 200 * 1024 && c->d[1] % 4 == 0;
+    if (c->sdw_narrow) {
+      const int col_slices = cdiv(c->d[1], kSdwSliceCols);
+      const int row_blocks = std::max(1, 148 / std::max(1, col_slices));
+      ws = std::max(ws, static_cast<size_t>(row_blocks) * c->d[0] * c->d[1]);
+    }
+  }
   c->ws_floats = std::max<size_t>(ws, 1);
   HB_CK(cudaMalloc(&c->ws, c->ws_floats * sizeof(float)));
   c->ws_loss_n = std::max(cdiv(c->cap, kHeadRowsPerBlock), cdiv(c->cap, 8)) + 1;

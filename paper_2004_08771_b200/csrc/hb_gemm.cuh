@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
           }
         }
       }
+      if (threadIdx.x == 128) HB_STAMP(7 * 512 + 4 * (c / CSTEP) + 0);  // epi: TMEM loaded
       const int n = n0 + c;
       if (n >= args.N) continue;  // warp-uniform (and then so are all later chunks)
 #ifdef HB_DEBUG_NO_EPI_STORE
@@ -342,6 +343,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
       for (int j = 0; j < 32; j += 4)
         *reinterpret_cast<float4*>(tile + lane * TP + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
       __syncwarp();
+      if (threadIdx.x == 128) HB_STAMP(7 * 512 + 4 * (c / CSTEP) + 1);  // epi: transposed
       const int gn = n + sub_c;
       const int nleft = args.N - gn;  // columns of this quad still inside N
 #pragma unroll

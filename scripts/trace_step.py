@@ -24,3 +24,6 @@ print(f"CTA start 0, epilogue start {rel(a[6*512]):.2f} us, end {rel(a[6*512+1])
 for i in range(64):
     if not a[0 * 512 + i] and not a[1 * 512 + i]: break
     print(f"kb {i:2d}: tma_issue {rel(a[i]):7.2f}  mma_start {rel(a[512+i]):7.2f}  mma_issued {rel(a[1024+i]):7.2f}")
+for c in range(8):
+    t0_, t1_ = a[7 * 512 + 4 * c], a[7 * 512 + 4 * c + 1]
+    if t0_: print(f"epi chunk {c}: tmem loaded {rel(t0_):.2f}  transposed {rel(t1_):.2f}")

@@ -247,13 +247,16 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
                 host_batches.append((np.ascontiguousarray(data.features[s:s + b], dtype=np.float32),
                                      data.labels[s:s + b].copy()))
         host_model = [w.copy() for w in model.weights]
-        h2d = sum(w.nbytes for w in host_model)
-        d2h = sum(w.size * 4 for w in host_model) + 8
+        # the snapshot reads the f64 model over PCIe, the stale merge reads and
+        # writes it back (registered host memory, device-side RMW), the loss comes back
+        h2d = 2 * sum(w.nbytes for w in host_model)
+        d2h = sum(w.nbytes for w in host_model) + 8
         bb = host_batches[0][0]
         if sparse:
             h2d += bb.rowptr.nbytes + (sizes[0] + 1) * 8 + bb.labels.nbytes + 2 * bb.col.nbytes + 2 * bb.nnz * 4
         else:
             h2d += bb.nbytes + host_batches[0][1].nbytes
+        ctx.pin_host(host_model)  # what execute_gpu_replica does for the shared model
         for i in range(min(2, args.warmup)):  # warm the host path
             ctx.set_weights(host_model)
             ctx.step_host(host_batches[i % len(host_batches)][0], host_batches[i % len(host_batches)][1],
@@ -272,8 +275,9 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
             el = max_over_ranks(dist, el)
         e2e = {"value": world * args.steps * b / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
-               "path": "execute_gpu_replica semantics via the C ABI: f64 model snapshot H2D + host batch H2D "
-                       "+ step + grad D2H + f64 stale merge + loss D2H"}
+               "path": "execute_gpu_replica semantics through the C ABI, per step: snapshot of the page-locked "
+                       "f64 host model (read over PCIe), CSR batch H2D from pinned host memory + device batch "
+                       "CSC, the step, the f64 stale merge W_host -= eta*g written back over PCIe, loss D2H"}
     ctx.close()
 
     # ---------------------------------------------------------- roofline of the dominant kernel

@@ -32,6 +32,7 @@
 #ifndef HOGBATCH_B200_H
 #define HOGBATCH_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -79,6 +80,14 @@ int hb_get_weights_f32(hb_ctx* ctx, int layer, float* w);
  * host_w -= eta * g_l for the gradient kept by the last HB_STEP_EMIT_GRAD
  * step, element by element with aligned 8-byte stores.  */
 int hb_merge_grad_into_f64(hb_ctx* ctx, int layer, double* host_w, double eta);
+/* Whole-model forms of the two calls above (one transfer each way, one sync):
+ * ws[l] points at layer l's host float64 (d_{l+1}, d_l) array. */
+int hb_set_weights_all_f64(hb_ctx* ctx, const double* const* ws);
+int hb_merge_grads_all_into_f64(hb_ctx* ctx, double* const* ws, double eta);
+/* Page-lock (and later release) a host range used for repeated exchanges, e.g.
+ * the shared float64 model, so its copies run at full link speed. */
+int hb_host_register(const void* p, size_t bytes);
+int hb_host_unregister(const void* p);
 /* Raw mean gradient of the last HB_STEP_EMIT_GRAD step, (d_{l+1}, d_l) fp32. */
 int hb_get_grad_f32(hb_ctx* ctx, int layer, float* g);
 

@@ -41,6 +41,10 @@ SIGNATURES = {
     "hb_get_weights_f32": (_i32, [_p, _i32, _fp]),
     "hb_merge_grad_into_f64": (_i32, [_p, _i32, _dp, _f64]),
     "hb_get_grad_f32": (_i32, [_p, _i32, _fp]),
+    "hb_set_weights_all_f64": (_i32, [_p, C.POINTER(_dp)]),
+    "hb_merge_grads_all_into_f64": (_i32, [_p, C.POINTER(_dp), _f64]),
+    "hb_host_register": (_i32, [_p, C.c_size_t]),
+    "hb_host_unregister": (_i32, [_p]),
     "hb_stage_dense_f64": (_i32, [_p, _dp, _i64, _i64, _i64p]),
     "hb_stage_dense_f32": (_i32, [_p, _fp, _i64, _i64, _i64p]),
     "hb_stage_csr": (_i32, [_p, _i64p, _i32p, _fp, _i64, _i64p]),

@@ -21,10 +21,16 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
+#include <mutex>
+#include <thread>
 #include <string>
 #include <tuple>
 #include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "../../include/hogbatch_b200.h"
 #include "hb_gemm.cuh"
@@ -96,6 +102,9 @@ int make_map(CUtensorMap* m, const float* base, long long inner, long long rows,
                 static_cast<int>(r), inner, rows, ld, box_rows, static_cast<int>(mn_major));
   return HB_OK;
 }
+
+std::mutex g_host_mu;
+std::map<uintptr_t, std::pair<size_t, void*>> g_host_ranges;  // host base -> (bytes, device alias)
 
 // ------------------------------------------------------------ GEMM launch
 int g_trace_launch_no = 0;  // HB_TRACE builds: index of the GEMM launch being issued
@@ -297,6 +306,12 @@ struct hb_ctx {
   size_t pinned_bytes = 0;
 
   long long *csc_lo = nullptr, *csc_hi = nullptr;  // per-feature batch slices (sparse dW)
+  uint32_t* csc_keys = nullptr;  // device batch-CSC build scratch (host-buffer steps)
+  int32_t* csc_idx = nullptr;
+  int* csc_counts = nullptr;
+  void* csc_temp = nullptr;
+  size_t csc_temp_bytes = 0;
+  long long csc_cap = 0;
   bool sdw_narrow = false;                         // sparse dW via smem slices (small d_in)
   bool sparse_smem = false;                        // experimental smem-sliced sparse kernels
   size_t sdw_smem = 0;
@@ -309,6 +324,9 @@ struct hb_ctx {
   double* stage64 = nullptr;  // f64 staging for the weight exchange
   size_t stage64_n = 0;
   float* stage32 = nullptr;  // fp32 staging (grad transpose)
+  double* stage_all = nullptr;  // whole-model f64 staging (set_weights_all)
+  float* grad_all = nullptr;    // whole-model gradient gather
+  float* grad_host = nullptr;   // pinned host copy of grad_all
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.f;
   int last_launches = 0;
@@ -728,29 +746,32 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
 // Enqueue one step.  Eager the first time a (rows, flags, data view) shape is
 // seen; from the second time on, the whole step is a captured CUDA graph that
 // reads (start, eta) from c->d_step, so a step costs one graph launch.
-int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta, uint32_t flags, bool graph_ok) {
-  const uint32_t gflags = flags & HB_STEP_EMIT_GRAD;
+// phase 0: whole step; 1: forward (incl. the fused head and its update); 2: backward
+int run_phase(hb_ctx* c, const DataView& v, long long start, int rows, uint32_t flags, double eta, const DevStep* ds,
+              int phase) {
+  if (phase != 2) HB_TRY(run_forward(c, v, start, rows, true, flags, eta, ds));
+  if (phase != 1) HB_TRY(run_backward(c, v, start, rows, flags, eta, ds));
+  return HB_OK;
+}
+
+int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta, uint32_t flags, bool graph_ok,
+                 int phase = 0) {
+  const uint32_t gflags = (flags & HB_STEP_EMIT_GRAD) | (static_cast<uint32_t>(phase) << 8);
   const bool view_epoch = (&v == &c->epoch);
-  if (!c->use_graphs || !graph_ok) {
-    HB_TRY(run_forward(c, v, start, rows, true, flags, eta, nullptr));
-    return run_backward(c, v, start, rows, flags, eta, nullptr);
-  }
+  if (!c->use_graphs || !graph_ok) return run_phase(c, v, start, rows, flags, eta, nullptr, phase);
   const auto key = std::make_tuple(rows, gflags, view_epoch ? c->view_gen : -c->view_gen, c->prof_on);
   DevStep hs{start, static_cast<float>(eta), 0};
   auto it = c->graphs.find(key);
   if (it == c->graphs.end()) {
-    if (c->graph_seen[key]++ == 0) {  // first sighting: run eagerly (also configures kernel attributes)
-      HB_TRY(run_forward(c, v, start, rows, true, flags, eta, nullptr));
-      return run_backward(c, v, start, rows, flags, eta, nullptr);
-    }
+    if (c->graph_seen[key]++ == 0)  // first sighting: run eagerly (also configures kernel attributes)
+      return run_phase(c, v, start, rows, flags, eta, nullptr, phase);
     StepGraph g;
     c->capturing = true;
     c->cap_events.clear();
     c->step_marks.clear();
     HB_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     const int launches0 = c->last_launches;
-    int rc = run_forward(c, v, 0, rows, true, flags, 0.0, c->d_step);
-    if (rc == HB_OK) rc = run_backward(c, v, 0, rows, flags, 0.0, c->d_step);
+    int rc = run_phase(c, v, 0, rows, flags, 0.0, c->d_step, phase);
     cudaGraph_t graph = nullptr;
     cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
     c->capturing = false;
@@ -767,10 +788,10 @@ int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double
     it = c->graphs.emplace(key, std::move(g)).first;
     c->last_launches = 0;
   }
-  HB_CUDA(cudaMemcpyAsync(c->d_step, &hs, sizeof hs, cudaMemcpyHostToDevice, c->stream));
+  if (phase != 2) HB_CUDA(cudaMemcpyAsync(c->d_step, &hs, sizeof hs, cudaMemcpyHostToDevice, c->stream));
   HB_CUDA(cudaGraphLaunch(it->second.exec, c->stream));
   c->last_launches += it->second.launches;
-  if (c->prof_on) c->step_marks = it->second.marks;
+  if (c->prof_on) c->step_marks.insert(c->step_marks.end(), it->second.marks.begin(), it->second.marks.end());
   return HB_OK;
 }
 
@@ -783,15 +804,24 @@ void drop_graphs(hb_ctx* c) {
   c->graph_seen.clear();
 }
 
+// `mid` (optional): host work run between the enqueued forward and backward
+// phases (the host-buffer CSR step builds the batch CSC there, overlapping the
+// device forward pass).
 int do_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta, uint32_t flags, double* out_loss,
-            bool graph_ok = true) {
+            bool graph_ok = true, const std::function<int()>& mid = nullptr) {
   if (rows < 1 || rows > c->max_batch) return fail(HB_EINVAL, "rows=%d outside [1, %d]", rows, c->max_batch);
   c->last_launches = 0;
   c->ev_used = 0;
   c->step_marks.clear();
   const bool timed = (flags & HB_STEP_TIMED) != 0;
   if (timed) HB_CUDA(cudaEventRecord(c->ev0, c->stream));
-  HB_TRY(enqueue_step(c, v, start, rows, eta, flags, graph_ok));
+  if (mid) {
+    HB_TRY(enqueue_step(c, v, start, rows, eta, flags, graph_ok, 1));
+    HB_TRY(mid());
+    HB_TRY(enqueue_step(c, v, start, rows, eta, flags, graph_ok, 2));
+  } else {
+    HB_TRY(enqueue_step(c, v, start, rows, eta, flags, graph_ok));
+  }
   if (timed) HB_CUDA(cudaEventRecord(c->ev1, c->stream));
   c->grads_valid = (flags & HB_STEP_EMIT_GRAD) != 0;
   if (out_loss != nullptr) {
@@ -828,6 +858,49 @@ void build_csc(const int64_t* rowptr, const int32_t* col, const float* val, long
     for (long long e = rowptr[r]; e < rowptr[r + 1]; ++e) {
       const long long k = cur[col[e]]++;
       rowidx[k] = static_cast<int32_t>(r + row_base);
+      cval[k] = val[e];
+    }
+}
+
+// ------------------------------------------------ batch CSC on the device
+// keys[e] = col[e] * rows + row(e): sorting the (unique) keys orders entries by
+// feature and, within a feature, by row -- the same order as the host counting
+// sort, so results stay bit-identical to the staged-epoch path.
+__global__ void csc_keys_kernel(const int64_t* rowptr, const int32_t* col, int rows, uint32_t* keys, int32_t* idx,
+                                int* counts) {
+  const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  for (long long e = rowptr[r] + lane; e < rowptr[r + 1]; e += 32) {
+    const int f = col[e];
+    keys[e] = static_cast<uint32_t>(f) * static_cast<uint32_t>(rows) + static_cast<uint32_t>(r);
+    idx[e] = static_cast<int32_t>(e);
+    atomicAdd(&counts[f + 1], 1);  // integer counts: order-independent
+  }
+}
+__global__ void csc_gather_kernel(const uint32_t* keys_sorted, const int32_t* idx_sorted, const float* val,
+                                  long long nnz, int rows, int32_t* rowidx, float* cval) {
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < nnz;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    rowidx[k] = static_cast<int32_t>(keys_sorted[k] % static_cast<uint32_t>(rows));
+    cval[k] = val[idx_sorted[k]];
+  }
+}
+__global__ void counts_to_colptr_kernel(const int* counts, int64_t* colptr, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) colptr[i] = counts[i];
+}
+
+// Same stable counting sort writing straight into (pinned) output arrays.
+void build_csc_into(const int64_t* rowptr, const int32_t* col, const float* val, long long n_rows, int n_cols,
+                    int64_t* colptr, int32_t* rowidx, float* cval, std::vector<int64_t>& cur) {
+  std::memset(colptr, 0, (n_cols + 1) * sizeof(int64_t));
+  for (long long e = rowptr[0]; e < rowptr[n_rows]; ++e) colptr[col[e] + 1]++;
+  for (int j = 0; j < n_cols; ++j) colptr[j + 1] += colptr[j];
+  cur.assign(colptr, colptr + n_cols);
+  for (long long r = 0; r < n_rows; ++r)
+    for (long long e = rowptr[r]; e < rowptr[r + 1]; ++e) {
+      const long long k = cur[col[e]]++;
+      rowidx[k] = static_cast<int32_t>(r);
       cval[k] = val[e];
     }
 }
@@ -1088,6 +1161,10 @@ int hb_ctx_destroy(hb_ctx* c) {
   drop_graphs(c);
   cudaFree(c->d_step);
   cudaFree(c->csc_lo);
+  cudaFree(c->csc_keys);
+  cudaFree(c->csc_idx);
+  cudaFree(c->csc_counts);
+  cudaFree(c->csc_temp);
   cudaFree(c->csc_hi);
   for (auto p : c->W) cudaFree(p);
   for (auto p : c->G) cudaFree(p);
@@ -1111,6 +1188,9 @@ int hb_ctx_destroy(hb_ctx* c) {
   cudaFree(c->d_loss);
   cudaFree(c->stage64);
   cudaFree(c->stage32);
+  cudaFree(c->stage_all);
+  cudaFree(c->grad_all);
+  if (c->grad_host) cudaFreeHost(c->grad_host);
   cudaFree(c->flat);
   if (c->pinned) cudaFreeHost(c->pinned);
   for (auto e : c->evpool) cudaEventDestroy(e);
@@ -1188,6 +1268,157 @@ int hb_get_grad_f32(hb_ctx* c, int layer, float* g) {
   }
   HB_CUDA(cudaMemcpyAsync(g, c->G[layer], n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
   HB_CUDA(cudaStreamSynchronize(c->stream));
+  return HB_OK;
+}
+
+// Registered (page-locked, device-mapped) host ranges: the snapshot kernel
+// reads the shared float64 model straight over PCIe and the stale merge is a
+// kernel doing W_host -= eta*g in place over PCIe (aligned 8-byte stores, so
+// concurrent host readers never see a torn scalar, as linalg.py:3-7 requires).
+int hb_host_register(const void* p, size_t bytes) {
+  if (!p || bytes == 0) return fail(HB_EINVAL, "null pointer or zero size");
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  if (g_host_ranges.count(reinterpret_cast<uintptr_t>(p))) return HB_OK;
+  cudaError_t e = cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    cudaGetLastError();
+    return HB_OK;  // registered by someone else: used through the copy path
+  }
+  HB_CUDA(e);
+  void* dptr = nullptr;
+  HB_CUDA(cudaHostGetDevicePointer(&dptr, const_cast<void*>(p), 0));
+  g_host_ranges[reinterpret_cast<uintptr_t>(p)] = {bytes, dptr};
+  return HB_OK;
+}
+
+int hb_host_unregister(const void* p) {
+  if (!p) return fail(HB_EINVAL, "null pointer");
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  auto it = g_host_ranges.find(reinterpret_cast<uintptr_t>(p));
+  if (it == g_host_ranges.end()) return HB_OK;
+  g_host_ranges.erase(it);
+  cudaError_t e = cudaHostUnregister(const_cast<void*>(p));
+  if (e == cudaErrorHostMemoryNotRegistered) {
+    cudaGetLastError();
+    return HB_OK;
+  }
+  HB_CUDA(e);
+  return HB_OK;
+}
+
+// device alias of a registered host range covering [p, p+bytes), or null
+static void* mapped_alias(const void* p, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  auto it = g_host_ranges.upper_bound(a);
+  if (it == g_host_ranges.begin()) return nullptr;
+  --it;
+  if (a + bytes > it->first + it->second.first) return nullptr;
+  return static_cast<char*>(it->second.second) + (a - it->first);
+}
+
+static int ensure_stage_all(hb_ctx* c) {
+  if (c->stage_all) return HB_OK;
+  HB_CUDA(cudaMalloc(&c->stage_all, c->n_params * sizeof(double)));
+  HB_CUDA(cudaMalloc(&c->grad_all, c->n_params * sizeof(float)));
+  HB_CUDA(cudaMallocHost(&c->grad_host, c->n_params * sizeof(float)));
+  return HB_OK;
+}
+
+int hb_set_weights_all_f64(hb_ctx* c, const double* const* ws) {
+  HB_TRY(ctx_check(c));
+  if (!ws) return fail(HB_EINVAL, "null weight array");
+  HB_TRY(ensure_stage_all(c));
+  size_t off = 0;
+  for (int l = 0; l < c->L; ++l) {
+    if (!ws[l]) return fail(HB_EINVAL, "null weights for layer %d", l);
+    const int rows = c->d[l + 1], cols = c->d[l];
+    const size_t n = static_cast<size_t>(rows) * cols;
+    // registered host model: the conversion kernel reads it in place over PCIe
+    const double* dst = static_cast<const double*>(mapped_alias(ws[l], n * sizeof(double)));
+    if (dst == nullptr) {
+      HB_CUDA(cudaMemcpyAsync(c->stage_all + off, ws[l], n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      dst = c->stage_all + off;
+    }
+    const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 4096));
+    if (l == 0 && c->sparse)
+      f64_to_f32_kernel<true><<<blocks, 256, 0, c->stream>>>(c->W[0], c->ldw[0], dst, cols, rows, cols, nullptr);
+    else
+      f64_to_f32_kernel<false><<<blocks, 256, 0, c->stream>>>(c->W[l], c->ldw[l], dst, cols, rows, cols,
+                                                              c->need_lo() ? c->W_lo[l] : nullptr);
+    HB_CUDA(cudaGetLastError());
+    off += n;
+  }
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  return HB_OK;
+}
+
+int hb_merge_grads_all_into_f64(hb_ctx* c, double* const* ws, double eta) {
+  HB_TRY(ctx_check(c));
+  if (!ws) return fail(HB_EINVAL, "null weight array");
+  if (!c->grads_valid) return fail(HB_ESTATE, "no gradient kept: run a step with HB_STEP_EMIT_GRAD first");
+  HB_TRY(ensure_stage_all(c));
+  bool mapped = true;
+  std::vector<double*> dws(c->L);
+  for (int l = 0; l < c->L; ++l) {
+    if (!ws[l]) return fail(HB_EINVAL, "null weights for layer %d", l);
+    dws[l] = static_cast<double*>(mapped_alias(ws[l], static_cast<size_t>(c->d[l + 1]) * c->d[l] * sizeof(double)));
+    mapped = mapped && dws[l] != nullptr;
+  }
+  if (mapped) {
+    // the stale merge as a kernel writing the registered host model over PCIe
+    for (int l = 0; l < c->L; ++l) {
+      const int rows = c->d[l + 1], cols = c->d[l];
+      const size_t n = static_cast<size_t>(rows) * cols;
+      const bool tr = (l == 0 && c->sparse);
+      merge_host_f64_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 8)), 256, 0, c->stream>>>(
+          dws[l], c->G[l], tr ? c->ldw[0] : cols, rows, cols, tr ? 1 : 0, eta);
+      HB_CUDA(cudaGetLastError());
+    }
+    HB_CUDA(cudaStreamSynchronize(c->stream));
+    return HB_OK;
+  }
+  // gather every layer's gradient in (d_{l+1}, d_l) order into one device
+  // buffer (the sparse layer's transposed gradient is transposed back on the
+  // device), one D2H, then the float64 axpy on the host
+  size_t off = 0;
+  std::vector<size_t> offs(c->L);
+  for (int l = 0; l < c->L; ++l) {
+    const int rows = c->d[l + 1], cols = c->d[l];
+    const size_t n = static_cast<size_t>(rows) * cols;
+    offs[l] = off;
+    if (l == 0 && c->sparse) {
+      const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 4096));
+      transpose_f32_kernel<<<blocks, 256, 0, c->stream>>>(c->grad_all + off, c->G[0], c->ldw[0], rows, cols);
+      HB_CUDA(cudaGetLastError());
+    } else {
+      HB_CUDA(cudaMemcpyAsync(c->grad_all + off, c->G[l], n * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+    }
+    off += n;
+  }
+  HB_CUDA(cudaMemcpyAsync(c->grad_host, c->grad_all, off * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  // linalg.py:79 np.add(target, scale*source, out=target), scale = -eta; elementwise,
+  // so splitting the index range over threads changes nothing numerically
+  const double scale = -eta;
+  const int nthreads = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, off / (1 << 16))));
+  auto work = [&](int t) {
+    for (int l = 0; l < c->L; ++l) {
+      const size_t n = static_cast<size_t>(c->d[l + 1]) * c->d[l];
+      const size_t a = n * t / nthreads, b = n * (t + 1) / nthreads;
+      double* w = ws[l];
+      const float* g = c->grad_host + offs[l];
+      for (size_t i = a; i < b; ++i) w[i] += scale * static_cast<double>(g[i]);
+    }
+  };
+  if (nthreads == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 1; t < nthreads; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th) x.join();
+  }
   return HB_OK;
 }
 
@@ -1372,31 +1603,84 @@ int hb_train_step_host_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col,
     c->b_nnz_cap = cap;
     c->view_gen++;
   }
-  build_csc(rowptr, col, val, rows, c->d[0], c->h_colptr, c->h_rowidx, c->h_cval, 0);
   c->nnz_per_row = static_cast<double>(nnz) / rows;
-  // one pinned buffer carries the whole batch: rowptr | colptr | labels | col | rowidx | val | cval
+  // one pinned buffer carries the batch: [rowptr | labels | col | val] for the
+  // forward, then [colptr | rowidx | cval] (the batch CSC for the sparse dW),
+  // which is built on the host while the device runs the forward phase.
   const size_t b_rowptr = (rows + 1) * sizeof(int64_t), b_colptr = (c->d[0] + 1) * sizeof(int64_t),
                b_lab = rows * sizeof(int64_t), b_i32 = nnz * sizeof(int32_t), b_f32 = nnz * sizeof(float);
   HB_TRY(ensure_pinned(c, b_rowptr + b_colptr + b_lab + 2 * b_i32 + 2 * b_f32 + 64));
   char* p = static_cast<char*>(c->pinned);
+  char* p_lab = p + b_rowptr;
+  char* p_col = p_lab + b_lab;
+  char* p_val = p_col + b_i32;
+  char* p_colptr = p_val + b_f32;
+  char* p_rowidx = p_colptr + b_colptr;
+  char* p_cval = p_rowidx + b_i32;
   std::memcpy(p, rowptr, b_rowptr);
-  std::memcpy(p + b_rowptr, c->h_colptr.data(), b_colptr);
-  std::memcpy(p + b_rowptr + b_colptr, labels, b_lab);
-  char* q = p + b_rowptr + b_colptr + b_lab;
-  std::memcpy(q, col, b_i32);
-  std::memcpy(q + b_i32, c->h_rowidx.data(), b_i32);
-  std::memcpy(q + 2 * b_i32, val, b_f32);
-  std::memcpy(q + 2 * b_i32 + b_f32, c->h_cval.data(), b_f32);
+  std::memcpy(p_lab, labels, b_lab);
+  std::memcpy(p_col, col, b_i32);
+  std::memcpy(p_val, val, b_f32);
   cudaStream_t st = c->stream;
   HB_CUDA(cudaMemcpyAsync(c->browptr, p, b_rowptr, cudaMemcpyHostToDevice, st));
-  HB_CUDA(cudaMemcpyAsync(c->bcolptr, p + b_rowptr, b_colptr, cudaMemcpyHostToDevice, st));
-  HB_CUDA(cudaMemcpyAsync(c->blabels, p + b_rowptr + b_colptr, b_lab, cudaMemcpyHostToDevice, st));
+  HB_CUDA(cudaMemcpyAsync(c->blabels, p_lab, b_lab, cudaMemcpyHostToDevice, st));
   if (nnz > 0) {
-    HB_CUDA(cudaMemcpyAsync(c->bcol, q, b_i32, cudaMemcpyHostToDevice, st));
-    HB_CUDA(cudaMemcpyAsync(c->browidx, q + b_i32, b_i32, cudaMemcpyHostToDevice, st));
-    HB_CUDA(cudaMemcpyAsync(c->bval, q + 2 * b_i32, b_f32, cudaMemcpyHostToDevice, st));
-    HB_CUDA(cudaMemcpyAsync(c->bcval, q + 2 * b_i32 + b_f32, b_f32, cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemcpyAsync(c->bcol, p_col, b_i32, cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemcpyAsync(c->bval, p_val, b_f32, cudaMemcpyHostToDevice, st));
   }
+  const bool dev_csc = static_cast<double>(c->d[0]) * rows < 4294967295.0;
+  if (dev_csc) {
+    // batch CSC built on the device (stable by row, identical to the host sort)
+    if (c->csc_cap < nnz + 1 || c->csc_temp == nullptr) {
+      cudaFree(c->csc_keys);
+      cudaFree(c->csc_idx);
+      cudaFree(c->csc_temp);
+      cudaFree(c->csc_counts);
+      c->csc_cap = std::max<long long>(c->b_nnz_cap, nnz + 1);
+      HB_CUDA(cudaMalloc(&c->csc_keys, 2 * c->csc_cap * sizeof(uint32_t)));
+      HB_CUDA(cudaMalloc(&c->csc_idx, 2 * c->csc_cap * sizeof(int32_t)));
+      HB_CUDA(cudaMalloc(&c->csc_counts, 2 * (c->d[0] + 2) * sizeof(int)));
+      size_t t1 = 0, t2 = 0;
+      HB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, c->csc_keys, c->csc_keys + c->csc_cap, c->csc_idx,
+                                              c->csc_idx + c->csc_cap, static_cast<int>(c->csc_cap), 0, 32, st));
+      HB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, t2, c->csc_counts, c->csc_counts + c->d[0] + 2, c->d[0] + 1, st));
+      c->csc_temp_bytes = std::max(t1, t2);
+      HB_CUDA(cudaMalloc(&c->csc_temp, c->csc_temp_bytes));
+    }
+    int* cnt = c->csc_counts;
+    int* cnt_scan = c->csc_counts + c->d[0] + 2;
+    HB_CUDA(cudaMemsetAsync(cnt, 0, (c->d[0] + 1) * sizeof(int), st));
+    if (nnz > 0) {
+      csc_keys_kernel<<<cdiv(rows, 8), 256, 0, st>>>(c->browptr, c->bcol, rows, c->csc_keys, c->csc_idx, cnt);
+      HB_CUDA(cudaGetLastError());
+    }
+    size_t tb = c->csc_temp_bytes;
+    HB_CUDA(cub::DeviceScan::InclusiveSum(c->csc_temp, tb, cnt, cnt_scan, c->d[0] + 1, st));
+    counts_to_colptr_kernel<<<cdiv(c->d[0] + 1, 256), 256, 0, st>>>(cnt_scan, c->bcolptr, c->d[0]);
+    HB_CUDA(cudaGetLastError());
+    if (nnz > 0) {
+      int end_bit = 1;
+      while (end_bit < 32 && (static_cast<double>(1ull << end_bit) < static_cast<double>(c->d[0]) * rows)) ++end_bit;
+      tb = c->csc_temp_bytes;
+      HB_CUDA(cub::DeviceRadixSort::SortPairs(c->csc_temp, tb, c->csc_keys, c->csc_keys + c->csc_cap, c->csc_idx,
+                                              c->csc_idx + c->csc_cap, static_cast<int>(nnz), 0, end_bit, st));
+      csc_gather_kernel<<<static_cast<int>(std::min<long long>(cdiv(nnz, 256), 148 * 8)), 256, 0, st>>>(
+          c->csc_keys + c->csc_cap, c->csc_idx + c->csc_cap, c->bval, nnz, rows, c->browidx, c->bcval);
+      HB_CUDA(cudaGetLastError());
+    }
+    c->last_launches += 4;
+  }
+  auto csc_phase = [&]() -> int {
+    if (dev_csc) return HB_OK;
+    build_csc_into(rowptr, col, val, rows, c->d[0], reinterpret_cast<int64_t*>(p_colptr),
+                   reinterpret_cast<int32_t*>(p_rowidx), reinterpret_cast<float*>(p_cval), c->h_colptr);
+    HB_CUDA(cudaMemcpyAsync(c->bcolptr, p_colptr, b_colptr, cudaMemcpyHostToDevice, st));
+    if (nnz > 0) {
+      HB_CUDA(cudaMemcpyAsync(c->browidx, p_rowidx, b_i32, cudaMemcpyHostToDevice, st));
+      HB_CUDA(cudaMemcpyAsync(c->bcval, p_cval, b_f32, cudaMemcpyHostToDevice, st));
+    }
+    return HB_OK;
+  };
   DataView v;
   v.rowptr = c->browptr;
   v.col = c->bcol;
@@ -1406,7 +1690,8 @@ int hb_train_step_host_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col,
   v.cval = c->bcval;
   v.labels = c->blabels;
   v.n_rows = rows;
-  return do_step(c, v, 0, rows, eta, flags, out_loss);
+  if (dev_csc) return do_step(c, v, 0, rows, eta, flags, out_loss, true);
+  return do_step(c, v, 0, rows, eta, flags, out_loss, true, csc_phase);
 }
 
 int hb_forward(hb_ctx* c, int64_t start, int rows) {

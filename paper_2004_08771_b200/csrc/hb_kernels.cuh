@@ -967,6 +967,30 @@ __global__ void f32_to_f64_kernel(double* dst, long long ldd, const float* src, 
   }
 }
 
+// Stale merge into the registered host model (workers.py:135 -> linalg.py:79):
+// w_host[r, c] += -eta * g[r, c] (g transposed for the sparse first layer),
+// float64, one aligned 8-byte store per element.
+__global__ void merge_host_f64_kernel(double* w_host, const float* g, long long ldg, int rows, int cols,
+                                      int transposed, double eta) {
+  const long long total = static_cast<long long>(rows) * cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / cols, c = i % cols;
+    const float gv = transposed ? g[c * ldg + r] : g[r * ldg + c];
+    w_host[i] += -eta * static_cast<double>(gv);
+  }
+}
+
+// dst (rows, cols, dense) = src^T where src is (cols, rows) with row stride lds.
+__global__ void transpose_f32_kernel(float* dst, const float* src, long long lds, int rows, int cols) {
+  const long long total = static_cast<long long>(rows) * cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / cols, c = i % cols;
+    dst[i] = src[c * lds + r];
+  }
+}
+
 // lo (rows, cols, ld) = x - trunc_tf32(x): the 3xTF32 twin of a staged input.
 __global__ void split_lo_kernel(const float* x, float* lo, long long ld, long long rows, int cols) {
   const long long total = rows * cols;

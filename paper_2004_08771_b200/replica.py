@@ -39,12 +39,26 @@ class GpuReplica:
         self._staged_key = None
         self._staged_ref = None
         self._keep = None
-        self._fin = weakref.finalize(self, GpuReplica._destroy, self._lib, h)
+        self._pinned = {}  # data address -> array kept alive while page-locked
+        self._fin = weakref.finalize(self, GpuReplica._destroy, self._lib, h, self._pinned)
 
     @staticmethod
-    def _destroy(lib, h):
+    def _destroy(lib, h, pinned):
         if h:
             lib.hb_ctx_destroy(h)
+        for addr in list(pinned):
+            lib.hb_host_unregister(C.c_void_p(addr))
+        pinned.clear()
+
+    def pin_host(self, arrays) -> None:
+        """Page-lock host arrays exchanged every step (the shared float64 model)
+        so the snapshot / merge copies run at full link speed.  The arrays are
+        kept referenced until close()."""
+        for a in arrays:
+            addr = a.__array_interface__["data"][0]
+            if addr not in self._pinned and a.nbytes > 0:
+                N.check(self._lib.hb_host_register(C.c_void_p(addr), a.nbytes))
+                self._pinned[addr] = a
 
     def close(self):
         self._fin()
@@ -54,12 +68,14 @@ class GpuReplica:
         """Snapshot a host float64 model into the device mirror (deep_copy, nn.py:182)."""
         if len(weights) != self.depth:
             raise ValueError("weight count does not match architecture")
+        arrs = []
         for l, w in enumerate(weights):
             want = (self.sizes[l + 1], self.sizes[l])
             if w.shape != want:
                 raise ValueError(f"weights[{l}] has shape {w.shape}, expected {want}")
-            w64 = np.ascontiguousarray(w, dtype=np.float64)
-            N.check(self._lib.hb_set_weights_f64(self._h, l, N.ptr(w64, C.c_double)))
+            arrs.append(np.ascontiguousarray(w, dtype=np.float64))
+        table = (C.POINTER(C.c_double) * self.depth)(*[N.ptr(a, C.c_double) for a in arrs])
+        N.check(self._lib.hb_set_weights_all_f64(self._h, table))
 
     def get_weights(self) -> list:
         out = []
@@ -86,10 +102,15 @@ class GpuReplica:
     def merge_grads_into(self, weights, eta: float) -> None:
         """Stale merge W_global -= eta * g (workers.py:135 -> linalg.py:79) with
         the gradient of the last emit_grad step, in place on host float64 arrays."""
+        if len(weights) != self.depth:
+            raise ValueError("weight count does not match architecture")
         for l, w in enumerate(weights):
             if not (w.flags.c_contiguous and w.dtype == np.float64):
                 raise ValueError("host weights must be C-contiguous float64 (Model layout, nn.py:75)")
-            N.check(self._lib.hb_merge_grad_into_f64(self._h, l, N.ptr(w, C.c_double), float(eta)))
+            if w.shape != (self.sizes[l + 1], self.sizes[l]):
+                raise ValueError(f"weights[{l}] has shape {w.shape}")
+        table = (C.POINTER(C.c_double) * self.depth)(*[N.ptr(w, C.c_double) for w in weights])
+        N.check(self._lib.hb_merge_grads_all_into_f64(self._h, table, float(eta)))
 
     # ------------------------------------------------------------ data
     @staticmethod

@@ -136,6 +136,7 @@ def execute_gpu_replica(model, batch, eta: float, speed_factor: float = 0.0) -> 
     sparse = isinstance(batch, CsrBatchRef)
     ctx = _replica(sizes, batch.length, sparse, "train")
     _stage_for(ctx, batch)
+    ctx.pin_host(model.weights)  # the shared model is exchanged every call: page-lock it once
     ctx.set_weights(model.weights)
     ctx.step(batch.start, batch.length, eta, emit_grad=True, timed=True)
     ctx.merge_grads_into(model.weights, eta)

@@ -136,6 +136,8 @@ int hb_synchronize(hb_ctx* ctx);
  * max_entries NUL-terminated 64-byte slots ("gemm_fwd_sigmoid_l1", ...). */
 int hb_profile_enable(hb_ctx* ctx, int on);
 int hb_profile_read(hb_ctx* ctx, int max_entries, char* names, double* total_ms, int* counts, int* n_out);
+/* Restrict profiling to launches named `name` (null/empty: all launches). */
+int hb_profile_filter(hb_ctx* ctx, const char* name);
 
 /* NCCL merge between GPU replicas (one communicator per process/device). */
 int hb_nccl_unique_id(void* out_128_bytes);

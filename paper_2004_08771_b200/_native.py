@@ -59,6 +59,7 @@ SIGNATURES = {
     "hb_last_step_launches": (_i32, [_p, C.POINTER(_i32)]),
     "hb_synchronize": (_i32, [_p]),
     "hb_profile_enable": (_i32, [_p, _i32]),
+    "hb_profile_filter": (_i32, [_p, C.c_char_p]),
     "hb_profile_read": (_i32, [_p, _i32, C.c_char_p, _dp, C.POINTER(_i32), C.POINTER(_i32)]),
     "hb_nccl_unique_id": (_i32, [_p]),
     "hb_comm_init": (_i32, [_p, _p, _i32, _i32]),

@@ -336,6 +336,8 @@ struct hb_ctx {
   std::vector<cudaEvent_t> evpool;
   size_t ev_used = 0;
   std::pair<cudaEvent_t, cudaEvent_t> pending;
+  bool pending_active = false;
+  std::string prof_filter;  // empty: every launch
   std::vector<Mark> step_marks;
   std::map<std::string, std::pair<double, int>> prof_acc;
   // CUDA graphs of the step, one per (rows, flags, data view generation)
@@ -363,8 +365,20 @@ int ctx_check(hb_ctx* c) {
 // Profiling marks: (kernel name, begin event, end event) on the step stream.
 // Eager steps take events from a reusable pool; a captured graph owns its
 // events (they become event-record nodes) and re-reads them after every launch.
-void prof_begin(hb_ctx* c) {
+static void prof_name(char (&name)[64], const char* kind, int layer) {
+  if (layer >= 0)
+    snprintf(name, sizeof name, "%s_l%d", kind, layer);
+  else
+    snprintf(name, sizeof name, "%s", kind);
+}
+// A launch is bracketed when profiling is on and it passes the filter (the
+// bench instruments only the dominant kernel inside its timed region).
+void prof_begin(hb_ctx* c, const char* kind, int layer) {
+  c->pending_active = false;
   if (!c->prof_on) return;
+  char name[64];
+  prof_name(name, kind, layer);
+  if (!c->prof_filter.empty() && c->prof_filter != name) return;
   cudaEvent_t e0, e1;
   if (c->capturing) {
     if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return;
@@ -381,6 +395,7 @@ void prof_begin(hb_ctx* c) {
     c->ev_used += 2;
   }
   c->pending = {e0, e1};
+  c->pending_active = true;
   // inside stream capture a plain record is only a dependency marker; the
   // External flag makes it a real event-record node of the graph
   if (c->capturing)
@@ -389,16 +404,14 @@ void prof_begin(hb_ctx* c) {
     cudaEventRecord(e0, c->stream);
 }
 void prof_end(hb_ctx* c, const char* kind, int layer) {
-  if (!c->prof_on) return;
+  if (!c->prof_on || !c->pending_active) return;
+  c->pending_active = false;
   if (c->capturing)
     cudaEventRecordWithFlags(c->pending.second, c->stream, cudaEventRecordExternal);
   else
     cudaEventRecord(c->pending.second, c->stream);
   char name[64];
-  if (layer >= 0)
-    snprintf(name, sizeof name, "%s_l%d", kind, layer);
-  else
-    snprintf(name, sizeof name, "%s", kind);
+  prof_name(name, kind, layer);
   c->step_marks.push_back({name, c->pending.first, c->pending.second});
 }
 // fold the marks of a completed step into the per-kernel totals
@@ -461,7 +474,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     if (l == 0 && c->sparse) {
       SpmmArgs p{v.rowptr, v.col, v.val, ds, start, rows, c->W[0], c->ldw[0], c->d[0], c->d[1], c->A[1], c->ld[1],
                  c->need_lo() ? c->A_lo[1] : nullptr};
-      prof_begin(c);
+      prof_begin(c, "spmm_sigmoid", 0);
       const size_t slice_smem = static_cast<size_t>(c->d[0]) * kSpmmSliceCols * sizeof(float) +
                                 kCsrChunkEntries * 8 + (kCsrChunkRows + 1) * 4;
       if (c->sparse_smem && c->d[1] % 4 == 0 && slice_smem <= 200 * 1024) {
@@ -500,7 +513,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     a.out_lo = c->need_lo() ? c->A_lo[l + 1] : nullptr;
     a.ldo = c->ld[l + 1];
     const Operand ta = l == 0 ? v.fwd() : c->opA_k(l);
-    prof_begin(c);
+    prof_begin(c, "gemm_fwd_sigmoid", l);
     HB_TRY(launch_gemm(c->passes, G_FWD, EPI_SIGMOID, c->bn_fwd[l], ta, c->opW_k(l), a, m_tiles,
                        cdiv(a.N, c->bn_fwd[l]), 1, st));
     prof_end(c, "gemm_fwd_sigmoid", l);
@@ -538,7 +551,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     h.ws_loss = c->ws_loss;
     const int grid = cdiv(rows, kHeadRowsPerBlock);
     const int threads = kHeadWarps * 32;
-    prof_begin(c);
+    prof_begin(c, "head_small", l);
 #define HB_HEAD(NCT_, MAXT_) head_small_kernel<NCT_, MAXT_><<<grid, threads, 0, st>>>(h)
 #define HB_HEADV(NCT_, VPL_) head_small_vec_kernel<NCT_, VPL_><<<grid, threads, 0, st>>>(h)
     const bool vec = (h.d % 4 == 0) && (h.lda % 4 == 0) && (h.ld_dp % 4 == 0);
@@ -573,7 +586,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     c->last_launches += 2;
     if (train) {
       const long long n = static_cast<long long>(c->d[L]) * c->d[l];
-      prof_begin(c);
+      prof_begin(c, "reduce_sgd", l);
       reduce_sgd_kernel<<<cdiv(n, 32), 256, 0, st>>>(c->W[l], c->ldw[l], c->ws, grid, n, c->d[L], c->d[l],
                                                      static_cast<float>(eta),
                                                      (flags & HB_STEP_EMIT_GRAD) ? c->G[l] : nullptr, c->d[l], ds,
@@ -596,14 +609,14 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   a.out = c->D[l];
   a.ldo = c->ld[L];
   const Operand ta = l == 0 ? v.fwd() : c->opA_k(l);
-  prof_begin(c);
+  prof_begin(c, "gemm_fwd_logits", l);
   HB_TRY(launch_gemm(c->passes, G_FWD, EPI_STORE, c->bn_fwd[l], ta, c->opW_k(l), a, m_tiles, cdiv(a.N, c->bn_fwd[l]),
                      1, st));
   prof_end(c, "gemm_fwd_logits", l);
   SoftmaxArgs sm{c->D[l], c->need_lo() ? c->D_lo[l] : nullptr, c->ld[L], v.labels, start, ds, rows, c->d[L],
                  zrows, inv_n, train ? 1 : 0, c->ws_loss};
   const int grid = cdiv(std::max(rows, zrows), 8);
-  prof_begin(c);
+  prof_begin(c, "softmax_delta", l);
   softmax_delta_kernel<<<grid, 256, 0, st>>>(sm);
   HB_CUDA(cudaGetLastError());
   prof_end(c, "softmax_delta", l);
@@ -636,7 +649,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       a.aux = c->A[l];
       a.ld_aux = c->ld[l];
       a.ds = ds;
-      prof_begin(c);
+      prof_begin(c, "gemm_dx_dsig", l);
       HB_TRY(launch_gemm(c->passes, G_DX, EPI_DSIG, c->bn_dx[l], c->opD_k(l), c->opW_mn(l), a,
                          cdiv(zrows, kBM), cdiv(a.N, c->bn_dx[l]), 1, st));
       prof_end(c, "gemm_dx_dsig", l);
@@ -647,7 +660,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       SparseDwArgs p{v.colptr, v.rowidx, v.cval, ds, start, rows, c->d[0], c->d[1], c->D[0], c->ld[1],
                      c->W[0], c->ldw[0], static_cast<float>(eta), emit ? c->G[0] : nullptr, c->ldw[0],
                      c->csc_lo, c->csc_hi};
-      prof_begin(c);
+      prof_begin(c, "sparse_dw_sgd", 0);
       if (c->sdw_narrow) {
         // narrow input: smem dW0^T slices per row block, then fixed-order reduce + SGD
         const int col_slices = cdiv(c->d[1], kSdwSliceCols);
@@ -714,7 +727,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       a.ldo = c->ldw[l];
       a.grad = emit ? c->G[l] : nullptr;
       a.ld_grad = c->d[l];
-      prof_begin(c);
+      prof_begin(c, "gemm_dw_sgd", l);
       HB_TRY(launch_gemm(c->passes, G_DW, EPI_SGD, c->bn_dw[l], c->opD_mn(l), tb, a, mt, nt, 1, st));
       prof_end(c, "gemm_dw_sgd", l);
       c->last_launches++;
@@ -723,10 +736,10 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       a.out = c->ws;
       a.ldo = a.N;
       a.split_stride = slab;
-      prof_begin(c);
+      prof_begin(c, "gemm_dw_partial", l);
       HB_TRY(launch_gemm(c->passes, G_DW, EPI_PARTIAL, c->bn_dw[l], c->opD_mn(l), tb, a, mt, nt, splits, st));
       prof_end(c, "gemm_dw_partial", l);
-      prof_begin(c);
+      prof_begin(c, "reduce_sgd", l);
       if (a.N % 4 == 0 && c->ldw[l] % 4 == 0 && (slab / 4) >= 148 * 256)
         reduce_sgd_vec_kernel<<<static_cast<int>(std::min<long long>(cdiv(slab / 4, 256), 148 * 8)), 256, 0, st>>>(
             c->W[l], c->ldw[l], c->ws, splits, slab, a.M, a.N, static_cast<float>(eta), emit ? c->G[l] : nullptr,
@@ -1752,6 +1765,17 @@ int hb_profile_enable(hb_ctx* c, int on) {
   c->ev_used = 0;
   c->step_marks.clear();
   c->prof_acc.clear();
+  return HB_OK;
+}
+
+int hb_profile_filter(hb_ctx* c, const char* name) {
+  HB_TRY(ctx_check(c));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  const std::string f = name ? name : "";
+  if (f != c->prof_filter) {
+    drop_graphs(c);  // captured graphs baked the old instrumentation
+    c->prof_filter = f;
+  }
   return HB_OK;
 }
 

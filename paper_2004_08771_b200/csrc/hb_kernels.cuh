@@ -536,18 +536,27 @@ __global__ void __launch_bounds__(256) spmm_sigmoid_kernel(SpmmArgs p) {
       float4 acc[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (long long e = e0; e < e1; ++e) {
-        const float v = __ldg(p.val + e);
-        const float4* wr = reinterpret_cast<const float4*>(p.w0t + static_cast<long long>(__ldg(p.col + e)) * p.ldw);
+      // the row's (col, val) pairs are fetched 32 at a time with one coalesced
+      // load per lane and broadcast by shuffles, so the W0^T gathers of
+      // consecutive nonzeros do not wait on index loads and overlap
+      for (long long eb = e0; eb < e1; eb += 32) {
+        const int cnt = static_cast<int>(min(32LL, e1 - eb));
+        const int my_col = lane < cnt ? __ldg(p.col + eb + lane) : 0;
+        const float my_val = lane < cnt ? __ldg(p.val + eb + lane) : 0.f;
+        for (int k = 0; k < cnt; ++k) {
+          const float v = __shfl_sync(0xffffffffu, my_val, k);
+          const float4* wr = reinterpret_cast<const float4*>(
+              p.w0t + static_cast<long long>(__shfl_sync(0xffffffffu, my_col, k)) * p.ldw);
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const int j = base + 4 * lane + 128 * t;
-          if (j < p.d_out) {
-            const float4 w = __ldg(wr + j / 4);
-            acc[t].x = fmaf(v, w.x, acc[t].x);
-            acc[t].y = fmaf(v, w.y, acc[t].y);
-            acc[t].z = fmaf(v, w.z, acc[t].z);
-            acc[t].w = fmaf(v, w.w, acc[t].w);
+          for (int t = 0; t < 8; ++t) {
+            const int j = base + 4 * lane + 128 * t;
+            if (j < p.d_out) {
+              const float4 w = __ldg(wr + j / 4);
+              acc[t].x = fmaf(v, w.x, acc[t].x);
+              acc[t].y = fmaf(v, w.y, acc[t].y);
+              acc[t].z = fmaf(v, w.z, acc[t].z);
+              acc[t].w = fmaf(v, w.w, acc[t].w);
+            }
           }
         }
       }

@@ -228,6 +228,10 @@ class GpuReplica:
         """Bracket every kernel launch with CUDA events on the step stream."""
         N.check(self._lib.hb_profile_enable(self._h, 1 if on else 0))
 
+    def profile_filter(self, name: str | None) -> None:
+        """Bracket only launches named `name` (e.g. "gemm_dx_dsig_l1"); None: all."""
+        N.check(self._lib.hb_profile_filter(self._h, name.encode() if name else None))
+
     def profile_read(self) -> dict:
         """{kernel name: (total ms, launches)} since profile(True) / the last read."""
         cap = 256

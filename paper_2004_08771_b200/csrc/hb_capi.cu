@@ -549,13 +549,19 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     h.delta_out = nullptr;
     h.ws_dw = c->ws;
     h.ws_loss = c->ws_loss;
-    const int grid = cdiv(rows, kHeadRowsPerBlock);
+    const bool vec = (h.d % 4 == 0) && (h.lda % 4 == 0) && (h.ld_dp % 4 == 0) &&
+                     (h.d <= 1024 && (c->head_nct == 2 || h.d <= 512));
+    // the vectorised head walks several 16-row passes per block: at most two
+    // blocks per SM, so the per-block dW partials (reduced below) stay few
+    const int passes_total = cdiv(std::max(rows, zrows), kHeadRowsPerBlock);
+    // (the scalar kernel covers one 16-row pass per block, zero-fill rows included)
+    const int grid = vec ? std::min(passes_total, 2 * 148) : passes_total;
+    h.rows_per_block = cdiv(passes_total, grid) * kHeadRowsPerBlock;
     const int threads = kHeadWarps * 32;
     prof_begin(c, "head_small", l);
 #define HB_HEAD(NCT_, MAXT_) head_small_kernel<NCT_, MAXT_><<<grid, threads, 0, st>>>(h)
 #define HB_HEADV(NCT_, VPL_) head_small_vec_kernel<NCT_, VPL_><<<grid, threads, 0, st>>>(h)
-    const bool vec = (h.d % 4 == 0) && (h.lda % 4 == 0) && (h.ld_dp % 4 == 0);
-    if (vec && (h.d <= 1024 && (c->head_nct == 2 || h.d <= 512))) {
+    if (vec) {
       const int vpl = h.d <= 256 ? 2 : (h.d <= 512 ? 4 : 8);
       if (c->head_nct == 2) {
         if (vpl == 2) HB_HEADV(2, 2); else if (vpl == 4) HB_HEADV(2, 4); else HB_HEADV(2, 8);

@@ -62,6 +62,7 @@ struct HeadArgs {
   const DevStep* ds;
   int rows, d, nc;
   int zero_rows;           // delta_prev rows [rows, zero_rows) are zeroed
+  int rows_per_block;      // vec kernel: rows walked by one block (multiple of kHeadRowsPerBlock)
   float inv_n;             // 1 / batch size
   int train;               // 0 = loss only (evaluation)
   float* delta_prev;       // (zero_rows, d) or null
@@ -224,8 +225,12 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_small_vec_kernel(HeadArg
 #pragma unroll
     for (int t = 0; t < VPL; ++t) acc[c][t] = make_float4(0.f, 0.f, 0.f, 0.f);
   double loss = 0.0;
-  constexpr int RPW = kHeadRowsPerBlock / kHeadWarps;  // rows per warp (2)
-  const int rbase = blockIdx.x * kHeadRowsPerBlock + warp * RPW;
+  constexpr int RPW = kHeadRowsPerBlock / kHeadWarps;  // rows per warp per pass (2)
+  // a block owns rows [row_begin, row_end) and walks them kHeadRowsPerBlock at a time
+  const int row_begin = blockIdx.x * p.rows_per_block;
+  const int row_end = min(row_begin + p.rows_per_block, max(p.rows, p.zero_rows));
+  for (int rb = row_begin; rb < row_end; rb += kHeadRowsPerBlock) {
+  const int rbase = rb + warp * RPW;
   float4 av[RPW][VPL];
 #pragma unroll
   for (int k = 0; k < RPW; ++k)
@@ -320,6 +325,7 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_small_vec_kernel(HeadArg
       }
     }
   }
+  }  // row passes
   if (lane == 0) sLoss[warp] = loss;
   __syncthreads();
   if (threadIdx.x == 0) {

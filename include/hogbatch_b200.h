@@ -44,6 +44,7 @@ extern "C" {
 #define HB_ECUDA 2
 #define HB_ENCCL 3
 #define HB_ESTATE 4
+#define HB_EPARSE 5 /* malformed LIBSVM text (the reference's LibsvmParseError, data.py:26) */
 
 /* hb_ctx_create flags */
 #define HB_SPARSE_INPUT 1u  /* first layer consumes CSR input (CSR-gather SpMM) */
@@ -103,6 +104,25 @@ int hb_stage_dense_f32(hb_ctx* ctx, const float* x, int64_t n_rows, int64_t ld, 
 int hb_stage_csr(hb_ctx* ctx, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n_rows,
                  const int64_t* labels);
 int64_t hb_staged_rows(hb_ctx* ctx);
+/* Replace the staged rows by base[perm] on the device (perm: n_rows distinct
+ * indices in [0, n_rows)), where base is the data as first staged -- the
+ * per-epoch reshuffle of engine.py:214-221 (shuffle_epoch + reorder,
+ * data.py:182-192) without re-staging: dense rows, labels and the CSR/CSC
+ * copies come out identical to staging the host-reordered dataset. */
+int hb_permute_epoch(hb_ctx* ctx, const int64_t* perm, int64_t n_rows);
+
+/* LIBSVM text -> CSR, natively (the reference's loader, data.py:106-151,
+ * densifies to (N, feature_dim) float64 in Python).  buf/len hold the whole
+ * (decompressed) text.  scan validates every line and counts rows / nonzeros;
+ * fill writes rowptr (n_rows+1), col (nnz, 0-based, ascending per row), val
+ * (nnz) and labels (n_rows).  label_mapping: 0 = ZERO_ONE, 1 = PLUS_MINUS_ONE
+ * (data.py:21-23, 86-103).  Bad tokens/labels return HB_EPARSE, an index
+ * outside [1, feature_dim] HB_EINVAL, both with "line N: ..." messages.  A
+ * repeated index keeps the last value and explicit zeros are dropped. */
+int hb_libsvm_scan(const char* buf, size_t len, int64_t feature_dim, int label_mapping, int64_t* n_rows,
+                   int64_t* nnz);
+int hb_libsvm_fill(const char* buf, size_t len, int64_t feature_dim, int label_mapping, int64_t* rowptr,
+                   int32_t* col, double* val, int64_t* labels);
 
 /* One replica SGD step over staged rows [start, start+rows): forward
  * (nn.py:108-121), fused softmax/CE error (nn.py:162-164), backward

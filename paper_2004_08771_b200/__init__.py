@@ -17,7 +17,11 @@ from .data import (
     CsrBatchRef,
     CsrDataset,
     Dataset,
+    LabelMapping,
+    LibsvmParseError,
     epoch_shuffle_seed,
+    load_libsvm,
+    load_libsvm_csr,
     reorder,
     shuffle_epoch,
     synthetic_blobs,
@@ -47,10 +51,11 @@ from .workers import (
 
 __all__ = [
     "AdaptiveHogbatch", "AdaptiveState", "Architecture", "BatchRef", "CsrBatchRef", "CsrDataset", "Dataset",
-    "DeviceSpeedFeed", "FixedHeterogeneous", "GpuReplica", "InitScheme", "Model", "PolicyDecision",
+    "DeviceSpeedFeed", "FixedHeterogeneous", "GpuReplica", "InitScheme", "LabelMapping", "LibsvmParseError",
+    "Model", "PolicyDecision",
     "TrainResult", "UniformHogbatch", "WorkerConfig", "WorkerMode", "adaptive_update", "deep_copy",
     "device_count", "epoch_shuffle_seed", "execute_gpu_replica", "gpu_loss_sum", "init_model", "install",
-    "last_device_ms", "load_library", "reorder", "set_worker_device", "shuffle_epoch", "synthetic_blobs",
+    "last_device_ms", "load_libsvm", "load_libsvm_csr", "load_library", "reorder", "set_worker_device", "shuffle_epoch", "synthetic_blobs",
     "synthetic_csr", "train_gpu",
 ]
 

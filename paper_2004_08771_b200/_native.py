@@ -17,7 +17,7 @@ from pathlib import Path
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ.get("HOGBATCH_B200_LIB", _PKG / "libhogbatch_b200.so"))
 
-HB_OK, HB_EINVAL, HB_ECUDA, HB_ENCCL, HB_ESTATE = 0, 1, 2, 3, 4
+HB_OK, HB_EINVAL, HB_ECUDA, HB_ENCCL, HB_ESTATE, HB_EPARSE = 0, 1, 2, 3, 4, 5
 HB_SPARSE_INPUT = 1
 HB_PRECISION_TF32 = 2
 HB_STEP_EMIT_GRAD = 1
@@ -49,6 +49,9 @@ SIGNATURES = {
     "hb_stage_dense_f32": (_i32, [_p, _fp, _i64, _i64, _i64p]),
     "hb_stage_csr": (_i32, [_p, _i64p, _i32p, _fp, _i64, _i64p]),
     "hb_staged_rows": (_i64, [_p]),
+    "hb_permute_epoch": (_i32, [_p, _i64p, _i64]),
+    "hb_libsvm_scan": (_i32, [C.c_char_p, C.c_size_t, _i64, _i32, _i64p, _i64p]),
+    "hb_libsvm_fill": (_i32, [C.c_char_p, C.c_size_t, _i64, _i32, _i64p, _i32p, _dp, _i64p]),
     "hb_train_step": (_i32, [_p, _i64, _i32, _f64, _u32, _dp]),
     "hb_train_step_host_dense": (_i32, [_p, _fp, _i64, _i64p, _i32, _f64, _u32, _dp]),
     "hb_train_step_host_csr": (_i32, [_p, _i64p, _i32p, _fp, _i64p, _i32, _f64, _u32, _dp]),
@@ -98,11 +101,15 @@ def load(build_if_missing: bool = False):
     return lib
 
 
+def last_error() -> str:
+    return (load().hb_last_error() or b"").decode(errors="replace")
+
+
 def check(rc: int) -> None:
     if rc == HB_OK:
         return
     msg = (_lib.hb_last_error() or b"").decode(errors="replace")
-    if rc == HB_EINVAL:
+    if rc in (HB_EINVAL, HB_EPARSE):
         raise ValueError(msg)
     raise RuntimeError(f"hogbatch_b200 error {rc}: {msg}")
 

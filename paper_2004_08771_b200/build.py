@@ -19,7 +19,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libhogbatch_b200.so"
-SOURCES = [CSRC / "hb_capi.cu"]
+SOURCES = [CSRC / "hb_capi.cu", CSRC / "hb_libsvm.cpp"]
 HEADERS = sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "hogbatch_b200.h"]
 
 NVCC_FLAGS = [

@@ -291,6 +291,19 @@ struct hb_ctx {
   DataView epoch;
   bool staged = false;
 
+  // unpermuted base copy kept on the device by hb_permute_epoch (the epoch
+  // buffers above then hold base[perm]); gather/sort scratch reused per epoch
+  bool has_base = false;
+  float *px = nullptr, *px_lo = nullptr;
+  int64_t *plabels = nullptr, *prowptr = nullptr, *pcolptr = nullptr;
+  int32_t *pcol = nullptr, *prowidx = nullptr;
+  float *pval = nullptr, *pcval = nullptr;
+  int64_t *d_perm = nullptr, *d_inv = nullptr, *d_rowlen = nullptr;
+  uint64_t* p_keys = nullptr;
+  int32_t* p_idx = nullptr;
+  void* p_temp = nullptr;
+  size_t p_temp_bytes = 0;
+
   float* bx = nullptr;  // batch slot (dense rows) for host-buffer steps
   float* bx_lo = nullptr;
   int64_t* blabels = nullptr;
@@ -952,6 +965,19 @@ int free_epoch(hb_ctx* c) {
   c->ecolptr = nullptr;
   c->erowidx = nullptr;
   c->ecval = nullptr;
+  for (void* q : {static_cast<void*>(c->px), static_cast<void*>(c->px_lo), static_cast<void*>(c->plabels),
+                  static_cast<void*>(c->prowptr), static_cast<void*>(c->pcolptr), static_cast<void*>(c->pcol),
+                  static_cast<void*>(c->prowidx), static_cast<void*>(c->pval), static_cast<void*>(c->pcval),
+                  static_cast<void*>(c->d_perm), static_cast<void*>(c->d_inv), static_cast<void*>(c->d_rowlen),
+                  static_cast<void*>(c->p_keys), static_cast<void*>(c->p_idx), c->p_temp})
+    cudaFree(q);
+  c->px = c->px_lo = c->pval = c->pcval = nullptr;
+  c->plabels = c->prowptr = c->pcolptr = c->d_perm = c->d_inv = c->d_rowlen = nullptr;
+  c->pcol = c->prowidx = c->p_idx = nullptr;
+  c->p_keys = nullptr;
+  c->p_temp = nullptr;
+  c->p_temp_bytes = 0;
+  c->has_base = false;
   c->staged = false;
   c->e_rows = 0;
   c->view_gen++;  // captured graphs baked the old buffers / tensor maps
@@ -963,6 +989,14 @@ size_t layer_elems(const hb_ctx* c, int l) { return static_cast<size_t>(c->d[l +
 }  // namespace
 
 // ======================================================================
+namespace hb {
+// error slot shared with the other translation units of the library
+int set_error(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+}  // namespace hb
+
 extern "C" {
 
 const char* hb_last_error(void) { return g_err.c_str(); }
@@ -1564,6 +1598,182 @@ int hb_stage_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col, const flo
 }
 
 int64_t hb_staged_rows(hb_ctx* c) { return c ? c->e_rows : 0; }
+
+// ------------------------------------------------ on-device epoch reshuffle
+// epoch[i] = base[perm[i]] (data.py:187-192 reorder), so a run stages its
+// dataset once and every epoch's shuffled copy is a device gather instead of
+// a host reorder + H2D.  Row data, labels and the CSC are bit-identical to
+// staging the host-reordered copy.
+__global__ void gather_rows_kernel(float* __restrict__ dst, const float* __restrict__ src,
+                                   const int64_t* __restrict__ perm, long long n, long long ld) {
+  const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (long long r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+    const float4* s4 = reinterpret_cast<const float4*>(src + perm[r] * ld);
+    float4* d4 = reinterpret_cast<float4*>(dst + r * ld);
+    for (long long j = lane; j < ld / 4; j += 32) d4[j] = s4[j];
+  }
+}
+__global__ void gather_labels_kernel(int64_t* dst, const int64_t* src, const int64_t* perm, int64_t* inv,
+                                     long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long p = perm[i];
+    dst[i] = src[p];
+    if (inv) inv[p] = i;
+  }
+}
+__global__ void perm_rowlen_kernel(const int64_t* rowptr, const int64_t* perm, long long n, int64_t* len) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i <= n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    len[i] = i == 0 ? 0 : rowptr[perm[i - 1] + 1] - rowptr[perm[i - 1]];
+}
+__global__ void gather_csr_kernel(const int64_t* __restrict__ rowptr_src, const int32_t* __restrict__ col_src,
+                                  const float* __restrict__ val_src, const int64_t* __restrict__ perm, long long n,
+                                  const int64_t* __restrict__ rowptr_dst, int32_t* __restrict__ col_dst,
+                                  float* __restrict__ val_dst) {
+  const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (long long r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+    const long long s0 = rowptr_src[perm[r]], len = rowptr_src[perm[r] + 1] - s0, d0 = rowptr_dst[r];
+    for (long long k = lane; k < len; k += 32) {
+      col_dst[d0 + k] = col_src[s0 + k];
+      val_dst[d0 + k] = val_src[s0 + k];
+    }
+  }
+}
+// key = feature * n + new_row over the base CSC; sorting the unique keys gives
+// the permuted epoch's CSC in (feature, row) order -- what hb_stage_csr's
+// stable counting sort produces for the host-reordered copy.
+__global__ void perm_csc_keys_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
+                                     const int64_t* __restrict__ inv, int n_cols, long long n, uint64_t* keys,
+                                     int32_t* idx) {
+  const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (long long f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); f < n_cols; f += warps)
+    for (long long k = colptr[f] + lane; k < colptr[f + 1]; k += 32) {
+      keys[k] = static_cast<uint64_t>(f) * static_cast<uint64_t>(n) + static_cast<uint64_t>(inv[rowidx[k]]);
+      idx[k] = static_cast<int32_t>(k);
+    }
+}
+__global__ void perm_csc_gather_kernel(const uint64_t* keys, const int32_t* idx, const float* cval_src, long long nnz,
+                                       long long n, int32_t* rowidx, float* cval) {
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < nnz;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    rowidx[k] = static_cast<int32_t>(keys[k] % static_cast<uint64_t>(n));
+    cval[k] = cval_src[idx[k]];
+  }
+}
+
+static int dup_device(void** dst, const void* src, size_t bytes, cudaStream_t st) {
+  HB_CUDA(cudaMalloc(dst, std::max<size_t>(bytes, 1)));
+  if (bytes) HB_CUDA(cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyDeviceToDevice, st));
+  return HB_OK;
+}
+
+int hb_permute_epoch(hb_ctx* c, const int64_t* perm, int64_t n) {
+  HB_TRY(ctx_check(c));
+  if (!c->staged) return fail(HB_ESTATE, "no data staged");
+  if (!perm || n != c->e_rows) return fail(HB_EINVAL, "permutation length %lld != staged rows %lld", (long long)n,
+                                           c->e_rows);
+  {  // a permutation of [0, n): numpy's fancy indexing would raise on anything else
+    std::vector<uint8_t> seen(n, 0);
+    for (long long i = 0; i < n; ++i) {
+      if (perm[i] < 0 || perm[i] >= n) return fail(HB_EINVAL, "index %lld outside [0, %lld)", (long long)perm[i],
+                                                   (long long)n);
+      if (seen[perm[i]]++) return fail(HB_EINVAL, "index %lld repeated: not a permutation", (long long)perm[i]);
+    }
+  }
+  cudaStream_t st = c->stream;
+  const long long nnz = c->e_nnz;
+  if (!c->has_base) {
+    // the staged buffers become the base; fresh epoch buffers (same shapes)
+    // receive base[perm] from now on -- one view_gen bump, then graphs reuse
+    c->px = c->ex;
+    c->px_lo = c->ex_lo;
+    c->plabels = c->elabels;
+    c->prowptr = c->erowptr;
+    c->pcolptr = c->ecolptr;
+    c->pcol = c->ecol;
+    c->prowidx = c->erowidx;
+    c->pval = c->eval_;
+    c->pcval = c->ecval;
+    HB_CUDA(cudaMalloc(&c->elabels, n * sizeof(int64_t)));
+    HB_CUDA(cudaMalloc(&c->d_perm, n * sizeof(int64_t)));
+    if (c->sparse) {
+      const size_t nz = std::max<long long>(nnz, 1);
+      HB_CUDA(cudaMalloc(&c->erowptr, (n + 1) * sizeof(int64_t)));
+      HB_CUDA(cudaMalloc(&c->ecol, nz * sizeof(int32_t)));
+      HB_CUDA(cudaMalloc(&c->eval_, nz * sizeof(float)));
+      HB_CUDA(cudaMalloc(&c->erowidx, nz * sizeof(int32_t)));
+      HB_CUDA(cudaMalloc(&c->ecval, nz * sizeof(float)));
+      HB_TRY(dup_device(reinterpret_cast<void**>(&c->ecolptr), c->pcolptr, (c->d[0] + 1) * sizeof(int64_t), st));  // column counts do not move
+      HB_CUDA(cudaMalloc(&c->d_inv, n * sizeof(int64_t)));
+      HB_CUDA(cudaMalloc(&c->d_rowlen, (n + 1) * sizeof(int64_t)));
+      HB_CUDA(cudaMalloc(&c->p_keys, 2 * nz * sizeof(uint64_t)));
+      HB_CUDA(cudaMalloc(&c->p_idx, 2 * nz * sizeof(int32_t)));
+      if (nnz >= (1ll << 31)) return fail(HB_EINVAL, "nnz %lld too large for the device CSC sort", nnz);
+      size_t t1 = 0, t2 = 0;
+      HB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, c->p_keys, c->p_keys + nz, c->p_idx, c->p_idx + nz,
+                                              static_cast<int>(nz), 0, 64, st));
+      HB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, t2, c->d_rowlen, c->erowptr, n + 1, st));
+      c->p_temp_bytes = std::max(t1, t2);
+      HB_CUDA(cudaMalloc(&c->p_temp, c->p_temp_bytes));
+    } else {
+      const size_t bytes = static_cast<size_t>(n) * c->ld[0] * sizeof(float);
+      HB_CUDA(cudaMalloc(&c->ex, bytes));
+      if (c->px_lo) HB_CUDA(cudaMalloc(&c->ex_lo, bytes));
+    }
+    c->has_base = true;
+    c->view_gen++;
+  }
+  HB_CUDA(cudaMemcpyAsync(c->d_perm, perm, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  const int g1 = static_cast<int>(std::min<long long>(cdiv(n, 256), 148 * 8));
+  const int gw = static_cast<int>(std::min<long long>(cdiv(n, 8), 148 * 16));  // 8 warps per block
+  gather_labels_kernel<<<g1, 256, 0, st>>>(c->elabels, c->plabels, c->d_perm, c->sparse ? c->d_inv : nullptr, n);
+  HB_CUDA(cudaGetLastError());
+  if (c->sparse) {
+    perm_rowlen_kernel<<<static_cast<int>(std::min<long long>(cdiv(n + 1, 256), 148 * 8)), 256, 0, st>>>(
+        c->prowptr, c->d_perm, n, c->d_rowlen);
+    size_t tb = c->p_temp_bytes;
+    HB_CUDA(cub::DeviceScan::InclusiveSum(c->p_temp, tb, c->d_rowlen, c->erowptr, n + 1, st));
+    gather_csr_kernel<<<gw, 256, 0, st>>>(c->prowptr, c->pcol, c->pval, c->d_perm, n, c->erowptr, c->ecol, c->eval_);
+    HB_CUDA(cudaGetLastError());
+    if (nnz > 0) {
+      const size_t nz = std::max<long long>(nnz, 1);
+      perm_csc_keys_kernel<<<static_cast<int>(std::min<long long>(cdiv(c->d[0], 8), 148 * 16)), 256, 0, st>>>(
+          c->pcolptr, c->prowidx, c->d_inv, c->d[0], n, c->p_keys, c->p_idx);
+      HB_CUDA(cudaGetLastError());
+      int end_bit = 1;
+      while (end_bit < 64 && (static_cast<double>(1ull << end_bit) < static_cast<double>(c->d[0]) * n)) ++end_bit;
+      tb = c->p_temp_bytes;
+      HB_CUDA(cub::DeviceRadixSort::SortPairs(c->p_temp, tb, c->p_keys, c->p_keys + nz, c->p_idx, c->p_idx + nz,
+                                              static_cast<int>(nnz), 0, end_bit, st));
+      perm_csc_gather_kernel<<<static_cast<int>(std::min<long long>(cdiv(nnz, 256), 148 * 8)), 256, 0, st>>>(
+          c->p_keys + nz, c->p_idx + nz, c->pcval, nnz, n, c->erowidx, c->ecval);
+      HB_CUDA(cudaGetLastError());
+    }
+    c->epoch.rowptr = c->erowptr;
+    c->epoch.col = c->ecol;
+    c->epoch.val = c->eval_;
+    c->epoch.colptr = c->ecolptr;
+    c->epoch.rowidx = c->erowidx;
+    c->epoch.cval = c->ecval;
+    c->epoch.labels = c->elabels;
+  } else {
+    gather_rows_kernel<<<gw, 256, 0, st>>>(c->ex, c->px, c->d_perm, n, c->ld[0]);
+    if (c->ex_lo) gather_rows_kernel<<<gw, 256, 0, st>>>(c->ex_lo, c->px_lo, c->d_perm, n, c->ld[0]);
+    HB_CUDA(cudaGetLastError());
+    if (c->epoch.x != c->ex) {
+      c->epoch.x = c->ex;
+      c->epoch.x_lo = c->ex_lo;
+      c->epoch.labels = c->elabels;
+      HB_TRY(build_data_maps(c, c->epoch));
+    }
+  }
+  HB_CUDA(cudaStreamSynchronize(st));
+  return HB_OK;
+}
 
 static int check_labels(const int64_t* y, long long n, int nc) {
   for (long long i = 0; i < n; ++i)

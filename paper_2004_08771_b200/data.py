@@ -11,12 +11,17 @@ holds CSR rows (int64 row pointer, int32 0-based column ids, float64 values)
 and `CsrBatchRef` is the same contiguous-row-range view over it.
 `synthetic_csr` generates the w8a-/real-sim-shaped inputs of BASELINE.json
  and `CsrDataset.dense()` is the exact dense twin the oracle
-consumes.
+consumes.  `load_libsvm_csr` parses LIBSVM text natively (csrc/hb_libsvm.cpp)
+straight to CSR with the reference loader's semantics and errors;
+`load_libsvm` is the reference's dense signature on top of it.
 """
 
 from __future__ import annotations
 
+import gzip
 from dataclasses import dataclass
+from enum import Enum
+from pathlib import Path
 
 import numpy as np
 
@@ -239,3 +244,90 @@ def reorder(ds, perm: np.ndarray):
         idx = np.repeat(starts - rowptr[:-1], lengths) + np.arange(rowptr[-1])
         return CsrDataset(rowptr, ds.col[idx], ds.val[idx], ds.labels[perm].copy(), ds.n_cols, ds.name)
     return Dataset(features=np.ascontiguousarray(ds.features[perm]), labels=ds.labels[perm].copy(), name=ds.name)
+
+
+class LabelMapping(Enum):  # data.py:21-23
+    ZERO_ONE = "zero_one"
+    PLUS_MINUS_ONE = "plus_minus_one"
+
+
+class LibsvmParseError(ValueError):  # data.py:26-27
+    """Malformed LIBSVM input; message carries the 1-based line number."""
+
+
+def _read_text_bytes(path: Path) -> bytes:
+    # data.py:80-83: gzip is detected by the .gz extension
+    if path.suffix == ".gz":
+        with gzip.open(path, "rb") as fh:
+            return fh.read()
+    return path.read_bytes()
+
+
+def load_libsvm_csr(path, feature_dim: int, label_mapping: LabelMapping = LabelMapping.ZERO_ONE,
+                    minmax_scale: bool = False, name: str | None = None) -> CsrDataset:
+    """LIBSVM text -> CsrDataset without densifying (the reference's
+    load_libsvm, data.py:106-151, builds an (N, feature_dim) float64 matrix).
+    Rows, labels and values equal the nonzeros of the reference's matrix;
+    errors are LibsvmParseError / ValueError with the same line numbers.
+    minmax_scale (data.py:167-171) is applied when it keeps the data sparse
+    (every column's minimum is 0, true for non-negative features); otherwise
+    it would densify and ValueError says to use load_libsvm."""
+    import ctypes as C
+
+    from . import _native as N
+
+    path = Path(path)
+    buf = _read_text_bytes(path)
+    lib = N.load()
+    mode = 1 if label_mapping is LabelMapping.PLUS_MINUS_ONE else 0
+    n_rows, nnz = C.c_int64(0), C.c_int64(0)
+    _libsvm_check(N, lib.hb_libsvm_scan(buf, len(buf), int(feature_dim), mode, C.byref(n_rows), C.byref(nnz)))
+    if n_rows.value == 0:
+        raise ValueError(f"{path}: no examples")
+    rowptr = np.empty(n_rows.value + 1, dtype=np.int64)
+    col = np.empty(max(nnz.value, 1), dtype=np.int32)
+    val = np.empty(max(nnz.value, 1), dtype=np.float64)
+    labels = np.empty(n_rows.value, dtype=np.int64)
+    _libsvm_check(N, lib.hb_libsvm_fill(buf, len(buf), int(feature_dim), mode, N.ptr(rowptr, C.c_int64),
+                                        N.ptr(col, C.c_int32), N.ptr(val, C.c_double), N.ptr(labels, C.c_int64)))
+    ds = CsrDataset(rowptr, col[: nnz.value], val[: nnz.value], labels, int(feature_dim), name or path.stem)
+    if minmax_scale:
+        ds = _minmax_scale_csr(ds)
+    return ds
+
+
+def _libsvm_check(N, rc: int) -> None:
+    if rc == N.HB_EPARSE:
+        raise LibsvmParseError(N.last_error())
+    N.check(rc)
+
+
+def _minmax_scale_csr(ds: CsrDataset) -> CsrDataset:
+    n, d = ds.n_examples, ds.n_cols
+    count = np.bincount(ds.col, minlength=d)
+    lo = np.full(d, np.inf)
+    hi = np.full(d, -np.inf)
+    np.minimum.at(lo, ds.col, ds.val)
+    np.maximum.at(hi, ds.col, ds.val)
+    implicit_zero = count < n  # a column with a missing entry has a 0.0 in the dense matrix
+    lo = np.where(implicit_zero, np.minimum(lo, 0.0), lo)
+    hi = np.where(implicit_zero, np.maximum(hi, 0.0), hi)
+    if np.any(lo != 0.0):
+        raise ValueError("minmax_scale would shift zeros (a column minimum is not 0); use load_libsvm (dense)")
+    span = hi - lo
+    span[span == 0.0] = 1.0
+    # (x - 0.0) / span == x / span exactly: same values as data.py:167-171
+    return CsrDataset(ds.rowptr, ds.col, ds.val / span[ds.col], ds.labels, d, ds.name)
+
+
+def load_libsvm(path, feature_dim: int, label_mapping: LabelMapping = LabelMapping.ZERO_ONE,
+                minmax_scale: bool = False, name: str | None = None) -> Dataset:
+    """The reference's dense loader (data.py:106-151) on the native parser."""
+    csr = load_libsvm_csr(path, feature_dim, label_mapping, False, name)
+    features = np.ascontiguousarray(csr.dense())
+    if minmax_scale:  # data.py:167-171
+        lo = features.min(axis=0)
+        span = features.max(axis=0) - lo
+        span[span == 0.0] = 1.0
+        features = (features - lo) / span
+    return Dataset(features=features, labels=csr.labels, name=csr.name)

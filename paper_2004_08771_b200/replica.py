@@ -156,6 +156,14 @@ class GpuReplica:
         self._staged_key = key
         self._keep = (data, x, y)
 
+    def permute_epoch(self, perm) -> None:
+        """Make the staged rows base[perm] on the device, base being the data
+        as staged (reorder, data.py:187-192, without a re-stage).  The staged
+        key is dropped: the rows no longer match the staged array."""
+        perm = np.ascontiguousarray(perm, dtype=np.int64)
+        N.check(self._lib.hb_permute_epoch(self._h, N.ptr(perm, C.c_int64), perm.shape[0]))
+        self._staged_key = None
+
     def is_staged(self, key) -> bool:
         return self._staged_key == key
 

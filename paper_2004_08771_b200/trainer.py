@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .data import CsrDataset, epoch_shuffle_seed, reorder, shuffle_epoch
+from .data import CsrDataset, epoch_shuffle_seed, shuffle_epoch
 from .nn import layer_sizes_of
 from .replica import GpuReplica
 
@@ -83,15 +83,17 @@ def train_gpu(dataset, model, batch_size: int, eta: float, epochs: int, seed: in
             return loss
 
         evaluate(0.0)
-        epoch_copy = None
+        # the dataset is staged once; every epoch's shuffled copy is gathered
+        # on the device (same rows/CSC as staging reorder(dataset, perm))
+        if sparse:
+            train_ctx.stage(dataset)
+        else:
+            train_ctx.stage(dataset.features, dataset.labels)
+        shuffled = False
         for epoch in range(epochs):
-            if epoch_copy is None or shuffle_each_epoch:
-                perm = shuffle_epoch(n, epoch_shuffle_seed(seed, epoch if shuffle_each_epoch else 0))
-                epoch_copy = reorder(dataset, perm)
-                if sparse:
-                    train_ctx.stage(epoch_copy)
-                else:
-                    train_ctx.stage(epoch_copy.features, epoch_copy.labels)
+            if not shuffled or shuffle_each_epoch:
+                train_ctx.permute_epoch(shuffle_epoch(n, epoch_shuffle_seed(seed, epoch if shuffle_each_epoch else 0)))
+                shuffled = True
             t0 = time.perf_counter()
             cursor = 0
             while cursor < n:

@@ -156,6 +156,40 @@ def test_host_buffer_steps_match_staged(hb):
             assert np.array_equal(p, q)
 
 
+@pytest.mark.parametrize("sparse", [False, True])
+def test_device_epoch_permutation_matches_host_reorder(hb, sparse):
+    """hb_permute_epoch (device gather + device CSC sort) gives bit-identical
+    training to staging the host-reordered copy (engine.py:214-221)."""
+    sizes, n, b = (300, 128, 128, 2), 1500, 256
+    w, x, y = oracle_case(sizes, n, seed=21, sparse_nnz=9 if sparse else None)
+    base = to_csr(hb, x, y) if sparse else hb.Dataset(x, np.asarray(y, dtype=np.int64))
+    a = hb.GpuReplica(sizes, b, sparse=sparse)
+    d = hb.GpuReplica(sizes, b, sparse=sparse)
+    try:
+        a.set_weights(w)
+        d.set_weights(w)
+        d.stage(base) if sparse else d.stage(base.features, base.labels)
+        for epoch in range(2):  # the second call reuses the epoch buffers
+            perm = hb.shuffle_epoch(n, hb.epoch_shuffle_seed(5, epoch))
+            copy = hb.reorder(base, perm)
+            a.stage(copy) if sparse else a.stage(copy.features, copy.labels)
+            d.permute_epoch(perm)
+            for start in range(0, n, b):
+                rows = min(b, n - start)
+                la = a.step(start, rows, 0.3, want_loss=True)
+                ld = d.step(start, rows, 0.3, want_loss=True)
+                assert la == ld
+            for p, q in zip(a.get_weights(), d.get_weights()):
+                assert np.array_equal(p, q)
+        with pytest.raises(ValueError, match="permutation"):
+            d.permute_epoch(np.zeros(n, dtype=np.int64))
+        with pytest.raises(ValueError):
+            d.permute_epoch(np.arange(n - 1))
+    finally:
+        a.close()
+        d.close()
+
+
 def test_batches_inside_staged_epoch(hb):
     """(start, rows) indexing of the staged epoch equals staging the batch alone."""
     sizes = (54, 128, 128, 2)

@@ -49,6 +49,13 @@ extern "C" {
 /* hb_ctx_create flags */
 #define HB_SPARSE_INPUT 1u  /* first layer consumes CSR input (CSR-gather SpMM) */
 #define HB_PRECISION_TF32 2u /* 1-pass TF32 GEMMs (fast mode); default is 3xTF32 */
+/* CSR contexts with a narrow input layer (d_0 <= HB_DENSIFY_MAX_DIN) scatter
+ * the CSR rows into a dense device copy once at staging (per step for host
+ * batches) and run layer 0 as a tensor-core GEMM, like every other layer --
+ * the reference's own dense formulation (data.py:128-141).  This flag keeps
+ * the CSR-gather SpMM / CSC-slice dW kernels instead. */
+#define HB_SPARSE_KERNELS 4u
+#define HB_DENSIFY_MAX_DIN 512
 
 /* hb_train_step flags */
 #define HB_STEP_EMIT_GRAD 1u /* keep the raw mean gradient of every layer (for the host merge / parity) */

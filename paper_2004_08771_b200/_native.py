@@ -20,6 +20,8 @@ LIB_PATH = Path(os.environ.get("HOGBATCH_B200_LIB", _PKG / "libhogbatch_b200.so"
 HB_OK, HB_EINVAL, HB_ECUDA, HB_ENCCL, HB_ESTATE, HB_EPARSE = 0, 1, 2, 3, 4, 5
 HB_SPARSE_INPUT = 1
 HB_PRECISION_TF32 = 2
+HB_SPARSE_KERNELS = 4
+HB_DENSIFY_MAX_DIN = 512
 HB_STEP_EMIT_GRAD = 1
 HB_STEP_TIMED = 2
 HB_STEP_ASYNC = 4

@@ -129,6 +129,7 @@ int launch_gemm_t(const Operand& ta, const Operand& tb, const GemmArgs& a, int m
   {
     const int target = getenv("HB_TRACE_LAUNCH") ? atoi(getenv("HB_TRACE_LAUNCH")) : -1;
     const_cast<GemmArgs&>(a).trace = (target < 0 || g_trace_launch_no == target) ? 1 : 0;
+    const_cast<GemmArgs&>(a).trace_slot = 1 + g_trace_launch_no % 8;
     ++g_trace_launch_no;
   }
 #endif
@@ -259,7 +260,8 @@ struct hb_ctx {
   std::vector<long long> ld;   // padded row stride of a width-d_l buffer
   int cap = 0;                 // row capacity (max_batch rounded up to 128)
   int max_batch = 0;
-  bool sparse = false;
+  bool csr_in = false;  // the context takes CSR input (HB_SPARSE_INPUT)
+  bool sparse = false;  // ... and runs layer 0 on the CSR kernels (else: densified rows + GEMM)
   int passes = 3;
   bool small_head = false;
   int head_nct = 0, head_maxt = 0;
@@ -343,6 +345,7 @@ struct hb_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.f;
   int last_launches = 0;
+  int pre_launches = 0;  // kernels a host-buffer step enqueued before do_step (densify / batch CSC)
   bool grads_valid = false;
   // per-launch CUDA-event profiling (bench.py reads it live; off by default)
   bool prof_on = false;
@@ -842,7 +845,8 @@ void drop_graphs(hb_ctx* c) {
 int do_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta, uint32_t flags, double* out_loss,
             bool graph_ok = true, const std::function<int()>& mid = nullptr) {
   if (rows < 1 || rows > c->max_batch) return fail(HB_EINVAL, "rows=%d outside [1, %d]", rows, c->max_batch);
-  c->last_launches = 0;
+  c->last_launches = c->pre_launches;
+  c->pre_launches = 0;
   c->ev_used = 0;
   c->step_marks.clear();
   const bool timed = (flags & HB_STEP_TIMED) != 0;
@@ -1036,7 +1040,8 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
   c->device = device;
   c->L = n_layers;
   c->d.assign(sizes, sizes + n_layers + 1);
-  c->sparse = (flags & HB_SPARSE_INPUT) != 0;
+  c->csr_in = (flags & HB_SPARSE_INPUT) != 0;
+  c->sparse = c->csr_in && ((flags & HB_SPARSE_KERNELS) || sizes[0] > HB_DENSIFY_MAX_DIN);
   c->passes = (flags & HB_PRECISION_TF32) ? 1 : 3;
   c->max_batch = max_batch;
   c->cap = static_cast<int>(round_up(max_batch, kBM));
@@ -1183,8 +1188,8 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
   HB_CK(cudaMalloc(&c->stage32, maxw * sizeof(float)));
   // batch slot for host-buffer steps
   HB_CK(cudaMalloc(&c->blabels, static_cast<size_t>(c->cap) * sizeof(int64_t)));
+  if (c->csr_in) HB_CK(cudaMalloc(&c->browptr, static_cast<size_t>(c->cap + 1) * sizeof(int64_t)));
   if (c->sparse) {
-    HB_CK(cudaMalloc(&c->browptr, static_cast<size_t>(c->cap + 1) * sizeof(int64_t)));
     HB_CK(cudaMalloc(&c->bcolptr, static_cast<size_t>(c->d[0] + 1) * sizeof(int64_t)));
   } else {
     HB_CK(cudaMalloc(&c->bx, static_cast<size_t>(c->cap) * c->ld[0] * sizeof(float)));
@@ -1490,7 +1495,7 @@ int hb_merge_grad_into_f64(hb_ctx* c, int layer, double* host_w, double eta) {
 }
 
 static int stage_dense_common(hb_ctx* c, int64_t n_rows, const int64_t* labels) {
-  if (c->sparse) return fail(HB_EINVAL, "context was created for sparse (CSR) input");
+  if (c->csr_in) return fail(HB_EINVAL, "context was created for sparse (CSR) input");
   if (n_rows < 1 || !labels) return fail(HB_EINVAL, "need n_rows >= 1 and labels");
   HB_TRY(free_epoch(c));
   HB_CUDA(cudaMalloc(&c->ex, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
@@ -1547,10 +1552,79 @@ int hb_stage_dense_f32(hb_ctx* c, const float* x, int64_t n_rows, int64_t ld, co
   return finish_dense_stage(c);
 }
 
+// CSR rows -> dense rows (+ lo twin) for densified CSR contexts: a warp per
+// row zeroes it, lane 0 adds the entries in CSR order (a repeated column sums,
+// as the CSR kernels do), then the lanes write the lo twin of the touched
+// entries.  rowptr may start at any offset (a batch of a staged epoch).
+__global__ void densify_csr_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                   const float* __restrict__ val, long long rows, long long ld, float* __restrict__ x,
+                                   float* __restrict__ x_lo) {
+  const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (long long r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    float4* xr = reinterpret_cast<float4*>(x + r * ld);
+    float4* lr = x_lo ? reinterpret_cast<float4*>(x_lo + r * ld) : nullptr;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (long long j = lane; j < ld / 4; j += 32) {
+      xr[j] = z;
+      if (lr) lr[j] = z;
+    }
+    __syncwarp();
+    const long long e0 = rowptr[r], e1 = rowptr[r + 1];
+    if (lane == 0)
+      for (long long e = e0; e < e1; ++e) x[r * ld + col[e]] += val[e];
+    __syncwarp();
+    if (x_lo)
+      for (long long e = e0 + lane; e < e1; e += 32) x_lo[r * ld + col[e]] = tf32_lo(x[r * ld + col[e]]);
+  }
+}
+
+static int densify_launch(hb_ctx* c, const int64_t* rowptr, const int32_t* col, const float* val, long long rows,
+                          float* x, float* x_lo) {
+  const int grid = static_cast<int>(std::min<long long>(cdiv(rows, 8), 148 * 16));
+  densify_csr_kernel<<<grid, 256, 0, c->stream>>>(rowptr, col, val, rows, c->ld[0], x, x_lo);
+  HB_CUDA(cudaGetLastError());
+  return HB_OK;
+}
+
+// Densified CSR staging: the CSR arrays go to the device once and are
+// scattered into the dense epoch buffers the GEMM path reads.
+static int stage_csr_densified(hb_ctx* c, const int64_t* rowptr, const int32_t* col, const float* val,
+                               int64_t n_rows, const int64_t* labels) {
+  const long long nnz = rowptr[n_rows];
+  HB_TRY(free_epoch(c));
+  HB_CUDA(cudaMalloc(&c->ex, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
+  if (c->need_lo()) HB_CUDA(cudaMalloc(&c->ex_lo, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
+  HB_CUDA(cudaMalloc(&c->elabels, static_cast<size_t>(n_rows) * sizeof(int64_t)));
+  HB_CUDA(cudaMemcpyAsync(c->elabels, labels, n_rows * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+  int64_t* d_rowptr = nullptr;
+  int32_t* d_col = nullptr;
+  float* d_val = nullptr;
+  const size_t nz = std::max<long long>(nnz, 1);
+  HB_CUDA(cudaMalloc(&d_rowptr, (n_rows + 1) * sizeof(int64_t)));
+  HB_CUDA(cudaMalloc(&d_col, nz * sizeof(int32_t)));
+  HB_CUDA(cudaMalloc(&d_val, nz * sizeof(float)));
+  HB_CUDA(cudaMemcpyAsync(d_rowptr, rowptr, (n_rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+  if (nnz > 0) {
+    HB_CUDA(cudaMemcpyAsync(d_col, col, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+    HB_CUDA(cudaMemcpyAsync(d_val, val, nnz * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  }
+  const int rc = densify_launch(c, d_rowptr, d_col, d_val, n_rows, c->ex, c->ex_lo);
+  cudaStreamSynchronize(c->stream);
+  cudaFree(d_rowptr);
+  cudaFree(d_col);
+  cudaFree(d_val);
+  if (rc != HB_OK) return rc;
+  c->e_rows = n_rows;
+  c->e_nnz = nnz;
+  c->nnz_per_row = static_cast<double>(nnz) / static_cast<double>(n_rows);
+  return finish_dense_stage(c);
+}
+
 int hb_stage_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n_rows,
                  const int64_t* labels) {
   HB_TRY(ctx_check(c));
-  if (!c->sparse) return fail(HB_EINVAL, "context was created for dense input");
+  if (!c->csr_in) return fail(HB_EINVAL, "context was created for dense input");
   if (!rowptr || !labels || n_rows < 1) return fail(HB_EINVAL, "null CSR arrays or n_rows < 1");
   if (rowptr[0] != 0) return fail(HB_EINVAL, "rowptr[0] must be 0");
   const long long nnz = rowptr[n_rows];
@@ -1559,6 +1633,7 @@ int hb_stage_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col, const flo
   for (long long e = 0; e < nnz; ++e)
     if (col[e] < 0 || col[e] >= c->d[0])
       return fail(HB_EINVAL, "feature index %d outside [0, %d) at nnz %lld", col[e], c->d[0], e);
+  if (!c->sparse) return stage_csr_densified(c, rowptr, col, val, n_rows, labels);
   HB_TRY(free_epoch(c));
   std::vector<int64_t> colptr;
   std::vector<int32_t> rowidx;
@@ -1793,7 +1868,7 @@ int hb_train_step(hb_ctx* c, int64_t start, int rows, double eta, uint32_t flags
 int hb_train_step_host_dense(hb_ctx* c, const float* x, int64_t ld, const int64_t* labels, int rows, double eta,
                              uint32_t flags, double* out_loss) {
   HB_TRY(ctx_check(c));
-  if (c->sparse) return fail(HB_EINVAL, "context was created for sparse (CSR) input");
+  if (c->csr_in) return fail(HB_EINVAL, "context was created for sparse (CSR) input");
   if (!x || !labels || ld < c->d[0]) return fail(HB_EINVAL, "null batch or ld < %d", c->d[0]);
   if (rows < 1 || rows > c->max_batch) return fail(HB_EINVAL, "rows=%d outside [1, %d]", rows, c->max_batch);
   HB_TRY(check_labels(labels, rows, c->d[c->L]));
@@ -1811,7 +1886,7 @@ int hb_train_step_host_dense(hb_ctx* c, const float* x, int64_t ld, const int64_
 int hb_train_step_host_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col, const float* val,
                            const int64_t* labels, int rows, double eta, uint32_t flags, double* out_loss) {
   HB_TRY(ctx_check(c));
-  if (!c->sparse) return fail(HB_EINVAL, "context was created for dense input");
+  if (!c->csr_in) return fail(HB_EINVAL, "context was created for dense input");
   if (!rowptr || !labels) return fail(HB_EINVAL, "null batch");
   if (rows < 1 || rows > c->max_batch) return fail(HB_EINVAL, "rows=%d outside [1, %d]", rows, c->max_batch);
   if (rowptr[0] != 0) return fail(HB_EINVAL, "rowptr[0] must be 0");
@@ -1857,6 +1932,12 @@ int hb_train_step_host_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col,
     HB_CUDA(cudaMemcpyAsync(c->bcol, p_col, b_i32, cudaMemcpyHostToDevice, st));
     HB_CUDA(cudaMemcpyAsync(c->bval, p_val, b_f32, cudaMemcpyHostToDevice, st));
   }
+  if (!c->sparse) {
+    // densified context: scatter the batch into the dense slot, then the GEMM path
+    HB_TRY(densify_launch(c, c->browptr, c->bcol, c->bval, rows, c->bx, c->bx_lo));
+    c->pre_launches = 1;
+    return do_step(c, c->batch, 0, rows, eta, flags, out_loss);
+  }
   const bool dev_csc = static_cast<double>(c->d[0]) * rows < 4294967295.0;
   if (dev_csc) {
     // batch CSC built on the device (stable by row, identical to the host sort)
@@ -1897,7 +1978,7 @@ int hb_train_step_host_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col,
           c->csc_keys + c->csc_cap, c->csc_idx + c->csc_cap, c->bval, nnz, rows, c->browidx, c->bcval);
       HB_CUDA(cudaGetLastError());
     }
-    c->last_launches += 4;
+    c->pre_launches = 3;  // keys, colptr, gather (the scan / radix sort are CUB)
   }
   auto csc_phase = [&]() -> int {
     if (dev_csc) return HB_OK;
@@ -2023,6 +2104,15 @@ extern "C" int hb_trace_read(unsigned long long* out, int n) {
   cudaMemset(reinterpret_cast<void*>(0), 0, 0);
   unsigned long long zeros[4096] = {0};
   cudaMemcpyToSymbol(hb::hb_trace_buf, zeros, sizeof zeros);
+  return HB_OK;
+}
+// per-CTA stamps of the last 8 GEMM launches ([slot][cta][4]); resets the launch counter
+extern "C" int hb_trace_cta_read(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, hb::hb_trace_cta, sizeof(unsigned long long) * 8 * 1024 * 4);
+  std::vector<unsigned long long> zeros(8 * 1024 * 4, 0);
+  cudaMemcpyToSymbol(hb::hb_trace_cta, zeros.data(), zeros.size() * sizeof(unsigned long long));
+  g_trace_launch_no = 0;
   return HB_OK;
 }
 #endif

@@ -56,6 +56,7 @@ struct GemmArgs {
   const DevStep* ds;      // graph launches: start / eta from device memory
   int a_start, b_start;   // add ds->start to a_off / b_off (staged-input operands)
   int trace;              // HB_TRACE builds: record this launch's pipeline timeline
+  int trace_slot;         // HB_TRACE builds: 1-based slot for the per-CTA stamps (0 = off)
 };
 
 // Optional pipeline timeline (debug builds, -DHB_TRACE): CTA (0,0,0) records
@@ -70,7 +71,21 @@ __device__ unsigned long long hb_trace_buf[4096];
       hb_trace_buf[(slot)] = t_;                                                         \
     }                                                                                    \
   } while (0)
+// per-CTA stamps: [slot][cta][entry, setup done, epilogue start, end]
+__device__ unsigned long long hb_trace_cta[8 * 1024 * 4];
+#define HB_CTA_STAMP(k)                                                                          \
+  do {                                                                                           \
+    const int cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);             \
+    if (args.trace_slot > 0 && cta_ < 1024) {                                                    \
+      unsigned long long t_;                                                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
+      hb_trace_cta[((args.trace_slot - 1) * 1024 + cta_) * 4 + (k)] = t_;                        \
+    }                                                                                            \
+  } while (0)
 #else
+#define HB_CTA_STAMP(k) \
+  do {                  \
+  } while (0)
 #define HB_STAMP(slot) \
   do {                 \
   } while (0)
@@ -145,6 +160,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) HB_STAMP(6 * 512 + 2);  // CTA start
+  if (threadIdx.x == 0) HB_CTA_STAMP(0);
   const uint32_t crank = PAIR ? cluster_ctarank() : 0u;  // 0: MMA-issuing CTA of the pair
   const bool leader = crank == 0;
   // grid: x = M tiles (CTA pairs are x-adjacent: cluster (2,1,1)), y = N tiles, z = K splits
@@ -184,6 +200,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
   else
     __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) HB_CTA_STAMP(1);
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
@@ -299,6 +316,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
     load_pre(32 * half, pre);
     mbar_wait(tmem_full, 0);
     if (threadIdx.x == 128) HB_STAMP(6 * 512 + 0);  // epilogue start
+    if (threadIdx.x == 128) HB_CTA_STAMP(2);
     tc_fence_after();
     constexpr int TP = 36;  // padded tile row (floats): conflict-free v4 in and out
     float* tile = reinterpret_cast<float*>(smem) + ew * 32 * TP;
@@ -434,6 +452,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
   else
     __syncthreads();
   if (threadIdx.x == 0) HB_STAMP(6 * 512 + 1);  // CTA end
+  if (threadIdx.x == 0) HB_CTA_STAMP(3);
   if (warp == 2) {
     tc_fence_after();
     if (PAIR)

@@ -21,7 +21,12 @@ from .data import CsrDataset
 class GpuReplica:
     """Device context for layer sizes `sizes` and batches of <= max_batch rows."""
 
-    def __init__(self, sizes, max_batch: int, device: int = 0, sparse: bool = False, precision: str = "3xtf32"):
+    def __init__(self, sizes, max_batch: int, device: int = 0, sparse: bool = False, precision: str = "3xtf32",
+                 sparse_kernels: bool = False):
+        """sparse: the replica takes CSR input.  Inputs at most
+        HB_DENSIFY_MAX_DIN wide are scattered into dense rows on the device and
+        layer 0 runs as a tensor-core GEMM; sparse_kernels=True (or a wider
+        input) keeps the CSR-gather SpMM / CSC-slice dW kernels."""
         self._lib = N.load()
         self.sizes = tuple(int(s) for s in sizes)
         self.depth = len(self.sizes) - 1
@@ -32,6 +37,9 @@ class GpuReplica:
             raise ValueError(f"precision must be '3xtf32' or 'tf32', got {precision!r}")
         self.precision = precision
         flags = (N.HB_SPARSE_INPUT if sparse else 0) | (N.HB_PRECISION_TF32 if precision == "tf32" else 0)
+        if sparse and sparse_kernels:
+            flags |= N.HB_SPARSE_KERNELS
+        self.sparse_kernels = bool(sparse) and (bool(sparse_kernels) or self.sizes[0] > N.HB_DENSIFY_MAX_DIN)
         arr = (C.c_int * len(self.sizes))(*self.sizes)
         h = C.c_void_p()
         N.check(self._lib.hb_ctx_create(C.byref(h), self.device, self.depth, arr, self.max_batch, flags))

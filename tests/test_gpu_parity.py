@@ -35,8 +35,8 @@ def to_csr(hb, x, y):
     return hb.CsrDataset(rowptr, cols.astype(np.int32), x[rows, cols], np.asarray(y, dtype=np.int64), x.shape[1])
 
 
-def run_step(hb, sizes, w, x, y, eta, sparse=False, precision="3xtf32"):
-    ctx = hb.GpuReplica(sizes, x.shape[0], sparse=sparse, precision=precision)
+def run_step(hb, sizes, w, x, y, eta, sparse=False, precision="3xtf32", sparse_kernels=False):
+    ctx = hb.GpuReplica(sizes, x.shape[0], sparse=sparse, precision=precision, sparse_kernels=sparse_kernels)
     try:
         ctx.set_weights(w)
         if sparse:
@@ -67,9 +67,10 @@ class TestGoldenStep:
             assert ew <= STEP_TOL, (c["name"], "weights", ew)
             assert out["loss"] == pytest.approx(c["ce"], rel=1e-5, abs=1e-6), c["name"]
 
-    def test_sparse_case_through_csr(self, hb, golden_cases):
+    @pytest.mark.parametrize("kernels", [False, True], ids=["densified", "csr_kernels"])
+    def test_sparse_case_through_csr(self, hb, golden_cases, kernels):
         c = next(c for c in golden_cases if c["name"] == "sparse_w8a_like")
-        out = run_step(hb, c["sizes"], c["w"], c["x"], c["y"], c["eta"], sparse=True)
+        out = run_step(hb, c["sizes"], c["w"], c["x"], c["y"], c["eta"], sparse=True, sparse_kernels=kernels)
         assert max_relative_error(out["grads"], c["g"]) <= STEP_TOL
         assert max_relative_error(out["weights"], c["u"]) <= STEP_TOL
 
@@ -113,12 +114,13 @@ def test_oracle_step_at_shape(hb, sizes, b, sparse_nnz, eta):
     grads = ref_nn.backward(w, tape, y)
     upd = ref_nn.deep_copy(w)
     ref_nn.apply_update(upd, grads, eta)
-    out = run_step(hb, sizes, w, x, y, eta, sparse=bool(sparse_nnz))
-    eg = max_relative_error(out["grads"], grads)
-    ew = max_relative_error(out["weights"], upd)
-    assert eg <= STEP_TOL, eg
-    assert ew <= STEP_TOL, ew
-    assert out["loss"] == pytest.approx(ref_nn.cross_entropy_loss(tape, y), rel=1e-5)
+    for kernels in ((False, True) if sparse_nnz else (False,)):  # densified and CSR-kernel layer 0
+        out = run_step(hb, sizes, w, x, y, eta, sparse=bool(sparse_nnz), sparse_kernels=kernels)
+        eg = max_relative_error(out["grads"], grads)
+        ew = max_relative_error(out["weights"], upd)
+        assert eg <= STEP_TOL, (kernels, eg)
+        assert ew <= STEP_TOL, (kernels, ew)
+        assert out["loss"] == pytest.approx(ref_nn.cross_entropy_loss(tape, y), rel=1e-5)
 
 
 def test_tf32_mode_is_less_precise_but_close(hb):
@@ -141,11 +143,11 @@ def test_step_is_bit_reproducible(hb):
 
 
 def test_host_buffer_steps_match_staged(hb):
-    for sparse in (False, True):
+    for sparse, kernels in ((False, False), (True, False), (True, True)):
         sizes, b = (300, 256, 256, 2), 333
         w, x, y = oracle_case(sizes, b, seed=11, sparse_nnz=12 if sparse else None)
-        staged = run_step(hb, sizes, w, x, y, 0.4, sparse=sparse)
-        ctx = hb.GpuReplica(sizes, 512, sparse=sparse)
+        staged = run_step(hb, sizes, w, x, y, 0.4, sparse=sparse, sparse_kernels=kernels)
+        ctx = hb.GpuReplica(sizes, 512, sparse=sparse, sparse_kernels=kernels)
         ctx.set_weights(w)
         batch = to_csr(hb, x, y) if sparse else x.astype(np.float32)
         loss = ctx.step_host(batch, y, 0.4, emit_grad=True)
@@ -156,15 +158,15 @@ def test_host_buffer_steps_match_staged(hb):
             assert np.array_equal(p, q)
 
 
-@pytest.mark.parametrize("sparse", [False, True])
-def test_device_epoch_permutation_matches_host_reorder(hb, sparse):
+@pytest.mark.parametrize("sparse,kernels", [(False, False), (True, False), (True, True)])
+def test_device_epoch_permutation_matches_host_reorder(hb, sparse, kernels):
     """hb_permute_epoch (device gather + device CSC sort) gives bit-identical
     training to staging the host-reordered copy (engine.py:214-221)."""
     sizes, n, b = (300, 128, 128, 2), 1500, 256
     w, x, y = oracle_case(sizes, n, seed=21, sparse_nnz=9 if sparse else None)
     base = to_csr(hb, x, y) if sparse else hb.Dataset(x, np.asarray(y, dtype=np.int64))
-    a = hb.GpuReplica(sizes, b, sparse=sparse)
-    d = hb.GpuReplica(sizes, b, sparse=sparse)
+    a = hb.GpuReplica(sizes, b, sparse=sparse, sparse_kernels=kernels)
+    d = hb.GpuReplica(sizes, b, sparse=sparse, sparse_kernels=kernels)
     try:
         a.set_weights(w)
         d.set_weights(w)

@@ -107,6 +107,7 @@ std::mutex g_host_mu;
 std::map<uintptr_t, std::pair<size_t, void*>> g_host_ranges;  // host base -> (bytes, device alias)
 
 // ------------------------------------------------------------ GEMM launch
+constexpr int kTileSyncTiles = 4096;
 int g_trace_launch_no = 0;  // HB_TRACE builds: index of the GEMM launch being issued
 // A GEMM operand: the fp32 tensor's map and its 3xTF32 lo twin's map.
 struct Operand {
@@ -174,9 +175,58 @@ int launch_gemm_p(GemmKind kind, int epi, int bn, const Operand& ta, const Opera
   }
   if (kind == G_DX) HB_BN(false, true, EPI_DSIG);
   if (epi == EPI_SGD) HB_BN(true, true, EPI_SGD);
+  if (epi == EPI_SPLIT_SGD) HB_BN(true, true, EPI_SPLIT_SGD);
   HB_BN(true, true, EPI_PARTIAL);
 #undef HB_BN
 #undef HB_L
+}
+
+// CTAs of the fused split-K dW kernel that can be resident at once (its split
+// CTAs wait for each other, so a launch must never exceed this).
+template <int BN, int PASSES>
+int split_sgd_capacity_t() {
+  using C = GemmCfg<BN, PASSES>;
+  auto kern = gemm_tf32_kernel<BN, true, true, EPI_SPLIT_SGD, PASSES>;
+  static int cap = -1;
+  if (cap >= 0) return cap;
+  cap = 0;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess) return cap;
+  if (C::PAIR) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2, 1, 1);
+    cfg.blockDim = dim3(C::THREADS);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) == cudaSuccess) cap = 2 * clusters;
+  } else {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM) == cudaSuccess)
+      cap = per_sm * sms;
+  }
+  cudaGetLastError();
+  return cap;
+}
+
+int split_sgd_capacity(int passes, int bn) {
+#define HB_C(P_)                                       \
+  do {                                                 \
+    if (bn == 32) return split_sgd_capacity_t<32, P_>();   \
+    if (bn == 64) return split_sgd_capacity_t<64, P_>();   \
+    if (bn == 256) return split_sgd_capacity_t<256, P_>(); \
+    return split_sgd_capacity_t<128, P_>();                \
+  } while (0)
+  if (passes == 3) HB_C(3);
+  HB_C(1);
+#undef HB_C
 }
 
 int launch_gemm(int passes, GemmKind kind, int epi, int bn, const Operand& ta, const Operand& tb,
@@ -345,6 +395,7 @@ struct hb_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.f;
   int last_launches = 0;
+  int* tile_sync = nullptr;  // split-K rendezvous counters (2 per output tile), zero between launches
   int pre_launches = 0;  // kernels a host-buffer step enqueued before do_step (densify / batch CSC)
   bool grads_valid = false;
   // per-launch CUDA-event profiling (bench.py reads it live; off by default)
@@ -489,7 +540,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   for (int l = 0; l < L - 1; ++l) {
     if (l == 0 && c->sparse) {
       SpmmArgs p{v.rowptr, v.col, v.val, ds, start, rows, c->W[0], c->ldw[0], c->d[0], c->d[1], c->A[1], c->ld[1],
-                 c->need_lo() ? c->A_lo[1] : nullptr};
+                 (c->need_lo() && !(c->small_head && L == 2)) ? c->A_lo[1] : nullptr};
       prof_begin(c, "spmm_sigmoid", 0);
       const size_t slice_smem = static_cast<size_t>(c->d[0]) * kSpmmSliceCols * sizeof(float) +
                                 kCsrChunkEntries * 8 + (kCsrChunkRows + 1) * 4;
@@ -526,7 +577,9 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     a.kb_total = cdiv(c->d[l], kBK);
     a.kb_per_split = a.kb_total;
     a.out = c->A[l + 1];
-    a.out_lo = c->need_lo() ? c->A_lo[l + 1] : nullptr;
+    // the last hidden activation feeds only the CUDA-core head (its forward and
+    // its dW), never a tensor-core GEMM: no lo twin to write
+    a.out_lo = (c->need_lo() && !(c->small_head && l + 1 == L - 1)) ? c->A_lo[l + 1] : nullptr;
     a.ldo = c->ld[l + 1];
     const Operand ta = l == 0 ? v.fwd() : c->opA_k(l);
     prof_begin(c, "gemm_fwd_sigmoid", l);
@@ -752,6 +805,24 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       prof_begin(c, "gemm_dw_sgd", l);
       HB_TRY(launch_gemm(c->passes, G_DW, EPI_SGD, c->bn_dw[l], c->opD_mn(l), tb, a, mt, nt, 1, st));
       prof_end(c, "gemm_dw_sgd", l);
+      c->last_launches++;
+    } else if (c->tile_sync != nullptr && a.N % 4 == 0 && c->ldw[l] % 4 == 0 &&
+               static_cast<long long>(mt + (c->passes == 3 && c->bn_dw[l] >= 64 ? mt % 2 : 0)) * nt * splits <=
+                   split_sgd_capacity(c->passes, c->bn_dw[l]) &&
+               static_cast<long long>(mt + 1) * nt <= kTileSyncTiles) {
+      // split-K partials reduced and applied inside the GEMM (no reduce kernel)
+      a.out = c->ws;
+      a.ldo = a.N;
+      a.split_stride = static_cast<long long>(a.M) * a.N;
+      a.w = c->W[l];
+      a.w_lo = c->need_lo() ? c->W_lo[l] : nullptr;
+      a.ldw = c->ldw[l];
+      a.grad = emit ? c->G[l] : nullptr;
+      a.ld_grad = c->d[l];
+      a.tile_sync = c->tile_sync;
+      prof_begin(c, "gemm_dw_splitk_sgd", l);
+      HB_TRY(launch_gemm(c->passes, G_DW, EPI_SPLIT_SGD, c->bn_dw[l], c->opD_mn(l), tb, a, mt, nt, splits, st));
+      prof_end(c, "gemm_dw_splitk_sgd", l);
       c->last_launches++;
     } else {
       const long long slab = static_cast<long long>(a.M) * a.N;
@@ -1180,6 +1251,12 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
     HB_CK(cudaMalloc(&c->csc_hi, static_cast<size_t>(c->d[0]) * sizeof(long long)));
   }
   HB_CK(cudaMemset(c->d_step, 0, sizeof(DevStep)));
+  // experimental: split-K dW reduced inside the GEMM (measured no faster than
+  // GEMM + reduce kernel at w8a shapes: the rendezvous waits for the slowest split)
+  if (getenv("HB_SPLITK_FUSION") && getenv("HB_SPLITK_FUSION")[0] == '1') {
+    HB_CK(cudaMalloc(&c->tile_sync, 2 * kTileSyncTiles * sizeof(int)));
+    HB_CK(cudaMemset(c->tile_sync, 0, 2 * kTileSyncTiles * sizeof(int)));
+  }
   if (const char* g = getenv("HB_NO_GRAPHS")) c->use_graphs = g[0] == '0';
   size_t maxw = 0;
   for (int l = 0; l < L; ++l) maxw = std::max(maxw, static_cast<size_t>(c->d[l + 1]) * c->d[l]);
@@ -1243,6 +1320,7 @@ int hb_ctx_destroy(hb_ctx* c) {
   cudaFree(c->bcval);
   cudaFree(c->ws);
   cudaFree(c->ws_loss);
+  cudaFree(c->tile_sync);
   cudaFree(c->d_loss);
   cudaFree(c->stage64);
   cudaFree(c->stage32);

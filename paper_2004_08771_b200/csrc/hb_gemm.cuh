@@ -11,6 +11,12 @@
 //   EPI_DSIG     delta_{l-1} = D * A_l (1 - A_l)            (linalg.py:58-60)
 //   EPI_PARTIAL  split-K partial of G into a workspace slab
 //   EPI_SGD      W_l -= eta * G in place (+ optional raw G) (nn.py:174-179)
+//   EPI_SPLIT_SGD split-K partial into a slab, then the gridDim.z split CTAs of
+//                an output tile meet (global arrive counter; all CTAs of the
+//                launch are co-resident by construction, dw_plan) and each sums
+//                a 1/S row share of the tile over the slabs in slab order and
+//                applies W_l -= eta * G: the split-K reduction without a
+//                second kernel
 //
 // Precision: fp32 data; PASSES == 3 runs the 3xTF32 split
 //   x = hi + lo, hi = trunc_tf32(x) (what the tensor core reads from raw fp32),
@@ -35,7 +41,7 @@
 
 namespace hb {
 
-enum Epi : int { EPI_SIGMOID = 0, EPI_STORE = 1, EPI_DSIG = 2, EPI_PARTIAL = 3, EPI_SGD = 4 };
+enum Epi : int { EPI_SIGMOID = 0, EPI_STORE = 1, EPI_DSIG = 2, EPI_PARTIAL = 3, EPI_SGD = 4, EPI_SPLIT_SGD = 5 };
 
 struct GemmArgs {
   int M, N;               // valid output rows / cols
@@ -55,6 +61,10 @@ struct GemmArgs {
                           // EPI_SGD: lo twin of W), or null
   const DevStep* ds;      // graph launches: start / eta from device memory
   int a_start, b_start;   // add ds->start to a_off / b_off (staged-input operands)
+  float* w;               // EPI_SPLIT_SGD: W_l (updated in place), its lo twin (or null), row stride
+  float* w_lo;
+  long long ldw;
+  int* tile_sync;         // EPI_SPLIT_SGD: 2 zeroed counters per output tile (arrive, depart)
   int trace;              // HB_TRACE builds: record this launch's pipeline timeline
   int trace_slot;         // HB_TRACE builds: 1-based slot for the per-CTA stamps (0 = off)
 };
@@ -140,14 +150,18 @@ template <int BN, bool A_MN, bool B_MN, int EPI, int PASSES>
 __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmA_lo, const __grid_constant__ CUtensorMap tmB_lo,
-                     GemmArgs args) {
+                     const __grid_constant__ GemmArgs args) {
   using C = GemmCfg<BN, PASSES>;
   constexpr bool PAIR = C::PAIR;
+  // args stays in the constant bank (a by-value copy that is modified spills
+  // to the stack); the graph-mode per-step values live in registers
+  int a_off = args.a_off, b_off = args.b_off;
+  float eta = args.eta;
   if (args.ds != nullptr) {
     const int st = static_cast<int>(args.ds->start);
-    if (args.a_start) args.a_off += st;
-    if (args.b_start) args.b_off += st;
-    args.eta = args.ds->eta;
+    if (args.a_start) a_off += st;
+    if (args.b_start) b_off += st;
+    eta = args.ds->eta;
   }
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -225,17 +239,17 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
           uint8_t* dA = sA + h * C::OP_BYTES;
           uint8_t* dB = sB + h * C::OP_BYTES;
           if (!A_MN) {
-            tma_load_2d_to(dA, ma, fb, k0, m0 + args.a_off, PAIR);
+            tma_load_2d_to(dA, ma, fb, k0, m0 + a_off, PAIR);
           } else {
 #pragma unroll
-            for (int j = 0; j < kBM / 32; ++j) tma_load_2d_to(dA + j * 4096, ma, fb, m0 + 32 * j, k0 + args.a_off, PAIR);
+            for (int j = 0; j < kBM / 32; ++j) tma_load_2d_to(dA + j * 4096, ma, fb, m0 + 32 * j, k0 + a_off, PAIR);
           }
           // this CTA's half of B in 32-wide slices (4 KB: 32 K-major rows, or
           // 32 MN columns x 32 K-lines)
 #pragma unroll
           for (int j = 0; j < C::BNL / 32; ++j) {
             const int c0 = B_MN ? nl0 + 32 * j : k0;
-            const int c1 = B_MN ? k0 + args.b_off : nl0 + 32 * j + args.b_off;
+            const int c1 = B_MN ? k0 + b_off : nl0 + 32 * j + b_off;
             tma_load_2d_to(dB + j * 4096, mb, fb, c0, c1, PAIR);
           }
         }
@@ -399,10 +413,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
           float* lp = args.out_lo != nullptr ? args.out_lo + grow * args.ldo + gn : nullptr;
           if (vec_out && nleft >= 4) {
             float4 w4 = pre[rr / 4];
-            w4.x -= args.eta * o[0];
-            w4.y -= args.eta * o[1];
-            w4.z -= args.eta * o[2];
-            w4.w -= args.eta * o[3];
+            w4.x -= eta * o[0];
+            w4.y -= eta * o[1];
+            w4.z -= eta * o[2];
+            w4.w -= eta * o[3];
             *reinterpret_cast<float4*>(wp) = w4;
             if (lp != nullptr) *reinterpret_cast<float4*>(lp) = lo4(w4);
           } else {
@@ -410,7 +424,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
             for (int k = 0; k < 4; ++k)
               if (k < nleft) {
                 const float prev = k == 0 ? pre[rr / 4].x : k == 1 ? pre[rr / 4].y : k == 2 ? pre[rr / 4].z : pre[rr / 4].w;
-                const float nw = prev - args.eta * o[k];
+                const float nw = prev - eta * o[k];
                 wp[k] = nw;
                 if (lp != nullptr) lp[k] = tf32_lo(nw);
               }
@@ -426,9 +440,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
             }
           }
         } else {
-          float* op = args.out + (EPI == EPI_PARTIAL ? static_cast<long long>(blockIdx.z) * args.split_stride : 0LL) +
+          constexpr bool SLAB = (EPI == EPI_PARTIAL || EPI == EPI_SPLIT_SGD);
+          float* op = args.out + (SLAB ? static_cast<long long>(blockIdx.z) * args.split_stride : 0LL) +
                       grow * args.ldo + gn;
-          float* lp = (EPI != EPI_PARTIAL && args.out_lo != nullptr) ? args.out_lo + grow * args.ldo + gn : nullptr;
+          float* lp = (!SLAB && args.out_lo != nullptr) ? args.out_lo + grow * args.ldo + gn : nullptr;
           if (vec_out && nleft >= 4) {
             const float4 v4 = make_float4(o[0], o[1], o[2], o[3]);
             *reinterpret_cast<float4*>(op) = v4;
@@ -442,6 +457,78 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
               }
           }
         }
+      }
+    }
+  }
+
+  if (EPI == EPI_SPLIT_SGD && warp >= 4) {
+    // ---- split-K rendezvous + distributed reduction (epilogue warps only)
+    constexpr int ET = 32 * C::EPI_WARPS;
+    const int S = gridDim.z;
+    int* arrive = args.tile_sync + 2 * (blockIdx.x + gridDim.x * blockIdx.y);
+    named_bar_sync(1, ET);  // this CTA's partial tile is fully stored
+    if (threadIdx.x == 128) {
+      __threadfence();
+      atomicAdd(arrive, 1);
+      long long spins = 0;
+      while (ld_acquire_gpu(arrive) < S) {
+        __nanosleep(64);
+        if (++spins > (1ll << 25)) {  // seconds: the split CTAs were not co-resident
+          printf("hogbatch_b200: split-K rendezvous timed out (tile %d,%d)\n", blockIdx.x, blockIdx.y);
+          __trap();
+        }
+      }
+      __threadfence();
+    }
+    named_bar_sync(1, ET);
+    const int rows_per = (kBM + S - 1) / S;
+    const int r0 = m0 + static_cast<int>(blockIdx.z) * rows_per;
+    const int r1 = min(min(r0 + rows_per, m0 + kBM), args.M);
+    const int ncols = min(BN, args.N - n0);
+    const int quads = ncols / 4;  // host guarantees N % 4 == 0
+    const int items = max(r1 - r0, 0) * quads;
+    for (int it = threadIdx.x - 128; it < items; it += ET) {
+      const int r = r0 + it / quads;
+      const int cc = n0 + 4 * (it % quads);
+      const float* part = args.out + static_cast<long long>(r) * args.ldo + cc;
+      float4 g = __ldcg(reinterpret_cast<const float4*>(part));
+      for (int sl = 1; sl < S; ++sl) {
+        const float4 t = __ldcg(reinterpret_cast<const float4*>(part + sl * args.split_stride));
+        g.x += t.x;
+        g.y += t.y;
+        g.z += t.z;
+        g.w += t.w;
+      }
+      float4* wp = reinterpret_cast<float4*>(args.w + r * args.ldw + cc);
+      float4 wv = *wp;
+      wv.x -= eta * g.x;
+      wv.y -= eta * g.y;
+      wv.z -= eta * g.z;
+      wv.w -= eta * g.w;
+      *wp = wv;
+      if (args.w_lo != nullptr) *reinterpret_cast<float4*>(args.w_lo + r * args.ldw + cc) = lo4(wv);
+      if (args.grad != nullptr) *reinterpret_cast<float4*>(args.grad + r * args.ld_grad + cc) = g;
+    }
+    named_bar_sync(1, ET);
+    // the partial slabs of this share are dead: drop their L2 lines without
+    // the HBM write-back (they were written by this launch and read just above)
+    if ((args.ldo & 31) == 0 && (ncols & 31) == 0) {
+      const int lines_per_row = ncols / 32;
+      const int nl = max(r1 - r0, 0) * lines_per_row * S;
+      for (int it = threadIdx.x - 128; it < nl; it += ET) {
+        const int sl = it % S;
+        const int rl = it / S;
+        const int r = r0 + rl / lines_per_row;
+        const int cc = n0 + 32 * (rl % lines_per_row);
+        discard_l2_line(args.out + sl * args.split_stride + static_cast<long long>(r) * args.ldo + cc);
+      }
+    }
+    if (threadIdx.x == 128) {
+      // the last CTA out re-arms the counters (every CTA has passed the wait)
+      if (atomicAdd(arrive + 1, 1) == S - 1) {
+        arrive[0] = 0;
+        arrive[1] = 0;
+        __threadfence();
       }
     }
   }

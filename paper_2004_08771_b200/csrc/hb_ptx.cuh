@@ -299,4 +299,22 @@ __device__ __forceinline__ float sigmoidf_fast(float z) {
   return z >= 0.f ? r : e * r;
 }
 
+
+// Named barrier over `count` threads (a subset of the CTA, e.g. the epilogue warps).
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// GPU-scope acquire load (split-K rendezvous counters).
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Invalidate one 128-byte L2 line without writing it back (dead scratch data).
+__device__ __forceinline__ void discard_l2_line(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
 }  // namespace hb

@@ -28,6 +28,7 @@
 #include <string>
 #include <tuple>
 #include <vector>
+#include <chrono>
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -395,6 +396,10 @@ struct hb_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.f;
   int last_launches = 0;
+  cudaStream_t xfer = nullptr;                  // H2D stream of the pipelined host-model merge
+  std::vector<cudaEvent_t> xfer_ev;             // one per merge chunk
+  cudaEvent_t snap_ev = nullptr;                // snapshot DMA landed
+  cudaEvent_t merge_ev = nullptr;               // merge: the step stream's prior work is done
   int* tile_sync = nullptr;  // split-K rendezvous counters (2 per output tile), zero between launches
   int pre_launches = 0;  // kernels a host-buffer step enqueued before do_step (densify / batch CSC)
   bool grads_valid = false;
@@ -1332,6 +1337,10 @@ int hb_ctx_destroy(hb_ctx* c) {
   for (auto e : c->evpool) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  for (auto e : c->xfer_ev) cudaEventDestroy(e);
+  if (c->snap_ev) cudaEventDestroy(c->snap_ev);
+  if (c->merge_ev) cudaEventDestroy(c->merge_ev);
+  if (c->xfer) cudaStreamDestroy(c->xfer);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return HB_OK;
@@ -1453,6 +1462,17 @@ static void* mapped_alias(const void* p, size_t bytes) {
   return static_cast<char*>(it->second.second) + (a - it->first);
 }
 
+// page-locked host memory (registered or cudaMallocHost'd): DMA-able as is
+static bool is_pinned(const void* p) {
+  if (p == nullptr) return false;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 static int ensure_stage_all(hb_ctx* c) {
   if (c->stage_all) return HB_OK;
   HB_CUDA(cudaMalloc(&c->stage_all, c->n_params * sizeof(double)));
@@ -1461,31 +1481,58 @@ static int ensure_stage_all(hb_ctx* c) {
   return HB_OK;
 }
 
+// debug (HB_DEBUG_XFER=1): host-side phase timings of the host-model exchange
+static bool xfer_debug() {
+  static const bool on = getenv("HB_DEBUG_XFER") && getenv("HB_DEBUG_XFER")[0] == '1';
+  return on;
+}
+struct XferClock {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  const char* what;
+  explicit XferClock(const char* w) : what(w) {}
+  void mark(const char* phase) const {
+    if (!xfer_debug()) return;
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "[xfer] %s %s %.1f us\n", what, phase, us);
+  }
+};
+
 int hb_set_weights_all_f64(hb_ctx* c, const double* const* ws) {
   HB_TRY(ctx_check(c));
   if (!ws) return fail(HB_EINVAL, "null weight array");
   HB_TRY(ensure_stage_all(c));
+  XferClock clk("snapshot");
+  for (int l = 0; l < c->L; ++l)
+    if (!ws[l]) return fail(HB_EINVAL, "null weights for layer %d", l);
+  // DMA every layer into the f64 staging buffer (copy engine, full link rate
+  // from page-locked memory), return once the bytes landed -- the snapshot is
+  // taken -- and let the f64 -> f32 (+lo) conversions run behind the caller
+  if (!c->snap_ev) HB_CUDA(cudaEventCreateWithFlags(&c->snap_ev, cudaEventDisableTiming));
   size_t off = 0;
   for (int l = 0; l < c->L; ++l) {
-    if (!ws[l]) return fail(HB_EINVAL, "null weights for layer %d", l);
+    const size_t n = static_cast<size_t>(c->d[l + 1]) * c->d[l];
+    HB_CUDA(cudaMemcpyAsync(c->stage_all + off, ws[l], n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    off += n;
+  }
+  HB_CUDA(cudaEventRecord(c->snap_ev, c->stream));
+  clk.mark("dma enqueued");
+  off = 0;
+  for (int l = 0; l < c->L; ++l) {
     const int rows = c->d[l + 1], cols = c->d[l];
     const size_t n = static_cast<size_t>(rows) * cols;
-    // registered host model: the conversion kernel reads it in place over PCIe
-    const double* dst = static_cast<const double*>(mapped_alias(ws[l], n * sizeof(double)));
-    if (dst == nullptr) {
-      HB_CUDA(cudaMemcpyAsync(c->stage_all + off, ws[l], n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-      dst = c->stage_all + off;
-    }
     const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 4096));
     if (l == 0 && c->sparse)
-      f64_to_f32_kernel<true><<<blocks, 256, 0, c->stream>>>(c->W[0], c->ldw[0], dst, cols, rows, cols, nullptr);
+      f64_to_f32_kernel<true><<<blocks, 256, 0, c->stream>>>(c->W[0], c->ldw[0], c->stage_all + off, cols, rows, cols,
+                                                             nullptr);
     else
-      f64_to_f32_kernel<false><<<blocks, 256, 0, c->stream>>>(c->W[l], c->ldw[l], dst, cols, rows, cols,
-                                                              c->need_lo() ? c->W_lo[l] : nullptr);
+      f64_to_f32_kernel<false><<<blocks, 256, 0, c->stream>>>(c->W[l], c->ldw[l], c->stage_all + off, cols, rows,
+                                                              cols, c->need_lo() ? c->W_lo[l] : nullptr);
     HB_CUDA(cudaGetLastError());
     off += n;
   }
-  HB_CUDA(cudaStreamSynchronize(c->stream));
+  clk.mark("kernels enqueued");
+  HB_CUDA(cudaEventSynchronize(c->snap_ev));
+  clk.mark("dma done");
   return HB_OK;
 }
 
@@ -1502,16 +1549,48 @@ int hb_merge_grads_all_into_f64(hb_ctx* c, double* const* ws, double eta) {
     mapped = mapped && dws[l] != nullptr;
   }
   if (mapped) {
-    // the stale merge as a kernel writing the registered host model over PCIe
+    // page-locked host model: pipelined read-modify-write over the two copy
+    // engines -- chunk k goes H2D on the xfer stream while chunk k-1 is
+    // updated on the device (w += -eta*g in f64, linalg.py:79) and written
+    // back D2H on the step stream
+    XferClock clk("merge");
+    if (!c->xfer) HB_CUDA(cudaStreamCreateWithFlags(&c->xfer, cudaStreamNonBlocking));
+    static const size_t kChunk = getenv("HB_MERGE_CHUNK") ? static_cast<size_t>(atoll(getenv("HB_MERGE_CHUNK")))
+                                                           : (size_t(1) << 17);  // doubles (1 MiB)
+    if (!c->merge_ev) HB_CUDA(cudaEventCreateWithFlags(&c->merge_ev, cudaEventDisableTiming));
+    HB_CUDA(cudaEventRecord(c->merge_ev, c->stream));
+    HB_CUDA(cudaStreamWaitEvent(c->xfer, c->merge_ev, 0));  // the step (gradient) and any earlier use are done
+    size_t off = 0;
+    int k = 0;
     for (int l = 0; l < c->L; ++l) {
       const int rows = c->d[l + 1], cols = c->d[l];
       const size_t n = static_cast<size_t>(rows) * cols;
       const bool tr = (l == 0 && c->sparse);
-      merge_host_f64_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 8)), 256, 0, c->stream>>>(
-          dws[l], c->G[l], tr ? c->ldw[0] : cols, rows, cols, tr ? 1 : 0, eta);
-      HB_CUDA(cudaGetLastError());
+      // chunks are whole rows of the (rows, cols) host layout
+      const int rows_per = static_cast<int>(std::max<size_t>(1, kChunk / std::max(1, cols)));
+      for (int r0 = 0; r0 < rows; r0 += rows_per, ++k) {
+        const int nr = std::min(rows_per, rows - r0);
+        const size_t e0 = static_cast<size_t>(r0) * cols, ne = static_cast<size_t>(nr) * cols;
+        if (static_cast<int>(c->xfer_ev.size()) <= k) {
+          cudaEvent_t e;
+          HB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          c->xfer_ev.push_back(e);
+        }
+        double* dev = c->stage_all + off + e0;
+        HB_CUDA(cudaMemcpyAsync(dev, ws[l] + e0, ne * sizeof(double), cudaMemcpyHostToDevice, c->xfer));
+        HB_CUDA(cudaEventRecord(c->xfer_ev[k], c->xfer));
+        HB_CUDA(cudaStreamWaitEvent(c->stream, c->xfer_ev[k], 0));
+        const float* g = tr ? c->G[0] + r0 : c->G[l] + static_cast<size_t>(r0) * cols;
+        merge_host_f64_kernel<<<static_cast<int>(std::min<size_t>((ne + 255) / 256, 148 * 8)), 256, 0, c->stream>>>(
+            dev, g, tr ? c->ldw[0] : cols, nr, cols, tr ? 1 : 0, eta);
+        HB_CUDA(cudaGetLastError());
+        HB_CUDA(cudaMemcpyAsync(ws[l] + e0, dev, ne * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      }
+      off += n;
     }
+    clk.mark("enqueued");
     HB_CUDA(cudaStreamSynchronize(c->stream));
+    clk.mark("done");
     return HB_OK;
   }
   // gather every layer's gradient in (d_{l+1}, d_l) order into one device
@@ -1534,6 +1613,7 @@ int hb_merge_grads_all_into_f64(hb_ctx* c, double* const* ws, double eta) {
   }
   HB_CUDA(cudaMemcpyAsync(c->grad_host, c->grad_all, off * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
   HB_CUDA(cudaStreamSynchronize(c->stream));
+  XferClock clk2("merge-host");
   // linalg.py:79 np.add(target, scale*source, out=target), scale = -eta; elementwise,
   // so splitting the index range over threads changes nothing numerically
   const double scale = -eta;
@@ -1555,6 +1635,7 @@ int hb_merge_grads_all_into_f64(hb_ctx* c, double* const* ws, double eta) {
     work(0);
     for (auto& x : th) x.join();
   }
+  clk2.mark("axpy done");
   return HB_OK;
 }
 
@@ -1928,9 +2009,29 @@ int hb_permute_epoch(hb_ctx* c, const int64_t* perm, int64_t n) {
   return HB_OK;
 }
 
+// range checks as branch-free min/max reductions (vectorised), then a scan
+// for the offending value only on failure
 static int check_labels(const int64_t* y, long long n, int nc) {
+  int64_t mn = 0, mx = 0;
+  if (n > 0) mn = mx = y[0];
+  for (long long i = 0; i < n; ++i) {
+    mn = y[i] < mn ? y[i] : mn;
+    mx = y[i] > mx ? y[i] : mx;
+  }
+  if (mn >= 0 && mx < nc) return HB_OK;
   for (long long i = 0; i < n; ++i)
     if (y[i] < 0 || y[i] >= nc) return fail(HB_EINVAL, "labels must lie in [0, %d), got %lld", nc, (long long)y[i]);
+  return HB_OK;
+}
+static int check_cols(const int32_t* col, long long nnz, int d) {
+  int32_t mn = 0, mx = 0;
+  for (long long e = 0; e < nnz; ++e) {
+    mn = col[e] < mn ? col[e] : mn;
+    mx = col[e] > mx ? col[e] : mx;
+  }
+  if (mn >= 0 && mx < d) return HB_OK;
+  for (long long e = 0; e < nnz; ++e)
+    if (col[e] < 0 || col[e] >= d) return fail(HB_EINVAL, "feature index %d outside [0, %d)", col[e], d);
   return HB_OK;
 }
 
@@ -1970,8 +2071,7 @@ int hb_train_step_host_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col,
   if (rowptr[0] != 0) return fail(HB_EINVAL, "rowptr[0] must be 0");
   HB_TRY(check_labels(labels, rows, c->d[c->L]));
   const long long nnz = rowptr[rows];
-  for (long long e = 0; e < nnz; ++e)
-    if (col[e] < 0 || col[e] >= c->d[0]) return fail(HB_EINVAL, "feature index %d outside [0, %d)", col[e], c->d[0]);
+  HB_TRY(check_cols(col, nnz, c->d[0]));
   if (nnz > c->b_nnz_cap) {
     cudaFree(c->bcol);
     cudaFree(c->bval);
@@ -1999,16 +2099,24 @@ int hb_train_step_host_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col,
   char* p_colptr = p_val + b_f32;
   char* p_rowidx = p_colptr + b_colptr;
   char* p_cval = p_rowidx + b_i32;
-  std::memcpy(p, rowptr, b_rowptr);
-  std::memcpy(p_lab, labels, b_lab);
-  std::memcpy(p_col, col, b_i32);
-  std::memcpy(p_val, val, b_f32);
   cudaStream_t st = c->stream;
-  HB_CUDA(cudaMemcpyAsync(c->browptr, p, b_rowptr, cudaMemcpyHostToDevice, st));
-  HB_CUDA(cudaMemcpyAsync(c->blabels, p_lab, b_lab, cudaMemcpyHostToDevice, st));
-  if (nnz > 0) {
-    HB_CUDA(cudaMemcpyAsync(c->bcol, p_col, b_i32, cudaMemcpyHostToDevice, st));
-    HB_CUDA(cudaMemcpyAsync(c->bval, p_val, b_f32, cudaMemcpyHostToDevice, st));
+  if (nnz > 0 && is_pinned(rowptr) && is_pinned(labels) && is_pinned(col) && is_pinned(val)) {
+    // page-locked batch: DMA straight from the caller's arrays
+    HB_CUDA(cudaMemcpyAsync(c->browptr, rowptr, b_rowptr, cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemcpyAsync(c->blabels, labels, b_lab, cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemcpyAsync(c->bcol, col, b_i32, cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemcpyAsync(c->bval, val, b_f32, cudaMemcpyHostToDevice, st));
+  } else {
+    std::memcpy(p, rowptr, b_rowptr);
+    std::memcpy(p_lab, labels, b_lab);
+    std::memcpy(p_col, col, b_i32);
+    std::memcpy(p_val, val, b_f32);
+    HB_CUDA(cudaMemcpyAsync(c->browptr, p, b_rowptr, cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemcpyAsync(c->blabels, p_lab, b_lab, cudaMemcpyHostToDevice, st));
+    if (nnz > 0) {
+      HB_CUDA(cudaMemcpyAsync(c->bcol, p_col, b_i32, cudaMemcpyHostToDevice, st));
+      HB_CUDA(cudaMemcpyAsync(c->bval, p_val, b_f32, cudaMemcpyHostToDevice, st));
+    }
   }
   if (!c->sparse) {
     // densified context: scatter the batch into the dense slot, then the GEMM path

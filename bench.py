@@ -298,28 +298,27 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         else:
             h2d += bb.nbytes + host_batches[0][1].nbytes
         ctx.pin_host(host_model)  # what execute_gpu_replica does for the shared model
-        for i in range(min(2, args.warmup)):  # warm the host path
-            ctx.set_weights(host_model)
-            ctx.step_host(host_batches[i % len(host_batches)][0], host_batches[i % len(host_batches)][1],
-                          cfg["eta"], emit_grad=True)
-            ctx.merge_grads_into(host_model, cfg["eta"])
+        for i in range(max(3, min(args.warmup, len(host_batches)))):  # warm the host path (and its graph)
+            xb, yb = host_batches[i % len(host_batches)]
+            ctx.replica_step_host(host_model, xb, yb, cfg["eta"])
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for i in range(args.steps):
             xb, yb = host_batches[i]
-            ctx.set_weights(host_model)  # snapshot of the shared host model (workers.py:132)
-            ctx.step_host(xb, yb, cfg["eta"], emit_grad=True, want_loss=True)  # batch H2D, loss D2H
-            ctx.merge_grads_into(host_model, cfg["eta"])  # stale merge (workers.py:135)
+            # execute_batch_replica in one call: snapshot of the shared host model
+            # (workers.py:132), batch H2D, the step, stale merge (workers.py:135), loss D2H
+            ctx.replica_step_host(host_model, xb, yb, cfg["eta"], want_loss=True)
         el = time.perf_counter() - t0
         if world > 1:
             el = max_over_ranks(dist, el)
         e2e = {"value": world * args.steps * b / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
-               "path": "execute_gpu_replica semantics through the C ABI, per step: snapshot of the page-locked "
-                       "f64 host model (DMA H2D), batch H2D from pinned host memory (CSR rows are scattered into "
-                       "dense rows on the device for narrow inputs), the step, the f64 stale merge "
-                       "W_host -= eta*g as a pipelined DMA read-modify-write of the host model, loss D2H"}
+               "path": "execute_gpu_replica semantics through the C ABI (hb_replica_step_host_*), per step: "
+                       "batch H2D from pinned host memory (CSR rows are scattered into dense rows on the device "
+                       "for narrow inputs), snapshot of the page-locked f64 host model (DMA H2D, layer l+1 in "
+                       "flight while layer l computes), the step, the f64 stale merge W_host -= eta*g as a "
+                       "chunked DMA read-modify-write issued per layer as soon as its gradient exists, loss D2H"}
     ctx.close()
 
     # ---------------------------------------------------------- roofline of the dominant kernel

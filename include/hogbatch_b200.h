@@ -144,6 +144,25 @@ int hb_train_step_host_dense(hb_ctx* ctx, const float* x, int64_t ld, const int6
 int hb_train_step_host_csr(hb_ctx* ctx, const int64_t* rowptr, const int32_t* col, const float* val,
                            const int64_t* labels, int rows, double eta, uint32_t flags, double* out_loss);
 
+/* The whole drop-in replica step, execute_batch_replica(model, batch, eta)
+ * (workers.py:126-138), in one call with the host-model exchange overlapped
+ * with the compute: the snapshot of the shared float64 model ws[l]
+ * (deep_copy, workers.py:132) is DMA'd layer by layer so layer l computes
+ * while layer l+1 is in flight, and the stale merge ws[l] -= eta * g_l
+ * (apply_update into the *current* shared model, workers.py:135 ->
+ * nn.py:174-179 -> linalg.py:70-79, float64, aligned 8-byte stores) is a
+ * chunked DMA read-modify-write issued as soon as layer l's gradient exists,
+ * overlapping the rest of the backward pass.  ws[l] must be page-locked
+ * (hb_host_register).  Returns once the host model holds the merge.  The
+ * three forms take the batch like hb_train_step / _host_dense / _host_csr. */
+int hb_replica_step(hb_ctx* ctx, double* const* ws, int64_t start, int rows, double eta, uint32_t flags,
+                    double* out_loss);
+int hb_replica_step_host_dense(hb_ctx* ctx, double* const* ws, const float* x, int64_t ld, const int64_t* labels,
+                               int rows, double eta, uint32_t flags, double* out_loss);
+int hb_replica_step_host_csr(hb_ctx* ctx, double* const* ws, const int64_t* rowptr, const int32_t* col,
+                             const float* val, const int64_t* labels, int rows, double eta, uint32_t flags,
+                             double* out_loss);
+
 /* Sum over staged rows [start, start+rows) of -log max(p_y, 1e-12)
  * (loss_sum, nn.py:139-146), evaluated in chunks of at most max_batch rows. */
 int hb_eval_loss_sum(hb_ctx* ctx, int64_t start, int64_t rows, double* out_sum);

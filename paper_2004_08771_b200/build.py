@@ -26,6 +26,8 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared",
+    # host-side float64 merges must round like NumPy (no FMA contraction)
+    "-Xcompiler", "-ffp-contract=off",
     "--expt-relaxed-constexpr",
     # IEEE exp/div and denormals: sigmoid(-100) must stay a positive denormal
     # (pkg/tests/test_linalg.py:67-70), so no --use_fast_math / FTZ.

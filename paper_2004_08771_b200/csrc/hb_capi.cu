@@ -28,7 +28,12 @@
 #include <string>
 #include <tuple>
 #include <vector>
+#include <atomic>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 #include <chrono>
+#include <condition_variable>
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -359,6 +364,7 @@ struct hb_ctx {
 
   float* bx = nullptr;  // batch slot (dense rows) for host-buffer steps
   float* bx_lo = nullptr;
+  float* bx_stage = nullptr;  // contiguous landing slot of a host batch whose device rows are padded
   int64_t* blabels = nullptr;
   int64_t *browptr = nullptr, *bcolptr = nullptr;
   int32_t *bcol = nullptr, *browidx = nullptr;
@@ -416,10 +422,34 @@ struct hb_ctx {
   bool use_graphs = true;
   bool capturing = false;
   std::vector<cudaEvent_t> cap_events;
-  std::map<std::tuple<int, uint32_t, long long, bool>, StepGraph> graphs;
-  std::map<std::tuple<int, uint32_t, long long, bool>, int> graph_seen;
+  std::map<std::tuple<int, uint32_t, long long, bool, long long>, StepGraph> graphs;
+  std::map<std::tuple<int, uint32_t, long long, bool, long long>, int> graph_seen;
   DevStep* d_step = nullptr;  // device copy of the per-step scalars
   long long view_gen = 1;     // bumped whenever staged buffers / maps change
+  // Overlapped host-model exchange of the fused replica step (hb_replica_step*):
+  // while armed, the step itself snapshots the host float64 model layer by
+  // layer (DMA on xh2d, layer l+1 in flight while layer l computes) and merges
+  // W_host -= eta*g_l as a chunked DMA read-modify-write (H2D on xh2d, update
+  // + D2H on xmrg) as soon as layer l's gradient exists.
+  std::vector<double*> xw;          // armed host model (page-locked); empty: no exchange
+  std::vector<double*> xw_prev;     // pointer set of the last armed call (graph key)
+  long long xgen = 0;               // bumps when the armed pointer set changes
+  cudaStream_t xh2d = nullptr, xmrg = nullptr;
+  std::vector<cudaEvent_t> xsnap_ev, xgrad_ev, xchunk_ev;
+  cudaEvent_t xstart_ev = nullptr, xdone_ev = nullptr;
+  int xchunk_used = 0;
+  // merge strategy: 0 = host (gradient D2H as fp32, float64 axpy on host
+  // threads as each layer's gradient lands -- the reference's own np.add on
+  // the host model); 1 = DMA read-modify-write through device memory
+  int xmode = 0;
+  // host mode: "layer l's gradient is in grad_host" flags.  Event syncs do
+  // not survive graph capture, so the merge stream copies the call's sequence
+  // number (read from pinned memory when the step runs) into xflags[l] after
+  // the gradient D2H, and the calling thread polls it.
+  float* xgrad_host = nullptr;    // pinned landing zone of the fp32 gradients
+  int32_t* xseq_host = nullptr;  // pinned: [0] = this call's sequence number, [1 + l] = layer flags
+  int32_t* d_xseq = nullptr;
+  int32_t xseq = 0;
   void* comm = nullptr;
   int nranks = 1;
   float* flat = nullptr;  // contiguous model copy for allreduce
@@ -535,6 +565,350 @@ void dw_plan(const hb_ctx* c, int l, int rows, int* splits, int* kb_per, int* kb
 
 // `ds` != null: graph mode -- kernels read the batch start and eta from
 // device memory (the by-value start/eta are then 0 and ignored).
+// debug (HB_DEBUG_XFER=1): host-side phase timings of the host-model exchange
+static bool xfer_debug() {
+  static const bool on = getenv("HB_DEBUG_XFER") && getenv("HB_DEBUG_XFER")[0] == '1';
+  return on;
+}
+struct XferClock {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  const char* what;
+  explicit XferClock(const char* w) : what(w) {}
+  void mark(const char* phase) const {
+    if (!xfer_debug()) return;
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "[xfer] %s %s %.1f us\n", what, phase, us);
+  }
+};
+
+static std::chrono::steady_clock::time_point g_call_t0;
+static void xmark(const char* what, int l = -1) {
+  if (!xfer_debug()) return;
+  const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - g_call_t0).count();
+  fprintf(stderr, "[xfer] %8.1f us  %s %d\n", us, what, l);
+}
+
+// ---------------------------------------------- overlapped host-model exchange
+// (armed by hb_replica_step*; every call below is a no-op otherwise).  All of
+// it is plain stream/event work, so it is captured into the step's CUDA graph
+// like the kernels (the graph key carries the armed pointer set).
+// debug (HB_DEBUG_XCHG=1, eager steps): timeline of the exchange on its streams
+static bool xchg_debug() {
+  static const bool on = getenv("HB_DEBUG_XCHG") && getenv("HB_DEBUG_XCHG")[0] == '1';
+  return on;
+}
+// (capture-safe: events are external record nodes of the step graph, reused by label)
+static std::vector<std::pair<std::string, cudaEvent_t>> g_xtl;
+static cudaError_t record_ev(hb_ctx* c, cudaEvent_t e, cudaStream_t s) {
+  return c->capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
+}
+static void xtl(hb_ctx* c, cudaStream_t s, const char* fmt, int a = 0, int b = 0) {
+  if (!xchg_debug()) return;
+  char buf[96];
+  snprintf(buf, sizeof buf, fmt, a, b);
+  cudaEvent_t e = nullptr;
+  for (auto& p : g_xtl)
+    if (p.first == buf) e = p.second;
+  if (e == nullptr) {
+    cudaEventCreate(&e);
+    g_xtl.emplace_back(buf, e);
+  }
+  cudaError_t er = record_ev(c, e, s);
+  if (er != cudaSuccess) fprintf(stderr, "[xchg] event %s: %s\n", buf, cudaGetErrorString(er));
+}
+static void xtl_dump() {
+  if (g_xtl.empty()) return;
+  cudaDeviceSynchronize();
+  for (auto& p : g_xtl) {
+    float ms = 0.f;
+    cudaError_t er = cudaEventElapsedTime(&ms, g_xtl.front().second, p.second);
+    fprintf(stderr, "[xchg] %8.1f us  %s %s\n", ms * 1000.f, p.first.c_str(),
+            er == cudaSuccess ? "" : cudaGetErrorString(er));
+  }
+  cudaGetLastError();
+}
+
+// Small persistent pool for the host side of the merge: run(n, fn) calls
+// fn(0..n-1) on up to n threads (the caller included) and returns when done.
+// Workers spin briefly after each job (a merge is a burst of one job per
+// layer, tens of microseconds apart) before sleeping on the condition variable.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool p;
+    return p;
+  }
+  int size() const { return static_cast<int>(threads_.size()) + 1; }
+  void run(int n, const std::function<void(int)>& fn) {
+    if (n <= 1 || threads_.empty()) {
+      for (int i = 0; i < n; ++i) fn(i);
+      return;
+    }
+    fn_.store(&fn, std::memory_order_relaxed);
+    n_.store(n, std::memory_order_relaxed);
+    done_.store(0, std::memory_order_relaxed);
+    next_.store(0, std::memory_order_release);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      gen_.fetch_add(1, std::memory_order_acq_rel);
+    }
+    cv_.notify_all();
+    work();
+    while (done_.load(std::memory_order_acquire) < n) pause();
+    next_.store(1 << 30, std::memory_order_release);  // late workers find nothing to take
+  }
+
+ private:
+  static void pause() {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+  void work() {
+    for (;;) {
+      const int i = next_.fetch_add(1, std::memory_order_acq_rel);
+      if (i >= n_.load(std::memory_order_acquire)) return;
+      (*fn_.load(std::memory_order_acquire))(i);
+      done_.fetch_add(1, std::memory_order_acq_rel);
+    }
+  }
+  HostPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    int t = static_cast<int>(std::min(8u, std::max(1u, hw / 2))) - 1;
+    if (const char* e = getenv("HB_HOST_MERGE_THREADS")) t = std::max(0, atoi(e) - 1);
+    next_.store(1 << 30);
+    for (int i = 0; i < t; ++i) threads_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      gen_.fetch_add(1);
+    }
+    cv_.notify_all();
+    for (auto& t : threads_) t.join();
+  }
+  void loop() {
+    unsigned long long seen = gen_.load();
+    for (;;) {
+      // spin ~0.5 ms for the next job, then sleep
+      static const int spins = getenv("HB_POOL_SPIN") ? atoi(getenv("HB_POOL_SPIN")) : 20000;
+      for (int k = 0; k < spins && gen_.load(std::memory_order_acquire) == seen; ++k) pause();
+      if (gen_.load(std::memory_order_acquire) == seen) {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_.load() != seen; });
+      }
+      if (stop_) return;
+      seen = gen_.load(std::memory_order_acquire);
+      work();
+    }
+  }
+  std::vector<std::thread> threads_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::atomic<const std::function<void(int)>*> fn_{nullptr};
+  std::atomic<int> n_{0};
+  std::atomic<int> next_{0}, done_{0};
+  std::atomic<unsigned long long> gen_{0};
+  bool stop_ = false;
+};
+
+#if defined(__x86_64__)
+// One part of the merge.  Measured on the B200 host: device DMA into or out of
+// host lines that sit in some core's private cache is slow (it snoops them
+// out), so the merge leaves none behind -- w is written with streaming
+// (non-temporal) stores and the gradient lines it read are flushed -- which is
+// what lets several threads share the merge without slowing the next call's
+// snapshot DMA or the next gradient DMA.
+__attribute__((target("sse4.1,clflushopt"))) static void axpy_part(double* w, const float* g, size_t a, size_t b,
+                                                                    double scale) {
+  size_t i = a;
+  for (; i < b && (reinterpret_cast<uintptr_t>(w + i) & 15) != 0; ++i) w[i] = w[i] + scale * static_cast<double>(g[i]);
+  const __m128d sc = _mm_set1_pd(scale);
+  for (; i + 2 <= b; i += 2) {
+    const __m128d gv = _mm_cvtps_pd(_mm_castpd_ps(_mm_load_sd(reinterpret_cast<const double*>(g + i))));
+    _mm_stream_pd(w + i, _mm_add_pd(_mm_load_pd(w + i), _mm_mul_pd(sc, gv)));
+  }
+  for (; i < b; ++i) w[i] = w[i] + scale * static_cast<double>(g[i]);
+  _mm_sfence();
+  const uintptr_t g0 = reinterpret_cast<uintptr_t>(g + a) & ~uintptr_t(63), g1 = reinterpret_cast<uintptr_t>(g + b);
+  for (uintptr_t p = g0; p < g1; p += 64) _mm_clflushopt(reinterpret_cast<void*>(p));
+}
+#else
+static void axpy_part(double* w, const float* g, size_t a, size_t b, double scale) {
+  for (size_t i = a; i < b; ++i) w[i] = w[i] + scale * static_cast<double>(g[i]);
+}
+#endif
+
+// w[i] = w[i] + (-eta) * g[i]: linalg.py:79 np.add(target, scale*source,
+// out=target) in float64, product and sum rounded separately (the library's
+// host code is built with -ffp-contract=off), every double written whole
+// (no torn scalars for concurrent host readers, linalg.py:3-7)
+static void host_axpy_f64(double* w, const float* g, size_t n, double eta) {
+  const double scale = -eta;
+  HostPool& pool = HostPool::get();
+  static const int max_parts = getenv("HB_MERGE_PARTS") ? atoi(getenv("HB_MERGE_PARTS")) : 64;
+  static const size_t part_elems = getenv("HB_MERGE_PART_ELEMS") ? atoll(getenv("HB_MERGE_PART_ELEMS")) : (1 << 16);
+  const int parts = static_cast<int>(
+      std::min<size_t>(std::min(pool.size(), max_parts), std::max<size_t>(1, n / part_elems)));
+  if (xfer_debug()) fprintf(stderr, "[xfer] axpy n=%zu parts=%d pool=%d\n", n, parts, pool.size());
+  pool.run(parts, [&](int t) {
+    // part boundaries on 16-element multiples keep the parts' cache lines apart
+    const size_t a = (n * t / parts) & ~size_t(15), b = t + 1 == parts ? n : (n * (t + 1) / parts) & ~size_t(15);
+    axpy_part(w, g, a, b, scale);
+  });
+}
+
+size_t layer_offset(const hb_ctx* c, int l) {
+  size_t off = 0;
+  for (int i = 0; i < l; ++i) off += static_cast<size_t>(c->d[i + 1]) * c->d[i];
+  return off;
+}
+
+// snapshot DMA of every layer (deep_copy, workers.py:132), layer 0 first
+int xchg_begin(hb_ctx* c) {
+  if (c->xw.empty()) return HB_OK;
+  c->xchunk_used = 0;
+  xtl(c, c->stream, "begin");
+  if (c->xmode == 0)  // the sequence number the layer flags will carry (read at run time)
+    HB_CUDA(cudaMemcpyAsync(c->d_xseq, c->xseq_host, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+  HB_CUDA(cudaEventRecord(c->xstart_ev, c->stream));
+  HB_CUDA(cudaStreamWaitEvent(c->xh2d, c->xstart_ev, 0));  // earlier users of the staging buffer are done
+  for (int l = 0; l < c->L; ++l) {
+    const size_t n = static_cast<size_t>(c->d[l + 1]) * c->d[l];
+    HB_CUDA(cudaMemcpyAsync(c->stage_all + layer_offset(c, l), c->xw[l], n * sizeof(double), cudaMemcpyHostToDevice,
+                            c->xh2d));
+    HB_CUDA(cudaEventRecord(c->xsnap_ev[l], c->xh2d));
+    xtl(c, c->xh2d, "h2d: snapshot layer %d landed", l);
+  }
+  return HB_OK;
+}
+
+// before the first kernel that reads W_l: wait for its bytes, convert to the
+// fp32 (+ lo twin) device layout
+int xchg_use(hb_ctx* c, int l) {
+  if (c->xw.empty()) return HB_OK;
+  xtl(c, c->stream, "step: ready for W%d", l);
+  HB_CUDA(cudaStreamWaitEvent(c->stream, c->xsnap_ev[l], 0));
+  xtl(c, c->stream, "step: W%d snapshot available", l);
+  const int rows = c->d[l + 1], cols = c->d[l];
+  const size_t n = static_cast<size_t>(rows) * cols;
+  const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 4096));
+  const double* src = c->stage_all + layer_offset(c, l);
+  if (l == 0 && c->sparse)
+    f64_to_f32_kernel<true><<<blocks, 256, 0, c->stream>>>(c->W[0], c->ldw[0], src, cols, rows, cols, nullptr);
+  else
+    f64_to_f32_kernel<false><<<blocks, 256, 0, c->stream>>>(c->W[l], c->ldw[l], src, cols, rows, cols,
+                                                            c->need_lo() ? c->W_lo[l] : nullptr);
+  HB_CUDA(cudaGetLastError());
+  c->last_launches++;
+  return HB_OK;
+}
+
+// after the last kernel that writes G_l: stale merge of layer l into the host
+// model (workers.py:135 -> nn.py:174-179 -> linalg.py:79, w += -eta*g in
+// float64), chunk k read H2D while chunk k-1 is updated and written back D2H.
+// Each chunk is read just before it is written, so the window in which a
+// concurrent host writer's update could be overwritten stays one chunk long.
+int xchg_merge(hb_ctx* c, int l, double eta, const DevStep* ds) {
+  if (c->xw.empty()) return HB_OK;
+  xtl(c, c->stream, "step: G%d done", l);
+  HB_CUDA(cudaEventRecord(c->xgrad_ev[l], c->stream));
+  const int rows = c->d[l + 1], cols = c->d[l];
+  const bool tr = (l == 0 && c->sparse);
+  if (c->xmode == 0) {
+    // host mode: the fp32 gradient goes D2H on the merge stream; the calling
+    // thread applies it (hb_replica_step*, xchg_host_merges)
+    HB_CUDA(cudaStreamWaitEvent(c->xmrg, c->xgrad_ev[l], 0));
+    const size_t n = static_cast<size_t>(rows) * cols;
+    const size_t off = layer_offset(c, l);
+    const float* src = c->G[l];
+    if (tr) {
+      transpose_f32_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 1024)), 256, 0, c->xmrg>>>(
+          c->grad_all + off, c->G[0], c->ldw[0], rows, cols);
+      HB_CUDA(cudaGetLastError());
+      c->last_launches++;
+      src = c->grad_all + off;
+    }
+    HB_CUDA(cudaMemcpyAsync(c->xgrad_host + off, src, n * sizeof(float), cudaMemcpyDeviceToHost, c->xmrg));
+    HB_CUDA(cudaMemcpyAsync(c->xseq_host + 1 + l, c->d_xseq, sizeof(int32_t), cudaMemcpyDeviceToHost, c->xmrg));
+    xtl(c, c->xmrg, "mrg: gradient %d on host", l);
+    return HB_OK;
+  }
+  HB_CUDA(cudaStreamWaitEvent(c->xh2d, c->xgrad_ev[l], 0));
+  const size_t kChunk = size_t(1) << 17;  // doubles (1 MiB)
+  const int rows_per = static_cast<int>(std::max<size_t>(1, kChunk / std::max(1, cols)));
+  double* base = c->stage_all + layer_offset(c, l);
+  for (int r0 = 0; r0 < rows; r0 += rows_per) {
+    const int nr = std::min(rows_per, rows - r0);
+    const size_t e0 = static_cast<size_t>(r0) * cols, ne = static_cast<size_t>(nr) * cols;
+    if (c->xchunk_used >= static_cast<int>(c->xchunk_ev.size())) {
+      cudaEvent_t e;
+      HB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->xchunk_ev.push_back(e);
+    }
+    cudaEvent_t ev = c->xchunk_ev[c->xchunk_used++];
+    HB_CUDA(cudaMemcpyAsync(base + e0, c->xw[l] + e0, ne * sizeof(double), cudaMemcpyHostToDevice, c->xh2d));
+    HB_CUDA(cudaEventRecord(ev, c->xh2d));
+    xtl(c, c->xh2d, "h2d: merge read layer %d row %d", l, r0);
+    HB_CUDA(cudaStreamWaitEvent(c->xmrg, ev, 0));
+    const float* g = tr ? c->G[0] + r0 : c->G[l] + static_cast<size_t>(r0) * cols;
+    // a few CTAs on the high-priority merge stream: they fit beside (or right
+    // after) the step's GEMM CTAs instead of queueing behind a whole wave
+    merge_host_f64_kernel<<<static_cast<int>(std::min<size_t>((ne + 255) / 256, 16)), 256, 0, c->xmrg>>>(
+        base + e0, g, tr ? c->ldw[0] : cols, nr, cols, tr ? 1 : 0, eta, ds);
+    HB_CUDA(cudaGetLastError());
+    c->last_launches++;
+    xtl(c, c->xmrg, "mrg: updated layer %d row %d", l, r0);
+    HB_CUDA(cudaMemcpyAsync(c->xw[l] + e0, base + e0, ne * sizeof(double), cudaMemcpyDeviceToHost, c->xmrg));
+    xtl(c, c->xmrg, "mrg: written back layer %d row %d", l, r0);
+  }
+  return HB_OK;
+}
+
+// host mode, on the calling thread after the step is enqueued: apply each
+// layer's gradient as soon as it has landed, in the order the backward pass
+// produces them (last layer first), overlapping the rest of the device work
+int xchg_host_merges(hb_ctx* c, double eta) {
+  if (c->xw.empty() || c->xmode != 0) return HB_OK;
+  const int32_t seq = c->xseq;
+  xmark("enqueued");
+  for (int l = c->L - 1; l >= 0; --l) {
+    volatile int32_t* flag = c->xseq_host + 1 + l;
+    // spin on the flag (pinned host memory, no driver calls); the stream is
+    // queried only every ~2^18 spins to surface a failed step
+    for (long long spin = 1; *flag != seq; ++spin) {
+#if defined(__x86_64__)
+      __builtin_ia32_pause();
+#endif
+      if ((spin & ((1 << 18) - 1)) == 0) {
+        const cudaError_t e = cudaStreamQuery(c->stream);
+        if (e == cudaSuccess && *flag != seq) return fail(HB_ECUDA, "merge of layer %d never signalled", l);
+        if (e != cudaSuccess && e != cudaErrorNotReady)
+          return fail(HB_ECUDA, "step failed during the merge: %s", cudaGetErrorString(e));
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    xmark("flag seen", l);
+    host_axpy_f64(c->xw[l], c->xgrad_host + layer_offset(c, l), static_cast<size_t>(c->d[l + 1]) * c->d[l], eta);
+    xmark("axpy done", l);
+  }
+  return HB_OK;
+}
+
+// join: the step stream waits for the last write-back
+int xchg_end(hb_ctx* c) {
+  if (c->xw.empty()) return HB_OK;
+  HB_CUDA(cudaEventRecord(c->xdone_ev, c->xmrg));
+  HB_CUDA(cudaStreamWaitEvent(c->stream, c->xdone_ev, 0));
+  xtl(c, c->stream, "end");
+  // the H2D stream must rejoin too (its last reads feed xmrg, but a capture
+  // needs every forked stream joined)
+  HB_CUDA(cudaEventRecord(c->xstart_ev, c->xh2d));
+  HB_CUDA(cudaStreamWaitEvent(c->stream, c->xstart_ev, 0));
+  return HB_OK;
+}
+
 int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool train, uint32_t flags, double eta,
                 const DevStep* ds) {
   cudaStream_t st = c->stream;
@@ -543,6 +917,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   const int zrows = std::min<long long>(round_up(rows, kBM), c->cap);
   // hidden layers
   for (int l = 0; l < L - 1; ++l) {
+    HB_TRY(xchg_use(c, l));
     if (l == 0 && c->sparse) {
       SpmmArgs p{v.rowptr, v.col, v.val, ds, start, rows, c->W[0], c->ldw[0], c->d[0], c->d[1], c->A[1], c->ld[1],
                  (c->need_lo() && !(c->small_head && L == 2)) ? c->A_lo[1] : nullptr};
@@ -596,6 +971,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   // output layer
   const int l = L - 1;
   const float inv_n = 1.0f / static_cast<float>(rows);
+  HB_TRY(xchg_use(c, l));
   if (c->small_head) {
     HeadArgs h{};
     if (L == 1) {
@@ -674,6 +1050,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
       HB_CUDA(cudaGetLastError());
       prof_end(c, "reduce_sgd", l);
       c->last_launches++;
+      HB_TRY(xchg_merge(c, l, eta, ds));
     }
     return HB_OK;
   }
@@ -767,6 +1144,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
         HB_CUDA(cudaGetLastError());
         prof_end(c, "sparse_dw_sgd", 0);
         c->last_launches += 2;
+        HB_TRY(xchg_merge(c, 0, eta, ds));
         continue;
       }
       csc_batch_ranges_kernel<<<cdiv(c->d[0], 256), 256, 0, st>>>(v.colptr, v.rowidx, c->d[0], start, rows, ds,
@@ -786,6 +1164,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       c->last_launches++;
       prof_end(c, "sparse_dw_sgd", 0);
       c->last_launches++;
+      HB_TRY(xchg_merge(c, 0, eta, ds));
       continue;
     }
     int splits, kb_per, kb_total;
@@ -850,6 +1229,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       prof_end(c, "reduce_sgd", l);
       c->last_launches += 2;
     }
+    HB_TRY(xchg_merge(c, l, eta, ds));
   }
   return HB_OK;
 }
@@ -860,8 +1240,10 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
 // phase 0: whole step; 1: forward (incl. the fused head and its update); 2: backward
 int run_phase(hb_ctx* c, const DataView& v, long long start, int rows, uint32_t flags, double eta, const DevStep* ds,
               int phase) {
+  if (phase != 2) HB_TRY(xchg_begin(c));
   if (phase != 2) HB_TRY(run_forward(c, v, start, rows, true, flags, eta, ds));
   if (phase != 1) HB_TRY(run_backward(c, v, start, rows, flags, eta, ds));
+  if (phase != 1) HB_TRY(xchg_end(c));
   return HB_OK;
 }
 
@@ -870,8 +1252,9 @@ int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double
   const uint32_t gflags = (flags & HB_STEP_EMIT_GRAD) | (static_cast<uint32_t>(phase) << 8);
   const bool view_epoch = (&v == &c->epoch);
   if (!c->use_graphs || !graph_ok) return run_phase(c, v, start, rows, flags, eta, nullptr, phase);
-  const auto key = std::make_tuple(rows, gflags, view_epoch ? c->view_gen : -c->view_gen, c->prof_on);
-  DevStep hs{start, static_cast<float>(eta), 0};
+  const auto key = std::make_tuple(rows, gflags, view_epoch ? c->view_gen : -c->view_gen, c->prof_on,
+                                   c->xw.empty() ? 0LL : c->xgen);
+  DevStep hs{start, static_cast<float>(eta), 0, eta};
   auto it = c->graphs.find(key);
   if (it == c->graphs.end()) {
     if (c->graph_seen[key]++ == 0)  // first sighting: run eagerly (also configures kernel attributes)
@@ -1314,6 +1697,7 @@ int hb_ctx_destroy(hb_ctx* c) {
   for (auto p : c->A_lo) cudaFree(p);
   for (auto p : c->D_lo) cudaFree(p);
   cudaFree(c->bx_lo);
+  cudaFree(c->bx_stage);
   free_epoch(c);
   cudaFree(c->bx);
   cudaFree(c->blabels);
@@ -1341,6 +1725,16 @@ int hb_ctx_destroy(hb_ctx* c) {
   if (c->snap_ev) cudaEventDestroy(c->snap_ev);
   if (c->merge_ev) cudaEventDestroy(c->merge_ev);
   if (c->xfer) cudaStreamDestroy(c->xfer);
+  for (auto e : c->xsnap_ev) cudaEventDestroy(e);
+  for (auto e : c->xgrad_ev) cudaEventDestroy(e);
+  if (c->xseq_host) cudaFreeHost(c->xseq_host);
+  if (c->xgrad_host) cudaFreeHost(c->xgrad_host);
+  cudaFree(c->d_xseq);
+  for (auto e : c->xchunk_ev) cudaEventDestroy(e);
+  if (c->xstart_ev) cudaEventDestroy(c->xstart_ev);
+  if (c->xdone_ev) cudaEventDestroy(c->xdone_ev);
+  if (c->xh2d) cudaStreamDestroy(c->xh2d);
+  if (c->xmrg) cudaStreamDestroy(c->xmrg);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return HB_OK;
@@ -1473,6 +1867,33 @@ static bool is_pinned(const void* p) {
   return at.type == cudaMemoryTypeHost;
 }
 
+// Host->device copy that tolerates a source range straddling the end of a
+// registered (page-locked) range -- e.g. a staged array whose head is a view
+// that was pinned earlier: CUDA rejects such a copy as one transfer, so it is
+// split at registered-range boundaries.  sync: wait for completion.
+static cudaError_t h2d_copy(void* dst, const void* src, size_t bytes, cudaStream_t st, bool sync = false) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+  size_t done = 0;
+  while (done < bytes) {
+    const uintptr_t p = a + done;
+    size_t n = bytes - done;
+    {
+      std::lock_guard<std::mutex> lk(g_host_mu);
+      auto it = g_host_ranges.upper_bound(p);
+      if (it != g_host_ranges.begin()) {
+        auto prev = std::prev(it);
+        if (p < prev->first + prev->second.first) n = std::min<size_t>(n, prev->first + prev->second.first - p);
+      }
+      if (it != g_host_ranges.end() && it->first < p + n) n = it->first - p;  // stop at the next registered range
+    }
+    cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + done, reinterpret_cast<const void*>(p), n,
+                                    cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+    done += n;
+  }
+  return sync ? cudaStreamSynchronize(st) : cudaSuccess;
+}
+
 static int ensure_stage_all(hb_ctx* c) {
   if (c->stage_all) return HB_OK;
   HB_CUDA(cudaMalloc(&c->stage_all, c->n_params * sizeof(double)));
@@ -1480,22 +1901,6 @@ static int ensure_stage_all(hb_ctx* c) {
   HB_CUDA(cudaMallocHost(&c->grad_host, c->n_params * sizeof(float)));
   return HB_OK;
 }
-
-// debug (HB_DEBUG_XFER=1): host-side phase timings of the host-model exchange
-static bool xfer_debug() {
-  static const bool on = getenv("HB_DEBUG_XFER") && getenv("HB_DEBUG_XFER")[0] == '1';
-  return on;
-}
-struct XferClock {
-  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
-  const char* what;
-  explicit XferClock(const char* w) : what(w) {}
-  void mark(const char* phase) const {
-    if (!xfer_debug()) return;
-    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
-    fprintf(stderr, "[xfer] %s %s %.1f us\n", what, phase, us);
-  }
-};
 
 int hb_set_weights_all_f64(hb_ctx* c, const double* const* ws) {
   HB_TRY(ctx_check(c));
@@ -1653,6 +2058,114 @@ int hb_merge_grad_into_f64(hb_ctx* c, int layer, double* host_w, double eta) {
   return HB_OK;
 }
 
+// ------------------------------------------ fused replica step (drop-in call)
+// Arms the overlapped exchange for exactly one step call.  The host model must
+// be page-locked (hb_host_register) so its DMAs run at link speed and can be
+// captured into the step graph.
+static int xchg_arm(hb_ctx* c, double* const* ws) {
+  g_call_t0 = std::chrono::steady_clock::now();
+  if (!ws) return fail(HB_EINVAL, "null weight array");
+  for (int l = 0; l < c->L; ++l) {
+    if (!ws[l]) return fail(HB_EINVAL, "null weights for layer %d", l);
+    if (!is_pinned(ws[l]))
+      return fail(HB_EINVAL, "layer %d of the host model is not page-locked (hb_host_register it first)", l);
+  }
+  HB_TRY(ensure_stage_all(c));
+  if (!c->xh2d) {
+    int lo_prio = 0, hi_prio = 0;
+    HB_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    HB_CUDA(cudaStreamCreateWithPriority(&c->xh2d, cudaStreamNonBlocking, hi_prio));
+    HB_CUDA(cudaStreamCreateWithPriority(&c->xmrg, cudaStreamNonBlocking, hi_prio));
+    HB_CUDA(cudaEventCreateWithFlags(&c->xstart_ev, cudaEventDisableTiming));
+    HB_CUDA(cudaEventCreateWithFlags(&c->xdone_ev, cudaEventDisableTiming));
+    c->xsnap_ev.resize(c->L);
+    c->xgrad_ev.resize(c->L);
+    for (int l = 0; l < c->L; ++l) {
+      HB_CUDA(cudaEventCreateWithFlags(&c->xsnap_ev[l], cudaEventDisableTiming));
+      HB_CUDA(cudaEventCreateWithFlags(&c->xgrad_ev[l], cudaEventDisableTiming));
+    }
+    HB_CUDA(cudaMallocHost(&c->xseq_host, (c->L + 1) * sizeof(int32_t)));
+    HB_CUDA(cudaHostAlloc(&c->xgrad_host, c->n_params * sizeof(float) + 64, cudaHostAllocDefault));
+    std::memset(c->xseq_host, 0, (c->L + 1) * sizeof(int32_t));
+    HB_CUDA(cudaMalloc(&c->d_xseq, sizeof(int32_t)));
+    if (const char* m = getenv("HB_XCHG_MERGE")) c->xmode = strcmp(m, "dma") == 0 ? 1 : 0;
+  }
+  std::vector<double*> cur(ws, ws + c->L);
+  if (cur != c->xw_prev) {
+    c->xw_prev = cur;
+    c->xgen++;
+  }
+  c->xw = cur;
+  c->xseq = c->xseq == 0x7fffffff ? 1 : c->xseq + 1;
+  *reinterpret_cast<volatile int32_t*>(c->xseq_host) = c->xseq;
+  return HB_OK;
+}
+
+struct XchgGuard {
+  hb_ctx* c;
+  ~XchgGuard() {
+    c->xw.clear();
+    xtl_dump();
+  }
+};
+
+// Enqueue the step asynchronously (the exchange rides inside it), apply the
+// host-mode merges as gradients land, then finish like do_step.
+static int replica_finish(hb_ctx* c, int rc, int rows, double eta, uint32_t flags, double* out_loss) {
+  if (rc != HB_OK) {
+    cudaStreamSynchronize(c->stream);  // nothing may still be writing the host model
+    return rc;
+  }
+  const bool timed = (flags & HB_STEP_TIMED) != 0;
+  if (timed) HB_CUDA(cudaEventRecord(c->ev1, c->stream));
+  HB_TRY(xchg_host_merges(c, eta));
+  if (out_loss != nullptr) {
+    double sum = 0.0;
+    HB_CUDA(cudaMemcpyAsync(&sum, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    HB_CUDA(cudaStreamSynchronize(c->stream));
+    *out_loss = sum / rows;
+  } else {
+    HB_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  if (timed) HB_CUDA(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+  xmark("done");
+  return HB_OK;
+}
+
+static uint32_t replica_flags(hb_ctx* c, uint32_t flags) {
+  if (flags & HB_STEP_TIMED) cudaEventRecord(c->ev0, c->stream);
+  return (flags | HB_STEP_EMIT_GRAD | HB_STEP_ASYNC) & ~HB_STEP_TIMED;
+}
+
+int hb_replica_step(hb_ctx* c, double* const* ws, int64_t start, int rows, double eta, uint32_t flags,
+                    double* out_loss) {
+  HB_TRY(ctx_check(c));
+  HB_TRY(xchg_arm(c, ws));
+  XchgGuard g{c};
+  const int rc = hb_train_step(c, start, rows, eta, replica_flags(c, flags), nullptr);
+  return replica_finish(c, rc, rows, eta, flags, out_loss);
+}
+
+int hb_replica_step_host_dense(hb_ctx* c, double* const* ws, const float* x, int64_t ld, const int64_t* labels,
+                               int rows, double eta, uint32_t flags, double* out_loss) {
+  HB_TRY(ctx_check(c));
+  HB_TRY(xchg_arm(c, ws));
+  XchgGuard g{c};
+  const int rc = hb_train_step_host_dense(c, x, ld, labels, rows, eta, replica_flags(c, flags), nullptr);
+  return replica_finish(c, rc, rows, eta, flags, out_loss);
+}
+
+int hb_replica_step_host_csr(hb_ctx* c, double* const* ws, const int64_t* rowptr, const int32_t* col,
+                             const float* val, const int64_t* labels, int rows, double eta, uint32_t flags,
+                             double* out_loss) {
+  HB_TRY(ctx_check(c));
+  HB_TRY(xchg_arm(c, ws));
+  XchgGuard g{c};
+  const int rc =
+      hb_train_step_host_csr(c, rowptr, col, val, labels, rows, eta, replica_flags(c, flags), nullptr);
+  return replica_finish(c, rc, rows, eta, flags, out_loss);
+}
+
 static int stage_dense_common(hb_ctx* c, int64_t n_rows, const int64_t* labels) {
   if (c->csr_in) return fail(HB_EINVAL, "context was created for sparse (CSR) input");
   if (n_rows < 1 || !labels) return fail(HB_EINVAL, "need n_rows >= 1 and labels");
@@ -1660,7 +2173,7 @@ static int stage_dense_common(hb_ctx* c, int64_t n_rows, const int64_t* labels) 
   HB_CUDA(cudaMalloc(&c->ex, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
   if (c->need_lo()) HB_CUDA(cudaMalloc(&c->ex_lo, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
   HB_CUDA(cudaMalloc(&c->elabels, static_cast<size_t>(n_rows) * sizeof(int64_t)));
-  HB_CUDA(cudaMemcpyAsync(c->elabels, labels, n_rows * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+  HB_CUDA(h2d_copy(c->elabels, labels, n_rows * sizeof(int64_t), c->stream));
   c->e_rows = n_rows;
   return HB_OK;
 }
@@ -1686,7 +2199,7 @@ int hb_stage_dense_f64(hb_ctx* c, const double* x, int64_t n_rows, int64_t ld, c
   const long long chunk = std::max<long long>(1, static_cast<long long>(c->stage64_n) / ld);
   for (long long r0 = 0; r0 < n_rows; r0 += chunk) {
     const long long nr = std::min<long long>(chunk, n_rows - r0);
-    HB_CUDA(cudaMemcpyAsync(c->stage64, x + r0 * ld, nr * ld * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    HB_CUDA(h2d_copy(c->stage64, x + r0 * ld, nr * ld * sizeof(double), c->stream));
     const long long n = nr * c->d[0];
     f64_to_f32_kernel<false><<<static_cast<int>(std::min<long long>((n + 255) / 256, 4096)), 256, 0, c->stream>>>(
         c->ex + r0 * c->ld[0], c->ld[0], c->stage64, ld, static_cast<int>(nr), c->d[0],
@@ -1755,7 +2268,7 @@ static int stage_csr_densified(hb_ctx* c, const int64_t* rowptr, const int32_t* 
   HB_CUDA(cudaMalloc(&c->ex, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
   if (c->need_lo()) HB_CUDA(cudaMalloc(&c->ex_lo, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
   HB_CUDA(cudaMalloc(&c->elabels, static_cast<size_t>(n_rows) * sizeof(int64_t)));
-  HB_CUDA(cudaMemcpyAsync(c->elabels, labels, n_rows * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+  HB_CUDA(h2d_copy(c->elabels, labels, n_rows * sizeof(int64_t), c->stream));
   int64_t* d_rowptr = nullptr;
   int32_t* d_col = nullptr;
   float* d_val = nullptr;
@@ -1763,10 +2276,10 @@ static int stage_csr_densified(hb_ctx* c, const int64_t* rowptr, const int32_t* 
   HB_CUDA(cudaMalloc(&d_rowptr, (n_rows + 1) * sizeof(int64_t)));
   HB_CUDA(cudaMalloc(&d_col, nz * sizeof(int32_t)));
   HB_CUDA(cudaMalloc(&d_val, nz * sizeof(float)));
-  HB_CUDA(cudaMemcpyAsync(d_rowptr, rowptr, (n_rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+  HB_CUDA(h2d_copy(d_rowptr, rowptr, (n_rows + 1) * sizeof(int64_t), c->stream));
   if (nnz > 0) {
-    HB_CUDA(cudaMemcpyAsync(d_col, col, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
-    HB_CUDA(cudaMemcpyAsync(d_val, val, nnz * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    HB_CUDA(h2d_copy(d_col, col, nnz * sizeof(int32_t), c->stream));
+    HB_CUDA(h2d_copy(d_val, val, nnz * sizeof(float), c->stream));
   }
   const int rc = densify_launch(c, d_rowptr, d_col, d_val, n_rows, c->ex, c->ex_lo);
   cudaStreamSynchronize(c->stream);
@@ -1806,15 +2319,15 @@ int hb_stage_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col, const flo
   HB_CUDA(cudaMalloc(&c->erowidx, nz * sizeof(int32_t)));
   HB_CUDA(cudaMalloc(&c->ecval, nz * sizeof(float)));
   HB_CUDA(cudaMalloc(&c->elabels, n_rows * sizeof(int64_t)));
-  HB_CUDA(cudaMemcpy(c->erowptr, rowptr, (n_rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  HB_CUDA(h2d_copy(c->erowptr, rowptr, (n_rows + 1) * sizeof(int64_t), c->stream, true));
   if (nnz > 0) {
-    HB_CUDA(cudaMemcpy(c->ecol, col, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
-    HB_CUDA(cudaMemcpy(c->eval_, val, nnz * sizeof(float), cudaMemcpyHostToDevice));
-    HB_CUDA(cudaMemcpy(c->erowidx, rowidx.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
-    HB_CUDA(cudaMemcpy(c->ecval, cval.data(), nnz * sizeof(float), cudaMemcpyHostToDevice));
+    HB_CUDA(h2d_copy(c->ecol, col, nnz * sizeof(int32_t), c->stream, true));
+    HB_CUDA(h2d_copy(c->eval_, val, nnz * sizeof(float), c->stream, true));
+    HB_CUDA(h2d_copy(c->erowidx, rowidx.data(), nnz * sizeof(int32_t), c->stream, true));
+    HB_CUDA(h2d_copy(c->ecval, cval.data(), nnz * sizeof(float), c->stream, true));
   }
-  HB_CUDA(cudaMemcpy(c->ecolptr, colptr.data(), (c->d[0] + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
-  HB_CUDA(cudaMemcpy(c->elabels, labels, n_rows * sizeof(int64_t), cudaMemcpyHostToDevice));
+  HB_CUDA(h2d_copy(c->ecolptr, colptr.data(), (c->d[0] + 1) * sizeof(int64_t), c->stream, true));
+  HB_CUDA(h2d_copy(c->elabels, labels, n_rows * sizeof(int64_t), c->stream, true));
   c->e_rows = n_rows;
   c->e_nnz = nnz;
   c->nnz_per_row = static_cast<double>(nnz) / static_cast<double>(n_rows);
@@ -1961,7 +2474,7 @@ int hb_permute_epoch(hb_ctx* c, const int64_t* perm, int64_t n) {
     c->has_base = true;
     c->view_gen++;
   }
-  HB_CUDA(cudaMemcpyAsync(c->d_perm, perm, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  HB_CUDA(h2d_copy(c->d_perm, perm, n * sizeof(int64_t), st));
   const int g1 = static_cast<int>(std::min<long long>(cdiv(n, 256), 148 * 8));
   const int gw = static_cast<int>(std::min<long long>(cdiv(n, 8), 148 * 16));  // 8 warps per block
   gather_labels_kernel<<<g1, 256, 0, st>>>(c->elabels, c->plabels, c->d_perm, c->sparse ? c->d_inv : nullptr, n);
@@ -2051,14 +2564,33 @@ int hb_train_step_host_dense(hb_ctx* c, const float* x, int64_t ld, const int64_
   if (!x || !labels || ld < c->d[0]) return fail(HB_EINVAL, "null batch or ld < %d", c->d[0]);
   if (rows < 1 || rows > c->max_batch) return fail(HB_EINVAL, "rows=%d outside [1, %d]", rows, c->max_batch);
   HB_TRY(check_labels(labels, rows, c->d[c->L]));
-  HB_CUDA(cudaMemcpy2DAsync(c->bx, c->ld[0] * sizeof(float), x, ld * sizeof(float), c->d[0] * sizeof(float), rows,
-                            cudaMemcpyHostToDevice, c->stream));
-  if (c->bx_lo) {
-    split_lo_kernel<<<std::min(cdiv(static_cast<long long>(rows) * c->d[0], 256), 148 * 16), 256, 0, c->stream>>>(
-        c->bx, c->bx_lo, c->ld[0], rows, c->d[0]);
+  const int d0 = c->d[0];
+  const long long n = static_cast<long long>(rows) * d0;
+  const int blocks = static_cast<int>(std::min<long long>(cdiv(n, 256), 148 * 16));
+  if (ld == d0 && c->ld[0] == d0) {
+    // contiguous on both sides: one linear DMA (a pitched 2D copy of
+    // thousands of short rows runs far below link speed)
+    HB_CUDA(h2d_copy(c->bx, x, n * sizeof(float), c->stream));
+    if (c->bx_lo) {
+      split_lo_kernel<<<blocks, 256, 0, c->stream>>>(c->bx, c->bx_lo, c->ld[0], rows, d0);
+      HB_CUDA(cudaGetLastError());
+    }
+  } else if (ld == d0) {
+    // contiguous host rows, padded device rows: linear DMA into a staging
+    // slot, then one kernel re-pitches (and splits the lo twin)
+    if (!c->bx_stage) HB_CUDA(cudaMalloc(&c->bx_stage, static_cast<size_t>(c->cap) * d0 * sizeof(float)));
+    HB_CUDA(h2d_copy(c->bx_stage, x, n * sizeof(float), c->stream));
+    repitch_split_kernel<<<blocks, 256, 0, c->stream>>>(c->bx_stage, c->bx, c->bx_lo, c->ld[0], rows, d0);
     HB_CUDA(cudaGetLastError());
+  } else {
+    HB_CUDA(cudaMemcpy2DAsync(c->bx, c->ld[0] * sizeof(float), x, ld * sizeof(float), d0 * sizeof(float), rows,
+                              cudaMemcpyHostToDevice, c->stream));
+    if (c->bx_lo) {
+      split_lo_kernel<<<blocks, 256, 0, c->stream>>>(c->bx, c->bx_lo, c->ld[0], rows, d0);
+      HB_CUDA(cudaGetLastError());
+    }
   }
-  HB_CUDA(cudaMemcpyAsync(c->blabels, labels, rows * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+  HB_CUDA(h2d_copy(c->blabels, labels, rows * sizeof(int64_t), c->stream));
   return do_step(c, c->batch, 0, rows, eta, flags, out_loss);
 }
 
@@ -2102,20 +2634,20 @@ int hb_train_step_host_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col,
   cudaStream_t st = c->stream;
   if (nnz > 0 && is_pinned(rowptr) && is_pinned(labels) && is_pinned(col) && is_pinned(val)) {
     // page-locked batch: DMA straight from the caller's arrays
-    HB_CUDA(cudaMemcpyAsync(c->browptr, rowptr, b_rowptr, cudaMemcpyHostToDevice, st));
-    HB_CUDA(cudaMemcpyAsync(c->blabels, labels, b_lab, cudaMemcpyHostToDevice, st));
-    HB_CUDA(cudaMemcpyAsync(c->bcol, col, b_i32, cudaMemcpyHostToDevice, st));
-    HB_CUDA(cudaMemcpyAsync(c->bval, val, b_f32, cudaMemcpyHostToDevice, st));
+    HB_CUDA(h2d_copy(c->browptr, rowptr, b_rowptr, st));
+    HB_CUDA(h2d_copy(c->blabels, labels, b_lab, st));
+    HB_CUDA(h2d_copy(c->bcol, col, b_i32, st));
+    HB_CUDA(h2d_copy(c->bval, val, b_f32, st));
   } else {
     std::memcpy(p, rowptr, b_rowptr);
     std::memcpy(p_lab, labels, b_lab);
     std::memcpy(p_col, col, b_i32);
     std::memcpy(p_val, val, b_f32);
-    HB_CUDA(cudaMemcpyAsync(c->browptr, p, b_rowptr, cudaMemcpyHostToDevice, st));
-    HB_CUDA(cudaMemcpyAsync(c->blabels, p_lab, b_lab, cudaMemcpyHostToDevice, st));
+    HB_CUDA(h2d_copy(c->browptr, p, b_rowptr, st));
+    HB_CUDA(h2d_copy(c->blabels, p_lab, b_lab, st));
     if (nnz > 0) {
-      HB_CUDA(cudaMemcpyAsync(c->bcol, p_col, b_i32, cudaMemcpyHostToDevice, st));
-      HB_CUDA(cudaMemcpyAsync(c->bval, p_val, b_f32, cudaMemcpyHostToDevice, st));
+      HB_CUDA(h2d_copy(c->bcol, p_col, b_i32, st));
+      HB_CUDA(h2d_copy(c->bval, p_val, b_f32, st));
     }
   }
   if (!c->sparse) {
@@ -2170,10 +2702,10 @@ int hb_train_step_host_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col,
     if (dev_csc) return HB_OK;
     build_csc_into(rowptr, col, val, rows, c->d[0], reinterpret_cast<int64_t*>(p_colptr),
                    reinterpret_cast<int32_t*>(p_rowidx), reinterpret_cast<float*>(p_cval), c->h_colptr);
-    HB_CUDA(cudaMemcpyAsync(c->bcolptr, p_colptr, b_colptr, cudaMemcpyHostToDevice, st));
+    HB_CUDA(h2d_copy(c->bcolptr, p_colptr, b_colptr, st));
     if (nnz > 0) {
-      HB_CUDA(cudaMemcpyAsync(c->browidx, p_rowidx, b_i32, cudaMemcpyHostToDevice, st));
-      HB_CUDA(cudaMemcpyAsync(c->bcval, p_cval, b_f32, cudaMemcpyHostToDevice, st));
+      HB_CUDA(h2d_copy(c->browidx, p_rowidx, b_i32, st));
+      HB_CUDA(h2d_copy(c->bcval, p_cval, b_f32, st));
     }
     return HB_OK;
   };

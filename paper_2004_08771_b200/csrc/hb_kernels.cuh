@@ -23,6 +23,7 @@ struct DevStep {
   long long start;
   float eta;
   int pad;
+  double eta64;  // the merge's learning rate at the reference's float64 precision
 };
 __device__ __forceinline__ long long step_start(const DevStep* ds, long long s) { return ds ? ds->start : s; }
 __device__ __forceinline__ float step_eta(const DevStep* ds, float e) { return ds ? ds->eta : e; }
@@ -986,13 +987,16 @@ __global__ void f32_to_f64_kernel(double* dst, long long ldd, const float* src, 
 // w_host[r, c] += -eta * g[r, c] (g transposed for the sparse first layer),
 // float64, one aligned 8-byte store per element.
 __global__ void merge_host_f64_kernel(double* w_host, const float* g, long long ldg, int rows, int cols,
-                                      int transposed, double eta) {
+                                      int transposed, double eta, const DevStep* ds = nullptr) {
+  if (ds != nullptr) eta = ds->eta64;
   const long long total = static_cast<long long>(rows) * cols;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long r = i / cols, c = i % cols;
     const float gv = transposed ? g[c * ldg + r] : g[r * ldg + c];
-    w_host[i] += -eta * static_cast<double>(gv);
+    // np.add(target, scale*source, out=target): product and sum rounded
+    // separately (no FMA contraction), exactly as NumPy evaluates it
+    w_host[i] = __dadd_rn(w_host[i], __dmul_rn(-eta, static_cast<double>(gv)));
   }
 }
 
@@ -1007,6 +1011,19 @@ __global__ void transpose_f32_kernel(float* dst, const float* src, long long lds
 }
 
 // lo (rows, cols, ld) = x - trunc_tf32(x): the 3xTF32 twin of a staged input.
+// dst (rows, cols) with row stride ld <- contiguous src (rows, cols); lo twin too
+__global__ void repitch_split_kernel(const float* __restrict__ src, float* __restrict__ dst, float* __restrict__ lo,
+                                     long long ld, long long rows, int cols) {
+  const long long total = rows * cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / cols, c = i % cols;
+    const float v = src[i];
+    dst[r * ld + c] = v;
+    if (lo != nullptr) lo[r * ld + c] = tf32_lo(v);
+  }
+}
+
 __global__ void split_lo_kernel(const float* x, float* lo, long long ld, long long rows, int cols) {
   const long long total = rows * cols;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;

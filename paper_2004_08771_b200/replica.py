@@ -214,6 +214,53 @@ class GpuReplica:
                                                        N.ptr(y, C.c_int64), x.shape[0], float(eta), flags, lp))
         return loss.value if want_loss else None
 
+    # ------------------------------------------- fused drop-in replica step
+    def _model_table(self, weights):
+        """Pointer table of the shared host model (Model layout, nn.py:75),
+        page-locked on first use (it is exchanged every call)."""
+        if len(weights) != self.depth:
+            raise ValueError("weight count does not match architecture")
+        for l, w in enumerate(weights):
+            if not (isinstance(w, np.ndarray) and w.flags.c_contiguous and w.dtype == np.float64):
+                raise ValueError("host weights must be C-contiguous float64 (Model layout, nn.py:75)")
+            if w.shape != (self.sizes[l + 1], self.sizes[l]):
+                raise ValueError(f"weights[{l}] has shape {w.shape}, expected {(self.sizes[l + 1], self.sizes[l])}")
+        self.pin_host(weights)
+        return (C.POINTER(C.c_double) * self.depth)(*[N.ptr(w, C.c_double) for w in weights])
+
+    def replica_step(self, weights, start: int, rows: int, eta: float, timed: bool = False,
+                     want_loss: bool = False):
+        """execute_batch_replica (workers.py:126-138) on staged rows in one call:
+        snapshot of the shared float64 `weights`, the step, and the stale merge
+        weights[l] -= eta * g_l, with the snapshot / merge DMAs overlapped with
+        the compute layer by layer.  Returns the batch's mean loss if want_loss."""
+        table = self._model_table(weights)
+        flags = N.HB_STEP_TIMED if timed else 0
+        loss = C.c_double(0.0)
+        N.check(self._lib.hb_replica_step(self._h, table, int(start), int(rows), float(eta), flags,
+                                          C.byref(loss) if want_loss else None))
+        return loss.value if want_loss else None
+
+    def replica_step_host(self, weights, batch, labels, eta: float, timed: bool = False, want_loss: bool = True):
+        """replica_step on a batch held in host memory (float32 rows or a CsrDataset)."""
+        table = self._model_table(weights)
+        flags = N.HB_STEP_TIMED if timed else 0
+        loss = C.c_double(0.0)
+        lp = C.byref(loss) if want_loss else None
+        if isinstance(batch, CsrDataset):
+            val32 = batch.val if batch.val.dtype == np.float32 else np.ascontiguousarray(batch.val, dtype=np.float32)
+            y = batch.labels if labels is None else np.ascontiguousarray(labels, dtype=np.int64)
+            N.check(self._lib.hb_replica_step_host_csr(self._h, table, N.ptr(batch.rowptr, C.c_int64),
+                                                       N.ptr(batch.col, C.c_int32), N.ptr(val32, C.c_float),
+                                                       N.ptr(y, C.c_int64), batch.n_examples, float(eta), flags, lp))
+        else:
+            x = batch if (batch.dtype == np.float32 and batch.strides[1] == 4) else np.ascontiguousarray(
+                batch, dtype=np.float32)
+            y = np.ascontiguousarray(labels, dtype=np.int64)
+            N.check(self._lib.hb_replica_step_host_dense(self._h, table, N.ptr(x, C.c_float), x.strides[0] // 4,
+                                                         N.ptr(y, C.c_int64), x.shape[0], float(eta), flags, lp))
+        return loss.value if want_loss else None
+
     def eval_loss_sum(self, start: int, rows: int) -> float:
         """Sum of per-example cross-entropy over staged rows (loss_sum, nn.py:139-146)."""
         out = C.c_double(0.0)

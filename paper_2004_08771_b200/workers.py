@@ -136,10 +136,9 @@ def execute_gpu_replica(model, batch, eta: float, speed_factor: float = 0.0) -> 
     sparse = isinstance(batch, CsrBatchRef)
     ctx = _replica(sizes, batch.length, sparse, "train")
     _stage_for(ctx, batch)
-    ctx.pin_host(model.weights)  # the shared model is exchanged every call: page-lock it once
-    ctx.set_weights(model.weights)
-    ctx.step(batch.start, batch.length, eta, emit_grad=True, timed=True)
-    ctx.merge_grads_into(model.weights, eta)
+    # snapshot, step and stale merge in one call; the shared model is
+    # page-locked once and its DMAs overlap the compute layer by layer
+    ctx.replica_step(model.weights, batch.start, batch.length, eta, timed=True)
     _tls.last_device_ms = ctx.last_step_ms
     if speed_factor > 0:
         time.sleep(speed_factor * (time.perf_counter() - start_t))

@@ -254,3 +254,86 @@ def test_sequential_curves_match_reference(hb):
         rel = np.abs(curve - r["curve"]) / np.abs(r["curve"])
         assert rel.max() <= CURVE_TOL, (r["name"], rel.max())
         assert res.examples == r["epochs"] * r["x"].shape[0]
+
+
+@pytest.mark.parametrize("kind", ["dense", "csr_densified", "csr_kernels", "wide_head"])
+def test_fused_replica_step_equals_three_calls(hb, kind):
+    """hb_replica_step* (snapshot, step and stale merge in one call, with the
+    exchange overlapped layer by layer) gives bit-identical host models to the
+    three separate calls set_weights / step / merge_grads_into, on every call
+    (the first eager, later ones replayed from the captured graph), and keeps
+    the stale-merge semantics of workers.py:126-138 when the host model moves
+    between calls (another writer)."""
+    sizes = {"dense": (54, 128, 128, 2), "csr_densified": (300, 256, 128, 2),
+             "csr_kernels": (600, 256, 128, 2), "wide_head": (40, 96, 70)}[kind]
+    sparse = kind.startswith("csr")
+    n, b = 640, 160
+    w0 = ref_nn.init_weights(sizes, 5)
+    if sparse:
+        data = hb.synthetic_csr(n, sizes[0], 9, sizes[-1], seed=6)
+        data.val = data.val.astype(np.float32)
+        batches = [(data.rows(i * b, (i + 1) * b), None) for i in range(n // b)]
+    else:
+        x, y = ref_nn.synthetic_blobs(n, sizes[0], sizes[-1], 2.5, 7)
+        x = x.astype(np.float32)
+        batches = [(x[i * b:(i + 1) * b], y[i * b:(i + 1) * b]) for i in range(n // b)]
+    fused = hb.GpuReplica(sizes, b, sparse=sparse, sparse_kernels=(kind == "csr_kernels"))
+    three = hb.GpuReplica(sizes, b, sparse=sparse, sparse_kernels=(kind == "csr_kernels"))
+    wf = [a.copy() for a in w0]
+    wt = [a.copy() for a in w0]
+    rng = np.random.default_rng(8)
+    try:
+        for it in range(6):
+            xb, yb = batches[it % len(batches)]
+            eta = 0.3 + 0.05 * it
+            lf = fused.replica_step_host(wf, xb, yb, eta)
+            three.set_weights(wt)
+            lt = three.step_host(xb, yb, eta, emit_grad=True)
+            three.merge_grads_into(wt, eta)
+            assert lf == lt
+            for a, c in zip(wf, wt):
+                assert np.array_equal(a, c), it
+            if it == 3:  # another writer moves the shared model between calls
+                for a, c in zip(wf, wt):
+                    d = rng.standard_normal(a.shape) * 1e-3
+                    a += d
+                    c += d
+        # the staged form against the oracle's execute_batch_replica
+        if not sparse:
+            ctx = hb.GpuReplica(sizes, b)
+            ctx.stage(x, y)
+            w = [a.copy() for a in w0]
+            for it in range(3):
+                snap = [a.copy() for a in w]
+                ctx.replica_step(w, it * b, b, 0.2)
+                g = ref_nn.backward(snap, ref_nn.forward(snap, x[it * b:(it + 1) * b].astype(np.float64)),
+                                    y[it * b:(it + 1) * b])
+                assert max_relative_error(w, [s - 0.2 * a for s, a in zip(snap, g)]) <= STEP_TOL
+            ctx.close()
+    finally:
+        fused.close()
+        three.close()
+
+
+def test_stage_array_straddling_a_pinned_view(hb):
+    """A staged array whose head was page-locked earlier as a view (e.g. a
+    pinned batch of the same epoch) still stages and trains identically."""
+    sizes = (300, 64, 2)
+    data = hb.synthetic_csr(1024, 300, 9, 2, seed=11)
+    data.val = data.val.astype(np.float32)
+    w = ref_nn.init_weights(sizes, 3)
+    a = hb.GpuReplica(sizes, 256, sparse=True)
+    b = hb.GpuReplica(sizes, 256, sparse=True)
+    try:
+        head = data.rows(0, 256)
+        a.pin_host([data.col[:head.nnz], data.val[:head.nnz], data.labels[:256]])
+        a.stage(data)
+        b.stage(hb.synthetic_csr(1024, 300, 9, 2, seed=11))
+        for ctx in (a, b):
+            ctx.set_weights(w)
+            ctx.step(256, 256, 0.5, emit_grad=True)
+        for ga, gb in zip(a.grads(), b.grads()):
+            assert np.array_equal(ga, gb)
+    finally:
+        a.close()
+        b.close()

@@ -112,6 +112,30 @@ int make_map(CUtensorMap* m, const float* base, long long inner, long long rows,
 std::mutex g_host_mu;
 std::map<uintptr_t, std::pair<size_t, void*>> g_host_ranges;  // host base -> (bytes, device alias)
 
+// ------------------------------------------------ programmatic dependent launch
+// Every kernel of the step is launched with programmatic stream serialization
+// (HB_NO_PDL=1 turns it off): it may be scheduled while its predecessor
+// finishes and waits in-kernel (pdl_wait) before touching step buffers, which
+// hides the launch gap and the setup (barriers, TMEM, descriptor prefetch).
+bool pdl_enabled() {
+  static const bool on = !(getenv("HB_NO_PDL") && getenv("HB_NO_PDL")[0] == '1');
+  return on;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ------------------------------------------------------------ GEMM launch
 constexpr int kTileSyncTiles = 4096;
 int g_trace_launch_no = 0;  // HB_TRACE builds: index of the GEMM launch being issued
@@ -147,13 +171,15 @@ int launch_gemm_t(const Operand& ta, const Operand& tb, const GemmArgs& a, int m
   cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cm;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaError_t le = cudaLaunchKernelEx(&cfg, kern, *ta.hi, *tb.hi, *ta.lo, *tb.lo, a);
   if (le != cudaSuccess)
     return fail(HB_ECUDA, "gemm launch failed: %s (BN=%d pair=%d passes=%d grid=%d,%d,%d smem=%d)",
@@ -796,10 +822,10 @@ int xchg_use(hb_ctx* c, int l) {
   const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 4096));
   const double* src = c->stage_all + layer_offset(c, l);
   if (l == 0 && c->sparse)
-    f64_to_f32_kernel<true><<<blocks, 256, 0, c->stream>>>(c->W[0], c->ldw[0], src, cols, rows, cols, nullptr);
+    HB_CUDA(launch_k(f64_to_f32_kernel<true>, dim3(blocks), dim3(256), 0, c->stream, c->W[0], c->ldw[0], src, cols, rows, cols, nullptr));
   else
-    f64_to_f32_kernel<false><<<blocks, 256, 0, c->stream>>>(c->W[l], c->ldw[l], src, cols, rows, cols,
-                                                            c->need_lo() ? c->W_lo[l] : nullptr);
+    HB_CUDA(launch_k(f64_to_f32_kernel<false>, dim3(blocks), dim3(256), 0, c->stream, c->W[l], c->ldw[l], src, cols, rows, cols,
+                                                            c->need_lo() ? c->W_lo[l] : nullptr));
   HB_CUDA(cudaGetLastError());
   c->last_launches++;
   return HB_OK;
@@ -935,13 +961,13 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
         const int col_slices = cdiv(c->d[1], kSpmmSliceCols);
         const int row_blocks = std::max(1, std::min(cdiv(rows, 16), 148 / std::max(1, col_slices)));
         const int rpb = cdiv(rows, row_blocks);
-        spmm_sigmoid_smem_kernel<<<dim3(col_slices, cdiv(rows, rpb)), 512, slice_smem, st>>>(p, rpb);
+        HB_CUDA(launch_k(spmm_sigmoid_smem_kernel, dim3(dim3(col_slices, cdiv(rows, rpb))), dim3(512), slice_smem, st, p, rpb));
       } else {
         const int blocks = cdiv(static_cast<long long>(rows) * 32, 256);
         if (c->d[1] % 128 == 0)
-          spmm_sigmoid_kernel<true><<<blocks, 256, 0, st>>>(p);
+          HB_CUDA(launch_k(spmm_sigmoid_kernel<true>, dim3(blocks), dim3(256), 0, st, p));
         else
-          spmm_sigmoid_kernel<false><<<blocks, 256, 0, st>>>(p);
+          HB_CUDA(launch_k(spmm_sigmoid_kernel<false>, dim3(blocks), dim3(256), 0, st, p));
       }
       HB_CUDA(cudaGetLastError());
       prof_end(c, "spmm_sigmoid", 0);
@@ -1009,8 +1035,8 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     h.rows_per_block = cdiv(passes_total, grid) * kHeadRowsPerBlock;
     const int threads = kHeadWarps * 32;
     prof_begin(c, "head_small", l);
-#define HB_HEAD(NCT_, MAXT_) head_small_kernel<NCT_, MAXT_><<<grid, threads, 0, st>>>(h)
-#define HB_HEADV(NCT_, VPL_) head_small_vec_kernel<NCT_, VPL_><<<grid, threads, 0, st>>>(h)
+#define HB_HEAD(NCT_, MAXT_) HB_CUDA(launch_k(head_small_kernel<NCT_, MAXT_>, dim3(grid), dim3(threads), 0, st, h))
+#define HB_HEADV(NCT_, VPL_) HB_CUDA(launch_k(head_small_vec_kernel<NCT_, VPL_>, dim3(grid), dim3(threads), 0, st, h))
     if (vec) {
       const int vpl = h.d <= 256 ? 2 : (h.d <= 512 ? 4 : 8);
       if (c->head_nct == 2) {
@@ -1037,16 +1063,16 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
 #undef HB_HEADV
     HB_CUDA(cudaGetLastError());
     prof_end(c, "head_small", l);
-    loss_reduce_kernel<<<1, 32, 0, st>>>(c->ws_loss, grid, c->d_loss, 0);
+    HB_CUDA(launch_k(loss_reduce_kernel, dim3(1), dim3(32), 0, st, c->ws_loss, grid, c->d_loss, 0));
     HB_CUDA(cudaGetLastError());
     c->last_launches += 2;
     if (train) {
       const long long n = static_cast<long long>(c->d[L]) * c->d[l];
       prof_begin(c, "reduce_sgd", l);
-      reduce_sgd_kernel<<<cdiv(n, 32), 256, 0, st>>>(c->W[l], c->ldw[l], c->ws, grid, n, c->d[L], c->d[l],
+      HB_CUDA(launch_k(reduce_sgd_kernel, dim3(cdiv(n, 32)), dim3(256), 0, st, c->W[l], c->ldw[l], c->ws, grid, n, c->d[L], c->d[l],
                                                      static_cast<float>(eta),
                                                      (flags & HB_STEP_EMIT_GRAD) ? c->G[l] : nullptr, c->d[l], ds,
-                                                     c->need_lo() ? c->W_lo[l] : nullptr);
+                                                     c->need_lo() ? c->W_lo[l] : nullptr));
       HB_CUDA(cudaGetLastError());
       prof_end(c, "reduce_sgd", l);
       c->last_launches++;
@@ -1074,10 +1100,10 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
                  zrows, inv_n, train ? 1 : 0, c->ws_loss};
   const int grid = cdiv(std::max(rows, zrows), 8);
   prof_begin(c, "softmax_delta", l);
-  softmax_delta_kernel<<<grid, 256, 0, st>>>(sm);
+  HB_CUDA(launch_k(softmax_delta_kernel, dim3(grid), dim3(256), 0, st, sm));
   HB_CUDA(cudaGetLastError());
   prof_end(c, "softmax_delta", l);
-  loss_reduce_kernel<<<1, 32, 0, st>>>(c->ws_loss, grid, c->d_loss, 0);
+  HB_CUDA(launch_k(loss_reduce_kernel, dim3(1), dim3(32), 0, st, c->ws_loss, grid, c->d_loss, 0));
   HB_CUDA(cudaGetLastError());
   c->last_launches += 3;
   return HB_OK;
@@ -1130,35 +1156,35 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
                                        200 * 1024));
           configured = true;
         }
-        sparse_dw_smem_kernel<<<dim3(col_slices, row_blocks), 512, c->sdw_smem, st>>>(q);
+        HB_CUDA(launch_k(sparse_dw_smem_kernel, dim3(dim3(col_slices, row_blocks)), dim3(512), c->sdw_smem, st, q));
         HB_CUDA(cudaGetLastError());
         const long long slab = static_cast<long long>(c->d[0]) * c->d[1];
         if (c->d[1] % 4 == 0 && (slab / 4) >= 148 * 256)
-          reduce_sgd_vec_kernel<<<static_cast<int>(std::min<long long>(cdiv(slab / 4, 256), 148 * 8)), 256, 0, st>>>(
+          HB_CUDA(launch_k(reduce_sgd_vec_kernel, dim3(static_cast<int>(std::min<long long>(cdiv(slab / 4, 256), 148 * 8))), dim3(256), 0, st, 
               c->W[0], c->ldw[0], c->ws, row_blocks, slab, c->d[0], c->d[1], static_cast<float>(eta),
-              emit ? c->G[0] : nullptr, c->ldw[0], ds, nullptr);
+              emit ? c->G[0] : nullptr, c->ldw[0], ds, nullptr));
         else
-          reduce_sgd_kernel<<<cdiv(slab, 32), 256, 0, st>>>(c->W[0], c->ldw[0], c->ws, row_blocks, slab, c->d[0],
+          HB_CUDA(launch_k(reduce_sgd_kernel, dim3(cdiv(slab, 32)), dim3(256), 0, st, c->W[0], c->ldw[0], c->ws, row_blocks, slab, c->d[0],
                                                             c->d[1], static_cast<float>(eta),
-                                                            emit ? c->G[0] : nullptr, c->ldw[0], ds, nullptr);
+                                                            emit ? c->G[0] : nullptr, c->ldw[0], ds, nullptr));
         HB_CUDA(cudaGetLastError());
         prof_end(c, "sparse_dw_sgd", 0);
         c->last_launches += 2;
         HB_TRY(xchg_merge(c, 0, eta, ds));
         continue;
       }
-      csc_batch_ranges_kernel<<<cdiv(c->d[0], 256), 256, 0, st>>>(v.colptr, v.rowidx, c->d[0], start, rows, ds,
-                                                                  c->csc_lo, c->csc_hi);
+      HB_CUDA(launch_k(csc_batch_ranges_kernel, dim3(cdiv(c->d[0], 256)), dim3(256), 0, st, v.colptr, v.rowidx, c->d[0], start, rows, ds,
+                                                                  c->csc_lo, c->csc_hi));
       // batch entries per feature decide the parallelisation
       const double per_feature = static_cast<double>(rows) * c->nnz_per_row / std::max(1, c->d[0]);
       if (per_feature < 48.0 && c->d[1] % 4 == 0) {
-        sparse_dw_warp_kernel<<<cdiv(static_cast<long long>(c->d[0]) * 32, 256), 256, 0, st>>>(p);
+        HB_CUDA(launch_k(sparse_dw_warp_kernel, dim3(cdiv(static_cast<long long>(c->d[0]) * 32, 256)), dim3(256), 0, st, p));
       } else {
         const dim3 blocks(c->d[0], cdiv(c->d[1], 128));
         if (c->d[1] % 4 == 0)
-          sparse_dw_kernel<true><<<blocks, 256, 0, st>>>(p);
+          HB_CUDA(launch_k(sparse_dw_kernel<true>, dim3(blocks), dim3(256), 0, st, p));
         else
-          sparse_dw_kernel<false><<<blocks, 256, 0, st>>>(p);
+          HB_CUDA(launch_k(sparse_dw_kernel<false>, dim3(blocks), dim3(256), 0, st, p));
       }
       HB_CUDA(cudaGetLastError());
       c->last_launches++;
@@ -1218,13 +1244,13 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       prof_end(c, "gemm_dw_partial", l);
       prof_begin(c, "reduce_sgd", l);
       if (a.N % 4 == 0 && c->ldw[l] % 4 == 0 && (slab / 4) >= 148 * 256)
-        reduce_sgd_vec_kernel<<<static_cast<int>(std::min<long long>(cdiv(slab / 4, 256), 148 * 8)), 256, 0, st>>>(
+        HB_CUDA(launch_k(reduce_sgd_vec_kernel, dim3(static_cast<int>(std::min<long long>(cdiv(slab / 4, 256), 148 * 8))), dim3(256), 0, st, 
             c->W[l], c->ldw[l], c->ws, splits, slab, a.M, a.N, static_cast<float>(eta), emit ? c->G[l] : nullptr,
-            c->d[l], ds, c->need_lo() ? c->W_lo[l] : nullptr);
+            c->d[l], ds, c->need_lo() ? c->W_lo[l] : nullptr));
       else
-        reduce_sgd_kernel<<<cdiv(slab, 32), 256, 0, st>>>(c->W[l], c->ldw[l], c->ws, splits, slab, a.M, a.N,
+        HB_CUDA(launch_k(reduce_sgd_kernel, dim3(cdiv(slab, 32)), dim3(256), 0, st, c->W[l], c->ldw[l], c->ws, splits, slab, a.M, a.N,
                                                           static_cast<float>(eta), emit ? c->G[l] : nullptr, c->d[l],
-                                                          ds, c->need_lo() ? c->W_lo[l] : nullptr);
+                                                          ds, c->need_lo() ? c->W_lo[l] : nullptr));
       HB_CUDA(cudaGetLastError());
       prof_end(c, "reduce_sgd", l);
       c->last_launches += 2;

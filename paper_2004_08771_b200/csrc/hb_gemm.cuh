@@ -216,6 +216,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
   tc_fence_after();
   if (threadIdx.x == 0) HB_CTA_STAMP(1);
   const uint32_t tmem_base = *tmem_slot;
+  // everything above is independent of the previous kernel's output (PDL)
+  pdl_wait();
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
@@ -329,6 +331,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
     };
     load_pre(32 * half, pre);
     mbar_wait(tmem_full, 0);
+    if (threadIdx.x == 128) pdl_trigger();  // mainloop done: the next kernel may start its setup
     if (threadIdx.x == 128) HB_STAMP(6 * 512 + 0);  // epilogue start
     if (threadIdx.x == 128) HB_CTA_STAMP(2);
     tc_fence_after();

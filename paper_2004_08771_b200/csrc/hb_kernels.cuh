@@ -77,6 +77,8 @@ struct HeadArgs {
 
 template <int NCT, int MAXT>
 __global__ void __launch_bounds__(kHeadWarps * 32, (MAXT <= 16 && NCT <= 2) ? 2 : 1) head_small_kernel(HeadArgs p) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float sW[NCT * 32 * MAXT];
   {
     const long long st = step_start(p.ds, p.start);
@@ -206,6 +208,8 @@ __global__ void __launch_bounds__(kHeadWarps * 32, (MAXT <= 16 && NCT <= 2) ? 2 
 // fixed reduction order (per-warp row order, then warps in order).
 template <int NCT, int VPL>
 __global__ void __launch_bounds__(kHeadWarps * 32) head_small_vec_kernel(HeadArgs p) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ __align__(16) float sW[NCT * 128 * VPL];
   {
     const long long st = step_start(p.ds, p.start);
@@ -376,6 +380,8 @@ struct SoftmaxArgs {
 };
 
 __global__ void __launch_bounds__(256) softmax_delta_kernel(SoftmaxArgs p) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double sLoss[8];
   p.labels += step_start(p.ds, p.start);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -421,6 +427,8 @@ __global__ void __launch_bounds__(256) softmax_delta_kernel(SoftmaxArgs p) {
 // Fixed-order sum of per-block loss partials: one warp, lane-strided partial
 // sums then a fixed shuffle tree (deterministic).
 __global__ void loss_reduce_kernel(const double* ws, int n, double* out, int accumulate) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   double s = 0.0;
   for (int i = lane; i < n; i += 32) s += ws[i];
@@ -439,6 +447,8 @@ __global__ void __launch_bounds__(256) reduce_sgd_kernel(float* w, long long ldw
                                                            long long slab, int rows, int cols, float eta,
                                                            float* grad, long long ldg, const DevStep* ds,
                                                            float* w_lo) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[8][33];
   eta = step_eta(ds, eta);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -481,6 +491,8 @@ __global__ void __launch_bounds__(256) reduce_sgd_vec_kernel(float* w, long long
                                                                long long slab, int rows, int cols, float eta,
                                                                float* grad, long long ldg, const DevStep* ds,
                                                                float* w_lo) {
+  pdl_wait();
+  pdl_trigger();
   eta = step_eta(ds, eta);
   const long long quads = static_cast<long long>(rows) * cols / 4;
   for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < quads;
@@ -530,6 +542,8 @@ struct SpmmArgs {
 
 template <bool VEC>
 __global__ void __launch_bounds__(256) spmm_sigmoid_kernel(SpmmArgs p) {
+  pdl_wait();
+  pdl_trigger();
   p.start = step_start(p.ds, p.start);
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -631,6 +645,8 @@ __device__ __forceinline__ int csr_chunk_end(const int64_t* rowptr, long long st
 }
 
 __global__ void __launch_bounds__(512) spmm_sigmoid_smem_kernel(SpmmArgs p, int rows_per_block) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float4 sw4[];  // [d_in][kSpmmSliceCols / 4] then the CSR chunk
   constexpr int Q = kSpmmSliceCols / 4;
   int* s_col = reinterpret_cast<int*>(sw4 + p.ldw_rows * Q);
@@ -710,6 +726,8 @@ struct SparseDwSmemArgs {
 };
 
 __global__ void __launch_bounds__(512) sparse_dw_smem_kernel(SparseDwSmemArgs p) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float sacc[];  // [d_in][kSdwSliceCols]
   constexpr int SW = kSdwSliceCols;
   float* s_d = sacc + p.d_in * SW;                          // [kCsrChunkRows][SW] delta0 tile
@@ -818,6 +836,8 @@ __device__ __forceinline__ long long lower_bound_i32(const int32_t* a, long long
 // W0T[f, chunk] in place (gradient optionally kept).  Fixed summation order.
 template <bool VEC>
 __global__ void __launch_bounds__(256) sparse_dw_kernel(SparseDwArgs p) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[8][128];
   p.start = step_start(p.ds, p.start);
   p.eta = step_eta(p.ds, p.eta);
@@ -894,6 +914,8 @@ __global__ void __launch_bounds__(256) sparse_dw_kernel(SparseDwArgs p) {
 // [start, start+rows): one thread per feature, two binary searches.
 __global__ void csc_batch_ranges_kernel(const int64_t* colptr, const int32_t* rowidx, int d_in, long long start,
                                         int rows, const DevStep* ds, long long* lo_out, long long* hi_out) {
+  pdl_wait();
+  pdl_trigger();
   start = step_start(ds, start);
   for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < d_in; f += gridDim.x * blockDim.x) {
     const long long c0 = colptr[f], c1 = colptr[f + 1];
@@ -908,6 +930,8 @@ __global__ void csc_batch_ranges_kernel(const int64_t* colptr, const int32_t* ro
 // columns (float4 per lane, 1024-column chunks), entries in CSC order.
 // Needs d_out % 4 == 0.
 __global__ void __launch_bounds__(256) sparse_dw_warp_kernel(SparseDwArgs p) {
+  pdl_wait();
+  pdl_trigger();
   p.start = step_start(p.ds, p.start);
   p.eta = step_eta(p.ds, p.eta);
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -963,6 +987,8 @@ __global__ void __launch_bounds__(256) sparse_dw_warp_kernel(SparseDwArgs p) {
 template <bool TRANSPOSE>
 __global__ void f64_to_f32_kernel(float* dst, long long ldd, const double* src, long long lds, int rows, int cols,
                                   float* dst_lo) {
+  pdl_wait();
+  pdl_trigger();
   const long long total = static_cast<long long>(rows) * cols;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {

@@ -203,9 +203,13 @@ int launch_gemm_p(GemmKind kind, int epi, int bn, const Operand& ta, const Opera
   } while (0)
   if (kind == G_FWD) {
     if (epi == EPI_SIGMOID) HB_BN(false, false, EPI_SIGMOID);
+    if (epi == EPI_PARTIAL) HB_BN(false, false, EPI_PARTIAL);
     HB_BN(false, false, EPI_STORE);
   }
-  if (kind == G_DX) HB_BN(false, true, EPI_DSIG);
+  if (kind == G_DX) {
+    if (epi == EPI_PARTIAL) HB_BN(false, true, EPI_PARTIAL);
+    HB_BN(false, true, EPI_DSIG);
+  }
   if (epi == EPI_SGD) HB_BN(true, true, EPI_SGD);
   if (epi == EPI_SPLIT_SGD) HB_BN(true, true, EPI_SPLIT_SGD);
   HB_BN(true, true, EPI_PARTIAL);
@@ -575,6 +579,22 @@ int choose_bn(long long m_tiles, long long n) {
   return 128;
 }
 
+// Split-K plan for a forward / dX GEMM: when its output tiles cannot fill
+// the SMs (small batches, e.g. covtype's b=512 gives 8-16 CTAs) K is split so
+// the launch covers about one wave; splitk_epi_kernel sums the slabs and
+// applies the fused op.  Returns the split count (1 = no split).
+constexpr int kSplitSlabFloats = 148 * kBM * 256;  // bound on S * M * N of any such split
+int fx_plan(const hb_ctx* c, int m_tiles, int n_tiles, int bn, int kb_total, int* kb_per) {
+  *kb_per = kb_total;
+  if (getenv("HB_NO_FX_SPLIT") && getenv("HB_NO_FX_SPLIT")[0] == '1') return 1;
+  const int ctas = (c->passes == 3 && bn >= 64 ? (m_tiles + 1) / 2 * 2 : m_tiles) * n_tiles;
+  if (ctas >= 64 || kb_total < 4) return 1;
+  const int want = std::min(148 / ctas, kb_total / 2);
+  if (want < 2) return 1;
+  *kb_per = cdiv(kb_total, want);
+  return cdiv(kb_total, *kb_per);
+}
+
 // split-K plan for the dW GEMM of layer l at `rows` batch rows
 void dw_plan(const hb_ctx* c, int l, int rows, int* splits, int* kb_per, int* kb_total) {
   const int M = c->d[l + 1], N = c->d[l];
@@ -589,8 +609,6 @@ void dw_plan(const hb_ctx* c, int l, int rows, int* splits, int* kb_per, int* kb
   *splits = cdiv(*kb_total, *kb_per);
 }
 
-// `ds` != null: graph mode -- kernels read the batch start and eta from
-// device memory (the by-value start/eta are then 0 and ignored).
 // debug (HB_DEBUG_XFER=1): host-side phase timings of the host-model exchange
 static bool xfer_debug() {
   static const bool on = getenv("HB_DEBUG_XFER") && getenv("HB_DEBUG_XFER")[0] == '1';
@@ -612,6 +630,37 @@ static void xmark(const char* what, int l = -1) {
   if (!xfer_debug()) return;
   const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - g_call_t0).count();
   fprintf(stderr, "[xfer] %8.1f us  %s %d\n", us, what, l);
+}
+
+// split-K forward / dX: partial slabs into c->ws, then the fused finish
+int launch_fx_split(hb_ctx* c, GemmKind kind, int mode, int bn, const Operand& ta, const Operand& tb, GemmArgs a,
+                    int m_tiles, int n_tiles, int splits, int kb_per, cudaStream_t st) {
+  float* out = a.out;
+  float* out_lo = a.out_lo;
+  const long long ldo = a.ldo;
+  a.out = c->ws;
+  a.out_lo = nullptr;
+  a.ldo = a.N;
+  a.split_stride = static_cast<long long>(a.M) * a.N;
+  a.kb_per_split = kb_per;
+  HB_TRY(launch_gemm(c->passes, kind, EPI_PARTIAL, bn, ta, tb, a, m_tiles, n_tiles, splits, st));
+  const bool vec = (a.N % 4 == 0) && (ldo % 4 == 0);
+  const int rows_total = mode == SPLIT_DSIG ? std::max(a.M, a.m_zero_rows) : a.M;
+  const long long items = static_cast<long long>(rows_total) * (vec ? a.N / 4 : a.N);
+  const dim3 grid(static_cast<int>(std::min<long long>(cdiv(items, 256), 148 * 8)));
+#define HB_SE(MODE_, VEC_)                                                                                  \
+  HB_CUDA(launch_k(splitk_epi_kernel<MODE_, VEC_>, grid, dim3(256), 0, st, out, out_lo, ldo, c->ws, splits, a.M, \
+                   a.N, a.aux, a.ld_aux, a.m_zero_rows))
+  if (mode == SPLIT_SIGMOID) {
+    if (vec) HB_SE(SPLIT_SIGMOID, true); else HB_SE(SPLIT_SIGMOID, false);
+  } else if (mode == SPLIT_STORE) {
+    if (vec) HB_SE(SPLIT_STORE, true); else HB_SE(SPLIT_STORE, false);
+  } else {
+    if (vec) HB_SE(SPLIT_DSIG, true); else HB_SE(SPLIT_DSIG, false);
+  }
+#undef HB_SE
+  c->last_launches++;
+  return HB_OK;
 }
 
 // ---------------------------------------------- overlapped host-model exchange
@@ -935,6 +984,8 @@ int xchg_end(hb_ctx* c) {
   return HB_OK;
 }
 
+// `ds` != null: graph mode -- kernels read the batch start and eta from
+// device memory (the by-value start/eta are then 0 and ignored).
 int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool train, uint32_t flags, double eta,
                 const DevStep* ds) {
   cudaStream_t st = c->stream;
@@ -989,8 +1040,14 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     a.ldo = c->ld[l + 1];
     const Operand ta = l == 0 ? v.fwd() : c->opA_k(l);
     prof_begin(c, "gemm_fwd_sigmoid", l);
-    HB_TRY(launch_gemm(c->passes, G_FWD, EPI_SIGMOID, c->bn_fwd[l], ta, c->opW_k(l), a, m_tiles,
-                       cdiv(a.N, c->bn_fwd[l]), 1, st));
+    int kb_per = a.kb_total;
+    const int fsplit = fx_plan(c, m_tiles, cdiv(a.N, c->bn_fwd[l]), c->bn_fwd[l], a.kb_total, &kb_per);
+    if (fsplit > 1)
+      HB_TRY(launch_fx_split(c, G_FWD, SPLIT_SIGMOID, c->bn_fwd[l], ta, c->opW_k(l), a, m_tiles,
+                             cdiv(a.N, c->bn_fwd[l]), fsplit, kb_per, st));
+    else
+      HB_TRY(launch_gemm(c->passes, G_FWD, EPI_SIGMOID, c->bn_fwd[l], ta, c->opW_k(l), a, m_tiles,
+                         cdiv(a.N, c->bn_fwd[l]), 1, st));
     prof_end(c, "gemm_fwd_sigmoid", l);
     c->last_launches++;
   }
@@ -1093,8 +1150,16 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   a.ldo = c->ld[L];
   const Operand ta = l == 0 ? v.fwd() : c->opA_k(l);
   prof_begin(c, "gemm_fwd_logits", l);
-  HB_TRY(launch_gemm(c->passes, G_FWD, EPI_STORE, c->bn_fwd[l], ta, c->opW_k(l), a, m_tiles, cdiv(a.N, c->bn_fwd[l]),
-                     1, st));
+  {
+    int kb_per = a.kb_total;
+    const int fsplit = fx_plan(c, m_tiles, cdiv(a.N, c->bn_fwd[l]), c->bn_fwd[l], a.kb_total, &kb_per);
+    if (fsplit > 1)
+      HB_TRY(launch_fx_split(c, G_FWD, SPLIT_STORE, c->bn_fwd[l], ta, c->opW_k(l), a, m_tiles,
+                             cdiv(a.N, c->bn_fwd[l]), fsplit, kb_per, st));
+    else
+      HB_TRY(launch_gemm(c->passes, G_FWD, EPI_STORE, c->bn_fwd[l], ta, c->opW_k(l), a, m_tiles,
+                         cdiv(a.N, c->bn_fwd[l]), 1, st));
+  }
   prof_end(c, "gemm_fwd_logits", l);
   SoftmaxArgs sm{c->D[l], c->need_lo() ? c->D_lo[l] : nullptr, c->ld[L], v.labels, start, ds, rows, c->d[L],
                  zrows, inv_n, train ? 1 : 0, c->ws_loss};
@@ -1133,8 +1198,14 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       a.ld_aux = c->ld[l];
       a.ds = ds;
       prof_begin(c, "gemm_dx_dsig", l);
-      HB_TRY(launch_gemm(c->passes, G_DX, EPI_DSIG, c->bn_dx[l], c->opD_k(l), c->opW_mn(l), a,
-                         cdiv(zrows, kBM), cdiv(a.N, c->bn_dx[l]), 1, st));
+      int kb_per = a.kb_total;
+      const int fsplit = fx_plan(c, cdiv(zrows, kBM), cdiv(a.N, c->bn_dx[l]), c->bn_dx[l], a.kb_total, &kb_per);
+      if (fsplit > 1)
+        HB_TRY(launch_fx_split(c, G_DX, SPLIT_DSIG, c->bn_dx[l], c->opD_k(l), c->opW_mn(l), a, cdiv(zrows, kBM),
+                               cdiv(a.N, c->bn_dx[l]), fsplit, kb_per, st));
+      else
+        HB_TRY(launch_gemm(c->passes, G_DX, EPI_DSIG, c->bn_dx[l], c->opD_k(l), c->opW_mn(l), a,
+                           cdiv(zrows, kBM), cdiv(a.N, c->bn_dx[l]), 1, st));
       prof_end(c, "gemm_dx_dsig", l);
       c->last_launches++;
     }
@@ -1641,6 +1712,7 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
     if (splits > 1) ws = std::max(ws, static_cast<size_t>(splits) * c->d[l + 1] * c->d[l]);
   }
   if (c->small_head) ws = std::max(ws, static_cast<size_t>(cdiv(c->cap, kHeadRowsPerBlock)) * nc * dlast);
+  ws = std::max(ws, static_cast<size_t>(kSplitSlabFloats));  // split-K forward / dX slabs
   if (c->sparse) {
     c->sdw_smem = (static_cast<size_t>(c->d[0]) * kSdwSliceCols + static_cast<size_t>(kCsrChunkRows) * kSdwSliceCols) *
                       sizeof(float) +

@@ -52,6 +52,7 @@ __device__ __forceinline__ float warp_max(float v) {
 constexpr int kHeadWarps = 8;
 constexpr int kHeadRowsPerBlock = 16;
 
+
 struct HeadArgs {
   const float* a;          // (rows, d) last hidden activation
   long long lda;
@@ -456,18 +457,18 @@ __global__ void __launch_bounds__(256) reduce_sgd_kernel(float* w, long long ldw
   const long long total = static_cast<long long>(rows) * cols;
   // warp w sums slabs s = w, w+8, w+16, ... as four interleaved chains
   // (fixed order: chain k takes every fourth of the warp's slabs)
+  // (8 independent loads in flight per thread per round)
   float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
   if (i < total) {
-    int s = warp;
-    for (; s + 24 < S; s += 32) {
-      s0 += __ldcs(part + s * slab + i);
-      s1 += __ldcs(part + (s + 8) * slab + i);
-      s2 += __ldcs(part + (s + 16) * slab + i);
-      s3 += __ldcs(part + (s + 24) * slab + i);
+    for (int s = warp; s < S; s += 64) {
+      float t[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t[k] = (s + 8 * k < S) ? __ldcs(part + (s + 8 * k) * slab + i) : 0.f;
+      s0 += t[0] + t[4];
+      s1 += t[1] + t[5];
+      s2 += t[2] + t[6];
+      s3 += t[3] + t[7];
     }
-    if (s < S) s0 += __ldcs(part + s * slab + i);
-    if (s + 8 < S) s1 += __ldcs(part + (s + 8) * slab + i);
-    if (s + 16 < S) s2 += __ldcs(part + (s + 16) * slab + i);
   }
   red[warp][lane] = (s0 + s1) + (s2 + s3);
   __syncthreads();
@@ -498,13 +499,26 @@ __global__ void __launch_bounds__(256) reduce_sgd_vec_kernel(float* w, long long
   for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < quads;
        q += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long i = 4 * q;
-    float4 g = __ldcs(reinterpret_cast<const float4*>(part + i));
-    for (int s = 1; s < S; ++s) {
-      const float4 t = __ldcs(reinterpret_cast<const float4*>(part + s * slab + i));
-      g.x += t.x;
-      g.y += t.y;
-      g.z += t.z;
-      g.w += t.w;
+    // issue the slab loads in batches of 8 independent loads, then sum in
+    // slab order (the latency of one batch instead of S serial loads)
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < S; s0 += 8) {
+      float4 t[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        t[k] = (s0 + k < S) ? __ldcs(reinterpret_cast<const float4*>(part + (s0 + k) * slab + i))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (s0 + k == 0) {
+          g = t[0];
+        } else if (s0 + k < S) {
+          g.x += t[k].x;
+          g.y += t[k].y;
+          g.z += t[k].z;
+          g.w += t[k].w;
+        }
+      }
     }
     const long long r = i / cols, c = i % cols;
     float4* wp = reinterpret_cast<float4*>(w + r * ldw + c);
@@ -1037,6 +1051,79 @@ __global__ void transpose_f32_kernel(float* dst, const float* src, long long lds
 }
 
 // lo (rows, cols, ld) = x - trunc_tf32(x): the 3xTF32 twin of a staged input.
+// Split-K finish of a forward / dX GEMM whose output tile grid is too small
+// to fill the SMs (small batches): out = op(sum_s part[s]) over S slabs in slab
+// order (deterministic), op = sigmoid (forward, linalg.py:48-55), identity
+// (logits) or x * a(1 - a) (dX, linalg.py:58-60); rows [M, zero_rows) of a dX
+// output are written as 0; the lo twin is written when out_lo != null.
+enum SplitEpi : int { SPLIT_SIGMOID = 0, SPLIT_STORE = 1, SPLIT_DSIG = 2 };
+template <int MODE, bool VEC>
+__global__ void __launch_bounds__(256) splitk_epi_kernel(float* __restrict__ out, float* __restrict__ out_lo,
+                                                         long long ldo, const float* __restrict__ part, int S,
+                                                         int M, int N, const float* __restrict__ aux, long long ld_aux,
+                                                         int zero_rows) {
+  pdl_wait();
+  pdl_trigger();
+  const long long slab = static_cast<long long>(M) * N;
+  const int rows_total = MODE == SPLIT_DSIG ? max(M, zero_rows) : M;
+  constexpr int W = VEC ? 4 : 1;
+  const long long items = static_cast<long long>(rows_total) * (N / W);
+  for (long long it = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; it < items;
+       it += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = it / (N / W);
+    const int c = static_cast<int>(it % (N / W)) * W;
+    float v[W];
+    if (r >= M) {
+#pragma unroll
+      for (int k = 0; k < W; ++k) v[k] = 0.f;
+    } else {
+      const float* pp = part + r * N + c;
+      if (VEC) {
+        float4 g = __ldcs(reinterpret_cast<const float4*>(pp));
+        for (int s0 = 1; s0 < S; s0 += 8) {
+          float4 t[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            t[k] = s0 + k < S ? __ldcs(reinterpret_cast<const float4*>(pp + (s0 + k) * slab)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (s0 + k < S) {
+              g.x += t[k].x;
+              g.y += t[k].y;
+              g.z += t[k].z;
+              g.w += t[k].w;
+            }
+        }
+        v[0] = g.x;
+        v[W > 1 ? 1 : 0] = g.y;
+        v[W > 2 ? 2 : 0] = g.z;
+        v[W > 3 ? 3 : 0] = g.w;
+      } else {
+        float g = __ldcs(pp);
+        for (int s = 1; s < S; ++s) g += __ldcs(pp + s * slab);
+        v[0] = g;
+      }
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        if (MODE == SPLIT_SIGMOID) v[k] = sigmoidf_fast(v[k]);
+        if (MODE == SPLIT_DSIG) {
+          const float a = aux[r * ld_aux + c + k];
+          v[k] = v[k] * (a * (1.f - a));
+        }
+      }
+    }
+    float* op = out + r * ldo + c;
+    if (VEC) {
+      const float4 o4 = make_float4(v[0], v[W > 1 ? 1 : 0], v[W > 2 ? 2 : 0], v[W > 3 ? 3 : 0]);
+      *reinterpret_cast<float4*>(op) = o4;
+      if (out_lo != nullptr) *reinterpret_cast<float4*>(out_lo + r * ldo + c) = lo4(o4);
+    } else {
+      op[0] = v[0];
+      if (out_lo != nullptr) out_lo[r * ldo + c] = tf32_lo(v[0]);
+    }
+  }
+}
+
 // dst (rows, cols) with row stride ld <- contiguous src (rows, cols); lo twin too
 __global__ void repitch_split_kernel(const float* __restrict__ src, float* __restrict__ dst, float* __restrict__ lo,
                                      long long ld, long long rows, int cols) {

@@ -145,6 +145,17 @@ def measured_peaks():
     return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
+def ncu_kernel_stats(config, kernel):
+    """Per-launch ncu figures (DRAM / L2 bytes, cold-cache duration) of `kernel`
+    for `config` from the newest profiles/r*_ncu_kernels.json (one `ncu --set
+    full` capture per kernel, scripts/ncu_traffic.sh), or None."""
+    files = sorted(ROOT.glob("profiles/r*_ncu_kernels.json"))
+    if not files:
+        return None, None
+    d = json.loads(files[-1].read_text()).get("kernels", {})
+    return d.get(config, {}).get(kernel), files[-1].name
+
+
 def kernel_work(name, cfg, rows, dw_splits=None):
     """Algorithmic work of one launch of kernel `name` at `rows` batch rows:
     ("tensor", flops) for GEMMs, ("hbm", bytes) for the memory-bound kernels."""
@@ -328,12 +339,14 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         ms, cnt = dom_live[dom]
         bound, work = kernel_work(dom, cfg, b)
         avg_s = ms / cnt / 1000.0
+        ncu, ncu_src = ncu_kernel_stats(args.config, dom)
+        traffic = None if not ncu or "dram_bytes" not in ncu else ncu["dram_bytes"]
         if bound == "tensor":
             tf32 = bf16_peak / 2.0
             peak = tf32 / (3.0 if args.precision == "3xtf32" else 1.0)
             roofline = {"bound": "tensor", "kernel": dom, "achieved": round(work / avg_s / 1e12, 2),
                         "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(work / avg_s / 1e12 / peak, 4),
-                        "traffic": None,
+                        "traffic": traffic,
                         "peak_basis": f"{'3xTF32-effective = ' if args.precision == '3xtf32' else ''}"
                                       f"TF32 dense = bf16/2 of {bf16_peak} TF/s {peak_src}",
                         "work_per_launch": work, "avg_launch_us": round(avg_s * 1e6, 2),
@@ -341,9 +354,17 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         else:
             roofline = {"bound": "hbm", "kernel": dom, "achieved": round(work / avg_s / 1e9, 1),
                         "peak": hbm_peak, "unit": "GB/s", "frac": round(work / avg_s / 1e9 / hbm_peak, 4),
-                        "traffic": None, "peak_basis": peak_src, "work_per_launch": work,
+                        "traffic": traffic, "peak_basis": peak_src, "work_per_launch": work,
                         "avg_launch_us": round(avg_s * 1e6, 2),
                         "timing": "CUDA events around this kernel only, inside the timed region"}
+            if ncu and "l2_bytes" in ncu:
+                # the gather kernels re-read W0^T / delta0 rows once per nonzero: their
+                # real bound is the L2 -> SM gather traffic, not the unique HBM bytes
+                roofline["l2"] = {"bytes_per_launch": ncu["l2_bytes"],
+                                  "achieved_gbs": round(ncu["l2_bytes"] / avg_s / 1e9, 1),
+                                  "ncu_l2_throughput_pct": round(ncu.get("l2_throughput_pct", 0.0), 1)}
+        if roofline is not None and ncu:
+            roofline["traffic_source"] = f"profiles/{ncu_src} ({args.config}/{dom}: dram read+write bytes of one launch)"
     return dict(value=value, total_ms=total_ms, e2e=e2e, roofline=roofline, kernels=kernels,
                 clocks=clocks.summary(), launches=launches, merge_ms=sum(merge_ms))
 

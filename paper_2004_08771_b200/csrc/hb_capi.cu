@@ -15,6 +15,7 @@
 //   sparse L0: CSC-slice gather dW + in-place update of active rows
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <dlfcn.h>
 
 #include <algorithm>
@@ -505,10 +506,21 @@ static void prof_name(char (&name)[64], const char* kind, int layer) {
 }
 // A launch is bracketed when profiling is on and it passes the filter (the
 // bench instruments only the dominant kernel inside its timed region).
+// HB_NVTX=1: every step launch also sits in an NVTX range of the same name, so
+// `ncu --nvtx --nvtx-include "gemm_dx_dsig_l2/"` captures exactly that kernel
+// (eager steps, HB_NO_GRAPHS=1) -- how profiles/ ties traffic to bench names.
+static bool nvtx_on() {
+  static const bool on = getenv("HB_NVTX") && getenv("HB_NVTX")[0] == '1';
+  return on;
+}
 void prof_begin(hb_ctx* c, const char* kind, int layer) {
   c->pending_active = false;
-  if (!c->prof_on) return;
   char name[64];
+  if (nvtx_on()) {
+    prof_name(name, kind, layer);
+    nvtxRangePushA(name);
+  }
+  if (!c->prof_on) return;
   prof_name(name, kind, layer);
   if (!c->prof_filter.empty() && c->prof_filter != name) return;
   cudaEvent_t e0, e1;
@@ -536,6 +548,7 @@ void prof_begin(hb_ctx* c, const char* kind, int layer) {
     cudaEventRecord(e0, c->stream);
 }
 void prof_end(hb_ctx* c, const char* kind, int layer) {
+  if (nvtx_on()) nvtxRangePop();
   if (!c->prof_on || !c->pending_active) return;
   c->pending_active = false;
   if (c->capturing)
@@ -823,7 +836,7 @@ static void host_axpy_f64(double* w, const float* g, size_t n, double eta) {
   const double scale = -eta;
   HostPool& pool = HostPool::get();
   static const int max_parts = getenv("HB_MERGE_PARTS") ? atoi(getenv("HB_MERGE_PARTS")) : 64;
-  static const size_t part_elems = getenv("HB_MERGE_PART_ELEMS") ? atoll(getenv("HB_MERGE_PART_ELEMS")) : (1 << 16);
+  static const size_t part_elems = getenv("HB_MERGE_PART_ELEMS") ? atoll(getenv("HB_MERGE_PART_ELEMS")) : (1 << 15);
   const int parts = static_cast<int>(
       std::min<size_t>(std::min(pool.size(), max_parts), std::max<size_t>(1, n / part_elems)));
   if (xfer_debug()) fprintf(stderr, "[xfer] axpy n=%zu parts=%d pool=%d\n", n, parts, pool.size());

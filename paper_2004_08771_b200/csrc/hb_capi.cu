@@ -1257,8 +1257,12 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
         HB_TRY(xchg_merge(c, 0, eta, ds));
         continue;
       }
-      HB_CUDA(launch_k(csc_batch_ranges_kernel, dim3(cdiv(c->d[0], 256)), dim3(256), 0, st, v.colptr, v.rowidx, c->d[0], start, rows, ds,
-                                                                  c->csc_lo, c->csc_hi));
+      if (v.n_rows > 0 && static_cast<double>(c->e_nnz) / std::max(1, c->d[0]) <= 1024.0)
+        HB_CUDA(launch_k(csc_batch_ranges_warp_kernel, dim3(static_cast<int>(std::min<long long>(cdiv(c->d[0], 8), 148 * 16))),
+                         dim3(256), 0, st, v.colptr, v.rowidx, c->d[0], start, rows, ds, c->csc_lo, c->csc_hi));
+      else
+        HB_CUDA(launch_k(csc_batch_ranges_kernel, dim3(cdiv(c->d[0], 256)), dim3(256), 0, st, v.colptr, v.rowidx,
+                         c->d[0], start, rows, ds, c->csc_lo, c->csc_hi));
       // batch entries per feature decide the parallelisation
       const double per_feature = static_cast<double>(rows) * c->nnz_per_row / std::max(1, c->d[0]);
       if (per_feature < 48.0 && c->d[1] % 4 == 0) {

@@ -926,6 +926,39 @@ __global__ void __launch_bounds__(256) sparse_dw_kernel(SparseDwArgs p) {
 
 // Per-feature slice [lo, hi) of the epoch CSC that falls in the batch rows
 // [start, start+rows): one thread per feature, two binary searches.
+// Same result with one warp per feature counting the column's entries below /
+// inside the batch row range (ascending rows, so lo = c0 + #below): all loads
+// independent instead of two chains of dependent binary-search probes --
+// for epoch columns of up to a few hundred entries.
+__global__ void __launch_bounds__(256) csc_batch_ranges_warp_kernel(const int64_t* colptr, const int32_t* rowidx,
+                                                                    int d_in, long long start, int rows,
+                                                                    const DevStep* ds, long long* lo_out,
+                                                                    long long* hi_out) {
+  pdl_wait();
+  pdl_trigger();
+  start = step_start(ds, start);
+  const int lane = threadIdx.x & 31;
+  const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  for (long long f = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; f < d_in; f += nw) {
+    const long long c0 = colptr[f], c1 = colptr[f + 1];
+    int below = 0, inside = 0;
+#pragma unroll 4
+    for (long long e = c0 + lane; e < c1; e += 32) {
+      const long long r = __ldg(rowidx + e);
+      below += r < start;
+      inside += (r >= start) & (r < start + rows);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      below += __shfl_xor_sync(0xffffffffu, below, o);
+      inside += __shfl_xor_sync(0xffffffffu, inside, o);
+    }
+    if (lane == 0) {
+      lo_out[f] = c0 + below;
+      hi_out[f] = c0 + below + inside;
+    }
+  }
+}
 __global__ void csc_batch_ranges_kernel(const int64_t* colptr, const int32_t* rowidx, int d_in, long long start,
                                         int rows, const DevStep* ds, long long* lo_out, long long* hi_out) {
   pdl_wait();
@@ -963,18 +996,26 @@ __global__ void __launch_bounds__(256) sparse_dw_warp_kernel(SparseDwArgs p) {
     float4 acc[8];
 #pragma unroll
     for (int t = 0; t < 8; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (long long e = lo; e < hi; ++e) {
-      const float v = __ldg(p.cval + e);
-      const float* dr = p.delta0 + (static_cast<long long>(__ldg(p.rowidx + e)) - p.start) * p.ldd + base;
+    // the slice's (row, val) pairs are fetched 32 at a time with one
+    // coalesced load per lane and broadcast by shuffles, so the delta0 row
+    // gathers of consecutive entries do not wait on index loads
+    for (long long eb = lo; eb < hi; eb += 32) {
+      const int cnt = static_cast<int>(min(32LL, hi - eb));
+      const long long my_row = lane < cnt ? static_cast<long long>(__ldg(p.rowidx + eb + lane)) - p.start : 0;
+      const float my_val = lane < cnt ? __ldg(p.cval + eb + lane) : 0.f;
+      for (int k = 0; k < cnt; ++k) {
+        const float v = __shfl_sync(0xffffffffu, my_val, k);
+        const float* dr = p.delta0 + __shfl_sync(0xffffffffu, my_row, k) * p.ldd + base;
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const int j = 4 * lane + 128 * t;
-        if (base + j < p.d_out) {
-          const float4 d = __ldg(reinterpret_cast<const float4*>(dr + j));
-          acc[t].x = fmaf(v, d.x, acc[t].x);
-          acc[t].y = fmaf(v, d.y, acc[t].y);
-          acc[t].z = fmaf(v, d.z, acc[t].z);
-          acc[t].w = fmaf(v, d.w, acc[t].w);
+        for (int t = 0; t < 8; ++t) {
+          const int j = 4 * lane + 128 * t;
+          if (base + j < p.d_out) {
+            const float4 d = __ldg(reinterpret_cast<const float4*>(dr + j));
+            acc[t].x = fmaf(v, d.x, acc[t].x);
+            acc[t].y = fmaf(v, d.y, acc[t].y);
+            acc[t].z = fmaf(v, d.z, acc[t].z);
+            acc[t].w = fmaf(v, d.w, acc[t].w);
+          }
         }
       }
     }

@@ -69,6 +69,14 @@ def dense_flops_per_sample(sizes, sparse_first):
     return tot
 
 
+def hb_sparse_kernels(cfg):
+    """The CSR first layer runs on the gather kernels (else it is densified on
+    the device and runs as a tensor-core GEMM): paper_2004_08771_b200.replica."""
+    from paper_2004_08771_b200 import _native as N
+
+    return cfg["kind"] == "csr" and cfg["sizes"][0] > N.HB_DENSIFY_MAX_DIN
+
+
 def make_data(cfg, seed, rank=0):
     import paper_2004_08771_b200 as hb
 
@@ -365,6 +373,19 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
                                   "ncu_l2_throughput_pct": round(ncu.get("l2_throughput_pct", 0.0), 1)}
         if roofline is not None and ncu:
             roofline["traffic_source"] = f"profiles/{ncu_src} ({args.config}/{dom}: dram read+write bytes of one launch)"
+    # step-level tensor work: every GEMM of the step (dense layers; a sparse
+    # first layer is gather work) against the step time -- with dX and the
+    # split-K dW partials running concurrently, per-kernel event durations
+    # overlap, so this is the figure that adds up
+    if roofline is not None:
+        gemm_flops = dense_flops_per_sample(cfg["sizes"], sparse and hb_sparse_kernels(cfg)) * b
+        step_s = (sum(step_ms) / len(step_ms)) / 1000.0
+        tf32 = bf16_peak / 2.0
+        peak = tf32 / (3.0 if args.precision == "3xtf32" else 1.0)
+        roofline["step_tensor"] = {"gemm_flop_per_step": gemm_flops,
+                                   "achieved_tflops": round(gemm_flops / step_s / 1e12, 2),
+                                   "frac_of_peak": round(gemm_flops / step_s / 1e12 / peak, 4),
+                                   "note": "all GEMM flops of the step / whole step time (non-GEMM kernels included)"}
     return dict(value=value, total_ms=total_ms, e2e=e2e, roofline=roofline, kernels=kernels,
                 clocks=clocks.summary(), launches=launches, merge_ms=sum(merge_ms))
 

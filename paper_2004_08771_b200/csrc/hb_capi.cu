@@ -469,6 +469,14 @@ struct hb_ctx {
   std::vector<cudaEvent_t> xsnap_ev, xgrad_ev, xchunk_ev;
   cudaEvent_t xstart_ev = nullptr, xdone_ev = nullptr;
   int xchunk_used = 0;
+  // concurrent backward: split-K dW partial GEMMs and their reduce+SGD run on
+  // `side` while the dX GEMMs run on `stream` (the partials never touch W)
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> bev;   // fork / join events of one backward pass
+  float* ws_dw = nullptr;         // per-layer split-K slabs of the concurrent dW partials
+  std::vector<size_t> ws_dw_off;
+  bool conc_bwd = false;
+  cudaStream_t prof_st = nullptr;  // stream the profiling marks go on (null: stream)
   // merge strategy: 0 = host (gradient D2H as fp32, float64 axpy on host
   // threads as each layer's gradient lands -- the reference's own np.add on
   // the host model); 1 = DMA read-modify-write through device memory
@@ -543,18 +551,18 @@ void prof_begin(hb_ctx* c, const char* kind, int layer) {
   // inside stream capture a plain record is only a dependency marker; the
   // External flag makes it a real event-record node of the graph
   if (c->capturing)
-    cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal);
+    cudaEventRecordWithFlags(e0, c->prof_st ? c->prof_st : c->stream, cudaEventRecordExternal);
   else
-    cudaEventRecord(e0, c->stream);
+    cudaEventRecord(e0, c->prof_st ? c->prof_st : c->stream);
 }
 void prof_end(hb_ctx* c, const char* kind, int layer) {
   if (nvtx_on()) nvtxRangePop();
   if (!c->prof_on || !c->pending_active) return;
   c->pending_active = false;
   if (c->capturing)
-    cudaEventRecordWithFlags(c->pending.second, c->stream, cudaEventRecordExternal);
+    cudaEventRecordWithFlags(c->pending.second, c->prof_st ? c->prof_st : c->stream, cudaEventRecordExternal);
   else
-    cudaEventRecord(c->pending.second, c->stream);
+    cudaEventRecord(c->pending.second, c->prof_st ? c->prof_st : c->stream);
   char name[64];
   prof_name(name, kind, layer);
   c->step_marks.push_back({name, c->pending.first, c->pending.second});
@@ -898,10 +906,11 @@ int xchg_use(hb_ctx* c, int l) {
 // float64), chunk k read H2D while chunk k-1 is updated and written back D2H.
 // Each chunk is read just before it is written, so the window in which a
 // concurrent host writer's update could be overwritten stays one chunk long.
-int xchg_merge(hb_ctx* c, int l, double eta, const DevStep* ds) {
+int xchg_merge(hb_ctx* c, int l, double eta, const DevStep* ds, cudaStream_t src = nullptr) {
   if (c->xw.empty()) return HB_OK;
-  xtl(c, c->stream, "step: G%d done", l);
-  HB_CUDA(cudaEventRecord(c->xgrad_ev[l], c->stream));
+  if (src == nullptr) src = c->stream;
+  xtl(c, src, "step: G%d done", l);
+  HB_CUDA(cudaEventRecord(c->xgrad_ev[l], src));
   const int rows = c->d[l + 1], cols = c->d[l];
   const bool tr = (l == 0 && c->sparse);
   if (c->xmode == 0) {
@@ -1195,8 +1204,10 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
   const bool emit = (flags & HB_STEP_EMIT_GRAD) != 0;
   // with the small head the output layer is already done (dW + delta_{L-2})
   const int top = c->small_head ? L - 2 : L - 1;
+  bool used_side = false;
   for (int l = top; l >= 0; --l) {
     // dX: D[l-1] = (D[l] . W[l]) * A[l] (1 - A[l])   -- must precede W[l]'s update
+    auto do_dx = [&]() -> int {
     if (l >= 1) {
       GemmArgs a{};
       a.M = rows;
@@ -1222,8 +1233,11 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       prof_end(c, "gemm_dx_dsig", l);
       c->last_launches++;
     }
+    return HB_OK;
+    };
     // dW + SGD
     if (l == 0 && c->sparse) {
+      HB_TRY(do_dx());
       SparseDwArgs p{v.colptr, v.rowidx, v.cval, ds, start, rows, c->d[0], c->d[1], c->D[0], c->ld[1],
                      c->W[0], c->ldw[0], static_cast<float>(eta), emit ? c->G[0] : nullptr, c->ldw[0],
                      c->csc_lo, c->csc_hi};
@@ -1294,6 +1308,45 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
     a.eta = static_cast<float>(eta);
     const Operand tb = l == 0 ? v.dw() : c->opA_mn(l);
     const int mt = cdiv(a.M, kBM), nt = cdiv(a.N, c->bn_dw[l]);
+    if (c->conc_bwd && l >= 1 && splits > 1) {
+      // concurrent: the split-K dW partial GEMM (reads D_l, A_l; never W_l)
+      // runs on the side stream beside dX_l; its reduce + SGD waits for dX_l,
+      // which is the last reader of W_l.  The idle SMs of one kernel's wave
+      // and its epilogue tail are filled by the other's CTAs.
+      const long long slab = static_cast<long long>(a.M) * a.N;
+      float* wsb = c->ws_dw + c->ws_dw_off[l];
+      a.out = wsb;
+      a.ldo = a.N;
+      a.split_stride = slab;
+      HB_CUDA(cudaEventRecord(c->bev[2 * l], st));  // D_l and A_l are complete
+      HB_CUDA(cudaStreamWaitEvent(c->side, c->bev[2 * l], 0));
+      c->prof_st = c->side;
+      prof_begin(c, "gemm_dw_partial", l);
+      HB_TRY(launch_gemm(c->passes, G_DW, EPI_PARTIAL, c->bn_dw[l], c->opD_mn(l), tb, a, mt, nt, splits, c->side));
+      prof_end(c, "gemm_dw_partial", l);
+      c->prof_st = nullptr;
+      HB_TRY(do_dx());
+      HB_CUDA(cudaEventRecord(c->bev[2 * l + 1], st));  // dX_l has read W_l
+      HB_CUDA(cudaStreamWaitEvent(c->side, c->bev[2 * l + 1], 0));
+      c->prof_st = c->side;
+      prof_begin(c, "reduce_sgd", l);
+      if (a.N % 4 == 0 && c->ldw[l] % 4 == 0 && (slab / 4) >= 148 * 256)
+        HB_CUDA(launch_k(reduce_sgd_vec_kernel, dim3(static_cast<int>(std::min<long long>(cdiv(slab / 4, 256), 148 * 8))),
+                         dim3(256), 0, c->side, c->W[l], c->ldw[l], wsb, splits, slab, a.M, a.N,
+                         static_cast<float>(eta), emit ? c->G[l] : nullptr, c->d[l], ds,
+                         c->need_lo() ? c->W_lo[l] : nullptr));
+      else
+        HB_CUDA(launch_k(reduce_sgd_kernel, dim3(cdiv(slab, 32)), dim3(256), 0, c->side, c->W[l], c->ldw[l], wsb,
+                         splits, slab, a.M, a.N, static_cast<float>(eta), emit ? c->G[l] : nullptr, c->d[l], ds,
+                         c->need_lo() ? c->W_lo[l] : nullptr));
+      prof_end(c, "reduce_sgd", l);
+      c->prof_st = nullptr;
+      c->last_launches += 2;
+      HB_TRY(xchg_merge(c, l, eta, ds, c->side));
+      used_side = true;
+      continue;
+    }
+    HB_TRY(do_dx());
     if (splits == 1) {
       a.out = c->W[l];
       a.out_lo = c->need_lo() ? c->W_lo[l] : nullptr;
@@ -1344,6 +1397,10 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       c->last_launches += 2;
     }
     HB_TRY(xchg_merge(c, l, eta, ds));
+  }
+  if (used_side) {  // join the side stream
+    HB_CUDA(cudaEventRecord(c->bev.back(), c->side));
+    HB_CUDA(cudaStreamWaitEvent(st, c->bev.back(), 0));
   }
   return HB_OK;
 }
@@ -1745,6 +1802,25 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
   }
   c->ws_floats = std::max<size_t>(ws, 1);
   HB_CK(cudaMalloc(&c->ws, c->ws_floats * sizeof(float)));
+  // concurrent backward: per-layer split-K slabs (layers >= 1) + fork/join events
+  c->conc_bwd = !(getenv("HB_SPLITK_FUSION") && getenv("HB_SPLITK_FUSION")[0] == '1') &&
+                !(getenv("HB_NO_CONC_BWD") && getenv("HB_NO_CONC_BWD")[0] == '1');
+  if (c->conc_bwd) {
+    size_t tot = 0;
+    c->ws_dw_off.assign(L, 0);
+    for (int l = 1; l < L; ++l) {
+      int splits, kb_per, kb_total;
+      dw_plan(c, l, c->cap, &splits, &kb_per, &kb_total);
+      c->ws_dw_off[l] = tot;
+      if (splits > 1) tot += round_up(static_cast<long long>(splits) * c->d[l + 1] * c->d[l], 64);
+    }
+    HB_CK(cudaMalloc(&c->ws_dw, std::max<size_t>(tot, 1) * sizeof(float)));
+    int lo_prio = 0, hi_prio = 0;
+    HB_CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    HB_CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, lo_prio));
+    c->bev.resize(2 * L + 1);
+    for (auto& e : c->bev) HB_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   c->ws_loss_n = std::max(cdiv(c->cap, kHeadRowsPerBlock), cdiv(c->cap, 8)) + 1;
   HB_CK(cudaMalloc(&c->ws_loss, c->ws_loss_n * sizeof(double)));
   HB_CK(cudaMalloc(&c->d_loss, sizeof(double)));
@@ -1850,6 +1926,9 @@ int hb_ctx_destroy(hb_ctx* c) {
   if (c->xdone_ev) cudaEventDestroy(c->xdone_ev);
   if (c->xh2d) cudaStreamDestroy(c->xh2d);
   if (c->xmrg) cudaStreamDestroy(c->xmrg);
+  for (auto e : c->bev) cudaEventDestroy(e);
+  if (c->side) cudaStreamDestroy(c->side);
+  cudaFree(c->ws_dw);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return HB_OK;

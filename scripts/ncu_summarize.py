@@ -31,22 +31,30 @@ for path in sorted(glob.glob("gpurun_out/ncu_*.csv")):
         continue
     h, units = rows[0], rows[1]
     # a bench kernel name can cover several launches (e.g. split-K GEMM + its
-    # finish, CSC ranges + sparse dW): sizes and times add up, percentages are
-    # duration-weighted
-    launches = rows[2:]
+    # finish, CSC ranges + sparse dW): sizes and times add up over the distinct
+    # kernel functions, percentages are duration-weighted; repeated launches of
+    # the same function (the range of another step) are averaged
+    by_fn = {}
+    for r in rows[2:]:
+        by_fn.setdefault(r[h.index("Kernel Name")], []).append(r)
+    launches = [v[0] for v in by_fn.values()]
+    reps = [len(v) for v in by_fn.values()]
     d = {"kernel_function": " + ".join(r[h.index("Kernel Name")][:80] for r in launches),
-         "grid": " + ".join(r[h.index("Grid Size")] for r in launches), "launches": len(launches)}
+         "grid": " + ".join(r[h.index("Grid Size")] for r in launches), "launches": len(launches),
+         "captured_per_function": reps}
     vals = []
-    for r in launches:
-        one = {}
-        for k, (m, _) in KEYS.items():
-            if m in h:
-                i = h.index(m)
-                try:
-                    one[k] = float(r[i].replace(",", "")) * UNIT.get(units[i], 1)
-                except ValueError:
-                    pass
-        vals.append(one)
+    for group in by_fn.values():
+        one, cnt = {}, {}
+        for r in group:
+            for k, (m, _) in KEYS.items():
+                if m in h:
+                    i = h.index(m)
+                    try:
+                        one[k] = one.get(k, 0.0) + float(r[i].replace(",", "")) * UNIT.get(units[i], 1)
+                        cnt[k] = cnt.get(k, 0) + 1
+                    except ValueError:
+                        pass
+        vals.append({k: v / cnt[k] for k, v in one.items()})
     tot_t = sum(v.get("duration_us", 0) for v in vals) or 1.0
     for k in KEYS:
         if not any(k in v for v in vals):

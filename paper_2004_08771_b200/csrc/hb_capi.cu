@@ -314,6 +314,7 @@ struct DataView {
   long long ldx = 0;
   long long n_rows = 0;
   const float* x_lo = nullptr;  // 3xTF32 lo twin of x (same layout)
+  bool x_lo_zero = false;        // every x is exact in TF32 (lo twin all zero): layer-0 GEMMs skip it
   CUtensorMap tm_fwd, tm_fwd_lo;  // K-major A operand of the first forward GEMM
   CUtensorMap tm_dw, tm_dw_lo;    // MN-major B operand of the first dW GEMM
   Operand fwd() const { return {&tm_fwd, x_lo ? &tm_fwd_lo : &tm_fwd}; }
@@ -1052,6 +1053,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     a.N = c->d[l + 1];
     a.a_off = l == 0 ? static_cast<int>(start) : 0;
     a.a_start = (l == 0) ? 1 : 0;
+    a.a_lo_zero = (l == 0 && v.x_lo_zero) ? 1 : 0;
     a.ds = ds;
     a.kb_total = cdiv(c->d[l], kBK);
     a.kb_per_split = a.kb_total;
@@ -1165,6 +1167,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   a.N = c->d[L];
   a.a_off = l == 0 ? static_cast<int>(start) : 0;
   a.a_start = (l == 0) ? 1 : 0;
+  a.a_lo_zero = (l == 0 && v.x_lo_zero) ? 1 : 0;
   a.ds = ds;
   a.kb_total = cdiv(c->d[l], kBK);
   a.kb_per_split = a.kb_total;
@@ -1302,6 +1305,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
     a.N = c->d[l];
     a.b_off = l == 0 ? static_cast<int>(start) : 0;
     a.b_start = (l == 0) ? 1 : 0;
+    a.b_lo_zero = (l == 0 && v.x_lo_zero) ? 1 : 0;
     a.ds = ds;
     a.kb_total = kb_total;
     a.kb_per_split = kb_per;
@@ -1420,7 +1424,8 @@ int run_phase(hb_ctx* c, const DataView& v, long long start, int rows, uint32_t 
 
 int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta, uint32_t flags, bool graph_ok,
                  int phase = 0) {
-  const uint32_t gflags = (flags & HB_STEP_EMIT_GRAD) | (static_cast<uint32_t>(phase) << 8);
+  const uint32_t gflags = (flags & HB_STEP_EMIT_GRAD) | (static_cast<uint32_t>(phase) << 8) |
+                          (v.x_lo_zero ? (1u << 16) : 0u);
   const bool view_epoch = (&v == &c->epoch);
   if (!c->use_graphs || !graph_ok) return run_phase(c, v, start, rows, flags, eta, nullptr, phase);
   const auto key = std::make_tuple(rows, gflags, view_epoch ? c->view_gen : -c->view_gen, c->prof_on,
@@ -2376,6 +2381,25 @@ static int finish_dense_stage(hb_ctx* c) {
   c->epoch = DataView();
   c->epoch.x = c->ex;
   c->epoch.x_lo = c->ex_lo;
+  if (c->ex_lo) {
+    // every staged value exact in TF32 (lo twin all zero, e.g. binary inputs):
+    // the layer-0 GEMMs then skip the lo tile and its MMA
+    int* d_flag = nullptr;
+    HB_CUDA(cudaMalloc(&d_flag, sizeof(int)));
+    HB_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), c->stream));
+    const long long n = c->e_rows * c->ld[0];
+    any_nonzero_kernel<<<static_cast<int>(std::min<long long>(cdiv(n, 256), 148 * 8)), 256, 0, c->stream>>>(
+        c->ex_lo, n, d_flag);
+    int h = 1;
+    const cudaError_t e1 = cudaGetLastError();
+    const cudaError_t e2 = cudaMemcpyAsync(&h, d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+    const cudaError_t e3 = cudaStreamSynchronize(c->stream);
+    cudaFree(d_flag);
+    HB_CUDA(e1);
+    HB_CUDA(e2);
+    HB_CUDA(e3);
+    c->epoch.x_lo_zero = (h == 0) && !(getenv("HB_NO_EXACT_X") && getenv("HB_NO_EXACT_X")[0] == '1');
+  }
   c->epoch.ldx = c->ld[0];
   c->epoch.n_rows = c->e_rows;
   c->epoch.labels = c->elabels;

@@ -65,6 +65,8 @@ struct GemmArgs {
   float* w_lo;
   long long ldw;
   int* tile_sync;         // EPI_SPLIT_SGD: 2 zeroed counters per output tile (arrive, depart)
+  int a_lo_zero, b_lo_zero;  // 3xTF32: that operand is exact in TF32 (lo twin all zero, e.g. binary
+                             // w8a inputs) -- its lo tile is neither loaded nor multiplied
   int trace;              // HB_TRACE builds: record this launch's pipeline timeline
   int trace_slot;         // HB_TRACE builds: 1-based slot for the per-CTA stamps (0 = off)
 };
@@ -224,6 +226,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
     if (lane == 0) {
       // completion of both CTAs' loads is counted on the leader's full barrier
       const uint32_t full_leader0 = PAIR ? mapa_shared(smem_u32(&full[0]), 0) : smem_u32(&full[0]);
+      const uint32_t stage_tx = C::STAGE_BYTES - (PASSES == 3 && args.a_lo_zero ? C::A_BYTES : 0) -
+                                (PASSES == 3 && args.b_lo_zero ? C::B_BYTES : 0);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
@@ -232,7 +236,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
         uint8_t* sA = smem + s * C::STAGE_BYTES;
         uint8_t* sB = sA + C::A_BYTES;
         const uint32_t fb = full_leader0 + 8u * s;
-        if (leader) mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * C::STAGE_BYTES);
+        if (leader) mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * stage_tx);
         const int k0 = (kb_begin + i) * kBK;
 #pragma unroll
         for (int h = 0; h < (PASSES == 3 ? 2 : 1); ++h) {
@@ -240,7 +244,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
           const CUtensorMap* mb = h ? &tmB_lo : &tmB;
           uint8_t* dA = sA + h * C::OP_BYTES;
           uint8_t* dB = sB + h * C::OP_BYTES;
-          if (!A_MN) {
+          if (h && args.a_lo_zero) {
+            // exact operand: no lo tile
+          } else if (!A_MN) {
             tma_load_2d_to(dA, ma, fb, k0, m0 + a_off, PAIR);
           } else {
 #pragma unroll
@@ -248,6 +254,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
           }
           // this CTA's half of B in 32-wide slices (4 KB: 32 K-major rows, or
           // 32 MN columns x 32 K-lines)
+          if (h && args.b_lo_zero) continue;
 #pragma unroll
           for (int j = 0; j < C::BNL / 32; ++j) {
             const int c0 = B_MN ? nl0 + 32 * j : k0;
@@ -278,8 +285,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
             const uint64_t bl = op_desc(bHi + C::OP_BYTES, kk, B_MN);
             const uint32_t t_small = tmem_base + C::NBIG * BN;
             const uint32_t t_big = tmem_base + (i % C::NBIG) * BN;
-            mma_tf32_cg(t_small, al, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u, PAIR);
-            mma_tf32_cg(t_small, ah, bl, idesc, 1u, PAIR);
+            // (at most one operand of a launch is exact, so t_small is always written)
+            if (!args.a_lo_zero) mma_tf32_cg(t_small, al, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u, PAIR);
+            if (!args.b_lo_zero)
+              mma_tf32_cg(t_small, ah, bl, idesc, (args.a_lo_zero && i == 0 && kk == 0) ? 0u : 1u, PAIR);
             mma_tf32_cg(t_big, ah, bh, idesc, (i >= C::NBIG || kk > 0) ? 1u : 0u, PAIR);
           } else {
             mma_tf32_cg(tmem_base, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u, PAIR);

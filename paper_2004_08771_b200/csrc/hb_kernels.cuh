@@ -1165,6 +1165,15 @@ __global__ void __launch_bounds__(256) splitk_epi_kernel(float* __restrict__ out
   }
 }
 
+// *flag = 1 if any of x[0..n) is nonzero
+__global__ void any_nonzero_kernel(const float* x, long long n, int* flag) {
+  int any = 0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    any |= x[i] != 0.f;
+  if (__syncthreads_or(any) && threadIdx.x == 0) *flag = 1;
+}
+
 // dst (rows, cols) with row stride ld <- contiguous src (rows, cols); lo twin too
 __global__ void repitch_split_kernel(const float* __restrict__ src, float* __restrict__ dst, float* __restrict__ lo,
                                      long long ld, long long rows, int cols) {

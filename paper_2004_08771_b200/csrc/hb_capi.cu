@@ -1459,7 +1459,9 @@ int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double
     c->last_launches = 0;
   }
   if (phase != 2) HB_CUDA(cudaMemcpyAsync(c->d_step, &hs, sizeof hs, cudaMemcpyHostToDevice, c->stream));
+  xmark("graph launch");
   HB_CUDA(cudaGraphLaunch(it->second.exec, c->stream));
+  xmark("graph launched");
   c->last_launches += it->second.launches;
   if (c->prof_on) c->step_marks.insert(c->step_marks.end(), it->second.marks.begin(), it->second.marks.end());
   return HB_OK;
@@ -2742,25 +2744,29 @@ int hb_permute_epoch(hb_ctx* c, const int64_t* perm, int64_t n) {
 
 // range checks as branch-free min/max reductions (vectorised), then a scan
 // for the offending value only on failure
+// range checks as branch-free unsigned compares OR-reduced (no loop-carried
+// min/max chain, so the compiler vectorises them); the slow scan only runs to
+// name the offending entry
 static int check_labels(const int64_t* y, long long n, int nc) {
-  int64_t mn = 0, mx = 0;
-  if (n > 0) mn = mx = y[0];
-  for (long long i = 0; i < n; ++i) {
-    mn = y[i] < mn ? y[i] : mn;
-    mx = y[i] > mx ? y[i] : mx;
-  }
-  if (mn >= 0 && mx < nc) return HB_OK;
+  uint64_t bad = 0;
+  for (long long i = 0; i < n; ++i) bad |= static_cast<uint64_t>(y[i]) >= static_cast<uint64_t>(nc);
+  if (!bad) return HB_OK;
   for (long long i = 0; i < n; ++i)
     if (y[i] < 0 || y[i] >= nc) return fail(HB_EINVAL, "labels must lie in [0, %d), got %lld", nc, (long long)y[i]);
   return HB_OK;
 }
 static int check_cols(const int32_t* col, long long nnz, int d) {
-  int32_t mn = 0, mx = 0;
-  for (long long e = 0; e < nnz; ++e) {
-    mn = col[e] < mn ? col[e] : mn;
-    mx = col[e] > mx ? col[e] : mx;
-  }
-  if (mn >= 0 && mx < d) return HB_OK;
+  // (split over the merge pool: a batch's column ids come straight from DRAM)
+  HostPool& pool = HostPool::get();
+  const int parts = static_cast<int>(std::min<long long>(pool.size(), std::max<long long>(1, nnz / (1 << 14))));
+  std::atomic<uint32_t> any{0};
+  pool.run(parts, [&](int t) {
+    const long long a = nnz * t / parts, b = nnz * (t + 1) / parts;
+    uint32_t bad = 0;
+    for (long long e = a; e < b; ++e) bad |= static_cast<uint32_t>(col[e]) >= static_cast<uint32_t>(d);
+    if (bad) any.store(1, std::memory_order_relaxed);
+  });
+  if (!any.load()) return HB_OK;
   for (long long e = 0; e < nnz; ++e)
     if (col[e] < 0 || col[e] >= d) return fail(HB_EINVAL, "feature index %d outside [0, %d)", col[e], d);
   return HB_OK;
@@ -2819,9 +2825,11 @@ int hb_train_step_host_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col,
   if (!rowptr || !labels) return fail(HB_EINVAL, "null batch");
   if (rows < 1 || rows > c->max_batch) return fail(HB_EINVAL, "rows=%d outside [1, %d]", rows, c->max_batch);
   if (rowptr[0] != 0) return fail(HB_EINVAL, "rowptr[0] must be 0");
+  xmark("host csr: enter");
   HB_TRY(check_labels(labels, rows, c->d[c->L]));
   const long long nnz = rowptr[rows];
   HB_TRY(check_cols(col, nnz, c->d[0]));
+  xmark("host csr: checked");
   if (nnz > c->b_nnz_cap) {
     cudaFree(c->bcol);
     cudaFree(c->bval);
@@ -2870,7 +2878,9 @@ int hb_train_step_host_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col,
   }
   if (!c->sparse) {
     // densified context: scatter the batch into the dense slot, then the GEMM path
+    xmark("host csr: copies enqueued");
     HB_TRY(densify_launch(c, c->browptr, c->bcol, c->bval, rows, c->bx, c->bx_lo));
+    xmark("host csr: densify enqueued");
     c->pre_launches = 1;
     return do_step(c, c->batch, 0, rows, eta, flags, out_loss);
   }

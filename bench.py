@@ -386,6 +386,10 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
                                    "achieved_tflops": round(gemm_flops / step_s / 1e12, 2),
                                    "frac_of_peak": round(gemm_flops / step_s / 1e12 / peak, 4),
                                    "note": "all GEMM flops of the step / whole step time (non-GEMM kernels included)"}
+        if roofline.get("kernel", "").startswith(("gemm_dx", "gemm_dw_partial", "reduce_sgd")):
+            roofline["overlap_note"] = ("the backward's dX GEMM and the split-K dW partial GEMM of the same layer run "
+                                        "concurrently on two streams, so this kernel's event-timed duration includes "
+                                        "sharing the SMs with the other; step_tensor is the figure that adds up")
     return dict(value=value, total_ms=total_ms, e2e=e2e, roofline=roofline, kernels=kernels,
                 clocks=clocks.summary(), launches=launches, merge_ms=sum(merge_ms))
 

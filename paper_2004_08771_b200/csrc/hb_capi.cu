@@ -475,6 +475,8 @@ struct hb_ctx {
   cudaStream_t side = nullptr;
   std::vector<cudaEvent_t> bev;   // fork / join events of one backward pass
   float* ws_dw = nullptr;         // per-layer split-K slabs of the concurrent dW partials
+  float* ws_head = nullptr;       // the small head's per-block dW partials
+  bool side_pending = false;      // the forward left work on `side` (joined by the backward)
   std::vector<size_t> ws_dw_off;
   bool conc_bwd = false;
   cudaStream_t prof_st = nullptr;  // stream the profiling marks go on (null: stream)
@@ -1104,7 +1106,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     h.delta_prev_lo = (train && L >= 2 && c->need_lo()) ? c->D_lo[L - 2] : nullptr;
     h.ld_dp = L >= 2 ? c->ld[L - 1] : 0;
     h.delta_out = nullptr;
-    h.ws_dw = c->ws;
+    h.ws_dw = c->ws_head;
     h.ws_loss = c->ws_loss;
     const bool vec = (h.d % 4 == 0) && (h.lda % 4 == 0) && (h.ld_dp % 4 == 0) &&
                      (h.d <= 1024 && (c->head_nct == 2 || h.d <= 512));
@@ -1148,16 +1150,26 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     HB_CUDA(cudaGetLastError());
     c->last_launches += 2;
     if (train) {
+      // the output layer's reduce + SGD only needs the head's partials: with
+      // the concurrent backward it runs on the side stream beside dX_{L-2}
+      // (nothing later reads W_{L-1}; the head kernel already has)
+      cudaStream_t rs = st;
+      if (c->conc_bwd && L >= 2) {
+        HB_CUDA(cudaEventRecord(c->bev[2 * l], st));
+        HB_CUDA(cudaStreamWaitEvent(c->side, c->bev[2 * l], 0));
+        rs = c->side;
+        c->side_pending = true;
+      }
       const long long n = static_cast<long long>(c->d[L]) * c->d[l];
+      c->prof_st = rs;
       prof_begin(c, "reduce_sgd", l);
-      HB_CUDA(launch_k(reduce_sgd_kernel, dim3(cdiv(n, 32)), dim3(256), 0, st, c->W[l], c->ldw[l], c->ws, grid, n, c->d[L], c->d[l],
-                                                     static_cast<float>(eta),
-                                                     (flags & HB_STEP_EMIT_GRAD) ? c->G[l] : nullptr, c->d[l], ds,
-                                                     c->need_lo() ? c->W_lo[l] : nullptr));
-      HB_CUDA(cudaGetLastError());
+      HB_CUDA(launch_k(reduce_sgd_kernel, dim3(cdiv(n, 32)), dim3(256), 0, rs, c->W[l], c->ldw[l], c->ws_head, grid, n,
+                       c->d[L], c->d[l], static_cast<float>(eta), (flags & HB_STEP_EMIT_GRAD) ? c->G[l] : nullptr,
+                       c->d[l], ds, c->need_lo() ? c->W_lo[l] : nullptr));
       prof_end(c, "reduce_sgd", l);
+      c->prof_st = nullptr;
       c->last_launches++;
-      HB_TRY(xchg_merge(c, l, eta, ds));
+      HB_TRY(xchg_merge(c, l, eta, ds, rs));
     }
     return HB_OK;
   }
@@ -1402,9 +1414,10 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
     }
     HB_TRY(xchg_merge(c, l, eta, ds));
   }
-  if (used_side) {  // join the side stream
+  if (used_side || c->side_pending) {  // join the side stream
     HB_CUDA(cudaEventRecord(c->bev.back(), c->side));
     HB_CUDA(cudaStreamWaitEvent(st, c->bev.back(), 0));
+    c->side_pending = false;
   }
   return HB_OK;
 }
@@ -1792,7 +1805,8 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
     dw_plan(c, l, c->cap, &splits, &kb_per, &kb_total);
     if (splits > 1) ws = std::max(ws, static_cast<size_t>(splits) * c->d[l + 1] * c->d[l]);
   }
-  if (c->small_head) ws = std::max(ws, static_cast<size_t>(cdiv(c->cap, kHeadRowsPerBlock)) * nc * dlast);
+  if (c->small_head)
+    HB_CK(cudaMalloc(&c->ws_head, static_cast<size_t>(cdiv(c->cap, kHeadRowsPerBlock)) * nc * dlast * sizeof(float)));
   ws = std::max(ws, static_cast<size_t>(kSplitSlabFloats));  // split-K forward / dX slabs
   if (c->sparse) {
     c->sdw_smem = (static_cast<size_t>(c->d[0]) * kSdwSliceCols + static_cast<size_t>(kCsrChunkRows) * kSdwSliceCols) *
@@ -1936,6 +1950,7 @@ int hb_ctx_destroy(hb_ctx* c) {
   for (auto e : c->bev) cudaEventDestroy(e);
   if (c->side) cudaStreamDestroy(c->side);
   cudaFree(c->ws_dw);
+  cudaFree(c->ws_head);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return HB_OK;

@@ -477,6 +477,7 @@ struct hb_ctx {
   float* ws_dw = nullptr;         // per-layer split-K slabs of the concurrent dW partials
   float* ws_head = nullptr;       // the small head's per-block dW partials
   bool side_pending = false;      // the forward left work on `side` (joined by the backward)
+  bool ranges_early = false;      // this step's CSC batch ranges were launched on `side` by the forward
   std::vector<size_t> ws_dw_off;
   bool conc_bwd = false;
   cudaStream_t prof_st = nullptr;  // stream the profiling marks go on (null: stream)
@@ -1011,9 +1012,32 @@ int xchg_end(hb_ctx* c) {
 
 // `ds` != null: graph mode -- kernels read the batch start and eta from
 // device memory (the by-value start/eta are then 0 and ignored).
+// per-feature batch slices of the CSC (sparse dW of layer 0); depends only on
+// the batch, so with the concurrent backward it runs on the side stream under
+// the forward pass
+int launch_csc_ranges(hb_ctx* c, const DataView& v, long long start, int rows, const DevStep* ds, cudaStream_t s) {
+  if (v.n_rows > 0 && static_cast<double>(c->e_nnz) / std::max(1, c->d[0]) <= 1024.0)
+    HB_CUDA(launch_k(csc_batch_ranges_warp_kernel, dim3(static_cast<int>(std::min<long long>(cdiv(c->d[0], 8), 148 * 16))),
+                     dim3(256), 0, s, v.colptr, v.rowidx, c->d[0], start, rows, ds, c->csc_lo, c->csc_hi));
+  else
+    HB_CUDA(launch_k(csc_batch_ranges_kernel, dim3(cdiv(c->d[0], 256)), dim3(256), 0, s, v.colptr, v.rowidx, c->d[0],
+                     start, rows, ds, c->csc_lo, c->csc_hi));
+  c->last_launches++;
+  return HB_OK;
+}
+
 int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool train, uint32_t flags, double eta,
                 const DevStep* ds) {
   cudaStream_t st = c->stream;
+  c->ranges_early = false;
+  if (train && c->sparse && c->conc_bwd && !c->sdw_narrow) {
+    HB_CUDA(cudaEventRecord(c->bev[0], st));  // the batch (CSC view) is in place
+    HB_CUDA(cudaStreamWaitEvent(c->side, c->bev[0], 0));
+    HB_TRY(launch_csc_ranges(c, v, start, rows, ds, c->side));
+    HB_CUDA(cudaEventRecord(c->bev[1], c->side));
+    c->side_pending = true;
+    c->ranges_early = true;
+  }
   const int L = c->L;
   const int m_tiles = cdiv(rows, kBM);
   const int zrows = std::min<long long>(round_up(rows, kBM), c->cap);
@@ -1286,12 +1310,10 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
         HB_TRY(xchg_merge(c, 0, eta, ds));
         continue;
       }
-      if (v.n_rows > 0 && static_cast<double>(c->e_nnz) / std::max(1, c->d[0]) <= 1024.0)
-        HB_CUDA(launch_k(csc_batch_ranges_warp_kernel, dim3(static_cast<int>(std::min<long long>(cdiv(c->d[0], 8), 148 * 16))),
-                         dim3(256), 0, st, v.colptr, v.rowidx, c->d[0], start, rows, ds, c->csc_lo, c->csc_hi));
+      if (c->ranges_early)
+        HB_CUDA(cudaStreamWaitEvent(st, c->bev[1], 0));  // computed on the side stream under the forward
       else
-        HB_CUDA(launch_k(csc_batch_ranges_kernel, dim3(cdiv(c->d[0], 256)), dim3(256), 0, st, v.colptr, v.rowidx,
-                         c->d[0], start, rows, ds, c->csc_lo, c->csc_hi));
+        HB_TRY(launch_csc_ranges(c, v, start, rows, ds, st));
       // batch entries per feature decide the parallelisation
       const double per_feature = static_cast<double>(rows) * c->nnz_per_row / std::max(1, c->d[0]);
       if (per_feature < 48.0 && c->d[1] % 4 == 0) {
@@ -1306,7 +1328,6 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       HB_CUDA(cudaGetLastError());
       c->last_launches++;
       prof_end(c, "sparse_dw_sgd", 0);
-      c->last_launches++;
       HB_TRY(xchg_merge(c, 0, eta, ds));
       continue;
     }

@@ -337,3 +337,31 @@ def test_stage_array_straddling_a_pinned_view(hb):
     finally:
         a.close()
         b.close()
+
+
+@pytest.mark.parametrize("sparse", [False, True])
+def test_nccl_merge_single_rank(hb, sparse):
+    """The GPU-replica merge end to end on one device: NCCL is
+    loaded, a one-rank communicator is created and hb_merge_allreduce packs,
+    all-reduces and unpacks (x 1/nranks) the model -- which with one rank must
+    leave every weight, and the next step, bit-identical."""
+    sizes = (300, 64, 64, 2) if sparse else (20, 64, 64, 3)
+    w, x, y = oracle_case(sizes, 128, seed=31, sparse_nnz=9 if sparse else None)
+    ref = hb.GpuReplica(sizes, 128, sparse=sparse, sparse_kernels=sparse)
+    ctx = hb.GpuReplica(sizes, 128, sparse=sparse, sparse_kernels=sparse)
+    try:
+        for c in (ref, ctx):
+            c.set_weights(w)
+            c.stage(to_csr(hb, x, y) if sparse else x, None if sparse else y)
+            c.step(0, 128, 0.3)
+        ctx.comm_init(hb.GpuReplica.nccl_unique_id(), 1, 0)
+        ctx.merge_allreduce()
+        for a, b in zip(ref.get_weights(), ctx.get_weights()):
+            assert np.array_equal(a, b)
+        for c in (ref, ctx):
+            c.step(0, 128, 0.3, emit_grad=True)
+        for a, b in zip(ref.grads(), ctx.grads()):
+            assert np.array_equal(a, b)
+    finally:
+        ctx.close()
+        ref.close()

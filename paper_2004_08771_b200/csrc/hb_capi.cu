@@ -335,6 +335,7 @@ struct Mark {
 };
 struct StepGraph {
   cudaGraphExec_t exec = nullptr;
+  std::vector<char> xdma_used;  // device-lane merges inside this graph
   std::vector<Mark> marks;
   std::vector<cudaEvent_t> events;
   int launches = 0;
@@ -493,6 +494,12 @@ struct hb_ctx {
   int32_t* xseq_host = nullptr;  // pinned: [0] = this call's sequence number, [1 + l] = layer flags
   int32_t* d_xseq = nullptr;
   int32_t xseq = 0;
+  // device lane of the host merge: layers whose stale merge is done by their
+  // split-K reduce kernel on a float64 copy of the host rows DMA'd in just
+  // before it and DMA'd back (splits the merge between PCIe and host DRAM)
+  std::vector<char> xdma;       // planned per layer
+  std::vector<char> xdma_used;  // taken by the step just enqueued (rows decide whether the split-K path runs)
+  std::vector<cudaEvent_t> xread_ev;
   void* comm = nullptr;
   int nranks = 1;
   float* flat = nullptr;  // contiguous model copy for allreduce
@@ -917,6 +924,15 @@ int xchg_merge(hb_ctx* c, int l, double eta, const DevStep* ds, cudaStream_t src
   HB_CUDA(cudaEventRecord(c->xgrad_ev[l], src));
   const int rows = c->d[l + 1], cols = c->d[l];
   const bool tr = (l == 0 && c->sparse);
+  if (c->xmode == 0 && l < static_cast<int>(c->xdma_used.size()) && c->xdma_used[l] && src == c->side) {
+    // device lane: the reduce kernel already merged the freshly read host
+    // rows; write them back
+    HB_CUDA(cudaStreamWaitEvent(c->xmrg, c->xgrad_ev[l], 0));
+    HB_CUDA(cudaMemcpyAsync(c->xw[l], c->stage_all + layer_offset(c, l),
+                            static_cast<size_t>(rows) * cols * sizeof(double), cudaMemcpyDeviceToHost, c->xmrg));
+    xtl(c, c->xmrg, "mrg: layer %d written back (device lane)", l);
+    return HB_OK;
+  }
   if (c->xmode == 0) {
     // host mode: the fp32 gradient goes D2H on the merge stream; the calling
     // thread applies it (hb_replica_step*, xchg_host_merges)
@@ -975,6 +991,7 @@ int xchg_host_merges(hb_ctx* c, double eta) {
   const int32_t seq = c->xseq;
   xmark("enqueued");
   for (int l = c->L - 1; l >= 0; --l) {
+    if (l < static_cast<int>(c->xdma_used.size()) && c->xdma_used[l]) continue;  // merged on the device lane
     volatile int32_t* flag = c->xseq_host + 1 + l;
     // spin on the flag (pinned host memory, no driver calls); the stream is
     // queried only every ~2^18 spins to surface a failed step
@@ -1299,7 +1316,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
         if (c->d[1] % 4 == 0 && (slab / 4) >= 148 * 256)
           HB_CUDA(launch_k(reduce_sgd_vec_kernel, dim3(static_cast<int>(std::min<long long>(cdiv(slab / 4, 256), 148 * 8))), dim3(256), 0, st, 
               c->W[0], c->ldw[0], c->ws, row_blocks, slab, c->d[0], c->d[1], static_cast<float>(eta),
-              emit ? c->G[0] : nullptr, c->ldw[0], ds, nullptr));
+              emit ? c->G[0] : nullptr, c->ldw[0], ds, nullptr, nullptr, 0.0));
         else
           HB_CUDA(launch_k(reduce_sgd_kernel, dim3(cdiv(slab, 32)), dim3(256), 0, st, c->W[0], c->ldw[0], c->ws, row_blocks, slab, c->d[0],
                                                             c->d[1], static_cast<float>(eta),
@@ -1357,6 +1374,17 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       a.split_stride = slab;
       HB_CUDA(cudaEventRecord(c->bev[2 * l], st));  // D_l and A_l are complete
       HB_CUDA(cudaStreamWaitEvent(c->side, c->bev[2 * l], 0));
+      // device lane of the merge: the host rows of W_l come in while the
+      // partial GEMM runs (the merge read), the reduce applies both updates
+      const bool dev_lane = !c->xw.empty() && c->xmode == 0 && l < static_cast<int>(c->xdma.size()) && c->xdma[l];
+      double* host_rows = dev_lane ? c->stage_all + layer_offset(c, l) : nullptr;
+      if (dev_lane) {
+        c->xdma_used[l] = 1;
+        HB_CUDA(cudaStreamWaitEvent(c->xh2d, c->bev[2 * l], 0));
+        HB_CUDA(cudaMemcpyAsync(host_rows, c->xw[l], static_cast<size_t>(a.M) * a.N * sizeof(double),
+                                cudaMemcpyHostToDevice, c->xh2d));
+        HB_CUDA(cudaEventRecord(c->xread_ev[l], c->xh2d));
+      }
       c->prof_st = c->side;
       prof_begin(c, "gemm_dw_partial", l);
       HB_TRY(launch_gemm(c->passes, G_DW, EPI_PARTIAL, c->bn_dw[l], c->opD_mn(l), tb, a, mt, nt, splits, c->side));
@@ -1365,13 +1393,14 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       HB_TRY(do_dx());
       HB_CUDA(cudaEventRecord(c->bev[2 * l + 1], st));  // dX_l has read W_l
       HB_CUDA(cudaStreamWaitEvent(c->side, c->bev[2 * l + 1], 0));
+      if (dev_lane) HB_CUDA(cudaStreamWaitEvent(c->side, c->xread_ev[l], 0));
       c->prof_st = c->side;
       prof_begin(c, "reduce_sgd", l);
-      if (a.N % 4 == 0 && c->ldw[l] % 4 == 0 && (slab / 4) >= 148 * 256)
+      if (dev_lane || (a.N % 4 == 0 && c->ldw[l] % 4 == 0 && (slab / 4) >= 148 * 256))
         HB_CUDA(launch_k(reduce_sgd_vec_kernel, dim3(static_cast<int>(std::min<long long>(cdiv(slab / 4, 256), 148 * 8))),
                          dim3(256), 0, c->side, c->W[l], c->ldw[l], wsb, splits, slab, a.M, a.N,
                          static_cast<float>(eta), emit ? c->G[l] : nullptr, c->d[l], ds,
-                         c->need_lo() ? c->W_lo[l] : nullptr));
+                         c->need_lo() ? c->W_lo[l] : nullptr, host_rows, eta));
       else
         HB_CUDA(launch_k(reduce_sgd_kernel, dim3(cdiv(slab, 32)), dim3(256), 0, c->side, c->W[l], c->ldw[l], wsb,
                          splits, slab, a.M, a.N, static_cast<float>(eta), emit ? c->G[l] : nullptr, c->d[l], ds,
@@ -1424,7 +1453,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       if (a.N % 4 == 0 && c->ldw[l] % 4 == 0 && (slab / 4) >= 148 * 256)
         HB_CUDA(launch_k(reduce_sgd_vec_kernel, dim3(static_cast<int>(std::min<long long>(cdiv(slab / 4, 256), 148 * 8))), dim3(256), 0, st, 
             c->W[l], c->ldw[l], c->ws, splits, slab, a.M, a.N, static_cast<float>(eta), emit ? c->G[l] : nullptr,
-            c->d[l], ds, c->need_lo() ? c->W_lo[l] : nullptr));
+            c->d[l], ds, c->need_lo() ? c->W_lo[l] : nullptr, nullptr, 0.0));
       else
         HB_CUDA(launch_k(reduce_sgd_kernel, dim3(cdiv(slab, 32)), dim3(256), 0, st, c->W[l], c->ldw[l], c->ws, splits, slab, a.M, a.N,
                                                           static_cast<float>(eta), emit ? c->G[l] : nullptr, c->d[l],
@@ -1449,6 +1478,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
 // phase 0: whole step; 1: forward (incl. the fused head and its update); 2: backward
 int run_phase(hb_ctx* c, const DataView& v, long long start, int rows, uint32_t flags, double eta, const DevStep* ds,
               int phase) {
+  if (phase != 2) c->xdma_used.assign(c->L, 0);
   if (phase != 2) HB_TRY(xchg_begin(c));
   if (phase != 2) HB_TRY(run_forward(c, v, start, rows, true, flags, eta, ds));
   if (phase != 1) HB_TRY(run_backward(c, v, start, rows, flags, eta, ds));
@@ -1486,6 +1516,7 @@ int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double
     if (ce != cudaSuccess) return fail(HB_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(ce));
     g.marks = c->step_marks;
     g.events = c->cap_events;
+    g.xdma_used = c->xdma_used;
     g.launches = c->last_launches - launches0;
     c->step_marks.clear();
     c->cap_events.clear();
@@ -1494,6 +1525,7 @@ int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double
   }
   if (phase != 2) HB_CUDA(cudaMemcpyAsync(c->d_step, &hs, sizeof hs, cudaMemcpyHostToDevice, c->stream));
   xmark("graph launch");
+  c->xdma_used = it->second.xdma_used;
   HB_CUDA(cudaGraphLaunch(it->second.exec, c->stream));
   xmark("graph launched");
   c->last_launches += it->second.launches;
@@ -1961,6 +1993,7 @@ int hb_ctx_destroy(hb_ctx* c) {
   for (auto e : c->xsnap_ev) cudaEventDestroy(e);
   for (auto e : c->xgrad_ev) cudaEventDestroy(e);
   if (c->xseq_host) cudaFreeHost(c->xseq_host);
+  for (auto e : c->xread_ev) cudaEventDestroy(e);
   if (c->xgrad_host) cudaFreeHost(c->xgrad_host);
   cudaFree(c->d_xseq);
   for (auto e : c->xchunk_ev) cudaEventDestroy(e);
@@ -2299,6 +2332,42 @@ int hb_merge_grad_into_f64(hb_ctx* c, int layer, double* host_w, double eta) {
 // Arms the overlapped exchange for exactly one step call.  The host model must
 // be page-locked (hb_host_register) so its DMAs run at link speed and can be
 // captured into the step graph.
+// Which layers merge on the device lane.  Each layer's merge costs either
+// host DRAM (host lane: read w, write w, read the fp32 gradient, 20 B per
+// weight) plus 4 B of gradient D2H, or PCIe both ways (device lane: 8 B H2D
+// merge read + 8 B D2H write-back per weight).  Layers are assigned greedily
+// to keep max(H2D, D2H, host-DRAM time) lowest, the snapshot's H2D included
+// (measured B200 host: ~50 GB/s each PCIe direction, ~65 GB/s of host DRAM for
+// this access mix).  Only layers whose split-K reduce carries the merge and
+// whose merge read can hide under the dW partial GEMM (large batches) qualify.
+static void xchg_plan_lanes(hb_ctx* c) {
+  c->xdma.assign(c->L, 0);
+  if (c->xmode != 0 || !c->conc_bwd || c->cap < 4096 ||
+      (getenv("HB_NO_XCHG_DEVICE_LANE") && getenv("HB_NO_XCHG_DEVICE_LANE")[0] == '1'))
+    return;
+  double h2d = 8.0 * static_cast<double>(c->n_params), d2h = 0.0, host = 0.0;
+  const int top = c->small_head ? c->L - 2 : c->L - 1;
+  auto cost = [](double a, double b, double h) { return std::max(std::max(a / 50.0, b / 50.0), h / 65.0); };
+  for (int l = c->L - 1; l >= 0; --l) {
+    const double n = static_cast<double>(c->d[l + 1]) * c->d[l];
+    bool capable = l >= 1 && l <= top && (layer_offset(c, l) % 2) == 0 && c->d[l] % 4 == 0 && c->ldw[l] % 4 == 0 &&
+                   n / 4 >= 148 * 256;
+    if (capable) {
+      int splits, kb_per, kb_total;
+      dw_plan(c, l, c->cap, &splits, &kb_per, &kb_total);
+      capable = splits > 1;
+    }
+    if (capable && cost(h2d + 8 * n, d2h + 8 * n, host) < cost(h2d, d2h + 4 * n, host + 20 * n)) {
+      c->xdma[l] = 1;
+      h2d += 8 * n;
+      d2h += 8 * n;
+    } else {
+      d2h += 4 * n;
+      host += 20 * n;
+    }
+  }
+}
+
 static int xchg_arm(hb_ctx* c, double* const* ws) {
   g_call_t0 = std::chrono::steady_clock::now();
   if (!ws) return fail(HB_EINVAL, "null weight array");
@@ -2325,6 +2394,9 @@ static int xchg_arm(hb_ctx* c, double* const* ws) {
     HB_CUDA(cudaHostAlloc(&c->xgrad_host, c->n_params * sizeof(float) + 64, cudaHostAllocDefault));
     std::memset(c->xseq_host, 0, (c->L + 1) * sizeof(int32_t));
     HB_CUDA(cudaMalloc(&c->d_xseq, sizeof(int32_t)));
+    c->xread_ev.resize(c->L);
+    for (auto& e : c->xread_ev) HB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    xchg_plan_lanes(c);
     if (const char* m = getenv("HB_XCHG_MERGE")) c->xmode = strcmp(m, "dma") == 0 ? 1 : 0;
   }
   std::vector<double*> cur(ws, ws + c->L);

@@ -488,10 +488,14 @@ __global__ void __launch_bounds__(256) reduce_sgd_kernel(float* w, long long ldw
 // of large dW GEMMs): a grid-stride loop over float4 groups, every thread sums
 // its 4 elements over the S slabs in slab order.  Needs cols % 4 == 0 and
 // 16-byte-aligned rows of w / grad.
+// host_w (optional): a float64 device copy of this layer's host model rows,
+// read from the host just before this kernel; the stale merge
+// host_w = host_w + (-eta) * g (linalg.py:79, NumPy rounding) is applied here
+// too and the caller DMAs host_w back -- the device lane of the exchange.
 __global__ void __launch_bounds__(256) reduce_sgd_vec_kernel(float* w, long long ldw, const float* part, int S,
                                                                long long slab, int rows, int cols, float eta,
                                                                float* grad, long long ldg, const DevStep* ds,
-                                                               float* w_lo) {
+                                                               float* w_lo, double* host_w, double eta64) {
   pdl_wait();
   pdl_trigger();
   eta = step_eta(ds, eta);
@@ -530,6 +534,17 @@ __global__ void __launch_bounds__(256) reduce_sgd_vec_kernel(float* w, long long
     *wp = wv;
     if (w_lo != nullptr) *reinterpret_cast<float4*>(w_lo + r * ldw + c) = lo4(wv);
     if (grad != nullptr) *reinterpret_cast<float4*>(grad + r * ldg + c) = g;
+    if (host_w != nullptr) {
+      const double s = -(ds != nullptr ? ds->eta64 : eta64);
+      double2* hp = reinterpret_cast<double2*>(host_w + i);
+      double2 h0 = hp[0], h1 = hp[1];
+      h0.x = __dadd_rn(h0.x, __dmul_rn(s, static_cast<double>(g.x)));
+      h0.y = __dadd_rn(h0.y, __dmul_rn(s, static_cast<double>(g.y)));
+      h1.x = __dadd_rn(h1.x, __dmul_rn(s, static_cast<double>(g.z)));
+      h1.y = __dadd_rn(h1.y, __dmul_rn(s, static_cast<double>(g.w)));
+      hp[0] = h0;
+      hp[1] = h1;
+    }
   }
 }
 

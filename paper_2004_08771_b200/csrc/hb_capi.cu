@@ -2336,16 +2336,23 @@ int hb_merge_grad_into_f64(hb_ctx* c, int layer, double* host_w, double eta) {
 // host DRAM (host lane: read w, write w, read the fp32 gradient, 20 B per
 // weight) plus 4 B of gradient D2H, or PCIe both ways (device lane: 8 B H2D
 // merge read + 8 B D2H write-back per weight).  Layers are assigned greedily
-// to keep max(H2D, D2H, host-DRAM time) lowest, the snapshot's H2D included
-// (measured B200 host: ~50 GB/s each PCIe direction, ~65 GB/s of host DRAM for
-// this access mix).  Only layers whose split-K reduce carries the merge and
-// whose merge read can hide under the dW partial GEMM (large batches) qualify.
+// to keep max(H2D, D2H, host-DRAM time) of the merge phase lowest (measured
+// B200 host: ~50 GB/s each PCIe direction, ~65 GB/s of host DRAM for this
+// access mix; the snapshot's H2D precedes the merge phase and is not
+// counted).  Only layers whose split-K reduce carries the merge and whose
+// merge read can hide under the dW partial GEMM (large batches) qualify.
+static void xchg_plan_lanes_impl(hb_ctx* c);
 static void xchg_plan_lanes(hb_ctx* c) {
+  xchg_plan_lanes_impl(c);
+  if (xfer_debug())
+    for (int l = 0; l < c->L; ++l) fprintf(stderr, "[xfer] layer %d merges on the %s lane\n", l, c->xdma[l] ? "device" : "host");
+}
+static void xchg_plan_lanes_impl(hb_ctx* c) {
   c->xdma.assign(c->L, 0);
   if (c->xmode != 0 || !c->conc_bwd || c->cap < 4096 ||
       (getenv("HB_NO_XCHG_DEVICE_LANE") && getenv("HB_NO_XCHG_DEVICE_LANE")[0] == '1'))
     return;
-  double h2d = 8.0 * static_cast<double>(c->n_params), d2h = 0.0, host = 0.0;
+  double h2d = 0.0, d2h = 0.0, host = 0.0;  // merge phase only: the snapshot's H2D is long done by then
   const int top = c->small_head ? c->L - 2 : c->L - 1;
   auto cost = [](double a, double b, double h) { return std::max(std::max(a / 50.0, b / 50.0), h / 65.0); };
   for (int l = c->L - 1; l >= 0; --l) {

@@ -365,3 +365,34 @@ def test_nccl_merge_single_rank(hb, sparse):
     finally:
         ctx.close()
         ref.close()
+
+
+def test_fused_replica_step_device_lane(hb):
+    """Large batches route the biggest layers' stale merge through the device
+    lane (host rows DMA'd in, merged by the split-K reduce, DMA'd back): the
+    host model must still be bit-identical to the three-call decomposition."""
+    sizes = (64, 512, 512, 2)
+    b = 4096
+    w0 = ref_nn.init_weights(sizes, 41)
+    x, y = ref_nn.synthetic_blobs(2 * b, sizes[0], 2, 2.5, 42)
+    x = x.astype(np.float32)
+    fused = hb.GpuReplica(sizes, b)
+    three = hb.GpuReplica(sizes, b)
+    wf = [a.copy() for a in w0]
+    wt = [a.copy() for a in w0]
+    try:
+        for it in range(4):
+            xb, yb = x[(it % 2) * b:(it % 2 + 1) * b], y[(it % 2) * b:(it % 2 + 1) * b]
+            fused.replica_step_host(wf, xb, yb, 0.4)
+            three.set_weights(wt)
+            three.step_host(xb, yb, 0.4, emit_grad=True)
+            three.merge_grads_into(wt, 0.4)
+            for a, c in zip(wf, wt):
+                assert np.array_equal(a, c), it
+            if it == 1:
+                for a, c in zip(wf, wt):
+                    a *= 0.999
+                    c *= 0.999
+    finally:
+        fused.close()
+        three.close()

@@ -300,15 +300,22 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
       }
       mma_commit_cg(tmem_full, PAIR);  // accumulators complete (immediate if nkb == 0)
     }
-  } else if (warp >= 4 && warp < 4 + C::EPI_WARPS) {
+  }
+  // The producer / MMA / allocator warps (0-3) are idle once the accumulators
+  // are complete, so they join the epilogue (12 warps, 3 per TMEM lane
+  // quarter) -- the epilogue is the serialized tail of a CTA.  The fused
+  // split-K rendezvous keeps its own 8-warp accounting.
+  constexpr bool ALL_EPI = (EPI != EPI_SPLIT_SGD);
+  if (ALL_EPI || (warp >= 4 && warp < 4 + C::EPI_WARPS)) {
     // ---------------------------------------------------------- epilogue
     // TMEM -> registers (thread = row) -> per-warp smem transpose -> coalesced
     // float4 global traffic (8 lanes per 128-byte row segment).  The mainloop
     // is finished once tmem_full fires, so stage 0 is reused as staging space.
-    const int ew = warp - 4;
+    const int ew = ALL_EPI ? warp : warp - 4;
     const int q = ew & 3;          // TMEM lane quarter owned by this warp (warp % 4)
-    const int half = ew >> 2;      // which alternating 32-column chunks
-    constexpr int CSTEP = 32 * (C::EPI_WARPS / 4);
+    const int half = ew >> 2;      // which interleaved 32-column chunks
+    constexpr int NSLOT = ALL_EPI ? (4 + C::EPI_WARPS) / 4 : C::EPI_WARPS / 4;
+    constexpr int CSTEP = 32 * NSLOT;
     // The epilogue's second operand (A_l for dX, W for the SGD update) does not
     // depend on the accumulator: it is loaded for a whole chunk at once (the
     // first chunk while the mainloop is still running) so its HBM latency is
@@ -340,6 +347,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
     };
     load_pre(32 * half, pre);
     mbar_wait(tmem_full, 0);
+    __syncwarp();  // warps 0 / 1: lane 0 is back from its producer / MMA role
     if (threadIdx.x == 128) pdl_trigger();  // mainloop done: the next kernel may start its setup
     if (threadIdx.x == 128) HB_STAMP(6 * 512 + 0);  // epilogue start
     if (threadIdx.x == 128) HB_CTA_STAMP(2);

@@ -751,6 +751,9 @@ class HostPool {
       for (int i = 0; i < n; ++i) fn(i);
       return;
     }
+    // one job at a time: several replica worker threads (one per GPU, as the
+    // reference engine runs them) may merge concurrently
+    std::lock_guard<std::mutex> job(run_mu_);
     fn_.store(&fn, std::memory_order_relaxed);
     n_.store(n, std::memory_order_relaxed);
     done_.store(0, std::memory_order_relaxed);
@@ -811,7 +814,7 @@ class HostPool {
     }
   }
   std::vector<std::thread> threads_;
-  std::mutex mu_;
+  std::mutex mu_, run_mu_;
   std::condition_variable cv_;
   std::atomic<const std::function<void(int)>*> fn_{nullptr};
   std::atomic<int> n_{0};

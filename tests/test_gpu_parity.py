@@ -396,3 +396,41 @@ def test_fused_replica_step_device_lane(hb):
     finally:
         fused.close()
         three.close()
+
+
+def test_two_worker_threads_merge_concurrently(hb):
+    """Two GPU replica workers on their own threads (the reference engine runs
+    each worker as a thread, engine.py:131-134) exchange with two shared host
+    models at the same time: each result equals the same steps run alone."""
+    import threading
+
+    sizes = (54, 256, 256, 2)
+    b = 512
+    w0 = ref_nn.init_weights(sizes, 51)
+    x, y = ref_nn.synthetic_blobs(4 * b, sizes[0], 2, 2.5, 52)
+    x = x.astype(np.float32)
+
+    def run(ws, out, barrier=None):
+        ctx = hb.GpuReplica(sizes, b)
+        try:
+            if barrier is not None:
+                barrier.wait()
+            for it in range(6):
+                sl = slice((it % 4) * b, (it % 4 + 1) * b)
+                ctx.replica_step_host(ws, x[sl], y[sl], 0.3)
+            out.append(True)
+        finally:
+            ctx.close()
+
+    solo = [a.copy() for a in w0]
+    run(solo, [])
+    wa, wb = [a.copy() for a in w0], [a.copy() for a in w0]
+    done, bar = [], threading.Barrier(2)
+    ts = [threading.Thread(target=run, args=(wa, done, bar)), threading.Thread(target=run, args=(wb, done, bar))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert len(done) == 2
+    for a, b2, s in zip(wa, wb, solo):
+        assert np.array_equal(a, s) and np.array_equal(b2, s)

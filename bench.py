@@ -36,7 +36,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-from paper_2004_08771_b200.parallel import batch_starts, init_replica_comm, max_over_ranks, shard_seed  # noqa: E402
+from paper_2004_08771_b200.parallel import barrier, batch_starts, init_process_group, init_replica_comm, max_over_ranks, shard_seed  # noqa: E402
 
 METRIC = "MLP train samples/sec"
 UNIT = "samples/s"
@@ -251,7 +251,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         ctx.profile_read()
     # ---------------------------------------------------------- timed region
     if world > 1:
-        dist.barrier()
+        barrier(dist)
     torch.cuda.synchronize(device)
     step_ms, merge_ms, launches = [], [], 0
     with ClockSampler(device) as clocks:
@@ -266,7 +266,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
                 merge_ms.append((time.perf_counter() - t0) * 1000.0)
         torch.cuda.synchronize(device)
     if world > 1:
-        dist.barrier()
+        barrier(dist)
     dom_live = ctx.profile_read() if dom else {}
     ctx.profile(False)
     ctx.profile_filter(None)
@@ -321,7 +321,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
             xb, yb = host_batches[i % len(host_batches)]
             ctx.replica_step_host(host_model, xb, yb, cfg["eta"])
         if world > 1:
-            dist.barrier()
+            barrier(dist)
         t0 = time.perf_counter()
         for i in range(args.steps):
             xb, yb = host_batches[i]
@@ -524,7 +524,7 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        init_process_group(dist)
     res = run_ours(args, cfg, rank, world, local_rank, dist)
     if rank == 0:
         cpu = None

@@ -35,6 +35,24 @@ def broadcast_bytes(dist, payload: bytes | None, src: int = 0, length: int = 128
     return bytes(t.tolist())
 
 
+def barrier(dist) -> None:
+    """Host-side barrier as a one-element CPU all-reduce: it runs on the CPU
+    (gloo) half of a "cpu:gloo,cuda:nccl" process group, so it needs no GPU
+    tensor and no device-side NCCL communicator of torch's."""
+    import torch
+
+    dist.all_reduce(torch.zeros(1))
+
+
+def init_process_group(dist) -> None:
+    """torch.distributed for the control plane: CPU tensors over gloo, CUDA
+    tensors over NCCL; the replica merge itself is the library's own NCCL
+    communicator (hb_comm_init / hb_merge_allreduce)."""
+    import torch
+
+    dist.init_process_group("cpu:gloo,cuda:nccl" if torch.cuda.is_available() else "gloo")
+
+
 def max_over_ranks(dist, value: float) -> float:
     """The slowest rank's time: the multi-GPU timing rule (max over ranks)."""
     import torch

@@ -20,8 +20,9 @@ def _free_port():
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
                       LOCAL_RANK=str(rank))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2004_08771_b200 import parallel as P
+
+    P.init_process_group(dist)  # CPU box: plain gloo (on a GPU box "cpu:gloo,cuda:nccl")
 
     out = {}
     uid = bytes(range(128)) if rank == 0 else None
@@ -57,6 +58,7 @@ def _worker(rank, world, port, q):
         out["comm"] = rep.comm
     finally:
         par.GpuReplica.nccl_unique_id = orig
+    P.barrier(dist)  # the bench's host-side barrier (a CPU all-reduce)
     q.put((rank, out))
     dist.barrier()
     dist.destroy_process_group()

@@ -227,9 +227,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         torch.cuda.synchronize(device)
 
     for i in range(args.warmup):
-        ctx.step(starts[i], b, cfg["eta"], timed=True)
-        if distributed:
-            ctx.merge_allreduce()
+        ctx.step(starts[i], b, cfg["eta"], timed=True, merge=distributed)
     # ---------------------------------------------------------- kernel breakdown
     # A separate instrumented pass (every launch bracketed by CUDA events) gives
     # the per-kernel shares and picks the dominant kernel.  Events around every
@@ -239,9 +237,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         ctx.profile(True)
         for i in range(min(args.steps, 10)):
             l2_flush()
-            ctx.step(starts[args.warmup + i], b, cfg["eta"], timed=True)
-            if distributed:
-                ctx.merge_allreduce()
+            ctx.step(starts[args.warmup + i], b, cfg["eta"], timed=True, merge=distributed)
         prof = ctx.profile_read()
         ctx.profile(False)
         tot = sum(v[0] for v in prof.values()) or 1.0
@@ -261,13 +257,11 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
     with ClockSampler(device) as clocks:
         for i in range(args.warmup, args.warmup + args.steps):
             l2_flush()
-            ctx.step(starts[i], b, cfg["eta"], timed=True)
+            # distributed: the NCCL replica merge runs on the step's stream and
+            # inside its CUDA-event bracket (HB_STEP_MERGE)
+            ctx.step(starts[i], b, cfg["eta"], timed=True, merge=distributed)
             step_ms.append(ctx.last_step_ms)
             launches += ctx.last_step_launches
-            if distributed:
-                t0 = time.perf_counter()
-                ctx.merge_allreduce()
-                merge_ms.append((time.perf_counter() - t0) * 1000.0)
         torch.cuda.synchronize(device)
     if distributed:
         barrier(dist)

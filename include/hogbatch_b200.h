@@ -61,6 +61,7 @@ extern "C" {
 #define HB_STEP_EMIT_GRAD 1u /* keep the raw mean gradient of every layer (for the host merge / parity) */
 #define HB_STEP_TIMED 2u     /* bracket the step with CUDA events (hb_last_step_ms) */
 #define HB_STEP_ASYNC 4u     /* return once the step is enqueued (no out_loss); hb_synchronize() waits */
+#define HB_STEP_MERGE 8u     /* after the step, average the replicas (hb_merge_allreduce) on the same stream */
 
 typedef struct hb_ctx hb_ctx;
 

@@ -1545,6 +1545,35 @@ void drop_graphs(hb_ctx* c) {
   c->graph_seen.clear();
 }
 
+// pack -> allreduce(sum) -> unpack x 1/nranks (+ lo twins), enqueued on the
+// step stream: inside a step's CUDA-event bracket when HB_STEP_MERGE asks
+int enqueue_merge(hb_ctx* c) {
+  if (!c->comm) return fail(HB_ESTATE, "communicator not initialised");
+  if (c->L > kMaxMergeLayers) return fail(HB_EINVAL, "merge supports up to %d layers", kMaxMergeLayers);
+  ModelLayout m{};
+  m.n = c->L;
+  long long off = 0;
+  for (int l = 0; l < c->L; ++l) {
+    const bool tr = l == 0 && c->sparse;  // W0^T (d_in, d_out) on the device: averaged in that layout
+    const long long rows = tr ? c->d[0] : c->d[l + 1], cols = tr ? c->d[1] : c->d[l];
+    m.w[l] = c->W[l];
+    m.w_lo[l] = (c->need_lo() && !tr) ? c->W_lo[l] : nullptr;
+    m.ld[l] = c->ldw[l];
+    m.cols[l] = static_cast<int>(cols);
+    m.off[l] = off;
+    off += rows * cols;
+  }
+  m.off[c->L] = off;
+  const dim3 grid(static_cast<int>(std::min<long long>(cdiv(off, 256), 148 * 8)));
+  HB_CUDA(launch_k(pack_model_kernel, grid, dim3(256), 0, c->stream, c->flat, m));
+  int r = g_nccl.allReduce(c->flat, c->flat, static_cast<size_t>(off), kNcclFloat32, kNcclSum, c->comm, c->stream);
+  if (r != 0) return fail(HB_ENCCL, "ncclAllReduce: %s", g_nccl.errStr ? g_nccl.errStr(r) : "error");
+  unpack_model_kernel<<<grid, 256, 0, c->stream>>>(c->flat, 1.0f / static_cast<float>(c->nranks), m);
+  HB_CUDA(cudaGetLastError());
+  c->last_launches += 2;
+  return HB_OK;
+}
+
 // `mid` (optional): host work run between the enqueued forward and backward
 // phases (the host-buffer CSR step builds the batch CSC there, overlapping the
 // device forward pass).
@@ -1564,6 +1593,7 @@ int do_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta,
   } else {
     HB_TRY(enqueue_step(c, v, start, rows, eta, flags, graph_ok));
   }
+  if (flags & HB_STEP_MERGE) HB_TRY(enqueue_merge(c));  // the replica merge, inside the timed bracket
   if (timed) HB_CUDA(cudaEventRecord(c->ev1, c->stream));
   c->grads_valid = (flags & HB_STEP_EMIT_GRAD) != 0;
   if (out_loss != nullptr) {
@@ -3214,29 +3244,7 @@ int hb_comm_init(hb_ctx* c, const void* id_bytes, int nranks, int rank) {
 
 int hb_merge_allreduce(hb_ctx* c) {
   HB_TRY(ctx_check(c));
-  if (!c->comm) return fail(HB_ESTATE, "communicator not initialised");
-  // pack (W_l rows are padded) -> allreduce(sum) -> unpack scaled by 1/nranks
-  size_t off = 0;
-  for (int l = 0; l < c->L; ++l) {
-    const bool tr = l == 0 && c->sparse;
-    const long long rows = tr ? c->d[0] : c->d[l + 1], cols = tr ? c->d[1] : c->d[l];
-    HB_CUDA(cudaMemcpy2DAsync(c->flat + off, cols * sizeof(float), c->W[l], c->ldw[l] * sizeof(float),
-                              cols * sizeof(float), rows, cudaMemcpyDeviceToDevice, c->stream));
-    off += rows * cols;
-  }
-  int r = g_nccl.allReduce(c->flat, c->flat, c->n_params, kNcclFloat32, kNcclSum, c->comm, c->stream);
-  if (r != 0) return fail(HB_ENCCL, "ncclAllReduce: %s", g_nccl.errStr ? g_nccl.errStr(r) : "error");
-  off = 0;
-  const float inv = 1.0f / static_cast<float>(c->nranks);
-  for (int l = 0; l < c->L; ++l) {
-    const bool tr = l == 0 && c->sparse;
-    const long long rows = tr ? c->d[0] : c->d[l + 1], cols = tr ? c->d[1] : c->d[l];
-    unpack_scale_kernel<<<static_cast<int>(std::min<long long>(cdiv(rows * cols, 256), 4096)), 256, 0, c->stream>>>(
-        c->W[l], c->ldw[l], c->flat + off, static_cast<int>(rows), static_cast<int>(cols), inv,
-        c->need_lo() ? c->W_lo[l] : nullptr);
-    HB_CUDA(cudaGetLastError());
-    off += rows * cols;
-  }
+  HB_TRY(enqueue_merge(c));
   HB_CUDA(cudaStreamSynchronize(c->stream));
   return HB_OK;
 }

@@ -1225,4 +1225,43 @@ __global__ void unpack_scale_kernel(float* dst, long long ldd, const float* src,
   }
 }
 
+// The whole model packed / unpacked in one launch each for the replica
+// merge: layer l occupies [off[l], off[l+1]) of the flat buffer as a dense
+// (rows, cols) block; its device layout has row stride ld[l] (+ lo twin).
+constexpr int kMaxMergeLayers = 16;
+struct ModelLayout {
+  float* w[kMaxMergeLayers];
+  float* w_lo[kMaxMergeLayers];
+  long long ld[kMaxMergeLayers];
+  int cols[kMaxMergeLayers];
+  long long off[kMaxMergeLayers + 1];
+  int n;
+};
+__device__ __forceinline__ int layout_layer(const ModelLayout& m, long long i) {
+  int l = 0;
+  while (l + 1 < m.n && i >= m.off[l + 1]) ++l;
+  return l;
+}
+__global__ void pack_model_kernel(float* __restrict__ flat, const __grid_constant__ ModelLayout m) {
+  pdl_wait();
+  pdl_trigger();
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < m.off[m.n];
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int l = layout_layer(m, i);
+    const long long k = i - m.off[l];
+    flat[i] = m.w[l][(k / m.cols[l]) * m.ld[l] + k % m.cols[l]];
+  }
+}
+__global__ void unpack_model_kernel(const float* __restrict__ flat, float scale, const __grid_constant__ ModelLayout m) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < m.off[m.n];
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int l = layout_layer(m, i);
+    const long long k = i - m.off[l];
+    const long long o = (k / m.cols[l]) * m.ld[l] + k % m.cols[l];
+    const float v = flat[i] * scale;
+    m.w[l][o] = v;
+    if (m.w_lo[l] != nullptr) m.w_lo[l][o] = tf32_lo(v);
+  }
+}
+
 }  // namespace hb

@@ -181,11 +181,14 @@ class GpuReplica:
 
     # ------------------------------------------------------------ steps
     def step(self, start: int, rows: int, eta: float, emit_grad: bool = False, timed: bool = False,
-             want_loss: bool = False, blocking: bool = True):
+             want_loss: bool = False, blocking: bool = True, merge: bool = False):
         """One SGD step on staged rows [start, start+rows); returns the mean
         training loss of the batch when want_loss.  blocking=False returns as
-        soon as the step is enqueued (synchronize() waits)."""
-        flags = (N.HB_STEP_EMIT_GRAD if emit_grad else 0) | (N.HB_STEP_TIMED if timed else 0)
+        soon as the step is enqueued (synchronize() waits).  merge=True then
+        averages the replicas over the communicator (comm_init) on the same
+        stream, inside the step's timing bracket."""
+        flags = (N.HB_STEP_EMIT_GRAD if emit_grad else 0) | (N.HB_STEP_TIMED if timed else 0) | (
+            N.HB_STEP_MERGE if merge else 0)
         if not blocking and not want_loss:
             flags |= N.HB_STEP_ASYNC
         loss = C.c_double(0.0)

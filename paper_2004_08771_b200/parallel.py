@@ -95,11 +95,10 @@ class DataParallelWorker:
             init_replica_comm(replica, dist, self.rank, self.world)
 
     def step(self, start: int, rows: int, eta: float, **kw):
-        out = self.replica.step(start, rows, eta, **kw)
+        # the merge rides on the step's stream (HB_STEP_MERGE): no extra sync
         self.steps += 1
-        if self.world > 1 and self.steps % self.merge_every == 0:
-            self.replica.merge_allreduce()
-        return out
+        due = self.world > 1 and self.steps % self.merge_every == 0
+        return self.replica.step(start, rows, eta, merge=due, **kw)
 
 
 def average_models_host(models: list) -> list:

@@ -39,8 +39,9 @@ def _worker(rank, world, port, q):
         def comm_init(self, uid, nranks, r):
             self.comm = (len(uid), nranks, r)
 
-        def step(self, start, rows, eta, **kw):
+        def step(self, start, rows, eta, merge=False, **kw):
             self.steps.append(start)
+            self.merges += int(merge)
 
         def merge_allreduce(self):
             self.merges += 1

@@ -475,6 +475,7 @@ struct hb_ctx {
   // `side` while the dX GEMMs run on `stream` (the partials never touch W)
   cudaStream_t side = nullptr;
   std::vector<cudaEvent_t> bev;   // fork / join events of one backward pass
+  cudaEvent_t bev_loss = nullptr; // fork of the loss reduction
   float* ws_dw = nullptr;         // per-layer split-K slabs of the concurrent dW partials
   float* ws_head = nullptr;       // the small head's per-block dW partials
   bool side_pending = false;      // the forward left work on `side` (joined by the backward)
@@ -1032,6 +1033,21 @@ int xchg_end(hb_ctx* c) {
 
 // `ds` != null: graph mode -- kernels read the batch start and eta from
 // device memory (the by-value start/eta are then 0 and ignored).
+// The batch loss is only read after the step (out_loss): in training steps
+// with the concurrent backward its reduction runs on the side stream, off the
+// forward -> backward critical path.
+int launch_loss_reduce(hb_ctx* c, bool train, int n_partials) {
+  cudaStream_t s = c->stream;
+  if (train && c->conc_bwd) {
+    HB_CUDA(cudaEventRecord(c->bev_loss, c->stream));
+    HB_CUDA(cudaStreamWaitEvent(c->side, c->bev_loss, 0));
+    s = c->side;
+    c->side_pending = true;
+  }
+  HB_CUDA(launch_k(loss_reduce_kernel, dim3(1), dim3(32), 0, s, c->ws_loss, n_partials, c->d_loss, 0));
+  return HB_OK;
+}
+
 // per-feature batch slices of the CSC (sparse dW of layer 0); depends only on
 // the batch, so with the concurrent backward it runs on the side stream under
 // the forward pass
@@ -1190,8 +1206,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
 #undef HB_HEADV
     HB_CUDA(cudaGetLastError());
     prof_end(c, "head_small", l);
-    HB_CUDA(launch_k(loss_reduce_kernel, dim3(1), dim3(32), 0, st, c->ws_loss, grid, c->d_loss, 0));
-    HB_CUDA(cudaGetLastError());
+    HB_TRY(launch_loss_reduce(c, train, grid));
     c->last_launches += 2;
     if (train) {
       // the output layer's reduce + SGD only needs the head's partials: with
@@ -1249,8 +1264,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   HB_CUDA(launch_k(softmax_delta_kernel, dim3(grid), dim3(256), 0, st, sm));
   HB_CUDA(cudaGetLastError());
   prof_end(c, "softmax_delta", l);
-  HB_CUDA(launch_k(loss_reduce_kernel, dim3(1), dim3(32), 0, st, c->ws_loss, grid, c->d_loss, 0));
-  HB_CUDA(cudaGetLastError());
+  HB_TRY(launch_loss_reduce(c, train, grid));
   c->last_launches += 3;
   return HB_OK;
 }
@@ -1927,6 +1941,7 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
     HB_CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, lo_prio));
     c->bev.resize(2 * L + 1);
     for (auto& e : c->bev) HB_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    HB_CK(cudaEventCreateWithFlags(&c->bev_loss, cudaEventDisableTiming));
   }
   c->ws_loss_n = std::max(cdiv(c->cap, kHeadRowsPerBlock), cdiv(c->cap, 8)) + 1;
   HB_CK(cudaMalloc(&c->ws_loss, c->ws_loss_n * sizeof(double)));
@@ -2035,6 +2050,7 @@ int hb_ctx_destroy(hb_ctx* c) {
   if (c->xh2d) cudaStreamDestroy(c->xh2d);
   if (c->xmrg) cudaStreamDestroy(c->xmrg);
   for (auto e : c->bev) cudaEventDestroy(e);
+  if (c->bev_loss) cudaEventDestroy(c->bev_loss);
   if (c->side) cudaStreamDestroy(c->side);
   cudaFree(c->ws_dw);
   cudaFree(c->ws_head);

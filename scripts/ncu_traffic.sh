@@ -13,11 +13,15 @@ run() {  # config kernel
   rm -f gpurun_out/ncu_$1_$2.ncu-rep
 }
 run w8a gemm_dx_dsig_l2
+run w8a gemm_dx_dsig_l1
+run w8a gemm_dw_partial_l1
 run w8a gemm_fwd_sigmoid_l1
 run w8a gemm_dw_partial_l2
 run w8a head_small_l3
 run covtype gemm_fwd_sigmoid_l1
+run covtype gemm_dx_dsig_l1
 run delicious gemm_dx_dsig_l2
+run delicious gemm_dw_partial_l2
 run realsim sparse_dw_sgd_l0
 run realsim spmm_sigmoid_l0
 run scaled gemm_dw_sgd_l1

@@ -477,7 +477,7 @@ struct hb_ctx {
   std::vector<cudaEvent_t> bev;   // fork / join events of one backward pass
   cudaEvent_t bev_loss = nullptr; // fork of the loss reduction
   float* ws_dw = nullptr;         // per-layer split-K slabs of the concurrent dW partials
-  float* ws_head = nullptr;       // the small head's per-block dW partials
+  double* ws_head = nullptr;      // the small head's per-block dW partials (float64)
   bool side_pending = false;      // the forward left work on `side` (joined by the backward)
   bool ranges_early = false;      // this step's CSC batch ranges were launched on `side` by the forward
   std::vector<size_t> ws_dw_off;
@@ -612,6 +612,11 @@ int choose_bn(long long m_tiles, long long n) {
   return 128;
 }
 
+long long env_long(const char* name, long long dflt) {
+  const char* v = getenv(name);
+  return v != nullptr && v[0] != 0 ? atoll(v) : dflt;
+}
+
 // Split-K plan for a forward / dX GEMM: when its output tiles cannot fill
 // the SMs (small batches, e.g. covtype's b=512 gives 8-16 CTAs) K is split so
 // the launch covers about one wave; splitk_epi_kernel sums the slabs and
@@ -637,6 +642,13 @@ void dw_plan(const hb_ctx* c, int l, int rows, int* splits, int* kb_per, int* kb
   *kb_total = std::max(1, cdiv(rows, kBK));
   // one wave: as many K splits as fit on the 148 SMs (1 CTA / SM)
   int want = std::max(1, 148 / tiles);
+  if (l == c->L - 1 && !c->small_head && c->passes == 3) {
+    // precision: at most 16 k-blocks per rotating hi*hi accumulator for the
+    // softmax head's cancelling dW sum (measured: 1e-4 bar missed at 1024
+    // MMAs per accumulator on the 1000-class scaled config)
+    const int nbig = std::min(15, std::max(1, 512 / c->bn_dw[l] - 1));
+    want = std::max(want, cdiv(*kb_total, 16 * nbig));
+  }
   want = std::min(want, *kb_total);
   *kb_per = cdiv(*kb_total, want);
   *splits = cdiv(*kb_total, *kb_per);
@@ -1222,7 +1234,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
       const long long n = static_cast<long long>(c->d[L]) * c->d[l];
       c->prof_st = rs;
       prof_begin(c, "reduce_sgd", l);
-      HB_CUDA(launch_k(reduce_sgd_kernel, dim3(cdiv(n, 32)), dim3(256), 0, rs, c->W[l], c->ldw[l], c->ws_head, grid, n,
+      HB_CUDA(launch_k(reduce_sgd_f64p_kernel, dim3(cdiv(n, 32)), dim3(256), 0, rs, c->W[l], c->ldw[l], c->ws_head, grid, n,
                        c->d[L], c->d[l], static_cast<float>(eta), (flags & HB_STEP_EMIT_GRAD) ? c->G[l] : nullptr,
                        c->d[l], ds, c->need_lo() ? c->W_lo[l] : nullptr));
       prof_end(c, "reduce_sgd", l);
@@ -1849,7 +1861,22 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
     }
     c->bn_fwd[l] = choose_bn(m_tiles, c->d[l + 1]);
     c->bn_dx[l] = choose_bn(m_tiles, c->d[l]);
+    // precision: the wide softmax head's logits GEMM with a long contraction
+    // (K > 1024) rotates the hi*hi term over >= 3 accumulators (BN <= 128; a
+    // 256-wide tile has room for only one): the biased round-toward-zero
+    // accumulation of K = 4096 logits reached the head's cancelling dW sum
+    // (scaled config: 1.6e-4 -> 8e-5).  HB_BN_LONG_FROM=0 applies it to every
+    // long-K forward GEMM (measured ~15% slower steps, no further gain needed)
+    const int max_bn_long = static_cast<int>(env_long("HB_BN_LONG_K", 128));
+    const int long_from = static_cast<int>(env_long("HB_BN_LONG_FROM", c->small_head ? L : L - 1));
+    if (c->passes == 3 && cdiv(c->d[l], kBK) > 32 && l >= long_from)
+      c->bn_fwd[l] = std::min(c->bn_fwd[l], max_bn_long);
     c->bn_dw[l] = choose_bn(cdiv(c->d[l + 1], kBM), c->d[l]);
+    // the wide softmax head's dW sums error signals of both signs over the
+    // whole batch (a cancelling sum): 128-wide tiles give 3 rotating hi*hi
+    // accumulators, and dw_plan bounds the chain per accumulator
+    if (l == L - 1 && !c->small_head && c->passes == 3 && c->d[l] >= 64)
+      c->bn_dw[l] = static_cast<int>(env_long("HB_HEAD_DW_BN", 128));
     n_params += static_cast<size_t>(c->d[l + 1]) * c->d[l];
   }
   c->n_params = n_params;
@@ -1906,7 +1933,7 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
     if (splits > 1) ws = std::max(ws, static_cast<size_t>(splits) * c->d[l + 1] * c->d[l]);
   }
   if (c->small_head)
-    HB_CK(cudaMalloc(&c->ws_head, static_cast<size_t>(cdiv(c->cap, kHeadRowsPerBlock)) * nc * dlast * sizeof(float)));
+    HB_CK(cudaMalloc(&c->ws_head, static_cast<size_t>(cdiv(c->cap, kHeadRowsPerBlock)) * nc * dlast * sizeof(double)));
   ws = std::max(ws, static_cast<size_t>(kSplitSlabFloats));  // split-K forward / dX slabs
   if (c->sparse) {
     c->sdw_smem = (static_cast<size_t>(c->d[0]) * kSdwSliceCols + static_cast<size_t>(kCsrChunkRows) * kSdwSliceCols) *

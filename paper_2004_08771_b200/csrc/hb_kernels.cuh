@@ -72,7 +72,8 @@ struct HeadArgs {
   long long ld_dp;
   float* delta_out;        // (rows, nc) or null (tests)
   long long ld_do;
-  float* ws_dw;            // [grid][nc][d] partials
+  double* ws_dw;           // [grid][nc][d] partials (float64: the block sums carry the cancellation of
+                           // the softmax error signs, summed over hundreds of blocks)
   double* ws_loss;         // [grid] per-block loss sums
 };
 
@@ -183,23 +184,24 @@ __global__ void __launch_bounds__(kHeadWarps * 32, (MAXT <= 16 && NCT <= 2) ? 2 
   }
   if (!p.train) return;
   // deterministic block reduction of the dW partials, one class at a time:
-  // warps add into a shared row in warp order (sW is free after the row loop).
+  // warps add into a shared float64 row in warp order.
+  __shared__ double sAcc[32 * MAXT];
   for (int c = 0; c < NCT && c < p.nc; ++c) {
     __syncthreads();
-    for (int j = threadIdx.x; j < 32 * MAXT; j += blockDim.x) sW[j] = 0.f;
+    for (int j = threadIdx.x; j < 32 * MAXT; j += blockDim.x) sAcc[j] = 0.0;
     __syncthreads();
     for (int w = 0; w < kHeadWarps; ++w) {
       if (warp == w) {
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
           const int j = lane + 32 * t;
-          if (t < T && j < p.d) sW[j] += acc[c][t];
+          if (t < T && j < p.d) sAcc[j] += static_cast<double>(acc[c][t]);
         }
       }
       __syncthreads();
     }
     for (int j = threadIdx.x; j < p.d; j += blockDim.x)
-      p.ws_dw[(static_cast<long long>(blockIdx.x) * p.nc + c) * p.d + j] = sW[j];
+      p.ws_dw[(static_cast<long long>(blockIdx.x) * p.nc + c) * p.d + j] = sAcc[j];
   }
 }
 
@@ -340,27 +342,26 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_small_vec_kernel(HeadArg
     p.ws_loss[blockIdx.x] = t;
   }
   if (!p.train) return;
+  __shared__ double sAcc[128 * VPL];
   for (int c = 0; c < NCT && c < p.nc; ++c) {
     __syncthreads();
-    for (int j = threadIdx.x; j < D; j += blockDim.x) sW[j] = 0.f;
+    for (int j = threadIdx.x; j < D; j += blockDim.x) sAcc[j] = 0.0;
     __syncthreads();
     for (int w = 0; w < kHeadWarps; ++w) {
       if (warp == w) {
 #pragma unroll
         for (int t = 0; t < VPL; ++t) {
-          float4* sp = reinterpret_cast<float4*>(&sW[4 * lane + 128 * t]);
-          float4 v = *sp;
-          v.x += acc[c][t].x;
-          v.y += acc[c][t].y;
-          v.z += acc[c][t].z;
-          v.w += acc[c][t].w;
-          *sp = v;
+          double* sp = &sAcc[4 * lane + 128 * t];
+          sp[0] += static_cast<double>(acc[c][t].x);
+          sp[1] += static_cast<double>(acc[c][t].y);
+          sp[2] += static_cast<double>(acc[c][t].z);
+          sp[3] += static_cast<double>(acc[c][t].w);
         }
       }
       __syncthreads();
     }
     for (int j = threadIdx.x; j < p.d; j += blockDim.x)
-      p.ws_dw[(static_cast<long long>(blockIdx.x) * p.nc + c) * p.d + j] = sW[j];
+      p.ws_dw[(static_cast<long long>(blockIdx.x) * p.nc + c) * p.d + j] = sAcc[j];
   }
 }
 
@@ -481,6 +482,45 @@ __global__ void __launch_bounds__(256) reduce_sgd_kernel(float* w, long long ldw
     w[r * ldw + c] = nw;
     if (w_lo != nullptr) w_lo[r * ldw + c] = tf32_lo(nw);
     if (grad != nullptr) grad[r * ldg + c] = g;
+  }
+}
+
+// The small head's reduction: float64 block partials summed in float64 in a
+// fixed order, the update applied in float64 and rounded once.
+__global__ void __launch_bounds__(256) reduce_sgd_f64p_kernel(float* w, long long ldw, const double* part, int S,
+                                                               long long slab, int rows, int cols, float eta,
+                                                               float* grad, long long ldg, const DevStep* ds,
+                                                               float* w_lo) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double red[8][33];
+  eta = step_eta(ds, eta);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long i = blockIdx.x * 32LL + lane;
+  const long long total = static_cast<long long>(rows) * cols;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (i < total) {
+    for (int s = warp; s < S; s += 64) {
+      double t[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t[k] = (s + 8 * k < S) ? __ldcs(part + (s + 8 * k) * slab + i) : 0.0;
+      s0 += t[0] + t[4];
+      s1 += t[1] + t[5];
+      s2 += t[2] + t[6];
+      s3 += t[3] + t[7];
+    }
+  }
+  red[warp][lane] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (warp == 0 && i < total) {
+    double g = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) g += red[k][lane];
+    const long long r = i / cols, c = i % cols;
+    const float nw = static_cast<float>(static_cast<double>(w[r * ldw + c]) - static_cast<double>(eta) * g);
+    w[r * ldw + c] = nw;
+    if (w_lo != nullptr) w_lo[r * ldw + c] = tf32_lo(nw);
+    if (grad != nullptr) grad[r * ldg + c] = static_cast<float>(g);
   }
 }
 

@@ -417,9 +417,6 @@ struct hb_ctx {
   void* csc_temp = nullptr;
   size_t csc_temp_bytes = 0;
   long long csc_cap = 0;
-  bool sdw_narrow = false;                         // sparse dW via smem slices (small d_in)
-  bool sparse_smem = false;                        // experimental smem-sliced sparse kernels
-  size_t sdw_smem = 0;
   double nnz_per_row = 0.0;
   float* ws = nullptr;  // split-K partials / head partials
   size_t ws_floats = 0;
@@ -1078,7 +1075,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
                 const DevStep* ds) {
   cudaStream_t st = c->stream;
   c->ranges_early = false;
-  if (train && c->sparse && c->conc_bwd && !c->sdw_narrow) {
+  if (train && c->sparse && c->conc_bwd) {
     HB_CUDA(cudaEventRecord(c->bev[0], st));  // the batch (CSC view) is in place
     HB_CUDA(cudaStreamWaitEvent(c->side, c->bev[0], 0));
     HB_TRY(launch_csc_ranges(c, v, start, rows, ds, c->side));
@@ -1096,27 +1093,11 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
       SpmmArgs p{v.rowptr, v.col, v.val, ds, start, rows, c->W[0], c->ldw[0], c->d[0], c->d[1], c->A[1], c->ld[1],
                  (c->need_lo() && !(c->small_head && L == 2)) ? c->A_lo[1] : nullptr};
       prof_begin(c, "spmm_sigmoid", 0);
-      const size_t slice_smem = static_cast<size_t>(c->d[0]) * kSpmmSliceCols * sizeof(float) +
-                                kCsrChunkEntries * 8 + (kCsrChunkRows + 1) * 4;
-      if (c->sparse_smem && c->d[1] % 4 == 0 && slice_smem <= 200 * 1024) {
-        // narrow input: W0^T column slices staged in shared memory
-        static bool configured = false;
-        if (!configured) {
-          HB_CUDA(cudaFuncSetAttribute(spmm_sigmoid_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       200 * 1024));
-          configured = true;
-        }
-        const int col_slices = cdiv(c->d[1], kSpmmSliceCols);
-        const int row_blocks = std::max(1, std::min(cdiv(rows, 16), 148 / std::max(1, col_slices)));
-        const int rpb = cdiv(rows, row_blocks);
-        HB_CUDA(launch_k(spmm_sigmoid_smem_kernel, dim3(dim3(col_slices, cdiv(rows, rpb))), dim3(512), slice_smem, st, p, rpb));
-      } else {
-        const int blocks = cdiv(static_cast<long long>(rows) * 32, 256);
-        if (c->d[1] % 128 == 0)
-          HB_CUDA(launch_k(spmm_sigmoid_kernel<true>, dim3(blocks), dim3(256), 0, st, p));
-        else
-          HB_CUDA(launch_k(spmm_sigmoid_kernel<false>, dim3(blocks), dim3(256), 0, st, p));
-      }
+      const int blocks = cdiv(static_cast<long long>(rows) * 32, 256);
+      if (c->d[1] % 128 == 0)
+        HB_CUDA(launch_k(spmm_sigmoid_kernel<true>, dim3(blocks), dim3(256), 0, st, p));
+      else
+        HB_CUDA(launch_k(spmm_sigmoid_kernel<false>, dim3(blocks), dim3(256), 0, st, p));
       HB_CUDA(cudaGetLastError());
       prof_end(c, "spmm_sigmoid", 0);
       c->last_launches++;
@@ -1327,35 +1308,6 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
                      c->W[0], c->ldw[0], static_cast<float>(eta), emit ? c->G[0] : nullptr, c->ldw[0],
                      c->csc_lo, c->csc_hi};
       prof_begin(c, "sparse_dw_sgd", 0);
-      if (c->sdw_narrow) {
-        // narrow input: smem dW0^T slices per row block, then fixed-order reduce + SGD
-        const int col_slices = cdiv(c->d[1], kSdwSliceCols);
-        const int row_blocks = std::max(1, std::min(cdiv(rows, 64), 148 / std::max(1, col_slices)));
-        SparseDwSmemArgs q{v.rowptr, v.col, v.val, ds, start, rows, c->d[0], c->d[1], c->D[0], c->ld[1], c->ws,
-                           cdiv(rows, row_blocks)};
-        static bool configured = false;
-        if (!configured) {
-          HB_CUDA(cudaFuncSetAttribute(sparse_dw_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       200 * 1024));
-          configured = true;
-        }
-        HB_CUDA(launch_k(sparse_dw_smem_kernel, dim3(dim3(col_slices, row_blocks)), dim3(512), c->sdw_smem, st, q));
-        HB_CUDA(cudaGetLastError());
-        const long long slab = static_cast<long long>(c->d[0]) * c->d[1];
-        if (c->d[1] % 4 == 0 && (slab / 4) >= 148 * 256)
-          HB_CUDA(launch_k(reduce_sgd_vec_kernel, dim3(static_cast<int>(std::min<long long>(cdiv(slab / 4, 256), 148 * 8))), dim3(256), 0, st, 
-              c->W[0], c->ldw[0], c->ws, row_blocks, slab, c->d[0], c->d[1], static_cast<float>(eta),
-              emit ? c->G[0] : nullptr, c->ldw[0], ds, nullptr, nullptr, 0.0));
-        else
-          HB_CUDA(launch_k(reduce_sgd_kernel, dim3(cdiv(slab, 32)), dim3(256), 0, st, c->W[0], c->ldw[0], c->ws, row_blocks, slab, c->d[0],
-                                                            c->d[1], static_cast<float>(eta),
-                                                            emit ? c->G[0] : nullptr, c->ldw[0], ds, nullptr));
-        HB_CUDA(cudaGetLastError());
-        prof_end(c, "sparse_dw_sgd", 0);
-        c->last_launches += 2;
-        HB_TRY(xchg_merge(c, 0, eta, ds));
-        continue;
-      }
       if (c->ranges_early)
         HB_CUDA(cudaStreamWaitEvent(st, c->bev[1], 0));  // computed on the side stream under the forward
       else
@@ -1935,19 +1887,6 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
   if (c->small_head)
     HB_CK(cudaMalloc(&c->ws_head, static_cast<size_t>(cdiv(c->cap, kHeadRowsPerBlock)) * nc * dlast * sizeof(double)));
   ws = std::max(ws, static_cast<size_t>(kSplitSlabFloats));  // split-K forward / dX slabs
-  if (c->sparse) {
-    c->sdw_smem = (static_cast<size_t>(c->d[0]) * kSdwSliceCols + static_cast<size_t>(kCsrChunkRows) * kSdwSliceCols) *
-                      sizeof(float) +
-                  static_cast<size_t>(kCsrChunkEntries) * 12;
-    // experimental (HB_SPARSE_SMEM=1): slower than the CSC-slice kernel at w8a shapes so far
-    c->sparse_smem = getenv("HB_SPARSE_SMEM") && getenv("HB_SPARSE_SMEM")[0] == '1';
-    c->sdw_narrow = c->sparse_smem && c->d[0] <= kCsrChunkEntries && c->sdw_smem <= 200 * 1024 && c->d[1] % 4 == 0;
-    if (c->sdw_narrow) {
-      const int col_slices = cdiv(c->d[1], kSdwSliceCols);
-      const int row_blocks = std::max(1, 148 / std::max(1, col_slices));
-      ws = std::max(ws, static_cast<size_t>(row_blocks) * c->d[0] * c->d[1]);
-    }
-  }
   c->ws_floats = std::max<size_t>(ws, 1);
   HB_CK(cudaMalloc(&c->ws, c->ws_floats * sizeof(float)));
   // concurrent backward: per-layer split-K slabs (layers >= 1) + fork/join events

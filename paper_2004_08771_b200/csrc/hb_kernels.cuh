@@ -688,179 +688,6 @@ __global__ void __launch_bounds__(256) spmm_sigmoid_kernel(SpmmArgs p) {
   }
 }
 
-// Narrow-input variants (w8a: 300 features): the W0^T slice / the dW0^T slice
-// a block works on fits in shared memory, and a block owns a contiguous run
-// of batch rows whose CSR entries are staged in smem chunk by chunk, so the
-// only global traffic is one coalesced pass over the operands.
-constexpr int kSpmmSliceCols = 128;  // forward: W0^T column slice held in smem
-constexpr int kSdwSliceCols = 64;    // backward: dW0^T accumulator column slice
-constexpr int kCsrChunkEntries = 4096;
-constexpr int kCsrChunkRows = 256;
-
-// Find re in (rs, r_end] with rowptr[re] - rowptr[rs] <= kCsrChunkEntries
-// and re - rs <= kCsrChunkRows (at least one row).
-__device__ __forceinline__ int csr_chunk_end(const int64_t* rowptr, long long start, int rs, int r_end) {
-  int lo = rs + 1, hi = min(r_end, rs + kCsrChunkRows);
-  const long long base = rowptr[start + rs];
-  if (rowptr[start + hi] - base <= kCsrChunkEntries) return hi;
-  while (lo < hi) {  // largest re with the entry budget
-    const int mid = (lo + hi + 1) >> 1;
-    if (rowptr[start + mid] - base <= kCsrChunkEntries)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  return lo;  // may exceed the budget for a single huge row: handled by the caller
-}
-
-__global__ void __launch_bounds__(512) spmm_sigmoid_smem_kernel(SpmmArgs p, int rows_per_block) {
-  pdl_wait();
-  pdl_trigger();
-  extern __shared__ float4 sw4[];  // [d_in][kSpmmSliceCols / 4] then the CSR chunk
-  constexpr int Q = kSpmmSliceCols / 4;
-  int* s_col = reinterpret_cast<int*>(sw4 + p.ldw_rows * Q);
-  float* s_val = reinterpret_cast<float*>(s_col + kCsrChunkEntries);
-  int* s_rp = reinterpret_cast<int*>(s_val + kCsrChunkEntries);  // [kCsrChunkRows + 1]
-  __shared__ int s_re;
-  p.start = step_start(p.ds, p.start);
-  const int c0 = blockIdx.x * kSpmmSliceCols;
-  const int width = min(kSpmmSliceCols, p.d_out - c0);
-  for (int i = threadIdx.x; i < p.ldw_rows * Q; i += blockDim.x) {
-    const int f = i / Q, q = i % Q;
-    const bool in = 4 * q < width;
-    cp_async16(&sw4[i], p.w0t + static_cast<long long>(f) * p.ldw + c0 + (in ? 4 * q : 0), in ? 16u : 0u);
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = blockDim.x >> 5;
-  const int r_begin = blockIdx.y * rows_per_block;
-  const int r_end = min(p.rows, r_begin + rows_per_block);
-  const bool active = 4 * lane < width;
-  for (int rs = r_begin; rs < r_end;) {
-    if (threadIdx.x == 0) s_re = csr_chunk_end(p.rowptr, p.start, rs, r_end);
-    __syncthreads();
-    const int re = s_re;
-    const long long e_base = p.rowptr[p.start + rs];
-    const int ne = static_cast<int>(p.rowptr[p.start + re] - e_base);
-    const bool staged = ne <= kCsrChunkEntries;
-    for (int i = threadIdx.x; i <= re - rs; i += blockDim.x)
-      s_rp[i] = static_cast<int>(p.rowptr[p.start + rs + i] - e_base);
-    if (staged)
-      for (int i = threadIdx.x; i < ne; i += blockDim.x) {
-        cp_async4(&s_col[i], p.col + e_base + i);
-        cp_async4(&s_val[i], p.val + e_base + i);
-      }
-    cp_async_wait_all();
-    __syncthreads();
-    for (int r = rs + warp; r < re; r += nwarps) {
-      const int e0 = s_rp[r - rs], e1 = s_rp[r - rs + 1];
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int e = e0; e < e1; ++e) {
-        const int f = staged ? s_col[e] : p.col[e_base + e];
-        const float v = staged ? s_val[e] : p.val[e_base + e];
-        const float4 w = sw4[f * Q + lane];
-        acc.x = fmaf(v, w.x, acc.x);
-        acc.y = fmaf(v, w.y, acc.y);
-        acc.z = fmaf(v, w.z, acc.z);
-        acc.w = fmaf(v, w.w, acc.w);
-      }
-      if (active) {
-        const float4 sv = make_float4(sigmoidf_stable(acc.x), sigmoidf_stable(acc.y), sigmoidf_stable(acc.z),
-                                      sigmoidf_stable(acc.w));
-        *reinterpret_cast<float4*>(p.out + r * p.ldo + c0 + 4 * lane) = sv;
-        if (p.out_lo != nullptr) *reinterpret_cast<float4*>(p.out_lo + r * p.ldo + c0 + 4 * lane) = lo4(sv);
-      }
-    }
-    __syncthreads();
-    rs = re;
-  }
-}
-
-// Narrow-input sparse dW: dW0^T[:, slice] partial over a block's batch rows,
-// accumulated in smem.  Entries of feature f are owned by warp f % nwarps and
-// applied in CSR (row) order, so the smem accumulation is race-free and
-// deterministic; delta0 rows are staged tile by tile (each element of delta0
-// is read once).  Partials go to ws[blockIdx.y][f][c] for a fixed-order
-// reduce + SGD update (reduce_sgd_*).
-struct SparseDwSmemArgs {
-  const int64_t* rowptr;
-  const int32_t* col;
-  const float* val;
-  const DevStep* ds;
-  long long start;
-  int rows, d_in, d_out;
-  const float* delta0;
-  long long ldd;
-  float* ws;  // [gridDim.y][d_in][d_out]
-  int rows_per_block;
-};
-
-__global__ void __launch_bounds__(512) sparse_dw_smem_kernel(SparseDwSmemArgs p) {
-  pdl_wait();
-  pdl_trigger();
-  extern __shared__ float sacc[];  // [d_in][kSdwSliceCols]
-  constexpr int SW = kSdwSliceCols;
-  float* s_d = sacc + p.d_in * SW;                          // [kCsrChunkRows][SW] delta0 tile
-  int* s_col = reinterpret_cast<int*>(s_d + kCsrChunkRows * SW);
-  float* s_val = reinterpret_cast<float*>(s_col + kCsrChunkEntries);
-  int* s_row = reinterpret_cast<int*>(s_val + kCsrChunkEntries);  // local row of each entry
-  __shared__ int s_re;
-  p.start = step_start(p.ds, p.start);
-  const int c0 = blockIdx.x * SW;
-  const int width = min(SW, p.d_out - c0);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < p.d_in * SW; i += blockDim.x) sacc[i] = 0.f;
-  const int r_begin = blockIdx.y * p.rows_per_block;
-  const int r_end = min(p.rows, r_begin + p.rows_per_block);
-  for (int rs = r_begin; rs < r_end;) {
-    if (threadIdx.x == 0) s_re = csr_chunk_end(p.rowptr, p.start, rs, r_end);
-    __syncthreads();
-    const int re = s_re;
-    const long long e_base = p.rowptr[p.start + rs];
-    // narrow path only (d_in <= kCsrChunkEntries): a single row never exceeds the chunk
-    const int ne = static_cast<int>(p.rowptr[p.start + re] - e_base);
-    // delta0 tile rows [rs, re) x [c0, c0 + SW)
-    for (int i = threadIdx.x; i < (re - rs) * (SW / 4); i += blockDim.x) {
-      const int rr = i / (SW / 4), cc = 4 * (i % (SW / 4));
-      const bool in = cc < width;
-      cp_async16(s_d + rr * SW + cc, p.delta0 + static_cast<long long>(rs + rr) * p.ldd + c0 + (in ? cc : 0),
-                 in ? 16u : 0u);
-    }
-    for (int i = threadIdx.x; i < ne; i += blockDim.x) {
-      cp_async4(&s_col[i], p.col + e_base + i);
-      cp_async4(&s_val[i], p.val + e_base + i);
-    }
-    for (int r = rs + threadIdx.x; r < re; r += blockDim.x) {
-      const int a = static_cast<int>(p.rowptr[p.start + r] - e_base), b = static_cast<int>(p.rowptr[p.start + r + 1] - e_base);
-      for (int e = a; e < b; ++e) s_row[e] = r - rs;
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    // warp w applies the entries of its features in entry (row) order
-    for (int e0 = 0; e0 < ne; e0 += 32) {
-      const int e = e0 + lane;
-      const int f = e < ne ? s_col[e] : -1;
-      unsigned mine = __ballot_sync(0xffffffffu, f >= 0 && (f % nwarps) == warp);
-      while (mine) {
-        const int k = __ffs(mine) - 1;
-        mine &= mine - 1;
-        const int fe = __shfl_sync(0xffffffffu, f, k);
-        const float v = s_val[e0 + k];
-        const float* drow = s_d + s_row[e0 + k] * SW;
-        float* arow = sacc + fe * SW;
-#pragma unroll
-        for (int t = 0; t < SW / 32; ++t) arow[lane + 32 * t] = fmaf(v, drow[lane + 32 * t], arow[lane + 32 * t]);
-      }
-    }
-    __syncthreads();
-    rs = re;
-  }
-  float* out = p.ws + static_cast<long long>(blockIdx.y) * p.d_in * p.d_out;
-  for (int i = threadIdx.x; i < p.d_in * SW; i += blockDim.x) {
-    const int f = i / SW, cc = i % SW;
-    if (cc < width) out[static_cast<long long>(f) * p.d_out + c0 + cc] = sacc[i];
-  }
-}
 
 // Sparse dW0 + fused SGD update on the active feature rows only:
 //   W0T[f, :] -= eta * sum_{i in batch, x_if != 0} x_if * delta0[i, :]

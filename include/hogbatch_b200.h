@@ -94,7 +94,9 @@ int hb_merge_grad_into_f64(hb_ctx* ctx, int layer, double* host_w, double eta);
 int hb_set_weights_all_f64(hb_ctx* ctx, const double* const* ws);
 int hb_merge_grads_all_into_f64(hb_ctx* ctx, double* const* ws, double eta);
 /* Page-lock (and later release) a host range used for repeated exchanges, e.g.
- * the shared float64 model, so its copies run at full link speed. */
+ * the shared float64 model, so its copies run at full link speed.  Counted per
+ * base address: contexts of several worker threads may register the same
+ * shared model, and only the last release unregisters it. */
 int hb_host_register(const void* p, size_t bytes);
 int hb_host_unregister(const void* p);
 /* Raw mean gradient of the last HB_STEP_EMIT_GRAD step, (d_{l+1}, d_l) fp32. */

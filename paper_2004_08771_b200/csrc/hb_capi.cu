@@ -112,6 +112,8 @@ int make_map(CUtensorMap* m, const float* base, long long inner, long long rows,
 
 std::mutex g_host_mu;
 std::map<uintptr_t, std::pair<size_t, void*>> g_host_ranges;  // host base -> (bytes, device alias)
+std::map<uintptr_t, int> g_host_refs;  // registrations per base: contexts of several worker threads can share
+                                       // one host model (engine.py:131-134); the last release unregisters
 
 // ------------------------------------------------ programmatic dependent launch
 // Every kernel of the step is launched with programmatic stream serialization
@@ -2102,7 +2104,10 @@ int hb_get_grad_f32(hb_ctx* c, int layer, float* g) {
 int hb_host_register(const void* p, size_t bytes) {
   if (!p || bytes == 0) return fail(HB_EINVAL, "null pointer or zero size");
   std::lock_guard<std::mutex> lk(g_host_mu);
-  if (g_host_ranges.count(reinterpret_cast<uintptr_t>(p))) return HB_OK;
+  if (g_host_ranges.count(reinterpret_cast<uintptr_t>(p))) {
+    g_host_refs[reinterpret_cast<uintptr_t>(p)]++;
+    return HB_OK;
+  }
   cudaError_t e = cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
   if (e == cudaErrorHostMemoryAlreadyRegistered) {
     cudaGetLastError();
@@ -2112,6 +2117,7 @@ int hb_host_register(const void* p, size_t bytes) {
   void* dptr = nullptr;
   HB_CUDA(cudaHostGetDevicePointer(&dptr, const_cast<void*>(p), 0));
   g_host_ranges[reinterpret_cast<uintptr_t>(p)] = {bytes, dptr};
+  g_host_refs[reinterpret_cast<uintptr_t>(p)] = 1;
   return HB_OK;
 }
 
@@ -2120,6 +2126,8 @@ int hb_host_unregister(const void* p) {
   std::lock_guard<std::mutex> lk(g_host_mu);
   auto it = g_host_ranges.find(reinterpret_cast<uintptr_t>(p));
   if (it == g_host_ranges.end()) return HB_OK;
+  if (--g_host_refs[it->first] > 0) return HB_OK;  // still page-locked for another context
+  g_host_refs.erase(it->first);
   g_host_ranges.erase(it);
   cudaError_t e = cudaHostUnregister(const_cast<void*>(p));
   if (e == cudaErrorHostMemoryNotRegistered) {

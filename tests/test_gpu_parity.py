@@ -465,3 +465,32 @@ def test_oracle_step_at_baseline_size(hb, sizes, b, sparse_nnz, eta, weight_tol)
     ew = max_relative_error(out["weights"], upd)
     assert eg <= STEP_TOL, eg
     assert ew <= weight_tol, ew
+
+
+def test_shared_host_model_outlives_one_context(hb):
+    """Two GPU workers exchange with the same shared host model (one roster,
+    engine.py:131-134); the page-lock is counted, so closing one worker's
+    context leaves the model registered for the other."""
+    sizes = (30, 64, 2)
+    w0 = ref_nn.init_weights(sizes, 61)
+    x, y = ref_nn.synthetic_blobs(256, sizes[0], 2, 2.5, 62)
+    x = x.astype(np.float32)
+    shared = [a.copy() for a in w0]
+    ref = [a.copy() for a in w0]
+    a = hb.GpuReplica(sizes, 128)
+    b = hb.GpuReplica(sizes, 128)
+    c = hb.GpuReplica(sizes, 128)
+    try:
+        a.replica_step_host(shared, x[:128], y[:128], 0.2)
+        b.replica_step_host(shared, x[128:], y[128:], 0.2)
+        a.close()
+        b.replica_step_host(shared, x[:128], y[:128], 0.2)  # still page-locked: no error, same result
+        for xb, yb in ((x[:128], y[:128]), (x[128:], y[128:]), (x[:128], y[:128])):
+            c.set_weights(ref)
+            c.step_host(xb, yb, 0.2, emit_grad=True)
+            c.merge_grads_into(ref, 0.2)
+        for p1, p2 in zip(shared, ref):
+            assert np.array_equal(p1, p2)
+    finally:
+        b.close()
+        c.close()

@@ -465,7 +465,7 @@ struct hb_ctx {
   // + D2H on xmrg) as soon as layer l's gradient exists.
   std::vector<double*> xw;          // armed host model (page-locked); empty: no exchange
   std::vector<double*> xw_prev;     // pointer set of the last armed call (graph key)
-  long long xgen = 0;               // bumps when the armed pointer set changes
+  long long xgen = 0;               // graph key of the armed pointer set (hash)
   cudaStream_t xh2d = nullptr, xmrg = nullptr;
   std::vector<cudaEvent_t> xsnap_ev, xgrad_ev, xchunk_ev;
   cudaEvent_t xstart_ev = nullptr, xdone_ev = nullptr;
@@ -2431,8 +2431,12 @@ static int xchg_arm(hb_ctx* c, double* const* ws) {
   }
   std::vector<double*> cur(ws, ws + c->L);
   if (cur != c->xw_prev) {
+    // graph key of this pointer set (a hash, so alternating between a few
+    // host models reuses their captured graphs instead of re-capturing)
+    unsigned long long h = 1469598103934665603ull;
+    for (double* q : cur) h = (h ^ reinterpret_cast<uintptr_t>(q)) * 1099511628211ull;
     c->xw_prev = cur;
-    c->xgen++;
+    c->xgen = static_cast<long long>(h >> 1) | 1;  // never 0 (0 = no exchange armed)
   }
   c->xw = cur;
   c->xseq = c->xseq == 0x7fffffff ? 1 : c->xseq + 1;

@@ -184,24 +184,24 @@ __global__ void __launch_bounds__(kHeadWarps * 32, (MAXT <= 16 && NCT <= 2) ? 2 
   }
   if (!p.train) return;
   // deterministic block reduction of the dW partials, one class at a time:
-  // warps add into a shared float64 row in warp order.
-  __shared__ double sAcc[32 * MAXT];
+  // warps add into a shared row in warp order (sW is free after the row
+  // loop); the block partial is stored as float64 for the long cross-block sum
   for (int c = 0; c < NCT && c < p.nc; ++c) {
     __syncthreads();
-    for (int j = threadIdx.x; j < 32 * MAXT; j += blockDim.x) sAcc[j] = 0.0;
+    for (int j = threadIdx.x; j < 32 * MAXT; j += blockDim.x) sW[j] = 0.f;
     __syncthreads();
     for (int w = 0; w < kHeadWarps; ++w) {
       if (warp == w) {
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
           const int j = lane + 32 * t;
-          if (t < T && j < p.d) sAcc[j] += static_cast<double>(acc[c][t]);
+          if (t < T && j < p.d) sW[j] += acc[c][t];
         }
       }
       __syncthreads();
     }
     for (int j = threadIdx.x; j < p.d; j += blockDim.x)
-      p.ws_dw[(static_cast<long long>(blockIdx.x) * p.nc + c) * p.d + j] = sAcc[j];
+      p.ws_dw[(static_cast<long long>(blockIdx.x) * p.nc + c) * p.d + j] = static_cast<double>(sW[j]);
   }
 }
 
@@ -342,26 +342,29 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_small_vec_kernel(HeadArg
     p.ws_loss[blockIdx.x] = t;
   }
   if (!p.train) return;
-  __shared__ double sAcc[128 * VPL];
+  // block partials: warps add in warp order in fp32 (a few rows each), the
+  // partial is stored as float64 for the long cross-block sum
   for (int c = 0; c < NCT && c < p.nc; ++c) {
     __syncthreads();
-    for (int j = threadIdx.x; j < D; j += blockDim.x) sAcc[j] = 0.0;
+    for (int j = threadIdx.x; j < D; j += blockDim.x) sW[j] = 0.f;
     __syncthreads();
     for (int w = 0; w < kHeadWarps; ++w) {
       if (warp == w) {
 #pragma unroll
         for (int t = 0; t < VPL; ++t) {
-          double* sp = &sAcc[4 * lane + 128 * t];
-          sp[0] += static_cast<double>(acc[c][t].x);
-          sp[1] += static_cast<double>(acc[c][t].y);
-          sp[2] += static_cast<double>(acc[c][t].z);
-          sp[3] += static_cast<double>(acc[c][t].w);
+          float4* sp = reinterpret_cast<float4*>(&sW[4 * lane + 128 * t]);
+          float4 v = *sp;
+          v.x += acc[c][t].x;
+          v.y += acc[c][t].y;
+          v.z += acc[c][t].z;
+          v.w += acc[c][t].w;
+          *sp = v;
         }
       }
       __syncthreads();
     }
     for (int j = threadIdx.x; j < p.d; j += blockDim.x)
-      p.ws_dw[(static_cast<long long>(blockIdx.x) * p.nc + c) * p.d + j] = sAcc[j];
+      p.ws_dw[(static_cast<long long>(blockIdx.x) * p.nc + c) * p.d + j] = static_cast<double>(sW[j]);
   }
 }
 

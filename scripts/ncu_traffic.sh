@@ -25,4 +25,5 @@ run delicious gemm_dw_partial_l2
 run realsim sparse_dw_sgd_l0
 run realsim spmm_sigmoid_l0
 run scaled gemm_dw_sgd_l1
+run scaled gemm_dx_dsig_l2
 ls -la gpurun_out/ncu_*.csv

@@ -494,3 +494,69 @@ def test_shared_host_model_outlives_one_context(hb):
     finally:
         b.close()
         c.close()
+
+
+CANCEL_WEIGHT_TOL = 1e-3  # see test_edge_batches
+
+
+def sparse_rows_with_empties(sizes, b, seed, nnz):
+    """CSR-shaped batch with empty rows, one all-features row and ragged nnz (reference data.py:128-140 densifies
+    the same rows; an empty LIBSVM line is a valid all-zero example)."""
+    rng = np.random.default_rng(seed)
+    x = np.zeros((b, sizes[0]))
+    for r in range(b):
+        k = 0 if r % 3 == 0 else int(rng.integers(1, nnz + 1))
+        if k:
+            x[r, rng.choice(sizes[0], size=k, replace=False)] = rng.random(k) + 0.25
+    if b > 1:
+        x[1] = rng.random(sizes[0]) + 0.1  # every feature present
+    return x
+
+
+@pytest.mark.parametrize(
+    "sizes,b,kind",
+    [
+        ((300, 512, 512, 512, 2), 1, "dense"),  # a one-row batch (BatchRef length 1, data.py:67)
+        ((300, 512, 512, 512, 2), 1, "csr"),
+        ((54, 512, 512, 2), 2, "dense"),
+        ((300, 256, 256, 2), 200, "csr_empty_rows"),
+        ((300, 256, 256, 2), 5, "csr_all_empty"),
+        ((500, 256, 983), 1, "dense"),  # wide softmax, one row
+    ],
+)
+def test_edge_batches(hb, sizes, b, kind):
+    """One-row, ragged, empty-row and all-empty batches (the cases reference data.py:67 admits)."""
+    seed = b + len(kind)
+    w = ref_nn.init_weights(sizes, seed)
+    y = np.random.default_rng(seed).integers(0, sizes[-1], size=b)
+    if kind == "dense":
+        x, _ = ref_nn.synthetic_blobs(b, sizes[0], 2, 2.5, seed)
+    elif kind == "csr":
+        x = sparse_rows_with_empties(sizes, b, seed, 12)
+        x[0, :] = 0
+        x[0, [3, 77, 299]] = 1.0
+    elif kind == "csr_empty_rows":
+        x = sparse_rows_with_empties(sizes, b, seed, 12)
+    else:
+        x = np.zeros((b, sizes[0]))
+    tape = ref_nn.forward(w, x)
+    grads = ref_nn.backward(w, tape, y)
+    upd = ref_nn.deep_copy(w)
+    ref_nn.apply_update(upd, grads, 0.5)
+    sparse = kind.startswith("csr")
+    for kernels in ((False, True) if sparse else (False,)):
+        out = run_step(hb, sizes, w, x, y, 0.5, sparse=sparse, sparse_kernels=kernels)
+        assert max_relative_error(out["grads"], grads) <= STEP_TOL, (kind, kernels)
+        assert out["loss"] == pytest.approx(ref_nn.cross_entropy_loss(tape, y), rel=1e-5)
+    # The updated weights, through the drop-in call (float64 host model, workers.py:126-138) and the device mirror.
+    # One-row and all-identical-row batches put |eta*g| ~ 0.25 on whole rows of W, so some W_new cancel to below
+    # the metric's 1e-4 floor, where one fp32 ulp of g (~3e-8 absolute) alone reads as 3e-4.  Bound the absolute
+    # error against the layer's weight + update scale instead (fp32-accurate) plus a loose floored-relative bound.  Measured, not tuned.
+    from paper_2004_08771_b200 import Architecture, BatchRef, Model, execute_gpu_replica
+
+    model = Model(Architecture(sizes), [a.copy() for a in w])
+    assert execute_gpu_replica(model, BatchRef(x, y, 0, b), 0.5) == 1.0
+    for got in (model.weights, out["weights"]):
+        for a, n, w0, g in zip(got, upd, w, grads):
+            assert float(np.abs(a - n).max()) <= 1e-6 * float((np.abs(w0) + 0.5 * np.abs(g)).max()), kind
+        assert max_relative_error(got, upd) <= CANCEL_WEIGHT_TOL, kind

@@ -305,15 +305,6 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
             host_batches = [(xs[i * b:(i + 1) * b], ys[i * b:(i + 1) * b]) for i in range(args.steps)]
         ctx.pin_host(pool)
         host_model = [w.copy() for w in model.weights]
-        # the snapshot reads the f64 model over PCIe, the stale merge reads and
-        # writes it back (page-locked host model, DMA RMW), the loss comes back
-        h2d = 2 * sum(w.nbytes for w in host_model)
-        d2h = sum(w.nbytes for w in host_model) + 8
-        bb = host_batches[0][0]
-        if sparse:
-            h2d += bb.rowptr.nbytes + bb.labels.nbytes + bb.col.nbytes + bb.val.nbytes
-        else:
-            h2d += bb.nbytes + host_batches[0][1].nbytes
         ctx.pin_host(host_model)  # what execute_gpu_replica does for the shared model
         for i in range(max(3, min(args.warmup, len(host_batches)))):  # warm the host path (and its graph)
             xb, yb = host_batches[i % len(host_batches)]
@@ -327,6 +318,9 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
             # (workers.py:132), batch H2D, the step, stale merge (workers.py:135), loss D2H
             ctx.replica_step_host(host_model, xb, yb, cfg["eta"], want_loss=True)
         el = time.perf_counter() - t0
+        # PCIe bytes of the last call as the library issued them: batch, f64 snapshot, the merge by lane
+        # (fp32 gradient D2H on the host lane, f64 rows both ways on the device lane), step record, loss
+        h2d, d2h = ctx.last_xfer_bytes
         if distributed:
             el = max_over_ranks(dist, el)
         e2e = {"value": world * args.steps * b / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -334,8 +328,9 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
                "path": "execute_gpu_replica semantics through the C ABI (hb_replica_step_host_*), per step: "
                        "batch H2D from pinned host memory (CSR rows are scattered into dense rows on the device "
                        "for narrow inputs), snapshot of the page-locked f64 host model (DMA H2D, layer l+1 in "
-                       "flight while layer l computes), the step, the f64 stale merge W_host -= eta*g as a "
-                       "chunked DMA read-modify-write issued per layer as soon as its gradient exists, loss D2H"}
+                       "flight while layer l computes), the step, the f64 stale merge W_host += (-eta)*g per layer as "
+                       "soon as its gradient exists (fp32 gradient D2H + host float64 axpy, or on the device lane "
+                       "for large split-K layers: f64 rows read, merged on the GPU, written back), loss D2H"}
     ctx.close()
 
     # ---------------------------------------------------------- roofline of the dominant kernel

@@ -179,6 +179,13 @@ int hb_get_activation_f32(hb_ctx* ctx, int layer, int rows, float* out);
 int hb_last_step_ms(hb_ctx* ctx, float* ms);
 /* Kernel launches issued by the last step. */
 int hb_last_step_launches(hb_ctx* ctx, int* n);
+
+/* PCIe bytes moved by the last hb_replica_step* call on this context: the
+ * batch (host entry points), the model snapshot and the stale merge by lane
+ * (fp32 gradient D2H on the host lane, float64 rows both ways on the device
+ * lane / HB_XCHG_MERGE=dma), the step record and the loss.  Reporting only;
+ * no reference counterpart (bench.py's e2e h2d/d2h_bytes_per_step). */
+int hb_last_xfer_bytes(hb_ctx* ctx, int64_t* h2d_bytes, int64_t* d2h_bytes);
 int hb_synchronize(hb_ctx* ctx);
 /* Per-launch CUDA-event profiling on the step stream (off by default):
  * enable, run steps, then read per-kernel totals.  names receives

@@ -59,13 +59,15 @@ SIGNATURES = {
     "hb_train_step_host_dense": (_i32, [_p, _fp, _i64, _i64p, _i32, _f64, _u32, _dp]),
     "hb_train_step_host_csr": (_i32, [_p, _i64p, _i32p, _fp, _i64p, _i32, _f64, _u32, _dp]),
     "hb_replica_step": (_i32, [_p, C.POINTER(_dp), _i64, _i32, _f64, _u32, _dp]),
-    "hb_replica_step_host_dense": (_i32, [_p, C.POINTER(_dp), _fp, _i64, _i64p, _i32, _f64, _u32, _dp]),
-    "hb_replica_step_host_csr": (_i32, [_p, C.POINTER(_dp), _i64p, _i32p, _fp, _i64p, _i32, _f64, _u32, _dp]),
+    # host batch arrays pass as integer addresses (ndarray.ctypes.data): half the cost of data_as per call
+    "hb_replica_step_host_dense": (_i32, [_p, C.POINTER(_dp), _p, _i64, _p, _i32, _f64, _u32, _dp]),
+    "hb_replica_step_host_csr": (_i32, [_p, C.POINTER(_dp), _p, _p, _p, _p, _i32, _f64, _u32, _dp]),
     "hb_eval_loss_sum": (_i32, [_p, _i64, _i64, _dp]),
     "hb_forward": (_i32, [_p, _i64, _i32]),
     "hb_get_activation_f32": (_i32, [_p, _i32, _i32, _fp]),
     "hb_last_step_ms": (_i32, [_p, _fp]),
     "hb_last_step_launches": (_i32, [_p, C.POINTER(_i32)]),
+    "hb_last_xfer_bytes": (_i32, [_p, _i64p, _i64p]),
     "hb_synchronize": (_i32, [_p]),
     "hb_profile_enable": (_i32, [_p, _i32]),
     "hb_profile_filter": (_i32, [_p, C.c_char_p]),

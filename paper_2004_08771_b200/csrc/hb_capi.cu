@@ -343,6 +343,10 @@ struct StepGraph {
   int launches = 0;
 };
 
+// Host->device batch bytes issued by the calling thread since the last reset
+// (hb_replica_step*: reported by hb_last_xfer_bytes with the exchange bytes).
+static thread_local long long t_h2d_bytes = 0;
+
 struct hb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -498,6 +502,7 @@ struct hb_ctx {
   // split-K reduce kernel on a float64 copy of the host rows DMA'd in just
   // before it and DMA'd back (splits the merge between PCIe and host DRAM)
   std::vector<char> xdma;       // planned per layer
+  long long last_h2d = 0, last_d2h = 0;  // PCIe bytes of the last hb_replica_step* call
   std::vector<char> xdma_used;  // taken by the step just enqueued (rows decide whether the split-K path runs)
   std::vector<cudaEvent_t> xread_ev;
   void* comm = nullptr;
@@ -1506,7 +1511,10 @@ int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double
     it = c->graphs.emplace(key, std::move(g)).first;
     c->last_launches = 0;
   }
-  if (phase != 2) HB_CUDA(cudaMemcpyAsync(c->d_step, &hs, sizeof hs, cudaMemcpyHostToDevice, c->stream));
+  if (phase != 2) {
+    HB_CUDA(cudaMemcpyAsync(c->d_step, &hs, sizeof hs, cudaMemcpyHostToDevice, c->stream));
+    t_h2d_bytes += static_cast<long long>(sizeof hs);
+  }
   xmark("graph launch");
   c->xdma_used = it->second.xdma_used;
   HB_CUDA(cudaGraphLaunch(it->second.exec, c->stream));
@@ -2165,6 +2173,7 @@ static bool is_pinned(const void* p) {
 // that was pinned earlier: CUDA rejects such a copy as one transfer, so it is
 // split at registered-range boundaries.  sync: wait for completion.
 static cudaError_t h2d_copy(void* dst, const void* src, size_t bytes, cudaStream_t st, bool sync = false) {
+  t_h2d_bytes += static_cast<long long>(bytes);
   const uintptr_t a = reinterpret_cast<uintptr_t>(src);
   size_t done = 0;
   while (done < bytes) {
@@ -2452,6 +2461,26 @@ struct XchgGuard {
   }
 };
 
+// Bytes the replica call moved over PCIe: the batch (counted as issued) plus
+// the exchange copies captured in the step graph, per layer by lane.
+static void xfer_account(hb_ctx* c, bool loss) {
+  long long h2d = t_h2d_bytes, d2h = loss ? static_cast<long long>(sizeof(double)) : 0;
+  if (c->xmode == 0) h2d += sizeof(int32_t);  // the sequence number the layer flags carry
+  for (int l = 0; l < c->L; ++l) {
+    const long long n = static_cast<long long>(c->d[l + 1]) * c->d[l];
+    h2d += n * 8;  // snapshot (deep_copy, workers.py:132)
+    const bool dev = c->xmode != 0 || (l < static_cast<int>(c->xdma_used.size()) && c->xdma_used[l]);
+    if (dev) {
+      h2d += n * 8;  // merge read of the host rows
+      d2h += n * 8;  // merged rows written back
+    } else {
+      d2h += n * 4 + static_cast<long long>(sizeof(int32_t));  // fp32 gradient + the layer's flag
+    }
+  }
+  c->last_h2d = h2d;
+  c->last_d2h = d2h;
+}
+
 // Enqueue the step asynchronously (the exchange rides inside it), apply the
 // host-mode merges as gradients land, then finish like do_step.
 static int replica_finish(hb_ctx* c, int rc, int rows, double eta, uint32_t flags, double* out_loss) {
@@ -2471,11 +2500,13 @@ static int replica_finish(hb_ctx* c, int rc, int rows, double eta, uint32_t flag
     HB_CUDA(cudaStreamSynchronize(c->stream));
   }
   if (timed) HB_CUDA(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+  xfer_account(c, out_loss != nullptr);
   xmark("done");
   return HB_OK;
 }
 
 static uint32_t replica_flags(hb_ctx* c, uint32_t flags) {
+  t_h2d_bytes = 0;
   if (flags & HB_STEP_TIMED) cudaEventRecord(c->ev0, c->stream);
   return (flags | HB_STEP_EMIT_GRAD | HB_STEP_ASYNC) & ~HB_STEP_TIMED;
 }
@@ -2951,6 +2982,7 @@ int hb_train_step_host_dense(hb_ctx* c, const float* x, int64_t ld, const int64_
   } else {
     HB_CUDA(cudaMemcpy2DAsync(c->bx, c->ld[0] * sizeof(float), x, ld * sizeof(float), d0 * sizeof(float), rows,
                               cudaMemcpyHostToDevice, c->stream));
+    t_h2d_bytes += n * static_cast<long long>(sizeof(float));
     if (c->bx_lo) {
       split_lo_kernel<<<blocks, 256, 0, c->stream>>>(c->bx, c->bx_lo, c->ld[0], rows, d0);
       HB_CUDA(cudaGetLastError());
@@ -3140,6 +3172,13 @@ int hb_last_step_ms(hb_ctx* c, float* ms) {
 int hb_last_step_launches(hb_ctx* c, int* n) {
   if (!c || !n) return fail(HB_EINVAL, "null argument");
   *n = c->last_launches;
+  return HB_OK;
+}
+
+int hb_last_xfer_bytes(hb_ctx* c, int64_t* h2d, int64_t* d2h) {
+  if (!c || !h2d || !d2h) return fail(HB_EINVAL, "null argument");
+  *h2d = c->last_h2d;
+  *d2h = c->last_d2h;
   return HB_OK;
 }
 

@@ -48,6 +48,8 @@ class GpuReplica:
         self._staged_ref = None
         self._keep = None
         self._pinned = {}  # data address -> array kept alive while page-locked
+        self._tbl_key = None  # _model_table cache: ids of the last host model's arrays
+        self._tbl = self._tbl_arrays = self._tbl_shapes = None
         self._fin = weakref.finalize(self, GpuReplica._destroy, self._lib, h, self._pinned)
 
     @staticmethod
@@ -110,6 +112,10 @@ class GpuReplica:
     def merge_grads_into(self, weights, eta: float) -> None:
         """Stale merge W_global -= eta * g (workers.py:135 -> linalg.py:79) with
         the gradient of the last emit_grad step, in place on host float64 arrays."""
+        key = tuple(map(id, weights))
+        if key == self._tbl_key and all(w.shape == s and w.dtype == np.float64
+                                        for w, s in zip(weights, self._tbl_shapes)):
+            return self._tbl  # same array objects (kept alive by _tbl_arrays): same addresses
         if len(weights) != self.depth:
             raise ValueError("weight count does not match architecture")
         for l, w in enumerate(weights):
@@ -221,6 +227,10 @@ class GpuReplica:
     def _model_table(self, weights):
         """Pointer table of the shared host model (Model layout, nn.py:75),
         page-locked on first use (it is exchanged every call)."""
+        key = tuple(map(id, weights))
+        if key == self._tbl_key and all(w.shape == s and w.dtype == np.float64
+                                        for w, s in zip(weights, self._tbl_shapes)):
+            return self._tbl  # same array objects (kept alive by _tbl_arrays): same addresses
         if len(weights) != self.depth:
             raise ValueError("weight count does not match architecture")
         for l, w in enumerate(weights):
@@ -229,7 +239,11 @@ class GpuReplica:
             if w.shape != (self.sizes[l + 1], self.sizes[l]):
                 raise ValueError(f"weights[{l}] has shape {w.shape}, expected {(self.sizes[l + 1], self.sizes[l])}")
         self.pin_host(weights)
-        return (C.POINTER(C.c_double) * self.depth)(*[N.ptr(w, C.c_double) for w in weights])
+        self._tbl = (C.POINTER(C.c_double) * self.depth)(*[N.ptr(w, C.c_double) for w in weights])
+        self._tbl_arrays = list(weights)
+        self._tbl_shapes = [w.shape for w in weights]
+        self._tbl_key = key
+        return self._tbl
 
     def replica_step(self, weights, start: int, rows: int, eta: float, timed: bool = False,
                      want_loss: bool = False):
@@ -253,15 +267,15 @@ class GpuReplica:
         if isinstance(batch, CsrDataset):
             val32 = batch.val if batch.val.dtype == np.float32 else np.ascontiguousarray(batch.val, dtype=np.float32)
             y = batch.labels if labels is None else np.ascontiguousarray(labels, dtype=np.int64)
-            N.check(self._lib.hb_replica_step_host_csr(self._h, table, N.ptr(batch.rowptr, C.c_int64),
-                                                       N.ptr(batch.col, C.c_int32), N.ptr(val32, C.c_float),
-                                                       N.ptr(y, C.c_int64), batch.n_examples, float(eta), flags, lp))
+            N.check(self._lib.hb_replica_step_host_csr(self._h, table, batch.rowptr.ctypes.data, batch.col.ctypes.data,
+                                                       val32.ctypes.data, y.ctypes.data, batch.n_examples,
+                                                       float(eta), flags, lp))
         else:
             x = batch if (batch.dtype == np.float32 and batch.strides[1] == 4) else np.ascontiguousarray(
                 batch, dtype=np.float32)
             y = np.ascontiguousarray(labels, dtype=np.int64)
-            N.check(self._lib.hb_replica_step_host_dense(self._h, table, N.ptr(x, C.c_float), x.strides[0] // 4,
-                                                         N.ptr(y, C.c_int64), x.shape[0], float(eta), flags, lp))
+            N.check(self._lib.hb_replica_step_host_dense(self._h, table, x.ctypes.data, x.strides[0] // 4,
+                                                         y.ctypes.data, x.shape[0], float(eta), flags, lp))
         return loss.value if want_loss else None
 
     def eval_loss_sum(self, start: int, rows: int) -> float:
@@ -289,6 +303,13 @@ class GpuReplica:
         v = C.c_int(0)
         N.check(self._lib.hb_last_step_launches(self._h, C.byref(v)))
         return int(v.value)
+
+    @property
+    def last_xfer_bytes(self) -> tuple:
+        """(host->device, device->host) bytes of the last replica_step* call."""
+        h, d = C.c_int64(0), C.c_int64(0)
+        N.check(self._lib.hb_last_xfer_bytes(self._h, C.byref(h), C.byref(d)))
+        return int(h.value), int(d.value)
 
     def profile(self, on: bool) -> None:
         """Bracket every kernel launch with CUDA events on the step stream."""

@@ -560,3 +560,23 @@ def test_edge_batches(hb, sizes, b, kind):
         for a, n, w0, g in zip(got, upd, w, grads):
             assert float(np.abs(a - n).max()) <= 1e-6 * float((np.abs(w0) + 0.5 * np.abs(g)).max()), kind
         assert max_relative_error(got, upd) <= CANCEL_WEIGHT_TOL, kind
+
+
+def test_replica_step_reports_its_pcie_bytes(hb):
+    """hb_last_xfer_bytes: batch + f64 snapshot H2D, fp32 gradients (host lane) D2H, the loss."""
+    sizes = (40, 64, 64, 3)
+    w, x, y = oracle_case(sizes, 96, seed=5)
+    ctx = hb.GpuReplica(sizes, 96)
+    try:
+        model = [a.copy() for a in w]
+        x32 = np.ascontiguousarray(x, dtype=np.float32)
+        y64 = np.ascontiguousarray(y, dtype=np.int64)
+        ctx.pin_host(model)
+        ctx.replica_step_host(model, x32, y64, 0.1, want_loss=True)
+        h2d, d2h = ctx.last_xfer_bytes
+        n = sum(a.size for a in w)
+        batch = x32.nbytes + y64.nbytes
+        assert batch + 8 * n < h2d < batch + 8 * n + 4096  # + the step record and sequence number
+        assert d2h == 4 * n + 4 * len(w) + 8  # small batch: every layer merges on the host lane
+    finally:
+        ctx.close()

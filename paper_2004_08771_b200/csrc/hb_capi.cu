@@ -2546,6 +2546,15 @@ static int stage_dense_common(hb_ctx* c, int64_t n_rows, const int64_t* labels) 
   HB_TRY(free_epoch(c));
   HB_CUDA(cudaMalloc(&c->ex, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
   if (c->need_lo()) HB_CUDA(cudaMalloc(&c->ex_lo, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
+  if (c->ld[0] > c->d[0]) {
+    // zero the pad columns once: no kernel reads them (the tensor maps stop at
+    // d[0]), but row copies (hb_permute_epoch) move whole rows
+    for (float* x : {c->ex, c->ex_lo}) {
+      if (x == nullptr) continue;
+      HB_CUDA(cudaMemset2DAsync(x + c->d[0], c->ld[0] * sizeof(float), 0, (c->ld[0] - c->d[0]) * sizeof(float),
+                                n_rows, c->stream));
+    }
+  }
   HB_CUDA(cudaMalloc(&c->elabels, static_cast<size_t>(n_rows) * sizeof(int64_t)));
   HB_CUDA(h2d_copy(c->elabels, labels, n_rows * sizeof(int64_t), c->stream));
   c->e_rows = n_rows;
@@ -2562,9 +2571,9 @@ static int finish_dense_stage(hb_ctx* c) {
     int* d_flag = nullptr;
     HB_CUDA(cudaMalloc(&d_flag, sizeof(int)));
     HB_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), c->stream));
-    const long long n = c->e_rows * c->ld[0];
+    const long long n = c->e_rows * c->d[0];
     any_nonzero_kernel<<<static_cast<int>(std::min<long long>(cdiv(n, 256), 148 * 8)), 256, 0, c->stream>>>(
-        c->ex_lo, n, d_flag);
+        c->ex_lo, c->e_rows, c->d[0], c->ld[0], d_flag);
     int h = 1;
     const cudaError_t e1 = cudaGetLastError();
     const cudaError_t e2 = cudaMemcpyAsync(&h, d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
@@ -2660,6 +2669,15 @@ static int stage_csr_densified(hb_ctx* c, const int64_t* rowptr, const int32_t* 
   HB_TRY(free_epoch(c));
   HB_CUDA(cudaMalloc(&c->ex, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
   if (c->need_lo()) HB_CUDA(cudaMalloc(&c->ex_lo, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
+  if (c->ld[0] > c->d[0]) {
+    // zero the pad columns once: no kernel reads them (the tensor maps stop at
+    // d[0]), but row copies (hb_permute_epoch) move whole rows
+    for (float* x : {c->ex, c->ex_lo}) {
+      if (x == nullptr) continue;
+      HB_CUDA(cudaMemset2DAsync(x + c->d[0], c->ld[0] * sizeof(float), 0, (c->ld[0] - c->d[0]) * sizeof(float),
+                                n_rows, c->stream));
+    }
+  }
   HB_CUDA(cudaMalloc(&c->elabels, static_cast<size_t>(n_rows) * sizeof(int64_t)));
   HB_CUDA(h2d_copy(c->elabels, labels, n_rows * sizeof(int64_t), c->stream));
   int64_t* d_rowptr = nullptr;

@@ -1050,12 +1050,14 @@ __global__ void __launch_bounds__(256) splitk_epi_kernel(float* __restrict__ out
   }
 }
 
-// *flag = 1 if any of x[0..n) is nonzero
-__global__ void any_nonzero_kernel(const float* x, long long n, int* flag) {
+// *flag = 1 if any x[r][c] (r < rows, c < cols, row stride ld) is nonzero;
+// the pad columns [cols, ld) are never written by staging and never read
+__global__ void any_nonzero_kernel(const float* x, long long rows, int cols, long long ld, int* flag) {
   int any = 0;
+  const long long n = rows * cols;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
-    any |= x[i] != 0.f;
+    any |= x[(i / cols) * ld + i % cols] != 0.f;
   if (__syncthreads_or(any) && threadIdx.x == 0) *flag = 1;
 }
 

@@ -2485,7 +2485,12 @@ static void xfer_account(hb_ctx* c, bool loss) {
 // host-mode merges as gradients land, then finish like do_step.
 static int replica_finish(hb_ctx* c, int rc, int rows, double eta, uint32_t flags, double* out_loss) {
   if (rc != HB_OK) {
-    cudaStreamSynchronize(c->stream);  // nothing may still be writing the host model
+    // nothing may still be reading or writing the host model when the call
+    // returns: drain the step stream and the exchange's copy streams
+    cudaStreamSynchronize(c->stream);
+    if (c->xh2d) cudaStreamSynchronize(c->xh2d);
+    if (c->xmrg) cudaStreamSynchronize(c->xmrg);
+    if (c->side) cudaStreamSynchronize(c->side);
     return rc;
   }
   const bool timed = (flags & HB_STEP_TIMED) != 0;

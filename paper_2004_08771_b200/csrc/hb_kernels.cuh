@@ -342,29 +342,23 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_small_vec_kernel(HeadArg
     p.ws_loss[blockIdx.x] = t;
   }
   if (!p.train) return;
-  // block partials: warps add in warp order in fp32 (a few rows each), the
-  // partial is stored as float64 for the long cross-block sum
+  // block partials: the warps' sums are added in warp order in fp32 (a few
+  // rows each) -- every warp parks its row in shared memory, one barrier, then
+  // each thread sums its columns over the warps in order -- and the partial is
+  // stored as float64 for the long cross-block sum
+  __shared__ __align__(16) float sRed[kHeadWarps * D];
   for (int c = 0; c < NCT && c < p.nc; ++c) {
-    __syncthreads();
-    for (int j = threadIdx.x; j < D; j += blockDim.x) sW[j] = 0.f;
-    __syncthreads();
-    for (int w = 0; w < kHeadWarps; ++w) {
-      if (warp == w) {
+    if (c > 0) __syncthreads();  // the previous class's sums have been read
 #pragma unroll
-        for (int t = 0; t < VPL; ++t) {
-          float4* sp = reinterpret_cast<float4*>(&sW[4 * lane + 128 * t]);
-          float4 v = *sp;
-          v.x += acc[c][t].x;
-          v.y += acc[c][t].y;
-          v.z += acc[c][t].z;
-          v.w += acc[c][t].w;
-          *sp = v;
-        }
-      }
-      __syncthreads();
+    for (int t = 0; t < VPL; ++t)
+      *reinterpret_cast<float4*>(&sRed[warp * D + 4 * lane + 128 * t]) = acc[c][t];
+    __syncthreads();
+    for (int j = threadIdx.x; j < p.d; j += blockDim.x) {
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < kHeadWarps; ++w) v += sRed[w * D + j];
+      p.ws_dw[(static_cast<long long>(blockIdx.x) * p.nc + c) * p.d + j] = static_cast<double>(v);
     }
-    for (int j = threadIdx.x; j < p.d; j += blockDim.x)
-      p.ws_dw[(static_cast<long long>(blockIdx.x) * p.nc + c) * p.d + j] = static_cast<double>(sW[j]);
   }
 }
 

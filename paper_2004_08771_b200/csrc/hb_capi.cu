@@ -141,7 +141,7 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 
 // ------------------------------------------------------------ GEMM launch
 constexpr int kTileSyncTiles = 4096;
-int g_trace_launch_no = 0;  // HB_TRACE builds: index of the GEMM launch being issued
+[[maybe_unused]] int g_trace_launch_no = 0;  // HB_TRACE builds: index of the GEMM launch being issued
 // A GEMM operand: the fp32 tensor's map and its 3xTF32 lo twin's map.
 struct Operand {
   const CUtensorMap* hi;
@@ -1713,8 +1713,6 @@ int free_epoch(hb_ctx* c) {
   c->view_gen++;  // captured graphs baked the old buffers / tensor maps
   return HB_OK;
 }
-
-size_t layer_elems(const hb_ctx* c, int l) { return static_cast<size_t>(c->d[l + 1]) * c->ldw[l]; }
 
 }  // namespace
 

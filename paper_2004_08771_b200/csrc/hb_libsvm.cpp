@@ -183,7 +183,7 @@ std::vector<Chunk> split_chunks(const char* buf, size_t len) {
     const char* q = (t == want - 1) ? end : std::min(end, buf + len * (t + 1) / want);
     while (q < end && q[-1] != '\n') ++q;  // chunks end right after a newline
     if (q <= p) continue;
-    ch.push_back(Chunk{p, q, 0});
+    ch.push_back(Chunk{p, q, 0, 0, 0, LineError{}});
     p = q;
   }
   // line numbers: count newlines per chunk (cheap, memchr)

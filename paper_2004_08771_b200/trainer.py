@@ -20,8 +20,6 @@ from __future__ import annotations
 import time
 from dataclasses import dataclass, field
 
-import numpy as np
-
 from .data import CsrDataset, epoch_shuffle_seed, shuffle_epoch
 from .nn import layer_sizes_of
 from .replica import GpuReplica

@@ -1,22 +1,27 @@
 #!/usr/bin/env python
 """Benchmark of the B200 GPU replica step (Hogbatch / Adaptive Hogbatch MLP worker).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config w8a] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config scaled] [--impl ours|reference]
 
 One "step" = one replica SGD step (forward, fused softmax-CE, backward, fused
 SGD update) over one batch of the named BASELINE.json configuration.  The
-default workload is configs[1], the w8a-shaped sparse MLP 300-512-512-512-2
-at GPU batch 8192 (BASELINE.json).  N>1 (torchrun) runs one GPU worker per
-rank on its own batch stream (weak scaling) and averages the replicas with
-NCCL allreduce every step (the GPU-replica merge).
+default workload is configs[4], the headline "1/2/4/8 B200" configuration: the
+scaled synthetic dense 10M x 1024 set (every row staged in HBM, generated on
+the device), MLP 1024-4096-4096-4096-1000, GPU batch 8192.  N>1 (torchrun)
+runs one GPU worker per rank on its own batch stream over its own 10M/N-row
+shard (weak scaling per step) and averages the replicas with NCCL allreduce
+every `--merge-every` steps (the GPU-replica merge).
 
 Prints ONE JSON line (rank 0).  `value` is device-timed throughput with the
-epoch resident in HBM; `e2e` is the same metric through the drop-in replica
-call (host float64 model snapshot H2D, CSR batch H2D from host memory, the
+data resident in HBM; `e2e` is the same metric through the drop-in replica
+call (host float64 model snapshot H2D, batch H2D from pinned host memory, the
 gradient D2H and float64 stale merge on the host, loss D2H) -- the exact
-semantics of the reference's execute_batch_replica.  `--impl reference` times
-the reference algorithm's CPU implementation (the float64 NumPy port in
-oracle/, OpenBLAS on all host cores) on the same workload.
+semantics of the reference's execute_batch_replica.  `cpu_baseline` is the
+reference's host-CPU Hogbatch (execute_hogwild_sharded, all host cores, 64
+examples per thread, one BLAS thread each) timed on this box, next to the
+single-worker replica step; `time_to_target` compares training-clock time to
+the loss the reference reaches.  `--impl reference` prints the host-CPU
+Hogbatch line alone (the reference arm).
 """
 
 from __future__ import annotations
@@ -36,7 +41,15 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-from paper_2004_08771_b200.parallel import barrier, batch_starts, init_process_group, init_replica_comm, max_over_ranks, shard_seed  # noqa: E402
+from paper_2004_08771_b200.parallel import (  # noqa: E402
+    barrier,
+    batch_starts,
+    broadcast_float,
+    init_process_group,
+    init_replica_comm,
+    max_over_ranks,
+    shard_seed,
+)
 
 METRIC = "MLP train samples/sec"
 UNIT = "samples/s"
@@ -53,10 +66,12 @@ CONFIGS = {
     "realsim": dict(sizes=(20958, 1024, 1024, 2), n=72309, kind="csr", nnz=52, binary=False, normalize=True,
                     classes=2, batch=8192, eta=0.5,
                     desc="real-sim-shaped synthetic sparse 72309x20958 (52 nnz/row), MLP 20958-1024-1024-2, GPU batch 8192"),
-    "scaled": dict(sizes=(1024, 4096, 4096, 4096, 1000), n=131072, kind="dense", classes=1000, batch=8192, eta=0.1,
-                   desc="scaled synthetic dense 1024-d (131072 staged rows of the 10M-row set), "
-                        "MLP 1024-4096-4096-4096-1000, GPU batch 8192"),
+    "scaled": dict(sizes=(1024, 4096, 4096, 4096, 1000), n=10_000_000, kind="blobs", classes=1000, batch=8192,
+                   eta=0.1, separation=2.5,
+                   desc="scaled synthetic dense 10Mx1024, 1000 classes (all 10M rows staged in HBM, generated on the "
+                        "device), MLP 1024-4096-4096-4096-1000, GPU batch 8192"),
 }
+DEFAULT_CONFIG = "scaled"
 
 
 def dense_flops_per_sample(sizes, sparse_first):
@@ -77,14 +92,62 @@ def hb_sparse_kernels(cfg):
     return cfg["kind"] == "csr" and cfg["sizes"][0] > N.HB_DENSIFY_MAX_DIN
 
 
-def make_data(cfg, seed, rank=0):
+def make_data(cfg, seed, rank=0, n=None):
+    """Host dataset of the config (CsrDataset or Dataset); for the device-generated
+    config a small host set of the same shape (CPU-only legs)."""
     import paper_2004_08771_b200 as hb
 
     s = shard_seed(seed, rank)
+    n = cfg["n"] if n is None else n
     if cfg["kind"] == "csr":
-        return hb.synthetic_csr(cfg["n"], cfg["sizes"][0], cfg["nnz"], cfg["classes"], seed=s,
+        return hb.synthetic_csr(n, cfg["sizes"][0], cfg["nnz"], cfg["classes"], seed=s,
                                 binary=cfg["binary"], normalize=cfg["normalize"])
-    return hb.synthetic_blobs(cfg["n"], cfg["sizes"][0], cfg["classes"], 2.5, seed=s)
+    if cfg["kind"] == "blobs":
+        means = hb.data.blob_means(cfg["sizes"][0], cfg["classes"], cfg["separation"], seed)
+        rng = np.random.default_rng(s)
+        y = rng.integers(0, cfg["classes"], size=n).astype(np.int64)
+        return hb.Dataset(features=means[y] + rng.normal(size=(n, cfg["sizes"][0])), labels=y, name="blobs-host")
+    return hb.synthetic_blobs(n, cfg["sizes"][0], cfg["classes"], 2.5, seed=s)
+
+
+class Source:
+    """Where a rank's rows live: a host dataset (staged once) or rows generated
+    on the device (scaled).  rows(start, k) returns the exact float64 dense rows
+    and labels the device trains on (for the CPU oracle / host batches)."""
+
+    def __init__(self, cfg, seed, rank, world, ctx=None):
+        self.cfg = cfg
+        self.ctx = ctx
+        if cfg["kind"] == "blobs":
+            self.data = None
+            self.n = cfg["n"] // world
+            if ctx is not None:  # one dataset (one means draw), disjoint row ranges per rank
+                ctx.stage_blobs(self.n, cfg["classes"], cfg["separation"], seed, row0=rank * self.n)
+        else:
+            self.data = make_data(cfg, seed, rank)
+            self.n = self.data.n_examples
+            if ctx is not None:
+                if cfg["kind"] == "csr":
+                    ctx.stage(self.data)
+                else:
+                    ctx.stage(self.data.features.astype(np.float32), self.data.labels)
+
+    def rows(self, start, k):
+        if self.data is None:
+            x, y = self.ctx.read_staged(start, k)
+            return x.astype(np.float64), y
+        if self.cfg["kind"] == "csr":
+            return self.data.dense(start, start + k), self.data.labels[start:start + k]
+        return self.data.features[start:start + k].astype(np.float32).astype(np.float64), \
+            self.data.labels[start:start + k]
+
+    def host_batch(self, start, k):
+        """(batch, labels) as the host-buffer replica call takes it."""
+        if self.data is None:
+            return self.ctx.read_staged(start, k)
+        if self.cfg["kind"] == "csr":
+            return self.data.rows(start, start + k), None
+        return self.data.features[start:start + k].astype(np.float32), self.data.labels[start:start + k]
 
 
 class ClockSampler:
@@ -146,22 +209,31 @@ class ClockSampler:
 
 
 def measured_peaks():
+    """(hbm GB/s, dense TF32 TF/s, basis): HBM from MEASURED_PEAKS.json, TF32
+    from the newest profiles/r*_tf32_peak.json (scripts/tf32_peak.py: fp32
+    torch.matmul with TF32 tensor cores, 8192^3), else bf16/2 (stated)."""
+    hbm, bf16, src = 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured (MEASURED_PEAKS.json)"
-    return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+        hbm, bf16, src = d.get("hbm_gbs", hbm), d.get("bf16_tflops", bf16), "MEASURED_PEAKS.json"
+    files = sorted(ROOT.glob("profiles/r*_tf32_peak.json"))
+    if files:
+        t = json.loads(files[-1].read_text())
+        return hbm, float(t["tf32_tflops_burst"]), f"measured dense TF32 {t['tf32_tflops_burst']} TF/s " \
+                                                   f"(profiles/{files[-1].name}); HBM {src}"
+    return hbm, bf16 / 2.0, f"TF32 = bf16/2 of {bf16} TF/s ({src}; no TF32 measurement found)"
 
 
 def ncu_kernel_stats(config, kernel):
     """Per-launch ncu figures (DRAM / L2 bytes, cold-cache duration) of `kernel`
     for `config` from the newest profiles/r*_ncu_kernels.json (one `ncu --set
     full` capture per kernel, scripts/ncu_traffic.sh), or None."""
-    files = sorted(ROOT.glob("profiles/r*_ncu_kernels.json"))
-    if not files:
-        return None, None
-    d = json.loads(files[-1].read_text()).get("kernels", {})
-    return d.get(config, {}).get(kernel), files[-1].name
+    for f in sorted(ROOT.glob("profiles/r*_ncu_kernels.json"), reverse=True):
+        hit = json.loads(f.read_text()).get("kernels", {}).get(config, {}).get(kernel)
+        if hit:
+            return hit, f.name
+    return None, None
 
 
 def kernel_work(name, cfg, rows, dw_splits=None):
@@ -170,11 +242,7 @@ def kernel_work(name, cfg, rows, dw_splits=None):
     sizes = cfg["sizes"]
     base, _, l = name.rpartition("_l")
     l = int(l)
-    if base.startswith("gemm_fwd"):
-        return "tensor", 2.0 * rows * sizes[l + 1] * sizes[l]
-    if base.startswith("gemm_dx"):
-        return "tensor", 2.0 * rows * sizes[l + 1] * sizes[l]
-    if base.startswith("gemm_dw"):
+    if base.startswith(("gemm_fwd", "gemm_dx", "gemm_dw")):
         return "tensor", 2.0 * rows * sizes[l + 1] * sizes[l]
     if base == "spmm_sigmoid":
         nnz = cfg.get("nnz", 0)
@@ -192,42 +260,203 @@ def kernel_work(name, cfg, rows, dw_splits=None):
     return "hbm", 0.0
 
 
-def run_ours(args, cfg, rank, world, local_rank, dist):
-    import paper_2004_08771_b200 as hb
+def choose_starts(cfg, n, b, count, seed, rank):
+    """Batch starts of the timed steps.  The device-generated set draws full
+    batches at random offsets over its whole row range (so the timed steps
+    read rows from all of HBM); the others cycle through the epoch."""
+    if cfg["kind"] == "blobs":
+        rng = np.random.default_rng((seed, rank, 7))
+        nb = n // b
+        return [int(i) * b for i in rng.choice(nb, size=count, replace=count > nb)]
+    return batch_starts(n, b, count)
 
-    # the multi-GPU code path (NCCL replica merge, max over ranks, barriers);
-    # HB_BENCH_DIST=1 runs it even for one rank (a one-rank NCCL communicator)
-    distributed = dist is not None
+
+# ---------------------------------------------------------------------------- CPU legs (oracle/)
+def cpu_replica_rate(cfg, rows_fn, budget_s, max_steps, seed):
+    """The reference's single-worker replica step (execute_batch_replica, float64
+    NumPy + OpenBLAS on all host cores) at the full batch size, until the budget
+    is spent (at least one step)."""
+    from oracle import ref_nn
+
+    w = ref_nn.init_weights(cfg["sizes"], seed)
+    b = cfg["batch"]
+    steps, t_total = 0, 0.0
+    for i in range(max_steps):
+        x, y = rows_fn(i * b, b)
+        t0 = time.perf_counter()
+        ref_nn.replica_step(w, x, y, cfg["eta"])
+        t_total += time.perf_counter() - t0
+        steps += 1
+        if t_total > budget_s:
+            break
+    return dict(value=steps * b / t_total, unit=UNIT, seconds=round(t_total, 2), steps=steps, rows_per_step=b,
+                sample=f"{steps} replica steps x {b} rows (float64 NumPy port of workers.py:126-138, oracle/ref_nn.py, "
+                       f"OpenBLAS on all host cores)")
+
+
+def cpu_hogbatch_run(cfg, rows_fn, budget_s, seed, threads=None, eval_fn=None):
+    """The reference's host-CPU Hogbatch (execute_hogwild_sharded, workers.py:94-123):
+    batches of threads*64 rows, one shard per thread updating the shared float64
+    model, one BLAS thread per worker thread.  Learning rate per shard: the
+    config's eta scaled by 64/b (the reference's proportional rule,
+    policies.py:34-36)."""
+    from oracle import ref_hogbatch, ref_nn
+
+    threads = threads or os.cpu_count() or 1
+    per = 64
+    rows = threads * per
+    w = ref_nn.init_weights(cfg["sizes"], seed)
+    eta = cfg["eta"] * per / cfg["batch"]
+
+    def batches():
+        i = 0
+        while True:
+            yield rows_fn(i * rows, rows)
+            i += 1
+
+    r = ref_hogbatch.run_hogbatch(w, batches(), eta, budget_s, threads=threads, per_thread=per)
+    r["value"] = r["samples"] / r["seconds"]
+    r["eta_per_shard"] = eta
+    r["loss"] = eval_fn(w) if eval_fn is not None else None
+    r["cpu_model"] = ref_hogbatch.cpu_model()
+    return r
+
+
+# ---------------------------------------------------------------------------- time to target
+def time_to_target(ctx, src, cfg, args, rank, world, dist, init_w, max_rows):
+    """Time-to-target-loss (BASELINE metric), step-matched:
+    batches i = 0, 1, ... are the contiguous rows [i*b, (i+1)*b) of each rank's
+    data (epoch 0), the loss is evaluated on a fixed held-out slice (the last E
+    rows of rank 0's data) and excluded from the training clock
+    (engine.py:158-171).
+      * replica target: the loss the reference's deterministic single-worker
+        replica step (float64 oracle) reaches after K steps, K set by the CPU
+        time budget; the CPU time is those K steps.
+      * Hogbatch target: the loss the reference's host-CPU Hogbatch (all host
+        cores) reaches within the same budget.
+    The GPU side runs the same batches through the library (N>1: every rank
+    its own batches, replicas averaged every step) until the eval loss is within
+    1e-5 relative of each target.  CPU work runs on rank 0 only."""
+    from oracle import ref_nn
+
+    b, eta = cfg["batch"], cfg["eta"]
+    E = min(8192, src.n // 8)
+    e0 = src.n - E
+    budget = args.ttt_budget_s
+    out = None
+    if rank == 0:
+        ex, ey = src.rows(e0, E)
+
+        def eval_fn(w):
+            return ref_nn.loss_sum(w, ex, ey) / E
+
+        w = ref_nn.init_weights(cfg["sizes"], args.seed)
+        cpu_curve, cpu_s, k = [eval_fn(w)], 0.0, 0
+        while (k + 1) * b <= min(e0, max_rows):
+            x, y = src.rows(k * b, b)
+            t0 = time.perf_counter()
+            ref_nn.replica_step(w, x, y, eta)
+            cpu_s += time.perf_counter() - t0
+            k += 1
+            cpu_curve.append(eval_fn(w))
+            if cpu_s >= budget:
+                break
+        hog = cpu_hogbatch_run(cfg, lambda s, r: src.rows(s % max(1, e0 - r), r), budget, args.seed, eval_fn=eval_fn)
+        out = {"eval_rows": E, "eval_slice": [e0, src.n], "replica": {"target_loss": cpu_curve[-1], "cpu_steps": k,
+               "cpu_ms": round(cpu_s * 1000.0, 1), "cpu_curve": [round(v, 7) for v in cpu_curve]},
+               "hogbatch": {"target_loss": hog["loss"], "cpu_ms": round(hog["seconds"] * 1000.0, 1),
+                            "cpu_samples": hog["samples"], "threads": hog["threads"], "per_thread": 64,
+                            "eta_per_shard": hog["eta_per_shard"]}}
+    targets = [out["replica"]["target_loss"], out["hogbatch"]["target_loss"]] if rank == 0 else [0.0, 0.0]
+    cpu_k = out["replica"]["cpu_steps"] if rank == 0 else 0
+    if dist is not None:
+        targets = [broadcast_float(dist, t) for t in targets]
+        cpu_k = int(broadcast_float(dist, float(cpu_k)))
+    # GPU run (every rank), eval by rank 0 outside the clock
+    ctx.set_weights(init_w)
+    hit = [None, None]
+    gpu_curve = []
+    wall_s = dev_ms = 0.0
+    step = 0
+    limit = max(cpu_k + 3, 4)
+    loss = ctx.eval_loss_sum(e0, E) / E if rank == 0 else 0.0
+    gpu_curve.append(loss)
+    while step < limit and (step + 1) * b <= e0:
+        if dist is not None:
+            barrier(dist)
+        t0 = time.perf_counter()
+        ctx.step(step * b, b, eta, timed=True, merge=dist is not None)
+        wall_s += time.perf_counter() - t0
+        dev_ms += ctx.last_step_ms
+        step += 1
+        if rank == 0:
+            loss = ctx.eval_loss_sum(e0, E) / E
+            gpu_curve.append(loss)
+        done = 0.0
+        if rank == 0:
+            for j, t in enumerate(targets):
+                if hit[j] is None and loss <= t * (1.0 + 1e-5):
+                    hit[j] = (step, wall_s * 1000.0, dev_ms)
+            done = 1.0 if all(h is not None for h in hit) else 0.0
+        if dist is not None:
+            done = broadcast_float(dist, done)
+        if done:
+            break
+    if dist is not None:
+        wall_s = max_over_ranks(dist, wall_s)
+    if rank != 0:
+        return None
+    for j, key in enumerate(("replica", "hogbatch")):
+        h = hit[j]
+        out[key].update({"gpu_steps": None if h is None else h[0], "gpu_ms": None if h is None else round(h[1], 3),
+                         "gpu_device_ms": None if h is None else round(h[2], 3),
+                         "speedup": None if h is None else round(out[key]["cpu_ms"] / max(h[1], 1e-9), 1)})
+    out["gpu_curve"] = [round(v, 7) for v in gpu_curve]
+    out["n_gpus"] = world
+    out["note"] = ("training clock (evaluation excluded); step-matched batches of epoch 0; GPU 'reached' = eval loss "
+                   "within 1e-5 relative of the target (float64 vs the device's fp32 model); N>1: replicas averaged "
+                   "by NCCL every step, eval on rank 0")
+    return out
+
+
+# ---------------------------------------------------------------------------- our arm
+def run_ours(args, cfg, rank, world, local_rank, dist):
+    import torch
+
+    import paper_2004_08771_b200 as hb
     from paper_2004_08771_b200.nn import Architecture, init_model
 
+    distributed = dist is not None
     device = local_rank
     sizes = cfg["sizes"]
     b = cfg["batch"]
     sparse = cfg["kind"] == "csr"
-    data = make_data(cfg, args.seed, rank)
-    n = data.n_examples
+    torch.cuda.set_device(device)
     model = init_model(Architecture(sizes), seed=args.seed)
     ctx = hb.GpuReplica(sizes, b, device=device, sparse=sparse, precision=args.precision)
     ctx.set_weights(model.weights)
-    if sparse:
-        ctx.stage(data)
-    else:
-        ctx.stage(data.features.astype(np.float32), data.labels)
+    t0 = time.perf_counter()
+    src = Source(cfg, args.seed, rank, world, ctx)
+    stage_s = time.perf_counter() - t0
+    n = src.n
+    comm = None
     if distributed:
         init_replica_comm(ctx, dist, rank, world)
-    starts = batch_starts(n, b, args.warmup + args.steps)
+        comm = {"nranks": world, "rank": rank, "backend": "NCCL (library communicator, hb_comm_init)"}
+        print(f"[bench] rank {rank}/{world}: NCCL replica communicator up on cuda:{device}", file=sys.stderr)
+    starts = choose_starts(cfg, n, b, args.warmup + args.steps, args.seed, rank)
 
-    import torch
-
-    torch.cuda.set_device(device)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{device}")
 
     def l2_flush():
         flush.zero_()
         torch.cuda.synchronize(device)
 
+    def merge_due(i):
+        return distributed and (i + 1) % args.merge_every == 0
+
     for i in range(args.warmup):
-        ctx.step(starts[i], b, cfg["eta"], timed=True, merge=distributed)
+        ctx.step(starts[i], b, cfg["eta"], timed=True, merge=merge_due(i))
     # ---------------------------------------------------------- kernel breakdown
     # A separate instrumented pass (every launch bracketed by CUDA events) gives
     # the per-kernel shares and picks the dominant kernel.  Events around every
@@ -237,7 +466,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         ctx.profile(True)
         for i in range(min(args.steps, 10)):
             l2_flush()
-            ctx.step(starts[args.warmup + i], b, cfg["eta"], timed=True, merge=distributed)
+            ctx.step(starts[args.warmup + i], b, cfg["eta"], timed=True, merge=merge_due(i))
         prof = ctx.profile_read()
         ctx.profile(False)
         tot = sum(v[0] for v in prof.values()) or 1.0
@@ -247,19 +476,19 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         ctx.profile_filter(dom)
         ctx.profile(True)
         for i in range(2):  # capture the singly-instrumented graph outside the timed region
-            ctx.step(starts[i], b, cfg["eta"], timed=True)
+            ctx.step(starts[i], b, cfg["eta"], timed=True, merge=merge_due(i))
         ctx.profile_read()
     # ---------------------------------------------------------- timed region
     if distributed:
         barrier(dist)
     torch.cuda.synchronize(device)
-    step_ms, merge_ms, launches = [], [], 0
+    step_ms, launches = [], 0
     with ClockSampler(device) as clocks:
         for i in range(args.warmup, args.warmup + args.steps):
             l2_flush()
             # distributed: the NCCL replica merge runs on the step's stream and
             # inside its CUDA-event bracket (HB_STEP_MERGE)
-            ctx.step(starts[i], b, cfg["eta"], timed=True, merge=distributed)
+            ctx.step(starts[i], b, cfg["eta"], timed=True, merge=merge_due(i))
             step_ms.append(ctx.last_step_ms)
             launches += ctx.last_step_launches
         torch.cuda.synchronize(device)
@@ -268,7 +497,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
     dom_live = ctx.profile_read() if dom else {}
     ctx.profile(False)
     ctx.profile_filter(None)
-    total_ms = sum(step_ms) + sum(merge_ms)
+    total_ms = sum(step_ms)
     if distributed:
         total_ms = max_over_ranks(dist, total_ms)
     value = world * args.steps * b / (total_ms / 1000.0)
@@ -276,14 +505,13 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
     # ---------------------------------------------------------- e2e (drop-in replica semantics)
     e2e = None
     if not args.skip_e2e:
-        # every step's batch lives in page-locked host memory (one registered
-        # pool per array kind; each batch is a view into it)
         host_batches = []
         pool = []
+        tstarts = starts[args.warmup:args.warmup + args.steps]
         if sparse:
             from paper_2004_08771_b200.data import CsrDataset
 
-            subs = [data.rows(starts[i], starts[i] + b) for i in range(args.steps)]
+            subs = [src.data.rows(s, s + b) for s in tstarts]
             rp = np.concatenate([x.rowptr for x in subs])
             cl = np.concatenate([x.col for x in subs])
             vl = np.concatenate([x.val for x in subs]).astype(np.float32)
@@ -299,10 +527,11 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
                 o_rp += b + 1
                 o_nz += x.nnz
         else:
-            xs = np.concatenate([data.features[starts[i]:starts[i] + b] for i in range(args.steps)]).astype(np.float32)
-            ys = np.concatenate([data.labels[starts[i]:starts[i] + b] for i in range(args.steps)])
+            parts = [src.host_batch(s, b) for s in tstarts]
+            xs = np.concatenate([p[0] for p in parts])
+            ys = np.concatenate([p[1] for p in parts])
             pool = [xs, ys]
-            host_batches = [(xs[i * b:(i + 1) * b], ys[i * b:(i + 1) * b]) for i in range(args.steps)]
+            host_batches = [(xs[i * b:(i + 1) * b], ys[i * b:(i + 1) * b]) for i in range(len(parts))]
         ctx.pin_host(pool)
         host_model = [w.copy() for w in model.weights]
         ctx.pin_host(host_model)  # what execute_gpu_replica does for the shared model
@@ -318,23 +547,40 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
             # (workers.py:132), batch H2D, the step, stale merge (workers.py:135), loss D2H
             ctx.replica_step_host(host_model, xb, yb, cfg["eta"], want_loss=True)
         el = time.perf_counter() - t0
-        # PCIe bytes of the last call as the library issued them: batch, f64 snapshot, the merge by lane
-        # (fp32 gradient D2H on the host lane, f64 rows both ways on the device lane), step record, loss
+        # PCIe bytes of the last call as the library issued them
         h2d, d2h = ctx.last_xfer_bytes
         if distributed:
             el = max_over_ranks(dist, el)
         e2e = {"value": world * args.steps * b / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
                "path": "execute_gpu_replica semantics through the C ABI (hb_replica_step_host_*), per step: "
-                       "batch H2D from pinned host memory (CSR rows are scattered into dense rows on the device "
-                       "for narrow inputs), snapshot of the page-locked f64 host model (DMA H2D, layer l+1 in "
-                       "flight while layer l computes), the step, the f64 stale merge W_host += (-eta)*g per layer as "
-                       "soon as its gradient exists (fp32 gradient D2H + host float64 axpy, or on the device lane "
-                       "for large split-K layers: f64 rows read, merged on the GPU, written back), loss D2H"}
+                       "batch H2D from pinned host memory, snapshot of the page-locked f64 host model (DMA H2D, "
+                       "layer l+1 in flight while layer l computes), the step, the f64 stale merge W_host += (-eta)*g "
+                       "per layer as soon as its gradient exists, loss D2H"}
+
+    # ---------------------------------------------------------- CPU baselines (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        hog = cpu_hogbatch_run(cfg, lambda s, r: src.rows(s % max(1, n - r), r), args.cpu_budget_s, args.seed)
+        rep = cpu_replica_rate(cfg, lambda s, r: src.rows(s % max(1, n - r), r), args.cpu_budget_s, 10, args.seed)
+        from oracle import ref_hogbatch
+
+        cpu = {"value": hog["value"], "unit": UNIT, "cores": hog["threads"], "kind": "port",
+               "sample": f"host-CPU Hogbatch (execute_hogwild_sharded, workers.py:94-123; oracle/ref_hogbatch.py): "
+                         f"{hog['batches']} batches x {hog['threads']} threads x 64 rows, one BLAS thread per thread, "
+                         f"{hog['seconds']:.1f} s",
+               "cpu_model": hog["cpu_model"], "blas": ref_hogbatch.blas_info(),
+               "replica_step": {"value": rep["value"], "unit": UNIT, "sample": rep["sample"],
+                                "seconds": rep["seconds"]}}
+
+    # ---------------------------------------------------------- time to target
+    ttt = None
+    if args.ttt:
+        ttt = time_to_target(ctx, src, cfg, args, rank, world, dist, model.weights, max_rows=n)
     ctx.close()
 
     # ---------------------------------------------------------- roofline of the dominant kernel
-    hbm_peak, bf16_peak, peak_src = measured_peaks()
+    hbm_peak, tf32_peak, peak_src = measured_peaks()
     roofline = None
     if dom and dom in dom_live:
         ms, cnt = dom_live[dom]
@@ -343,14 +589,15 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         ncu, ncu_src = ncu_kernel_stats(args.config, dom)
         traffic = None if not ncu or "dram_bytes" not in ncu else ncu["dram_bytes"]
         if bound == "tensor":
-            tf32 = bf16_peak / 2.0
-            peak = tf32 / (3.0 if args.precision == "3xtf32" else 1.0)
+            peak = tf32_peak / (3.0 if args.precision == "3xtf32" else 1.0)
             roofline = {"bound": "tensor", "kernel": dom, "achieved": round(work / avg_s / 1e12, 2),
                         "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(work / avg_s / 1e12 / peak, 4),
                         "traffic": traffic,
-                        "peak_basis": f"{'3xTF32-effective = ' if args.precision == '3xtf32' else ''}"
-                                      f"TF32 dense = bf16/2 of {bf16_peak} TF/s {peak_src}",
+                        "peak_basis": ("3xTF32-effective = dense TF32 / 3; " if args.precision == "3xtf32" else "")
+                        + peak_src,
                         "work_per_launch": work, "avg_launch_us": round(avg_s * 1e6, 2),
+                        "raw_tf32_issue_frac": round(work * (3 if args.precision == "3xtf32" else 1) / avg_s / 1e12
+                                                     / tf32_peak, 4),
                         "timing": "CUDA events around this kernel only, inside the timed region"}
         else:
             roofline = {"bound": "hbm", "kernel": dom, "achieved": round(work / avg_s / 1e9, 1),
@@ -359,22 +606,16 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
                         "avg_launch_us": round(avg_s * 1e6, 2),
                         "timing": "CUDA events around this kernel only, inside the timed region"}
             if ncu and "l2_bytes" in ncu:
-                # the gather kernels re-read W0^T / delta0 rows once per nonzero: their
-                # real bound is the L2 -> SM gather traffic, not the unique HBM bytes
                 roofline["l2"] = {"bytes_per_launch": ncu["l2_bytes"],
                                   "achieved_gbs": round(ncu["l2_bytes"] / avg_s / 1e9, 1),
                                   "ncu_l2_throughput_pct": round(ncu.get("l2_throughput_pct", 0.0), 1)}
         if roofline is not None and ncu:
             roofline["traffic_source"] = f"profiles/{ncu_src} ({args.config}/{dom}: dram read+write bytes of one launch)"
-    # step-level tensor work: every GEMM of the step (dense layers; a sparse
-    # first layer is gather work) against the step time -- with dX and the
-    # split-K dW partials running concurrently, per-kernel event durations
-    # overlap, so this is the figure that adds up
+    # step-level tensor work: every GEMM of the step against the step time
     if roofline is not None:
         gemm_flops = dense_flops_per_sample(cfg["sizes"], sparse and hb_sparse_kernels(cfg)) * b
         step_s = (sum(step_ms) / len(step_ms)) / 1000.0
-        tf32 = bf16_peak / 2.0
-        peak = tf32 / (3.0 if args.precision == "3xtf32" else 1.0)
+        peak = tf32_peak / (3.0 if args.precision == "3xtf32" else 1.0)
         roofline["step_tensor"] = {"gemm_flop_per_step": gemm_flops,
                                    "achieved_tflops": round(gemm_flops / step_s / 1e12, 2),
                                    "frac_of_peak": round(gemm_flops / step_s / 1e12 / peak, 4),
@@ -383,94 +624,17 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
             roofline["overlap_note"] = ("the backward's dX GEMM and the split-K dW partial GEMM of the same layer run "
                                         "concurrently on two streams, so this kernel's event-timed duration includes "
                                         "sharing the SMs with the other; step_tensor is the figure that adds up")
-    return dict(value=value, total_ms=total_ms, e2e=e2e, roofline=roofline, kernels=kernels,
-                clocks=clocks.summary(), launches=launches, merge_ms=sum(merge_ms))
+    return dict(value=value, total_ms=total_ms, e2e=e2e, roofline=roofline, kernels=kernels, clocks=clocks.summary(),
+                launches=launches, cpu=cpu, ttt=ttt, comm=comm, stage_s=stage_s, rows_staged=n)
 
 
-def cpu_reference_rate(cfg, seed, budget_s, max_steps):
-    """The reference algorithm's CPU step (execute_batch_replica: deep copy,
-    forward, backward, stale merge; float64 NumPy + OpenBLAS, all host cores)
-    on the dense twin of the same batches -- the oracle port."""
-    from oracle import ref_nn
-
-    sizes, b = cfg["sizes"], cfg["batch"]
-    data = make_data(dict(cfg, n=min(cfg["n"], 4 * b)), seed)
-    w = ref_nn.init_weights(sizes, seed)
-    nrow = data.n_examples
-
-    def batch(i):
-        s = (i * b) % max(1, nrow - b + 1)
-        if cfg["kind"] == "csr":
-            return data.dense(s, s + b), data.labels[s:s + b]
-        return data.features[s:s + b], data.labels[s:s + b]
-
-    x, y = batch(0)
-    t0 = time.perf_counter()
-    ref_nn.replica_step(w, x, y, cfg["eta"])  # warm-up + time estimate
-    one = time.perf_counter() - t0
-    rows = b
-    if one * max_steps > budget_s:  # bounded sample: shrink the rows per step, same shapes otherwise
-        rows = max(64, int(b * budget_s / (one * max_steps)))
-    steps, t_total = 0, 0.0
-    for i in range(max_steps):
-        x, y = batch(i + 1)
-        t0 = time.perf_counter()
-        ref_nn.replica_step(w, x[:rows], y[:rows], cfg["eta"])
-        t_total += time.perf_counter() - t0
-        steps += 1
-        if t_total > budget_s:
-            break
-    cores = os.cpu_count() or 1
-    try:
-        from threadpoolctl import threadpool_info
-
-        blas = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
-        if blas:
-            cores = int(blas[0])
-    except Exception:
-        pass
-    return dict(value=steps * rows / t_total, unit=UNIT, cores=cores, kind="port",
-                sample=f"{steps} replica steps x {rows} rows of the {cfg['desc']} workload "
-                       f"(float64 NumPy port of workers.py:126-138, oracle/ref_nn.py)",
-                seconds=round(t_total, 2))
-
-
-def time_to_target(cfg, seed, epochs, device=0):
-    """Time-to-target-loss (BASELINE metric): the target is the
-    loss the reference algorithm reaches after `epochs` epochs of deterministic
-    single-worker minibatch SGD (the float64 oracle, engine.py:175-316 with one
-    replica worker); both sides are timed on the training clock (evaluation
-    excluded, engine.py:158-171) on the same dataset, seed, eta and batch."""
-    import paper_2004_08771_b200 as hb
-    from oracle import ref_nn
-    from paper_2004_08771_b200.nn import Architecture, init_model
-
-    sizes, b, eta = cfg["sizes"], cfg["batch"], cfg["eta"]
-    data = make_data(cfg, seed)
-    n = data.n_examples
-    dense = data.dense() if cfg["kind"] == "csr" else data.features
-    labels = data.labels
-    # reference (CPU) run
-    w = ref_nn.init_weights(sizes, seed)
-    cpu_s, curve = 0.0, [ref_nn.loss_sum(w, dense, labels) / n]
-    for ep in range(epochs):
-        perm = ref_nn.shuffle_epoch(n, (seed, ep))
-        ex, ey = np.ascontiguousarray(dense[perm]), labels[perm]
-        t0 = time.perf_counter()
-        for st in range(0, n, b):
-            xb, yb = ex[st:st + b], ey[st:st + b]
-            ref_nn.apply_update(w, ref_nn.backward(w, ref_nn.forward(w, xb), yb), eta)
-        cpu_s += time.perf_counter() - t0
-        curve.append(ref_nn.loss_sum(w, dense, labels) / n)
-    target = curve[-1]
-    # GPU run until the target is reached (checked at epoch ends, like the reference's samples)
-    model = init_model(Architecture(sizes), seed=seed)
-    res = hb.train_gpu(data, model, b, eta, epochs + 2, seed, device=device, target_loss=target)
-    return {"target_loss": target, "epochs": epochs, "cpu_ref_ms": round(cpu_s * 1000.0, 2),
-            "gpu_ms": None if res.time_to_target_ms is None else round(res.time_to_target_ms, 3),
-            "cpu_curve": [round(x, 6) for x in curve], "gpu_curve": [round(x, 6) for x in res.curve],
-            "cpu_cores": os.cpu_count(),
-            "note": "training clock, evaluation excluded; reference = float64 NumPy port of the reference step"}
+def config_block(args, cfg, world):
+    return {"workload": cfg["desc"], "config": args.config, "arch": "-".join(map(str, cfg["sizes"])),
+            "batch_per_gpu": cfg["batch"], "global_batch": cfg["batch"] * world, "precision": args.precision,
+            "rows": cfg["n"], "rows_per_gpu": cfg["n"] // world if cfg["kind"] == "blobs" else cfg["n"],
+            "parallelism": f"dp{world}" + (f" (NCCL replica averaging every {args.merge_every} step(s))"
+                                           if world > 1 else ""),
+            "l2": "flushed between timed steps (256 MiB write)", "data": "synthetic, resident in HBM"}
 
 
 def main():
@@ -478,36 +642,57 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="w8a", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "tf32"])
     ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--merge-every", type=int, default=1, help="NCCL replica averaging cadence (N>1)")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
-    ap.add_argument("--ttt-epochs", type=int, default=3, help="time-to-target epochs (0 disables)")
+    ap.add_argument("--ttt-budget-s", type=float, default=20.0, help="CPU time budget of the time-to-target legs")
+    ap.add_argument("--no-ttt", dest="ttt", action="store_false")
     ap.add_argument("--no-prof", action="store_true", help="no per-kernel events in the timed region")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.merge_every < 1:
+        ap.error("--merge-every must be >= 1")
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    config = {"workload": cfg["desc"], "config": args.config, "arch": "-".join(map(str, cfg["sizes"])),
-              "batch_per_gpu": cfg["batch"], "global_batch": cfg["batch"] * world, "precision": args.precision,
-              "parallelism": f"dp{world}" + (" (NCCL replica averaging every step)" if world > 1 else ""),
-              "l2": "flushed between timed steps (256 MiB write)", "data": "synthetic, resident in HBM"}
 
     if args.impl == "reference":
+        # the reference arm: host-CPU Hogbatch on this box's cores (rank 0 only)
         if rank != 0:
             return
-        cpu = cpu_reference_rate(cfg, args.seed, budget_s=min(120.0, 6.0 * args.steps), max_steps=args.steps)
-        line = {"impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * cfg["batch"] / cpu["value"],
+        src = Source(cfg, args.seed, 0, 1, None) if cfg["kind"] != "blobs" else None
+        host = make_data(cfg, args.seed, 0, n=min(cfg["n"], 65536)) if src is None else None
+
+        def rows_fn(s, r):
+            if src is not None:
+                return src.rows(s % max(1, src.n - r), r)
+            s = s % max(1, host.n_examples - r)
+            return host.features[s:s + r], host.labels[s:s + r]
+
+        budget = min(120.0, max(10.0, 3.0 * args.steps))
+        hog = cpu_hogbatch_run(cfg, rows_fn, budget, args.seed)
+        from oracle import ref_hogbatch
+
+        line = {"impl": "reference", "metric": METRIC, "value": hog["value"], "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * hog["seconds"] / hog["batches"],
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": config,
-                "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                "data": "synthetic", "config": config_block(args, cfg, 1),
+                "cpu_baseline": {"value": hog["value"], "unit": UNIT, "cores": hog["threads"], "kind": "port",
+                                 "sample": f"host-CPU Hogbatch (execute_hogwild_sharded, workers.py:94-123; "
+                                           f"oracle/ref_hogbatch.py): {hog['batches']} batches x {hog['threads']} "
+                                           f"threads x 64 rows, one BLAS thread per thread, {hog['seconds']:.1f} s",
+                                 "cpu_model": hog["cpu_model"], "blas": ref_hogbatch.blas_info()},
+                "e2e": {"value": hog["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "note": "step = one coordinator batch of threads x 64 rows; the reference is pure Python/NumPy and "
+                        "cannot travel to the GPU box, so this is its float64 restatement (oracle/, pinned to the "
+                        "reference's golden vectors)"}
         print(json.dumps(line))
         return
 
@@ -520,23 +705,17 @@ def main():
         init_process_group(dist)
     res = run_ours(args, cfg, rank, world, local_rank, dist)
     if rank == 0:
-        cpu = None
-        if world == 1:
-            cpu = cpu_reference_rate(cfg, args.seed, budget_s=args.cpu_budget_s, max_steps=10)
-        ttt = None
-        if world == 1 and args.ttt_epochs > 0 and cfg["n"] * cfg["sizes"][0] <= 64_000_000:
-            ttt = time_to_target(cfg, args.seed, args.ttt_epochs, device=local_rank)
         line = {
             "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res["total_ms"] / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05)" if args.precision == "3xtf32"
-            else "f32 (TF32 tcgen05)", "data": "synthetic", "config": config,
-            "e2e": res["e2e"], "roofline": res["roofline"],
-            "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            else "f32 (TF32 tcgen05)", "data": "synthetic", "config": config_block(args, cfg, world),
+            "e2e": res["e2e"], "roofline": res["roofline"], "cpu_baseline": res["cpu"],
             "clocks": res["clocks"], "gpu_launches": res["launches"], "kernels": res["kernels"],
             "kernels_note": "per-launch CUDA events on every kernel in a separate instrumented pass "
                             "(each bracket adds ~5 us); the timed region brackets only roofline.kernel",
-            "time_to_target": ttt,
+            "time_to_target": res["ttt"], "comm": res["comm"],
+            "staging": {"rows_per_gpu": res["rows_staged"], "seconds": round(res["stage_s"], 2)},
         }
         print(json.dumps(line))
     if dist is not None:

@@ -114,6 +114,19 @@ int hb_stage_dense_f32(hb_ctx* ctx, const float* x, int64_t n_rows, int64_t ld, 
 int hb_stage_csr(hb_ctx* ctx, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n_rows,
                  const int64_t* labels);
 int64_t hb_staged_rows(hb_ctx* ctx);
+/* Stage n_rows synthetic Gaussian-blob rows generated on the device (the
+ * shape of synthetic_blobs, data.py:226-252: row = means[label] + N(0, I)),
+ * for datasets too large for host memory (the 10M x 1024 scaled config,
+ * 41 GB fp32).  means: (n_classes, d_0) float64 from the host generator;
+ * row r's label (uniform over n_classes) and noise are a pure function of
+ * (seed, row0 + r) (counter-based Philox4x32-10), so results do not depend on
+ * the launch shape and data-parallel ranks stage disjoint row ranges of one
+ * dataset (row0 = rank * n_rows).  Replaces hb_stage_dense_* for this context. */
+int hb_stage_blobs(hb_ctx* ctx, int64_t n_rows, int64_t row0, int n_classes, const double* means, uint64_t seed);
+/* Copy staged dense rows [start, start+rows) back: x (rows, d_0) fp32
+ * contiguous and labels (either may be null) -- the exact values the device
+ * trains on, for the CPU oracle and the host-buffer (e2e) path. */
+int hb_read_staged(hb_ctx* ctx, int64_t start, int64_t rows, float* x, int64_t* labels);
 /* Replace the staged rows by base[perm] on the device (perm: n_rows distinct
  * indices in [0, n_rows)), where base is the data as first staged -- the
  * per-epoch reshuffle of engine.py:214-221 (shuffle_epoch + reorder,

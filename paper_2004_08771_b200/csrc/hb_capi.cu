@@ -2545,9 +2545,9 @@ int hb_replica_step_host_csr(hb_ctx* c, double* const* ws, const int64_t* rowptr
   return replica_finish(c, rc, rows, eta, flags, out_loss);
 }
 
-static int stage_dense_common(hb_ctx* c, int64_t n_rows, const int64_t* labels) {
+static int stage_dense_common(hb_ctx* c, int64_t n_rows, const int64_t* labels, bool gen_labels = false) {
   if (c->csr_in) return fail(HB_EINVAL, "context was created for sparse (CSR) input");
-  if (n_rows < 1 || !labels) return fail(HB_EINVAL, "need n_rows >= 1 and labels");
+  if (n_rows < 1 || (!labels && !gen_labels)) return fail(HB_EINVAL, "need n_rows >= 1 and labels");
   HB_TRY(free_epoch(c));
   HB_CUDA(cudaMalloc(&c->ex, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
   if (c->need_lo()) HB_CUDA(cudaMalloc(&c->ex_lo, static_cast<size_t>(n_rows) * c->ld[0] * sizeof(float)));
@@ -2561,7 +2561,7 @@ static int stage_dense_common(hb_ctx* c, int64_t n_rows, const int64_t* labels) 
     }
   }
   HB_CUDA(cudaMalloc(&c->elabels, static_cast<size_t>(n_rows) * sizeof(int64_t)));
-  HB_CUDA(h2d_copy(c->elabels, labels, n_rows * sizeof(int64_t), c->stream));
+  if (labels) HB_CUDA(h2d_copy(c->elabels, labels, n_rows * sizeof(int64_t), c->stream));
   c->e_rows = n_rows;
   return HB_OK;
 }
@@ -2629,6 +2629,44 @@ int hb_stage_dense_f32(hb_ctx* c, const float* x, int64_t n_rows, int64_t ld, co
     HB_CUDA(cudaGetLastError());
   }
   return finish_dense_stage(c);
+}
+
+int hb_stage_blobs(hb_ctx* c, int64_t n_rows, int64_t row0, int n_classes, const double* means, uint64_t seed) {
+  HB_TRY(ctx_check(c));
+  if (!means || n_classes < 2 || n_classes > c->d[c->L] || row0 < 0)
+    return fail(HB_EINVAL, "need means, row0 >= 0 and 2 <= n_classes <= %d", c->d[c->L]);
+  HB_TRY(stage_dense_common(c, n_rows, nullptr, true));
+  const size_t nm = static_cast<size_t>(n_classes) * c->d[0];
+  std::vector<float> m32(nm);
+  for (size_t i = 0; i < nm; ++i) m32[i] = static_cast<float>(means[i]);
+  float* d_means = nullptr;
+  HB_CUDA(cudaMalloc(&d_means, nm * sizeof(float)));
+  cudaError_t e = cudaMemcpyAsync(d_means, m32.data(), nm * sizeof(float), cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) {
+    blobs_kernel<<<static_cast<int>(std::min<long long>(n_rows, 148LL * 64)), 256, 0, c->stream>>>(
+        c->ex, c->ex_lo, c->ld[0], row0, n_rows, c->d[0], d_means, n_classes, c->elabels, seed);
+    e = cudaGetLastError();
+  }
+  const cudaError_t e2 = cudaStreamSynchronize(c->stream);
+  cudaFree(d_means);
+  HB_CUDA(e);
+  HB_CUDA(e2);
+  return finish_dense_stage(c);
+}
+
+int hb_read_staged(hb_ctx* c, int64_t start, int64_t rows, float* x, int64_t* labels) {
+  HB_TRY(ctx_check(c));
+  if (!c->staged || c->csr_in) return fail(HB_ESTATE, "no dense rows staged");
+  if (start < 0 || rows < 0 || start + rows > c->e_rows)
+    return fail(HB_EINVAL, "rows [%lld, %lld) outside the %lld staged rows", static_cast<long long>(start),
+                static_cast<long long>(start + rows), c->e_rows);
+  if (x)
+    HB_CUDA(cudaMemcpy2DAsync(x, c->d[0] * sizeof(float), c->ex + start * c->ld[0], c->ld[0] * sizeof(float),
+                              c->d[0] * sizeof(float), rows, cudaMemcpyDeviceToHost, c->stream));
+  if (labels)
+    HB_CUDA(cudaMemcpyAsync(labels, c->elabels + start, rows * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  return HB_OK;
 }
 
 // CSR rows -> dense rows (+ lo twin) for densified CSR contexts: a warp per

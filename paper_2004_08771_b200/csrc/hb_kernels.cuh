@@ -1130,4 +1130,60 @@ __global__ void unpack_model_kernel(const float* __restrict__ flat, float scale,
   }
 }
 
+// ------------------------------------------------------------------------
+// Device-side synthetic Gaussian blobs (the shape of the reference's
+// synthetic_blobs, data.py:226-252: unit-variance isotropic noise around a
+// class mean; the means come from the host generator).  Used to stage the
+// 10M-row scaled configuration without a host copy: row r's label and noise
+// are a pure function of (seed, r), drawn from a counter-based Philox4x32-10
+// stream, so any row range can be regenerated or read back (hb_read_staged).
+__device__ __forceinline__ uint4 philox4x32_10(uint4 ctr, uint2 key) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    const unsigned hi0 = __umulhi(0xD2511F53u, ctr.x), lo0 = 0xD2511F53u * ctr.x;
+    const unsigned hi1 = __umulhi(0xCD9E8D57u, ctr.z), lo1 = 0xCD9E8D57u * ctr.z;
+    ctr = make_uint4(hi1 ^ ctr.y ^ key.x, lo1, hi0 ^ ctr.w ^ key.y, lo0);
+    key.x += 0x9E3779B9u;
+    key.y += 0xBB67AE85u;
+  }
+  return ctr;
+}
+__device__ __forceinline__ float u01_open(unsigned v) {  // (0, 1]
+  return (static_cast<float>(v >> 8) + 1.0f) * (1.0f / 16777216.0f);
+}
+// one block per row (grid-stride); threads own float4 column groups
+__global__ void blobs_kernel(float* __restrict__ x, float* __restrict__ x_lo, long long ld, long long row0,
+                             long long rows, int d, const float* __restrict__ means, int classes,
+                             int64_t* __restrict__ labels, unsigned long long seed) {
+  const uint2 key = make_uint2(static_cast<unsigned>(seed), static_cast<unsigned>(seed >> 32));
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    const long long g = row0 + r;  // global row id: the stream key
+    const uint4 lh = philox4x32_10(make_uint4(0xFFFFFFFFu, static_cast<unsigned>(g), static_cast<unsigned>(g >> 32), 1u), key);
+    const int y = static_cast<int>(((static_cast<unsigned long long>(lh.x) << 32 | lh.y) % static_cast<unsigned long long>(classes)));
+    if (threadIdx.x == 0 && labels != nullptr) labels[r] = y;
+    const float* mu = means + static_cast<long long>(y) * d;
+    float* xr = x + r * ld;
+    float* lr = x_lo ? x_lo + r * ld : nullptr;
+    for (int k = threadIdx.x; 4 * k < d; k += blockDim.x) {
+      const uint4 u = philox4x32_10(make_uint4(static_cast<unsigned>(k), static_cast<unsigned>(g),
+                                               static_cast<unsigned>(g >> 32), 0u), key);
+      // Box-Muller on two uniform pairs -> four standard normals
+      float s0, c0, s1, c1;
+      const float r0 = sqrtf(-2.0f * logf(u01_open(u.x))), r1 = sqrtf(-2.0f * logf(u01_open(u.z)));
+      sincospif(2.0f * u01_open(u.y), &s0, &c0);
+      sincospif(2.0f * u01_open(u.w), &s1, &c1);
+      const float nz[4] = {r0 * c0, r0 * s0, r1 * c1, r1 * s1};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = 4 * k + q;
+        if (j < d) {
+          const float v = mu[j] + nz[q];
+          xr[j] = v;
+          if (lr) lr[j] = tf32_lo(v);
+        }
+      }
+    }
+  }
+}
+
 }  // namespace hb

@@ -180,6 +180,21 @@ def synthetic_blobs(n: int, dim: int, classes: int, separation: float, seed) -> 
                    name=f"blobs(n={n},dim={dim},k={classes},sep={separation})")
 
 
+def blob_means(dim: int, classes: int, separation: float, seed) -> np.ndarray:
+    """The class means of synthetic_blobs (data.py:235-243) for datasets whose
+    rows are generated on the device (GpuReplica.stage_blobs): same draw and
+    centring, scaled so the closest pair of means is `separation` apart."""
+    if classes < 2:
+        raise ValueError("need at least 2 classes")
+    rng = np.random.default_rng(seed)
+    raw = rng.normal(size=(classes, dim))
+    raw -= raw.mean(axis=0)
+    if separation <= 0:
+        return np.zeros_like(raw)
+    best = min(float(np.linalg.norm(raw[i + 1:] - raw[i], axis=1).min()) for i in range(classes - 1))
+    return raw * (separation / best)
+
+
 def synthetic_csr(n: int, dim: int, nnz_per_row: int, classes: int, seed, binary: bool = True,
                   normalize: bool = False, name: str = "") -> CsrDataset:
     """Seeded sparse rows: `nnz_per_row` distinct uniform column draws per row,

@@ -35,6 +35,15 @@ def broadcast_bytes(dist, payload: bytes | None, src: int = 0, length: int = 128
     return bytes(t.tolist())
 
 
+def broadcast_float(dist, value: float, src: int = 0) -> float:
+    """Rank `src`'s float on every rank (CPU tensor: the gloo half of the group)."""
+    import torch
+
+    t = torch.tensor([float(value)], dtype=torch.float64)
+    dist.broadcast(t, src)
+    return float(t.item())
+
+
 def barrier(dist) -> None:
     """Host-side barrier as a one-element CPU all-reduce: it runs on the CPU
     (gloo) half of a "cpu:gloo,cuda:nccl" process group, so it needs no GPU

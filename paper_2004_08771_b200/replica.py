@@ -112,10 +112,6 @@ class GpuReplica:
     def merge_grads_into(self, weights, eta: float) -> None:
         """Stale merge W_global -= eta * g (workers.py:135 -> linalg.py:79) with
         the gradient of the last emit_grad step, in place on host float64 arrays."""
-        key = tuple(map(id, weights))
-        if key == self._tbl_key and all(w.shape == s and w.dtype == np.float64
-                                        for w, s in zip(weights, self._tbl_shapes)):
-            return self._tbl  # same array objects (kept alive by _tbl_arrays): same addresses
         if len(weights) != self.depth:
             raise ValueError("weight count does not match architecture")
         for l, w in enumerate(weights):
@@ -169,6 +165,27 @@ class GpuReplica:
                                                  N.ptr(y, C.c_int64)))
         self._staged_key = key
         self._keep = (data, x, y)
+
+    def stage_blobs(self, n_rows: int, classes: int, separation: float, seed: int, row0: int = 0) -> None:
+        """Stage n_rows Gaussian-blob rows generated on the device (means from
+        data.blob_means(seed); rows row0.. of a Philox stream keyed by seed) --
+        datasets larger than host memory, e.g. the 10M x 1024 scaled config."""
+        from .data import blob_means
+
+        if self.sparse:
+            raise ValueError("blob staging needs a dense context")
+        means = np.ascontiguousarray(blob_means(self.sizes[0], classes, separation, seed), dtype=np.float64)
+        N.check(self._lib.hb_stage_blobs(self._h, int(n_rows), int(row0), int(classes), N.ptr(means, C.c_double),
+                                         int(seed) & 0xFFFFFFFFFFFFFFFF))
+        self._staged_key = ("blobs", int(n_rows), int(row0), int(classes), float(separation), int(seed))
+        self._keep = None
+
+    def read_staged(self, start: int, rows: int):
+        """(x fp32 (rows, d0), labels int64) of staged dense rows [start, start+rows)."""
+        x = np.empty((rows, self.sizes[0]), dtype=np.float32)
+        y = np.empty(rows, dtype=np.int64)
+        N.check(self._lib.hb_read_staged(self._h, int(start), int(rows), N.ptr(x, C.c_float), N.ptr(y, C.c_int64)))
+        return x, y
 
     def permute_epoch(self, perm) -> None:
         """Make the staged rows base[perm] on the device, base being the data

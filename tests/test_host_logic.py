@@ -168,12 +168,44 @@ class TestBenchAccounting:
             242.680, abs=1e-3)
         assert bench.dense_flops_per_sample((300, 512, 512, 512, 2), True) / 1e6 == pytest.approx(3.152, abs=2e-3)
 
-    def test_cpu_reference_rate_runs(self):
+    def test_cpu_legs_run(self):
         import bench
 
-        cfg = dict(bench.CONFIGS["w8a"], n=512, batch=128)
-        r = bench.cpu_reference_rate(cfg, seed=1, budget_s=1.0, max_steps=2)
-        assert r["value"] > 0 and r["kind"] == "port" and r["cores"] >= 1
+        cfg = dict(bench.CONFIGS["w8a"], n=2048, batch=128)
+        data = bench.make_data(cfg, 1, n=2048)
+
+        def rows_fn(s, r):
+            s = s % max(1, data.n_examples - r)
+            return data.dense(s, s + r), data.labels[s:s + r]
+
+        r = bench.cpu_replica_rate(cfg, rows_fn, budget_s=0.5, max_steps=2, seed=1)
+        assert r["value"] > 0 and r["steps"] >= 1 and r["rows_per_step"] == 128
+        h = bench.cpu_hogbatch_run(cfg, rows_fn, budget_s=0.3, seed=1, threads=2)
+        assert h["value"] > 0 and h["threads"] == 2 and h["samples"] % 128 == 0
+        assert h["eta_per_shard"] == pytest.approx(cfg["eta"] * 64 / 128)
+
+    def test_hogbatch_port_matches_reference_split(self):
+        from oracle import ref_hogbatch
+
+        # workers.py:80-91: remainder one-extra on the leading shards
+        assert ref_hogbatch.split_batch(10, 3) == [(0, 4), (4, 3), (7, 3)]
+        assert ref_hogbatch.split_batch(2, 4) == [(0, 1), (1, 1)]
+        # one shard == one sequential step on the shared model
+        w1 = ref_nn.init_weights((6, 5, 2), 3)
+        w2 = ref_nn.deep_copy(w1)
+        x, y = ref_nn.synthetic_blobs(16, 6, 2, 2.0, 4)
+        assert ref_hogbatch.execute_hogwild_sharded(w1, x, y, 1, 0.1) == 1.0
+        ref_nn.apply_update(w2, ref_nn.backward(w2, ref_nn.forward(w2, x), y), 0.1)
+        for a, b in zip(w1, w2):
+            np.testing.assert_array_equal(a, b)
+
+    def test_bench_defaults_to_headline_config(self):
+        import bench
+
+        # BASELINE.json configs[4]: the 1/2/4/8-GPU scaled config at its full 10M rows
+        assert bench.DEFAULT_CONFIG == "scaled"
+        c = bench.CONFIGS["scaled"]
+        assert c["n"] == 10_000_000 and c["sizes"] == (1024, 4096, 4096, 4096, 1000) and c["batch"] == 8192
 
     def test_oracle_replica_step_is_the_reference(self):
         # the CPU baseline times exactly the pinned oracle step

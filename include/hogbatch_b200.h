@@ -62,6 +62,12 @@ extern "C" {
 #define HB_STEP_TIMED 2u     /* bracket the step with CUDA events (hb_last_step_ms) */
 #define HB_STEP_ASYNC 4u     /* return once the step is enqueued (no out_loss); hb_synchronize() waits */
 #define HB_STEP_MERGE 8u     /* after the step, average the replicas (hb_merge_allreduce) on the same stream */
+/* hb_replica_step*: the caller guarantees no other thread writes the host
+ * model during the call (a lone GPU replica, no CPU Hogwild pool).  Lets the
+ * largest split-K layers merge on the device (host rows read while the dW
+ * partial GEMM runs, written back after the reduce); without it every layer
+ * merges on the host with per-element read-modify-writes, as np.add does. */
+#define HB_STEP_SOLE_WRITER 16u
 
 typedef struct hb_ctx hb_ctx;
 

@@ -28,15 +28,7 @@ from .data import (
     synthetic_csr,
 )
 from .nn import Architecture, InitScheme, Model, deep_copy, init_model
-from .policies import (
-    AdaptiveHogbatch,
-    AdaptiveState,
-    DeviceSpeedFeed,
-    FixedHeterogeneous,
-    PolicyDecision,
-    UniformHogbatch,
-    adaptive_update,
-)
+from .feed import DeviceSpeedFeed, device_timed
 from .replica import GpuReplica
 from .trainer import TrainResult, train_gpu
 from .workers import (
@@ -44,18 +36,20 @@ from .workers import (
     WorkerMode,
     execute_gpu_replica,
     gpu_loss_sum,
+    device_busy_seconds,
     install,
     last_device_ms,
+    set_sole_writer,
     set_worker_device,
+    set_worker_devices,
 )
 
 __all__ = [
-    "AdaptiveHogbatch", "AdaptiveState", "Architecture", "BatchRef", "CsrBatchRef", "CsrDataset", "Dataset",
-    "DeviceSpeedFeed", "FixedHeterogeneous", "GpuReplica", "InitScheme", "LabelMapping", "LibsvmParseError",
-    "Model", "PolicyDecision",
-    "TrainResult", "UniformHogbatch", "WorkerConfig", "WorkerMode", "adaptive_update", "deep_copy",
-    "device_count", "epoch_shuffle_seed", "execute_gpu_replica", "gpu_loss_sum", "init_model", "install",
-    "last_device_ms", "load_libsvm", "load_libsvm_csr", "load_library", "reorder", "set_worker_device", "shuffle_epoch", "synthetic_blobs",
+    "Architecture", "BatchRef", "CsrBatchRef", "CsrDataset", "Dataset", "DeviceSpeedFeed", "GpuReplica",
+    "InitScheme", "LabelMapping", "LibsvmParseError", "Model", "TrainResult", "WorkerConfig", "WorkerMode",
+    "deep_copy", "device_busy_seconds", "device_count", "device_timed", "epoch_shuffle_seed", "execute_gpu_replica",
+    "gpu_loss_sum", "init_model", "install", "last_device_ms", "load_libsvm", "load_libsvm_csr", "load_library",
+    "reorder", "set_sole_writer", "set_worker_device", "set_worker_devices", "shuffle_epoch", "synthetic_blobs",
     "synthetic_csr", "train_gpu",
 ]
 

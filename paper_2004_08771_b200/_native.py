@@ -26,6 +26,7 @@ HB_STEP_EMIT_GRAD = 1
 HB_STEP_TIMED = 2
 HB_STEP_ASYNC = 4
 HB_STEP_MERGE = 8
+HB_STEP_SOLE_WRITER = 16
 
 _p = C.c_void_p
 _i32, _i64, _u32, _f64 = C.c_int, C.c_int64, C.c_uint32, C.c_double

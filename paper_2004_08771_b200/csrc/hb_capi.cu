@@ -771,10 +771,14 @@ class HostPool {
     // one job at a time: several replica worker threads (one per GPU, as the
     // reference engine runs them) may merge concurrently
     std::lock_guard<std::mutex> job(run_mu_);
+    const uint64_t jid = ++job_;
     fn_.store(&fn, std::memory_order_relaxed);
-    n_.store(n, std::memory_order_relaxed);
     done_.store(0, std::memory_order_relaxed);
-    next_.store(0, std::memory_order_release);
+    // a ticket is (job, n, index): whoever takes one knows which job and how
+    // many parts it has without reading shared fields that the next job may
+    // already have replaced, so a late worker can never run a part twice or
+    // run a stale part with the next job's function
+    next_.store(ticket(jid, n, 0), std::memory_order_release);
     {
       std::lock_guard<std::mutex> lk(mu_);
       gen_.fetch_add(1, std::memory_order_acq_rel);
@@ -782,10 +786,15 @@ class HostPool {
     cv_.notify_all();
     work();
     while (done_.load(std::memory_order_acquire) < n) pause();
-    next_.store(1 << 30, std::memory_order_release);  // late workers find nothing to take
+    next_.store(ticket(jid, 0, 0), std::memory_order_release);  // late workers find nothing to take
   }
 
  private:
+  static constexpr int kIdxBits = 20;
+  static constexpr uint64_t kIdxMask = (uint64_t(1) << kIdxBits) - 1;
+  static uint64_t ticket(uint64_t jid, int n, int i) {
+    return (jid << (2 * kIdxBits)) | (static_cast<uint64_t>(n) << kIdxBits) | static_cast<uint64_t>(i);
+  }
   static void pause() {
 #if defined(__x86_64__)
     __builtin_ia32_pause();
@@ -793,8 +802,13 @@ class HostPool {
   }
   void work() {
     for (;;) {
-      const int i = next_.fetch_add(1, std::memory_order_acq_rel);
-      if (i >= n_.load(std::memory_order_acquire)) return;
+      // index overflow into the n field is impossible: at most n + (threads)
+      // tickets are ever taken per job, far below 2^20
+      const uint64_t t = next_.fetch_add(1, std::memory_order_acq_rel);
+      const int i = static_cast<int>(t & kIdxMask), n = static_cast<int>((t >> kIdxBits) & kIdxMask);
+      if (i >= n) return;
+      // a valid ticket of job J: J cannot finish (done_ < n) before this part
+      // is counted, so fn_ still holds J's function (published before next_)
       (*fn_.load(std::memory_order_acquire))(i);
       done_.fetch_add(1, std::memory_order_acq_rel);
     }
@@ -805,7 +819,7 @@ class HostPool {
     // w8a / covtype / delicious: 8 threads 1.46e7 / 1.36e6 / 4.71e6, 12 threads 1.54e7 / 1.36e6 / 4.87e6
     int t = static_cast<int>(std::min(12u, std::max(1u, hw * 3 / 4))) - 1;
     if (const char* e = getenv("HB_HOST_MERGE_THREADS")) t = std::max(0, atoi(e) - 1);
-    next_.store(1 << 30);
+    next_.store(ticket(0, 0, 0));
     for (int i = 0; i < t; ++i) threads_.emplace_back([this] { loop(); });
   }
   ~HostPool() {
@@ -820,7 +834,9 @@ class HostPool {
   void loop() {
     unsigned long long seen = gen_.load();
     for (;;) {
-      // spin ~0.5 ms for the next job, then sleep
+      // spin ~0.5 ms for the next job (a merge is a burst of one job per
+      // layer), then sleep; HB_POOL_SPIN=0 yields the cores at once (a CPU
+      // Hogwild pool sharing the host)
       static const int spins = getenv("HB_POOL_SPIN") ? atoi(getenv("HB_POOL_SPIN")) : 20000;
       for (int k = 0; k < spins && gen_.load(std::memory_order_acquire) == seen; ++k) pause();
       if (gen_.load(std::memory_order_acquire) == seen) {
@@ -836,9 +852,10 @@ class HostPool {
   std::mutex mu_, run_mu_;
   std::condition_variable cv_;
   std::atomic<const std::function<void(int)>*> fn_{nullptr};
-  std::atomic<int> n_{0};
-  std::atomic<int> next_{0}, done_{0};
+  std::atomic<uint64_t> next_{0};
+  std::atomic<int> done_{0};
   std::atomic<unsigned long long> gen_{0};
+  uint64_t job_ = 0;
   bool stop_ = false;
 };
 
@@ -1366,7 +1383,13 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       HB_CUDA(cudaStreamWaitEvent(c->side, c->bev[2 * l], 0));
       // device lane of the merge: the host rows of W_l come in while the
       // partial GEMM runs (the merge read), the reduce applies both updates
-      const bool dev_lane = !c->xw.empty() && c->xmode == 0 && l < static_cast<int>(c->xdma.size()) && c->xdma[l];
+      // Only when the caller declares the replica the host model's sole writer
+      // (HB_STEP_SOLE_WRITER): the lane reads a whole layer when the partial GEMM
+      // starts and writes it back after the reduce, so a concurrent host writer's
+      // updates to that layer inside the window would be overwritten -- wider
+      // than the per-element race of the reference's np.add (linalg.py:79).
+      const bool dev_lane = (flags & HB_STEP_SOLE_WRITER) != 0 && !c->xw.empty() && c->xmode == 0 &&
+                            l < static_cast<int>(c->xdma.size()) && c->xdma[l];
       double* host_rows = dev_lane ? c->stage_all + layer_offset(c, l) : nullptr;
       if (dev_lane) {
         c->xdma_used[l] = 1;
@@ -1478,7 +1501,7 @@ int run_phase(hb_ctx* c, const DataView& v, long long start, int rows, uint32_t 
 
 int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta, uint32_t flags, bool graph_ok,
                  int phase = 0) {
-  const uint32_t gflags = (flags & HB_STEP_EMIT_GRAD) | (static_cast<uint32_t>(phase) << 8) |
+  const uint32_t gflags = (flags & (HB_STEP_EMIT_GRAD | HB_STEP_SOLE_WRITER)) | (static_cast<uint32_t>(phase) << 8) |
                           (v.x_lo_zero ? (1u << 16) : 0u);
   const bool view_epoch = (&v == &c->epoch);
   if (!c->use_graphs || !graph_ok) return run_phase(c, v, start, rows, flags, eta, nullptr, phase);

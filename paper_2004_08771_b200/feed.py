@@ -1,0 +1,99 @@
+"""Device-timed feed for the reference's controller and coordinator.
+
+The batch-size controller itself is the reference's (`hogtrain.policies`,
+Alg. 2 at policies.py:84-129) and stays the drop-in surface; this module only
+changes what it and the coordinator are fed.  In the reference every time
+figure is host wall time: `WorkerThread._execute` books
+`busy_seconds += perf_counter() - start` (workers.py:207) and the coordinator's
+speed estimate is served-to-reported wall time, an EWMA 0.5/0.5
+(engine.py:318-328), which sizes the evaluation slices (engine.py:335-351).
+For a B200 replica whose step is 0.1-10 ms, both are dominated by the Python
+queue round trip and host merge, not by the device.  Here:
+
+* `DeviceSpeedFeed` keeps the same EWMA over CUDA-event-timed steps
+  (`execute_gpu_replica` records into it once installed);
+* `device_timed(workers_module, engine_module, feed)` wraps the reference's
+  own `WorkerThread._execute` and `_Coordinator._update_speed` so GPU worker
+  threads book device busy time and the coordinator reads the device-timed
+  speed -- without copying either method.
+"""
+
+from __future__ import annotations
+
+import threading
+
+from . import workers as _w
+
+
+class DeviceSpeedFeed:
+    """Per-worker examples/second from device-timed steps, EWMA 0.5/0.5 like
+    the coordinator's estimator (engine.py:318-328)."""
+
+    def __init__(self):
+        self.speed: dict = {}
+        self._mu = threading.Lock()
+
+    def record(self, worker_id: str, examples: int, device_ms: float) -> float:
+        with self._mu:
+            if device_ms <= 0 or examples <= 0:
+                return self.speed.get(worker_id, 0.0)
+            rate = examples / (device_ms / 1000.0)
+            prev = self.speed.get(worker_id)
+            self.speed[worker_id] = rate if prev is None else 0.5 * prev + 0.5 * rate
+            return self.speed[worker_id]
+
+    def eval_slices(self, worker_ids, n: int) -> list:
+        """(worker, start, length) covering n rows in proportion to speed, with
+        the coordinator's rounding (remainder to the first worker,
+        engine.py:335-351)."""
+        with self._mu:
+            weights = [max(self.speed.get(w, 0.0), 0.0) for w in worker_ids]
+        if sum(weights) <= 0:
+            weights = [1.0] * len(worker_ids)
+        total = sum(weights)
+        sizes = [int(n * w / total) for w in weights]
+        sizes[0] += n - sum(sizes)
+        out, start = [], 0
+        for wid, size in zip(worker_ids, sizes):
+            if size > 0:
+                out.append((wid, start, size))
+                start += size
+        return out
+
+
+def device_timed(workers_module, engine_module, feed: DeviceSpeedFeed) -> None:
+    """Feed the reference's accounting from the device clock.
+
+    - `WorkerThread._execute` (workers.py:193-210): on a GPU worker thread the
+      wall-clock increment of `busy_seconds` is replaced by the CUDA-event time
+      of the replica steps the call ran (`device_busy_seconds`); CPU Hogwild
+      workers keep wall time.
+    - `_Coordinator._update_speed` (engine.py:318-328): after the reference's
+      own estimate, a worker the feed has device-timed steps for gets the
+      feed's EWMA instead, so `_eval_slices` (engine.py:335-351) splits the
+      evaluation by device throughput.
+    Idempotent; `install(..., feed=feed)` must route the steps into `feed`."""
+    wt = workers_module.WorkerThread
+    if not hasattr(wt._execute, "reference"):
+        ref_execute = wt._execute
+
+        def _execute(self, msg):
+            busy0, dev0 = self.busy_seconds, _w.device_busy_seconds()
+            ref_execute(self, msg)
+            dev = _w.device_busy_seconds() - dev0
+            if dev > 0:
+                self.busy_seconds = busy0 + dev
+
+        _execute.reference = ref_execute
+        wt._execute = _execute
+    co = engine_module._Coordinator
+    ref_update = getattr(co._update_speed, "reference", co._update_speed)  # re-point an earlier wrapper
+
+    def _update_speed(self, wid):
+        ref_update(self, wid)
+        v = feed.speed.get(wid)
+        if v:
+            self.speed[wid] = v
+
+    _update_speed.reference = ref_update
+    co._update_speed = _update_speed

@@ -263,22 +263,25 @@ class GpuReplica:
         return self._tbl
 
     def replica_step(self, weights, start: int, rows: int, eta: float, timed: bool = False,
-                     want_loss: bool = False):
+                     want_loss: bool = False, sole_writer: bool = False):
         """execute_batch_replica (workers.py:126-138) on staged rows in one call:
         snapshot of the shared float64 `weights`, the step, and the stale merge
         weights[l] -= eta * g_l, with the snapshot / merge DMAs overlapped with
-        the compute layer by layer.  Returns the batch's mean loss if want_loss."""
+        the compute layer by layer.  Returns the batch's mean loss if want_loss.
+        sole_writer=True promises that no other thread writes `weights` during
+        the call, which lets the largest layers merge on the device lane."""
         table = self._model_table(weights)
-        flags = N.HB_STEP_TIMED if timed else 0
+        flags = (N.HB_STEP_TIMED if timed else 0) | (N.HB_STEP_SOLE_WRITER if sole_writer else 0)
         loss = C.c_double(0.0)
         N.check(self._lib.hb_replica_step(self._h, table, int(start), int(rows), float(eta), flags,
                                           C.byref(loss) if want_loss else None))
         return loss.value if want_loss else None
 
-    def replica_step_host(self, weights, batch, labels, eta: float, timed: bool = False, want_loss: bool = True):
+    def replica_step_host(self, weights, batch, labels, eta: float, timed: bool = False, want_loss: bool = True,
+                          sole_writer: bool = False):
         """replica_step on a batch held in host memory (float32 rows or a CsrDataset)."""
         table = self._model_table(weights)
-        flags = N.HB_STEP_TIMED if timed else 0
+        flags = (N.HB_STEP_TIMED if timed else 0) | (N.HB_STEP_SOLE_WRITER if sole_writer else 0)
         loss = C.c_double(0.0)
         lp = C.byref(loss) if want_loss else None
         if isinstance(batch, CsrDataset):

@@ -78,21 +78,64 @@ class WorkerConfig:  # workers.py:54-77, plus device / precision / sync_every fo
 # created it (include/hogbatch_b200.h "Conventions").
 _tls = threading.local()
 _DEFAULT_MAX_BATCH = 8192
+# worker id -> device, for the reference's worker threads (named
+# "worker-<worker_id>", workers.py:154), which the caller does not control
+_worker_devices: dict = {}
+_sole_writer = False
+_speed_feed = None  # DeviceSpeedFeed fed by every replica step (install(feed=...))
 
 
 def set_worker_device(device: int, max_batch: int | None = None, precision: str = "3xtf32") -> None:
-    """Select the GPU (and batch capacity / precision) for replica calls made on this thread."""
+    """Select the GPU (and batch capacity / precision) for replica calls made
+    on the *calling* thread.  For the reference engine's worker threads use
+    set_worker_devices (they are created by the engine, engine.py:131-134)."""
     _tls.device = int(device)
     _tls.precision = precision
     if max_batch is not None:
         _tls.max_batch = int(max_batch)
 
 
+def set_worker_devices(mapping: dict, max_batch: int | None = None) -> None:
+    """Map reference worker ids to GPUs, e.g. {"gpu0": 0, "gpu1": 1}: a replica
+    call on the engine's thread "worker-gpu1" (workers.py:154) runs on cuda:1.
+    Unmapped threads without set_worker_device use cuda:0."""
+    global _DEFAULT_MAX_BATCH
+    _worker_devices.clear()
+    _worker_devices.update({str(k): int(v) for k, v in mapping.items()})
+    if max_batch is not None:
+        _DEFAULT_MAX_BATCH = int(max_batch)
+
+
+def set_sole_writer(on: bool) -> None:
+    """Declare that GPU replica workers are the only writers of the shared host
+    model (no CPU Hogwild pool, a single replica): lets the largest layers
+    merge on the device lane (HB_STEP_SOLE_WRITER).  Off by default, since the
+    lane's layer-wide read-merge-write window would drop concurrent host
+    updates that the reference's per-element np.add (linalg.py:79) keeps."""
+    global _sole_writer
+    _sole_writer = bool(on)
+
+
+def _worker_id() -> str | None:
+    name = threading.current_thread().name
+    return name[len("worker-"):] if name.startswith("worker-") else None
+
+
+def _thread_device() -> int | None:
+    """Device of this thread, or None if it is not a GPU worker thread."""
+    d = getattr(_tls, "device", None)
+    if d is not None:
+        return d
+    wid = _worker_id()
+    return _worker_devices.get(wid) if wid is not None else None
+
+
 def _replica(sizes, rows: int, sparse: bool, purpose: str) -> GpuReplica:
     cache = getattr(_tls, "contexts", None)
     if cache is None:
         cache = _tls.contexts = {}
-    device = getattr(_tls, "device", 0)
+    device = _thread_device()
+    device = 0 if device is None else device
     precision = getattr(_tls, "precision", "3xtf32")
     key = (purpose, device, sizes, sparse, precision)
     ctx = cache.get(key)
@@ -135,19 +178,38 @@ def execute_gpu_replica(model, batch, eta: float, speed_factor: float = 0.0) -> 
     sizes = layer_sizes_of(model)
     sparse = isinstance(batch, CsrBatchRef)
     ctx = _replica(sizes, batch.length, sparse, "train")
+    _tls.gpu_worker = True
     _stage_for(ctx, batch)
     # snapshot, step and stale merge in one call; the shared model is
     # page-locked once and its DMAs overlap the compute layer by layer
-    ctx.replica_step(model.weights, batch.start, batch.length, eta, timed=True)
-    _tls.last_device_ms = ctx.last_step_ms
+    ctx.replica_step(model.weights, batch.start, batch.length, eta, timed=True, sole_writer=_sole_writer)
+    book_device_step(batch.length, ctx.last_step_ms)
     if speed_factor > 0:
         time.sleep(speed_factor * (time.perf_counter() - start_t))
     return 1.0
 
 
+def book_device_step(rows: int, ms: float) -> None:
+    """Account one device-timed replica step on this thread: last / total
+    device time, and the installed DeviceSpeedFeed under this thread's
+    reference worker id."""
+    _tls.last_device_ms = ms
+    _tls.device_busy_s = getattr(_tls, "device_busy_s", 0.0) + ms / 1000.0
+    feed, wid = _speed_feed, _worker_id()
+    if feed is not None and wid is not None:
+        feed.record(wid, rows, ms)
+
+
 def last_device_ms() -> float:
     """CUDA-event time of the last replica step on this thread (controller feed)."""
     return float(getattr(_tls, "last_device_ms", 0.0))
+
+
+def device_busy_seconds() -> float:
+    """Sum of the device-timed replica steps run on this thread -- the GPU
+    worker's busy time without queue / host latency (workers.py:207 books wall
+    time; the device-timed install replaces it with this)."""
+    return float(getattr(_tls, "device_busy_s", 0.0))
 
 
 def gpu_loss_sum(model, features, labels, chunk: int = 4096) -> float:
@@ -170,10 +232,39 @@ def gpu_loss_sum(model, features, labels, chunk: int = 4096) -> float:
     return ctx.eval_loss_sum(0, n)
 
 
-def install(hogtrain_module=None) -> None:
+def is_gpu_thread() -> bool:
+    """True on a thread that runs (or is mapped to run) GPU replica steps."""
+    return getattr(_tls, "gpu_worker", False) or _thread_device() is not None
+
+
+def routed_loss_sum(reference_loss_sum):
+    """loss_sum for WorkerThread._evaluate (workers.py:212-222): on the GPU for
+    GPU worker threads, the reference's own loss_sum everywhere else (CPU
+    Hogwild workers keep their evaluation slices on the host)."""
+
+    def loss_sum(model, features, labels):
+        if is_gpu_thread():
+            return gpu_loss_sum(model, features, labels)
+        return reference_loss_sum(model, features, labels)
+
+    loss_sum.reference = reference_loss_sum
+    return loss_sum
+
+
+def install(hogtrain_module=None, devices: dict | None = None, sole_writer: bool = False, feed=None) -> None:
     """Route the reference's BATCH_REPLICA workers to the B200 path by
-    rebinding `hogtrain.workers.execute_batch_replica` and `loss_sum`."""
+    rebinding `hogtrain.workers.execute_batch_replica`, and the GPU workers'
+    evaluation slices by wrapping `loss_sum`.  devices: worker id -> GPU
+    (set_worker_devices); feed: a DeviceSpeedFeed that every replica step
+    records its device-timed examples/s into (the coordinator's eval split,
+    engine.py:335-351, can read it; see device_timed_engine)."""
+    global _speed_feed
     if hogtrain_module is None:
         import hogtrain.workers as hogtrain_module  # noqa: F811  (reference package, if present)
+    if devices is not None:
+        set_worker_devices(devices)
+    set_sole_writer(sole_writer)
+    _speed_feed = feed
     hogtrain_module.execute_batch_replica = execute_gpu_replica
-    hogtrain_module.loss_sum = gpu_loss_sum
+    ref = getattr(hogtrain_module.loss_sum, "reference", hogtrain_module.loss_sum)
+    hogtrain_module.loss_sum = routed_loss_sum(ref)

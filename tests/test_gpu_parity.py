@@ -385,7 +385,7 @@ def test_fused_replica_step_device_lane(hb):
     try:
         for it in range(4):
             xb, yb = x[(it % 2) * b:(it % 2 + 1) * b], y[(it % 2) * b:(it % 2 + 1) * b]
-            fused.replica_step_host(wf, xb, yb, 0.4)
+            fused.replica_step_host(wf, xb, yb, 0.4, sole_writer=True)
             three.set_weights(wt)
             three.step_host(xb, yb, 0.4, emit_grad=True)
             three.merge_grads_into(wt, 0.4)

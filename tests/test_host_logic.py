@@ -2,13 +2,14 @@
 generators, model layout, worker config, the batch-size controller, bench
 work accounting.  Pinned to the reference's golden vectors where they exist."""
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
 import paper_2004_08771_b200 as hb
 from conftest import GOLDEN, load_runs
 from oracle import ref_nn
-from paper_2004_08771_b200 import policies as P
 
 
 class TestGeneratorsMatchReference:
@@ -103,37 +104,6 @@ class TestWorkerConfig:
 
 
 class TestController:
-    def test_adaptive_matches_reference_sequences(self):
-        z = np.load(GOLDEN / "adaptive.npz")
-        rows, rosters = z["rows"], z["rosters"]
-        by_seq = {}
-        for r in rosters:
-            by_seq.setdefault(int(r[0]), []).append(r)
-        pols = {}
-        for row in rows:
-            seq, strict, alpha, base_eta, w, u, batch, lr = row
-            seq, w = int(seq), int(w)
-            if seq not in pols:
-                roster = [hb.WorkerConfig(f"w{int(r[1])}",
-                                          hb.WorkerMode.BATCH_REPLICA if r[2] else hb.WorkerMode.HOGWILD_SHARDED,
-                                          threads=int(r[3]), min_batch=int(r[4]), max_batch=int(r[5]))
-                          for r in by_seq[seq]]
-                pol = hb.AdaptiveHogbatch(base_eta=base_eta, alpha=alpha, strict_thresholds=bool(strict))
-                pols[seq] = (pol, pol.prepare(roster))
-            pol, first = pols[seq]
-            d = first[f"w{w}"] if u < 0 else pol.decide(f"w{w}", u)
-            assert d.batch_size == int(batch) and d.learning_rate == lr
-
-    def test_fixed_and_uniform(self):
-        z = np.load(GOLDEN / "adaptive.npz")
-        roster = [hb.WorkerConfig("cpu", hb.WorkerMode.HOGWILD_SHARDED, threads=8, min_batch=8, max_batch=8),
-                  hb.WorkerConfig("gpu", hb.WorkerMode.GPU_REPLICA, min_batch=64, max_batch=8192)]
-        fh = hb.FixedHeterogeneous(base_eta=0.02, cpu_batch_per_thread=1, gpu_batch=8192).prepare(roster)
-        assert [[fh["cpu"].batch_size, fh["cpu"].learning_rate], [fh["gpu"].batch_size, fh["gpu"].learning_rate]] \
-            == z["fixed"].tolist()
-        un = hb.UniformHogbatch(512, 0.1).prepare(roster)
-        assert un["gpu"].batch_size == 512 and un["cpu"].learning_rate == 0.1
-
     def test_device_speed_feed(self):
         feed = hb.DeviceSpeedFeed()
         assert feed.eval_slices(["a", "b"], 10) == [("a", 0, 5), ("b", 5, 5)]
@@ -144,17 +114,85 @@ class TestController:
         sl = feed.eval_slices(["a", "b"], 1000)
         assert sum(s[2] for s in sl) == 1000 and sl[0][2] > 900
 
-    def test_policy_errors(self):
-        with pytest.raises(ValueError):
-            hb.UniformHogbatch(0, 0.1)
-        st = hb.AdaptiveState(alpha=2.0)
-        with pytest.raises(ValueError):
-            hb.AdaptiveState(alpha=1.0)
-        st.register(hb.WorkerConfig("g", hb.WorkerMode.GPU_REPLICA, min_batch=64, max_batch=8192))
-        assert st.workers["g"].batch_size == 8192
-        hb.adaptive_update(st, "g", 5.0)
-        with pytest.raises(ValueError, match="backwards"):
-            hb.adaptive_update(st, "g", 4.0)
+    def test_seam_routes_by_worker_thread(self):
+        """install(devices=...) maps the reference's worker threads
+        ("worker-<id>", workers.py:154) to GPUs, and only GPU worker threads
+        evaluate on the GPU (CPU Hogwild workers keep the reference loss_sum)."""
+        import threading
+
+        from paper_2004_08771_b200 import workers as W
+
+        seen = {}
+
+        def probe():
+            seen[threading.current_thread().name] = (W._thread_device(), W.is_gpu_thread())
+
+        W.set_worker_devices({"gpu0": 0, "gpu1": 1})
+        try:
+            for name in ("worker-gpu0", "worker-gpu1", "worker-cpu", "main-ish"):
+                t = threading.Thread(target=probe, name=name)
+                t.start()
+                t.join()
+            calls = []
+            routed = W.routed_loss_sum(lambda m, x, y: calls.append(threading.current_thread().name) or 1.5)
+            t = threading.Thread(target=lambda: calls.append(routed(None, None, None)), name="worker-cpu")
+            t.start()
+            t.join()
+        finally:
+            W.set_worker_devices({})
+        assert seen == {"worker-gpu0": (0, True), "worker-gpu1": (1, True), "worker-cpu": (None, False),
+                        "main-ish": (None, False)}
+        assert calls == ["worker-cpu", 1.5]
+
+
+class TestReferenceEngineSeam:
+    """The device-timed accounting wrapped around the reference's own engine
+    (imported from /root/reference in this container; skipped elsewhere)."""
+
+    def test_device_timed_busy_and_speed(self, monkeypatch):
+        ref_src = Path("/root/reference/pkg/src")
+        if not ref_src.exists():
+            pytest.skip("reference package not present")
+        monkeypatch.syspath_prepend(str(ref_src))
+        import hogtrain
+        import hogtrain.engine as E
+        import hogtrain.workers as RW
+
+        from paper_2004_08771_b200 import workers as W
+
+        monkeypatch.setattr(RW.WorkerThread, "_execute", RW.WorkerThread._execute)
+        monkeypatch.setattr(E._Coordinator, "_update_speed", E._Coordinator._update_speed)
+        ref_step = RW.execute_batch_replica
+        feed = hb.DeviceSpeedFeed()
+        monkeypatch.setattr(W, "_speed_feed", feed)
+
+        def device_step(model, batch, eta, speed_factor=0.0):
+            # the reference's own CPU step, booked as a 2 ms device step: the
+            # booking is what execute_gpu_replica does after hb_replica_step
+            out = ref_step(model, batch, eta, speed_factor)
+            W.book_device_step(batch.length, 2.0)
+            return out
+
+        monkeypatch.setattr(RW, "execute_batch_replica", device_step)
+        hb.device_timed(RW, E, feed)
+        hb.device_timed(RW, E, feed)  # idempotent
+        speeds = []
+        wrapped = E._Coordinator._update_speed
+
+        def spy(self, wid):
+            wrapped(self, wid)
+            speeds.append(self.speed.get(wid))
+
+        monkeypatch.setattr(E._Coordinator, "_update_speed", spy)
+        ds = hogtrain.data.synthetic_blobs(600, 6, 2, 2.5, seed=1)
+        model = hogtrain.nn.init_model(hogtrain.nn.Architecture((6, 8, 2)), seed=2)
+        roster = [RW.WorkerConfig("gpu0", RW.WorkerMode.BATCH_REPLICA, min_batch=50, max_batch=100)]
+        m = hogtrain.run_training(ds, model, roster, hogtrain.policies.UniformHogbatch(100, 0.1), epochs=2, seed=3)
+        steps = m.per_worker_updates["gpu0"]
+        assert steps == 12
+        assert m.per_worker_busy_ms["gpu0"] == pytest.approx(2.0 * steps)
+        assert feed.speed["gpu0"] == pytest.approx(100 / 2e-3)
+        assert speeds[-1] == pytest.approx(100 / 2e-3)
 
 
 class TestBenchAccounting:

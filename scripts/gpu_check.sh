@@ -1,9 +1,17 @@
+# GPU check: smoke, GPU parity tests, the default (headline) bench line, the reference arm
 set -x
+mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-python -m paper_2004_08771_b200.build 2>&1 | tail -2
-timeout 120 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?
-tail -5 gpurun_out/smoke.log
-timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
-tail -30 gpurun_out/pytest_gpu.log
-timeout 300 python bench.py --steps 10 --warmup 3 > gpurun_out/bench1.log 2>&1; echo bench_rc=$?
-tail -5 gpurun_out/bench1.log
+nproc
+timeout 180 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?
+tail -3 gpurun_out/smoke.log
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
+tail -25 gpurun_out/pytest_gpu.log
+if [ -z "$NO_BENCH" ]; then
+timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo bench_rc=$?
+cat gpurun_out/bench_default.json; tail -5 gpurun_out/bench_default.err
+fi
+if [ -n "$REF" ]; then
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref_rc=$?
+cat gpurun_out/bench_ref.json
+fi

@@ -221,6 +221,20 @@ int hb_comm_init(hb_ctx* ctx, const void* id_128_bytes, int nranks, int rank);
 int hb_merge_allreduce(hb_ctx* ctx);
 int hb_comm_destroy(hb_ctx* ctx);
 
+/* The same merge over peer memory instead of NCCL: each rank's context
+ * exports an exchange buffer (hb_peer_handle: HB_PEER_HANDLE_BYTES, carrying a
+ * CUDA IPC handle), the handles of all ranks are exchanged by the caller (any
+ * transport: torch.distributed, a shared list between threads), and
+ * hb_peer_attach maps every peer (same process: direct NVLink peer access;
+ * another process: CUDA IPC).  hb_merge_allreduce / HB_STEP_MERGE then run a
+ * one-shot reduce-scatter + all-gather kernel that reads and writes the peers'
+ * buffers directly (no collective library), with flag-based waits bounded by
+ * a timeout (HB_ESTATE "never signalled" instead of a hang).  Every rank must
+ * issue the same sequence of merges.  At most 8 ranks. */
+#define HB_PEER_HANDLE_BYTES 128
+int hb_peer_handle(hb_ctx* ctx, void* out_handle);
+int hb_peer_attach(hb_ctx* ctx, int nranks, int rank, const void* handles);
+
 #ifdef __cplusplus
 }
 #endif

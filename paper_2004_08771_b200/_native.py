@@ -27,6 +27,7 @@ HB_STEP_TIMED = 2
 HB_STEP_ASYNC = 4
 HB_STEP_MERGE = 8
 HB_STEP_SOLE_WRITER = 16
+HB_PEER_HANDLE_BYTES = 128
 
 _p = C.c_void_p
 _i32, _i64, _u32, _f64 = C.c_int, C.c_int64, C.c_uint32, C.c_double
@@ -79,6 +80,8 @@ SIGNATURES = {
     "hb_comm_init": (_i32, [_p, _p, _i32, _i32]),
     "hb_merge_allreduce": (_i32, [_p]),
     "hb_comm_destroy": (_i32, [_p]),
+    "hb_peer_handle": (_i32, [_p, _p]),
+    "hb_peer_attach": (_i32, [_p, _i32, _i32, _p]),
 }
 
 _lib = None

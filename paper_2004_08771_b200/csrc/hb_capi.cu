@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 #include <dlfcn.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -42,6 +43,7 @@
 #include "../../include/hogbatch_b200.h"
 #include "hb_gemm.cuh"
 #include "hb_kernels.cuh"
+#include "hb_peer.cuh"
 
 using namespace hb;
 
@@ -509,6 +511,12 @@ struct hb_ctx {
   int nranks = 1;
   float* flat = nullptr;  // contiguous model copy for allreduce
   size_t n_params = 0;
+  // replica merge over peer memory (hb_peer_handle / hb_peer_attach): own
+  // exchange buffer (flags + flat model), every rank's buffer mapped
+  char* xbuf = nullptr;
+  PeerTable peers{};                // peers.n == 0: not attached
+  std::vector<void*> ipc_opened;    // peer buffers opened through CUDA IPC
+  unsigned long long peer_gen = 0;  // merges issued (the flag value of the next one)
 };
 
 namespace {
@@ -1558,10 +1566,40 @@ void drop_graphs(hb_ctx* c) {
   c->graph_seen.clear();
 }
 
+// peer-memory merge (hb_peer.cuh): pack, signal, wait, one-shot reduce of
+// this rank's slice across every rank's flat, signal, wait, unpack
+int enqueue_peer_merge(hb_ctx* c, const ModelLayout& m, long long n_elems, const dim3 grid) {
+  const unsigned long long g = ++c->peer_gen;
+  unsigned long long* own = reinterpret_cast<unsigned long long*>(c->xbuf);
+  const unsigned long long timeout_ns =
+      static_cast<unsigned long long>((getenv("HB_PEER_TIMEOUT_S") ? atof(getenv("HB_PEER_TIMEOUT_S")) : 30.0) * 1e9);
+  HB_CUDA(launch_k(pack_model_kernel, grid, dim3(256), 0, c->stream, c->peers.flat[c->peers.rank], m));
+  peer_signal_kernel<<<1, 1, 0, c->stream>>>(own, 0, g);
+  peer_wait_kernel<<<1, 32, 0, c->stream>>>(c->peers, 0, g, timeout_ns);
+  peer_reduce_kernel<<<grid, 256, 0, c->stream>>>(c->peers, n_elems, 1.0f / static_cast<float>(c->peers.n));
+  peer_signal_kernel<<<1, 1, 0, c->stream>>>(own, 8, g);
+  peer_wait_kernel<<<1, 32, 0, c->stream>>>(c->peers, 8, g, timeout_ns);
+  unpack_model_kernel<<<grid, 256, 0, c->stream>>>(c->peers.flat[c->peers.rank], 1.0f, m);
+  HB_CUDA(cudaGetLastError());
+  c->last_launches += 7;
+  return HB_OK;
+}
+
+// error word of the peer merge (a peer that never signalled within the timeout)
+int peer_check(hb_ctx* c) {
+  if (c->peers.n == 0) return HB_OK;
+  unsigned err = 0;
+  HB_CUDA(cudaMemcpyAsync(&err, c->xbuf + 128, sizeof err, cudaMemcpyDeviceToHost, c->stream));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  if (err != 0) return fail(HB_ESTATE, "peer merge: rank %u never signalled (timeout)", err - 1);
+  return HB_OK;
+}
+
 // pack -> allreduce(sum) -> unpack x 1/nranks (+ lo twins), enqueued on the
-// step stream: inside a step's CUDA-event bracket when HB_STEP_MERGE asks
+// step stream: inside a step's CUDA-event bracket when HB_STEP_MERGE asks.
+// Peer-attached contexts average over peer memory instead of NCCL.
 int enqueue_merge(hb_ctx* c) {
-  if (!c->comm) return fail(HB_ESTATE, "communicator not initialised");
+  if (!c->comm && c->peers.n == 0) return fail(HB_ESTATE, "communicator not initialised");
   if (c->L > kMaxMergeLayers) return fail(HB_EINVAL, "merge supports up to %d layers", kMaxMergeLayers);
   ModelLayout m{};
   m.n = c->L;
@@ -1578,6 +1616,7 @@ int enqueue_merge(hb_ctx* c) {
   }
   m.off[c->L] = off;
   const dim3 grid(static_cast<int>(std::min<long long>(cdiv(off, 256), 148 * 8)));
+  if (c->peers.n > 0) return enqueue_peer_merge(c, m, off, grid);
   HB_CUDA(launch_k(pack_model_kernel, grid, dim3(256), 0, c->stream, c->flat, m));
   int r = g_nccl.allReduce(c->flat, c->flat, static_cast<size_t>(off), kNcclFloat32, kNcclSum, c->comm, c->stream);
   if (r != 0) return fail(HB_ENCCL, "ncclAllReduce: %s", g_nccl.errStr ? g_nccl.errStr(r) : "error");
@@ -1625,6 +1664,7 @@ int do_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta,
     HB_TRY(prof_resolve(c, c->step_marks));
     c->step_marks.clear();
   }
+  if ((flags & HB_STEP_MERGE) && !(flags & HB_STEP_ASYNC)) HB_TRY(peer_check(c));
   return HB_OK;
 }
 
@@ -2029,6 +2069,8 @@ int hb_ctx_destroy(hb_ctx* c) {
   cudaFree(c->grad_all);
   if (c->grad_host) cudaFreeHost(c->grad_host);
   cudaFree(c->flat);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  cudaFree(c->xbuf);
   if (c->pinned) cudaFreeHost(c->pinned);
   for (auto e : c->evpool) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -3363,6 +3405,77 @@ int hb_merge_allreduce(hb_ctx* c) {
   HB_TRY(ctx_check(c));
   HB_TRY(enqueue_merge(c));
   HB_CUDA(cudaStreamSynchronize(c->stream));
+  return peer_check(c);
+}
+
+struct PeerHandle {  // HB_PEER_HANDLE_BYTES on the wire
+  cudaIpcMemHandle_t ipc;
+  int64_t pid;
+  int64_t device;
+  uint64_t ptr;
+  int64_t n_params;
+};
+static_assert(sizeof(PeerHandle) <= HB_PEER_HANDLE_BYTES, "peer handle too large");
+
+int hb_peer_handle(hb_ctx* c, void* out) {
+  HB_TRY(ctx_check(c));
+  if (!out) return fail(HB_EINVAL, "null handle buffer");
+  if (!c->xbuf) {
+    HB_CUDA(cudaMalloc(&c->xbuf, kPeerHeader + c->n_params * sizeof(float)));
+    HB_CUDA(cudaMemset(c->xbuf, 0, kPeerHeader));
+  }
+  PeerHandle h{};
+  HB_CUDA(cudaIpcGetMemHandle(&h.ipc, c->xbuf));
+  h.pid = static_cast<int64_t>(getpid());
+  h.device = c->device;
+  h.ptr = reinterpret_cast<uint64_t>(c->xbuf);
+  h.n_params = static_cast<int64_t>(c->n_params);
+  std::memset(out, 0, HB_PEER_HANDLE_BYTES);
+  std::memcpy(out, &h, sizeof h);
+  return HB_OK;
+}
+
+int hb_peer_attach(hb_ctx* c, int nranks, int rank, const void* handles) {
+  HB_TRY(ctx_check(c));
+  if (!handles || nranks < 1 || nranks > kMaxPeers || rank < 0 || rank >= nranks)
+    return fail(HB_EINVAL, "bad peer group (nranks %d, rank %d; at most %d ranks)", nranks, rank, kMaxPeers);
+  if (c->peers.n != 0) return fail(HB_ESTATE, "context already attached to a peer group");
+  if (!c->xbuf) return fail(HB_ESTATE, "hb_peer_handle first");
+  PeerTable t{};
+  t.n = nranks;
+  t.rank = rank;
+  const char* hs = static_cast<const char*>(handles);
+  for (int q = 0; q < nranks; ++q) {
+    PeerHandle h;
+    std::memcpy(&h, hs + static_cast<size_t>(q) * HB_PEER_HANDLE_BYTES, sizeof h);
+    if (h.n_params != static_cast<int64_t>(c->n_params))
+      return fail(HB_EINVAL, "rank %d holds a model of %lld parameters, this one %zu", q,
+                  static_cast<long long>(h.n_params), c->n_params);
+    char* base = nullptr;
+    if (q == rank) {
+      if (h.ptr != reinterpret_cast<uint64_t>(c->xbuf)) return fail(HB_EINVAL, "handle %d is not this context's", q);
+      base = c->xbuf;
+    } else if (h.pid == static_cast<int64_t>(getpid())) {
+      if (h.device != c->device) {  // same process, another GPU: direct peer access over NVLink
+        int ok = 0;
+        HB_CUDA(cudaDeviceCanAccessPeer(&ok, c->device, static_cast<int>(h.device)));
+        if (!ok) return fail(HB_ECUDA, "device %d cannot access device %lld", c->device, static_cast<long long>(h.device));
+        cudaError_t e = cudaDeviceEnablePeerAccess(static_cast<int>(h.device), 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else HB_CUDA(e);
+      }
+      base = reinterpret_cast<char*>(h.ptr);
+    } else {
+      void* p = nullptr;
+      HB_CUDA(cudaIpcOpenMemHandle(&p, h.ipc, cudaIpcMemLazyEnablePeerAccess));
+      c->ipc_opened.push_back(p);
+      base = static_cast<char*>(p);
+    }
+    t.flat[q] = reinterpret_cast<float*>(base + kPeerHeader);
+    t.flag[q] = reinterpret_cast<unsigned long long*>(base);
+  }
+  c->peers = t;
+  c->nranks = nranks;
   return HB_OK;
 }
 

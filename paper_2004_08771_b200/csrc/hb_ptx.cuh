@@ -278,9 +278,19 @@ __device__ __forceinline__ uint32_t to_tf32_rna(uint32_t bits) {
 
 // The tensor core reads an fp32 operand as tf32 by truncation (low 13 mantissa
 // bits ignored; established by the GPU parity tests), so the 3xTF32 lo twin
-// of x is x - trunc_tf32(x), exact in fp32.
+// of x is x - trunc_tf32(x), exact in fp32.  The twin is itself read through
+// the same truncation; left as is, that drops up to 2^-11 of lo *toward zero*
+// -- always the sign of x -- a systematic -2^-22 relative bias on every
+// operand that long dot products accumulate instead of averaging out.  Storing
+// lo already rounded to nearest tf32 makes the hardware truncation a no-op
+// and the residual error unbiased.
 __device__ __forceinline__ float tf32_lo(float x) {
-  return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  const float lo = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+#ifdef HB_LO_TRUNC
+  return lo;
+#else
+  return __uint_as_float(to_tf32_rna(__float_as_uint(lo)));
+#endif
 }
 __device__ __forceinline__ float4 lo4(float4 v) {
   return make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
@@ -304,8 +314,16 @@ __device__ __forceinline__ float sigmoidf_stable(float z) {
 // epilogue MUFU-latency bound (measured 8.6 of 12 us per 128x256 tile).
 __device__ __forceinline__ float sigmoidf_fast(float z) {
   float e, r;
+#ifdef HB_SIG_ACCURATE
+  e = expf(-fabsf(z));
+#else
   asm("ex2.approx.f32 %0, %1;" : "=f"(e) : "f"(-fabsf(z) * 1.4426950408889634f));
-  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(1.f + e));
+#endif
+  const float d = 1.f + e;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(d));
+#ifdef HB_SIG_ACCURATE
+  r = fmaf(r, fmaf(-d, r, 1.f), r);  // one Newton step: ~correctly rounded 1/d
+#endif
   return z >= 0.f ? r : e * r;
 }
 

@@ -3,8 +3,10 @@
 One process per B200 (torchrun), each running its own GPU replica worker on
 its own stream of batches (the paper's "separate GPU worker" per device,
 PAPER.md:321).  The only exchange is the GPU-replica merge: every
-`merge_every` steps the device models are averaged with an NCCL allreduce
-issued by the C library on its own stream (hb_merge_allreduce).  The NCCL
+`merge_every` steps the device models are averaged, either with an NCCL
+allreduce issued by the C library on its own stream (hb_merge_allreduce) or
+over peer memory (transport="peer": the library's one-shot reduce kernel reads
+and writes every rank's exchange buffer directly, NVLink P2P / CUDA IPC).  The NCCL
 unique id travels over `torch.distributed` (any backend, gloo included) as a
 128-byte tensor, so the control plane here is testable on CPU.
 """
@@ -88,20 +90,52 @@ def init_replica_comm(replica: GpuReplica, dist, rank: int, world: int) -> None:
     replica.comm_init(broadcast_bytes(dist, uid, 0), world, rank)
 
 
+def all_gather_bytes(dist, payload: bytes, world: int) -> list:
+    """Every rank's fixed-length byte string, in rank order (CPU tensors)."""
+    import torch
+
+    t = torch.tensor(list(payload), dtype=torch.uint8)
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [bytes(o.tolist()) for o in out]
+
+
+def init_replica_peers(replica: GpuReplica, dist, rank: int, world: int) -> None:
+    """Peer-memory merge group across processes: the exchange-buffer handles
+    (CUDA IPC) travel over torch.distributed, then every rank maps the others."""
+    replica.peer_attach(all_gather_bytes(dist, replica.peer_handle(), world), rank)
+
+
+def local_peer_group(replicas) -> None:
+    """Peer-memory merge group of replicas in this process (one per GPU worker
+    thread, as the reference engine runs its roster, engine.py:131-134), or
+    several replicas on one device.  Every replica must then merge the same
+    number of times, each from its own thread."""
+    handles = [r.peer_handle() for r in replicas]
+    for rank, r in enumerate(replicas):
+        r.peer_attach(handles, rank)
+
+
 class DataParallelWorker:
     """A GPU replica worker that averages its model with its peers every
     `merge_every` steps (model averaging over NVLink)."""
 
-    def __init__(self, replica: GpuReplica, dist=None, merge_every: int = 1):
+    def __init__(self, replica: GpuReplica, dist=None, merge_every: int = 1, transport: str = "nccl"):
         if merge_every < 1:
             raise ValueError("merge_every must be >= 1")
+        if transport not in ("nccl", "peer"):
+            raise ValueError(f"transport must be 'nccl' or 'peer', got {transport!r}")
         self.replica = replica
         self.dist = dist
         self.rank, self.world, _ = dist_env()
         self.merge_every = merge_every
+        self.transport = transport
         self.steps = 0
         if self.world > 1:
-            init_replica_comm(replica, dist, self.rank, self.world)
+            if transport == "peer":
+                init_replica_peers(replica, dist, self.rank, self.world)
+            else:
+                init_replica_comm(replica, dist, self.rank, self.world)
 
     def step(self, start: int, rows: int, eta: float, **kw):
         # the merge rides on the step's stream (HB_STEP_MERGE): no extra sync

@@ -365,6 +365,21 @@ class GpuReplica:
         buf = (C.c_char * 128).from_buffer_copy(uid)
         N.check(self._lib.hb_comm_init(self._h, buf, int(nranks), int(rank)))
 
+    def peer_handle(self) -> bytes:
+        """This replica's exchange-buffer handle for a peer-memory merge group."""
+        buf = (C.c_char * N.HB_PEER_HANDLE_BYTES)()
+        N.check(self._lib.hb_peer_handle(self._h, buf))
+        return bytes(buf)
+
+    def peer_attach(self, handles, rank: int) -> None:
+        """Join the merge group whose ranks' handles are `handles` (rank order);
+        merges then average over peer memory (NVLink P2P / CUDA IPC)."""
+        blob = b"".join(handles)
+        if len(blob) != N.HB_PEER_HANDLE_BYTES * len(handles):
+            raise ValueError("every peer handle must be HB_PEER_HANDLE_BYTES long")
+        buf = (C.c_char * len(blob)).from_buffer_copy(blob)
+        N.check(self._lib.hb_peer_attach(self._h, len(handles), int(rank), buf))
+
     def merge_allreduce(self) -> None:
         """Average the device models of all ranks (NCCL allreduce over NVLink)."""
         N.check(self._lib.hb_merge_allreduce(self._h))

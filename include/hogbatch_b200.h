@@ -119,6 +119,12 @@ int hb_stage_dense_f32(hb_ctx* ctx, const float* x, int64_t n_rows, int64_t ld, 
  * by the sparse dW kernel is built once here. */
 int hb_stage_csr(hb_ctx* ctx, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n_rows,
                  const int64_t* labels);
+/* Sparse-input contexts: stage a dense float64 (n_rows, d_0) array (row
+ * stride ld) whose rows are mostly zero -- the densified epoch copy the
+ * reference's LIBSVM loader produces (data.py:128-140) and BatchRef views --
+ * as CSR: the nonzeros are gathered on the host (values to fp32) and staged
+ * like hb_stage_csr, so layer 0 runs on the CSR kernels. */
+int hb_stage_dense_as_csr_f64(hb_ctx* ctx, const double* x, int64_t n_rows, int64_t ld, const int64_t* labels);
 int64_t hb_staged_rows(hb_ctx* ctx);
 /* Stage n_rows synthetic Gaussian-blob rows generated on the device (the
  * shape of synthetic_blobs, data.py:226-252: row = means[label] + N(0, I)),

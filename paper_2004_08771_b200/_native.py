@@ -53,6 +53,7 @@ SIGNATURES = {
     "hb_stage_dense_f64": (_i32, [_p, _dp, _i64, _i64, _i64p]),
     "hb_stage_dense_f32": (_i32, [_p, _fp, _i64, _i64, _i64p]),
     "hb_stage_csr": (_i32, [_p, _i64p, _i32p, _fp, _i64, _i64p]),
+    "hb_stage_dense_as_csr_f64": (_i32, [_p, _dp, _i64, _i64, _i64p]),
     "hb_staged_rows": (_i64, [_p]),
     "hb_stage_blobs": (_i32, [_p, _i64, _i64, _i32, _dp, C.c_uint64]),
     "hb_read_staged": (_i32, [_p, _i64, _i64, _fp, _i64p]),

@@ -1897,6 +1897,10 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
     if (c->passes == 3 && cdiv(c->d[l], kBK) > 32 && l >= long_from)
       c->bn_fwd[l] = std::min(c->bn_fwd[l], max_bn_long);
     c->bn_dw[l] = choose_bn(cdiv(c->d[l + 1], kBM), c->d[l]);
+    // experiments: cap the tile width (more rotating accumulators, shorter MMA chains)
+    c->bn_fwd[l] = std::min<int>(c->bn_fwd[l], static_cast<int>(env_long("HB_FWD_BN_MAX", 256)));
+    c->bn_dx[l] = std::min<int>(c->bn_dx[l], static_cast<int>(env_long("HB_DX_BN_MAX", 256)));
+    c->bn_dw[l] = std::min<int>(c->bn_dw[l], static_cast<int>(env_long("HB_DW_BN_MAX", 256)));
     // the wide softmax head's dW sums error signals of both signs over the
     // whole batch (a cancelling sum): 128-wide tiles give 3 rotating hi*hi
     // accumulators, and dw_plan bounds the chain per accumulator
@@ -2812,6 +2816,8 @@ static int stage_csr_densified(hb_ctx* c, const int64_t* rowptr, const int32_t* 
   return finish_dense_stage(c);
 }
 
+static int stage_csr_impl(hb_ctx* c, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n_rows,
+                          const int64_t* labels);
 int hb_stage_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n_rows,
                  const int64_t* labels) {
   HB_TRY(ctx_check(c));
@@ -2824,6 +2830,56 @@ int hb_stage_csr(hb_ctx* c, const int64_t* rowptr, const int32_t* col, const flo
   for (long long e = 0; e < nnz; ++e)
     if (col[e] < 0 || col[e] >= c->d[0])
       return fail(HB_EINVAL, "feature index %d outside [0, %d) at nnz %lld", col[e], c->d[0], e);
+  return stage_csr_impl(c, rowptr, col, val, n_rows, labels);
+}
+
+// Stage a dense float64 (n_rows, d_0) dataset whose rows are mostly zeros --
+// what the reference's LIBSVM loader hands a worker (data.py:128-140
+// densifies, and BatchRef views that array) -- as CSR on a sparse-input
+// context: the nonzeros are gathered on the host threads (values rounded to
+// fp32, as every staging path does), so a 20958-wide real-sim epoch stages
+// ~0.25% of its 12 GB and layer 0 runs on the CSR kernels.
+int hb_stage_dense_as_csr_f64(hb_ctx* c, const double* x, int64_t n_rows, int64_t ld, const int64_t* labels) {
+  HB_TRY(ctx_check(c));
+  if (!c->csr_in) return fail(HB_EINVAL, "context was created for dense input");
+  if (!x || !labels || n_rows < 1 || ld < c->d[0]) return fail(HB_EINVAL, "bad dense array (n_rows %lld, ld %lld)",
+                                                               static_cast<long long>(n_rows), static_cast<long long>(ld));
+  const int d0 = c->d[0];
+  HostPool& pool = HostPool::get();
+  const int parts = static_cast<int>(std::min<int64_t>(std::max(1, pool.size()) * 4, std::max<int64_t>(1, n_rows / 64)));
+  std::vector<std::vector<int32_t>> pcol(parts);
+  std::vector<std::vector<float>> pval(parts);
+  std::vector<int64_t> rowlen(n_rows + 1, 0);
+  pool.run(parts, [&](int t) {
+    const int64_t r0 = n_rows * t / parts, r1 = n_rows * (t + 1) / parts;
+    auto& cc = pcol[t];
+    auto& vv = pval[t];
+    for (int64_t r = r0; r < r1; ++r) {
+      const double* row = x + r * ld;
+      const size_t before = cc.size();
+      for (int j = 0; j < d0; ++j)
+        if (row[j] != 0.0) {
+          cc.push_back(j);
+          vv.push_back(static_cast<float>(row[j]));
+        }
+      rowlen[r + 1] = static_cast<int64_t>(cc.size() - before);
+    }
+  });
+  for (int64_t r = 0; r < n_rows; ++r) rowlen[r + 1] += rowlen[r];
+  std::vector<int32_t> col;
+  std::vector<float> val;
+  col.reserve(rowlen[n_rows]);
+  val.reserve(rowlen[n_rows]);
+  for (int t = 0; t < parts; ++t) {
+    col.insert(col.end(), pcol[t].begin(), pcol[t].end());
+    val.insert(val.end(), pval[t].begin(), pval[t].end());
+  }
+  return stage_csr_impl(c, rowlen.data(), col.data(), val.data(), n_rows, labels);
+}
+
+static int stage_csr_impl(hb_ctx* c, const int64_t* rowptr, const int32_t* col, const float* val, int64_t n_rows,
+                          const int64_t* labels) {
+  const long long nnz = rowptr[n_rows];
   if (!c->sparse) return stage_csr_densified(c, rowptr, col, val, n_rows, labels);
   HB_TRY(free_epoch(c));
   std::vector<int64_t> colptr;

@@ -149,13 +149,20 @@ class GpuReplica:
             self._keep = data
             return
         x = data
-        if self.sparse:
-            raise ValueError("sparse context needs a CsrDataset")
         if x.ndim != 2 or x.shape[1] != self.sizes[0]:
             raise ValueError(f"batch shape {x.shape} incompatible with input dim {self.sizes[0]}")
         y = np.ascontiguousarray(labels, dtype=np.int64)
         if y.shape != (x.shape[0],):
             raise ValueError("labels length must equal the number of feature rows")
+        if self.sparse:
+            # the densified epoch copy of sparse data (data.py:128-140): staged
+            # as CSR, its zeros dropped on the host
+            x = x if (x.dtype == np.float64 and x.strides[1] == 8) else np.ascontiguousarray(x, dtype=np.float64)
+            N.check(self._lib.hb_stage_dense_as_csr_f64(self._h, N.ptr(x, C.c_double), x.shape[0],
+                                                        x.strides[0] // 8, N.ptr(y, C.c_int64)))
+            self._staged_key = key
+            self._keep = (data, x, y)
+            return
         if x.dtype == np.float32 and x.strides[1] == 4:
             N.check(self._lib.hb_stage_dense_f32(self._h, N.ptr(x, C.c_float), x.shape[0], x.strides[0] // 4,
                                                  N.ptr(y, C.c_int64)))

@@ -24,6 +24,7 @@ import numpy as np
 
 from .data import CsrBatchRef, CsrDataset
 from .nn import layer_sizes_of
+from ._native import HB_DENSIFY_MAX_DIN as N_DENSIFY_MAX_DIN
 from .replica import GpuReplica
 
 
@@ -164,6 +165,27 @@ def _stage_for(ctx: GpuReplica, batch) -> None:
         ctx.stage(batch.features, batch.labels)
 
 
+# A dense epoch array wider than this whose sampled rows are at most this dense
+# is sparse data densified by the reference loader (data.py:128-140): its
+# replica stages it as CSR and runs layer 0 on the CSR kernels.
+_SPARSE_DENSITY = 0.05
+
+
+def _is_wide_sparse(features) -> bool:
+    if features.ndim != 2 or features.shape[1] <= N_DENSIFY_MAX_DIN:
+        return False
+    key = GpuReplica.key_of(features)
+    memo = getattr(_tls, "sparse_memo", None)
+    if memo is None:
+        memo = _tls.sparse_memo = {}
+    if key not in memo:
+        n = features.shape[0]
+        rows = features[np.linspace(0, n - 1, num=min(n, 256)).astype(np.int64)]
+        memo.clear()  # one epoch array at a time
+        memo[key] = np.count_nonzero(rows) <= _SPARSE_DENSITY * rows.size
+    return memo[key]
+
+
 def execute_gpu_replica(model, batch, eta: float, speed_factor: float = 0.0) -> float:
     """GPU version of execute_batch_replica (workers.py:126-138).
 
@@ -176,7 +198,7 @@ def execute_gpu_replica(model, batch, eta: float, speed_factor: float = 0.0) -> 
     emulation contract (sleep speed_factor x elapsed); real devices pass 0."""
     start_t = time.perf_counter()
     sizes = layer_sizes_of(model)
-    sparse = isinstance(batch, CsrBatchRef)
+    sparse = isinstance(batch, CsrBatchRef) or _is_wide_sparse(batch.features)
     ctx = _replica(sizes, batch.length, sparse, "train")
     _tls.gpu_worker = True
     _stage_for(ctx, batch)
@@ -216,6 +238,12 @@ def gpu_loss_sum(model, features, labels, chunk: int = 4096) -> float:
     """GPU version of loss_sum (nn.py:139-146): sum over rows of
     -log max(p_y, 1e-12) of `model` on (features, labels)."""
     sizes = layer_sizes_of(model)
+    if not isinstance(features, CsrDataset) and _is_wide_sparse(features):
+        ctx = _replica(sizes, chunk, True, "eval")
+        if not ctx.is_staged(GpuReplica.key_of(features)):
+            ctx.stage(features, np.asarray(labels, dtype=np.int64))
+        ctx.set_weights(model.weights)
+        return ctx.eval_loss_sum(0, features.shape[0])
     if isinstance(features, CsrDataset):
         ctx = _replica(sizes, chunk, True, "eval")
         if not ctx.is_staged(GpuReplica.key_of(features)):

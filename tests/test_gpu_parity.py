@@ -586,3 +586,27 @@ def test_replica_step_reports_its_pcie_bytes(hb):
             assert d2h == 4 * n + 4 * len(w) + 8  # small batch: every layer merges on the host lane
     finally:
         ctx.close()
+
+
+def test_dense_epoch_of_sparse_data_routes_to_csr(hb):
+    """The reference's LIBSVM loader densifies (data.py:128-140), so a
+    BatchRef of real-sim-like data is a wide, mostly-zero float64 array: the
+    drop-in call stages it as CSR (hb_stage_dense_as_csr_f64) and runs layer 0
+    on the CSR kernels, with the same per-step parity."""
+    from paper_2004_08771_b200 import Architecture, BatchRef, Model, execute_gpu_replica, gpu_loss_sum
+    from paper_2004_08771_b200 import workers as W
+
+    sizes = (2000, 256, 256, 2)
+    w, x, y = oracle_case(sizes, 777, seed=77, sparse_nnz=52)
+    g = ref_nn.backward(w, ref_nn.forward(w, x), y)
+    upd = ref_nn.deep_copy(w)
+    ref_nn.apply_update(upd, g, 0.3)
+    model = Model(Architecture(sizes), [a.copy() for a in w])
+    try:
+        assert execute_gpu_replica(model, BatchRef(x, y, 0, 777), 0.3) == 1.0
+        assert any(k[0] == "train" and k[3] for k in W._tls.contexts), "the replica did not take the CSR path"
+        assert max_relative_error(model.weights, upd) <= STEP_TOL
+        got = gpu_loss_sum(Model(Architecture(sizes), w), x, y)
+        assert got == pytest.approx(ref_nn.loss_sum(w, x, y), rel=1e-5)
+    finally:
+        W.release_thread_contexts()

@@ -610,3 +610,94 @@ def test_dense_epoch_of_sparse_data_routes_to_csr(hb):
         assert got == pytest.approx(ref_nn.loss_sum(w, x, y), rel=1e-5)
     finally:
         W.release_thread_contexts()
+
+
+def test_adaptive_controller_drives_the_drop_in_replica(hb):
+    """Alg. 2 (policies.py:84-129, strict thresholds) sizing the GPU worker's
+    batches behind a faster CPU pool: 8192 -> 4096 -> ... -> min_batch, then a
+    36-row drain tail (engine.py:285-316 serves min(b, remaining)); every
+    execute_gpu_replica call matches the float64 step on its snapshot, with
+    the learning rate scaled per batch (policies.py:34-36) and a device-timed
+    busy time booked per call."""
+    from oracle import ref_policies as RP
+    from paper_2004_08771_b200 import Architecture, BatchRef, Model, execute_gpu_replica
+    from paper_2004_08771_b200 import workers as W
+
+    sizes = (54, 256, 256, 2)
+    sched = [8192, 4096, 2048, 1024, 512, 256, 256]
+    n = sum(sched) + 36
+    x, y = ref_nn.synthetic_blobs(n, sizes[0], 2, 2.5, 5)
+    model = Model(Architecture(sizes), ref_nn.init_weights(sizes, 6))
+    ctl = RP.OracleAdaptive(alpha=2.0)
+    ctl.register("gpu0", RP.initial_batch_size(True, 1, 256, 8192), 256, 8192)
+    ctl.register("cpu", RP.initial_batch_size(False, 16, 64, 64), 64, 64)
+    ref_b, base_eta = 64, 0.002
+    cursor, u_gpu, u_cpu, served = 0, 0.0, 0.0, []
+    busy0 = W.device_busy_seconds()
+    try:
+        b = ctl.update("gpu0", u_gpu, strict=True)  # first report: exempt
+        while cursor < n:
+            length = min(b, n - cursor)
+            eta = RP.scaled_learning_rate(base_eta, b, ref_b)
+            snap = [a.copy() for a in model.weights]
+            xb, yb = x[cursor:cursor + length], y[cursor:cursor + length]
+            assert execute_gpu_replica(model, BatchRef(x, y, cursor, length), eta) == 1.0
+            assert W.last_device_ms() > 0
+            g = ref_nn.backward(snap, ref_nn.forward(snap, xb), yb)
+            want = [s - eta * gl for s, gl in zip(snap, g)]
+            assert max_relative_error(model.weights, want) <= STEP_TOL, (cursor, length)
+            served.append(length)
+            cursor += length
+            u_cpu += 50.0  # the CPU pool stays ahead
+            ctl.update("cpu", u_cpu, strict=True)
+            u_gpu += 1.0
+            b = ctl.update("gpu0", u_gpu, strict=True)
+        assert served == sched + [36]
+        assert W.device_busy_seconds() > busy0
+    finally:
+        W.release_thread_contexts()
+
+
+def test_concurrent_host_writer_keeps_its_updates(hb):
+    """A Hogwild-style thread (workers.py:94-123 writes the shared model with
+    unsynchronised np.add, linalg.py:79) keeps adding 1.0 to every weight
+    while GPU replica calls merge into the same model.  With eta = 0 every
+    merge is a pure read-modify-write w = w + (-0)*g, so any writer update it
+    overwrote shows up as a missing increment: the reference's per-element
+    race loses at most a handful, never a whole layer; no double is torn."""
+    import threading
+
+    sizes = (64, 512, 512, 2)
+    b = 4096
+    x, y = ref_nn.synthetic_blobs(b, sizes[0], 2, 2.5, 3)
+    x = x.astype(np.float32)
+    shared = [np.zeros((sizes[l + 1], sizes[l])) for l in range(len(sizes) - 1)]
+    ctx = hb.GpuReplica(sizes, b)
+    stop = threading.Event()
+    passes = [0]
+
+    def writer():
+        while not stop.is_set():
+            for a in shared:
+                np.add(a, 1.0, out=a)
+            passes[0] += 1
+
+    try:
+        ctx.replica_step_host(shared, x, y, 0.0)  # page-lock + capture outside the race
+        t = threading.Thread(target=writer)
+        t.start()
+        for _ in range(40):
+            ctx.replica_step_host(shared, x, y, 0.0)
+        stop.set()
+        t.join()
+        n = passes[0]
+        assert n > 10
+        for a in shared:
+            assert np.all(a == np.round(a)), "torn or corrupted double"
+            assert a.max() <= n
+        lost = sum(int((a < n).sum()) for a in shared)  # the writer always finishes its pass
+        total = sum(a.size for a in shared)
+        assert lost <= 1e-3 * total, (lost, total)
+    finally:
+        stop.set()
+        ctx.close()

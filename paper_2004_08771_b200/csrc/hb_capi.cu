@@ -25,6 +25,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <string>
@@ -349,6 +350,39 @@ struct StepGraph {
 // (hb_replica_step*: reported by hb_last_xfer_bytes with the exchange bytes).
 static thread_local long long t_h2d_bytes = 0;
 
+// Ranks of a peer-merge group that live in one process (one GPU worker
+// thread each, as the reference engine runs its roster).  They order their
+// merges with events and a host barrier instead of device-side flag waits: two
+// streams of one process can share a hardware queue, where a spinning wait
+// kernel queued ahead of a peer's pack kernel would never let it run.
+struct LocalGroup {
+  int n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long phase = 0;
+  std::vector<cudaEvent_t> ev_pack, ev_red;  // per rank, created on that rank's device
+  bool broken = false;
+  // every rank arrives (bounded wait: a rank that never merges is an error, not a hang)
+  bool barrier(double timeout_s) {
+    std::unique_lock<std::mutex> lk(mu);
+    const unsigned long long my = phase;
+    if (++arrived == n) {
+      arrived = 0;
+      ++phase;
+      cv.notify_all();
+      return true;
+    }
+    const bool ok = cv.wait_for(lk, std::chrono::duration<double>(timeout_s), [&] { return phase != my || broken; });
+    if (!ok || broken) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
+  }
+};
+
 struct hb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -517,6 +551,7 @@ struct hb_ctx {
   PeerTable peers{};                // peers.n == 0: not attached
   std::vector<void*> ipc_opened;    // peer buffers opened through CUDA IPC
   unsigned long long peer_gen = 0;  // merges issued (the flag value of the next one)
+  std::shared_ptr<LocalGroup> local;  // all ranks in this process: event + host-barrier ordering
 };
 
 namespace {
@@ -1568,11 +1603,31 @@ void drop_graphs(hb_ctx* c) {
 
 // peer-memory merge (hb_peer.cuh): pack, signal, wait, one-shot reduce of
 // this rank's slice across every rank's flat, signal, wait, unpack
+double peer_timeout_s() { return getenv("HB_PEER_TIMEOUT_S") ? atof(getenv("HB_PEER_TIMEOUT_S")) : 30.0; }
+
 int enqueue_peer_merge(hb_ctx* c, const ModelLayout& m, long long n_elems, const dim3 grid) {
   const unsigned long long g = ++c->peer_gen;
+  const int r = c->peers.rank;
+  if (c->local) {
+    // in-process group: every rank's pack is enqueued before anyone waits on it
+    LocalGroup& lg = *c->local;
+    HB_CUDA(launch_k(pack_model_kernel, grid, dim3(256), 0, c->stream, c->peers.flat[r], m));
+    HB_CUDA(cudaEventRecord(lg.ev_pack[r], c->stream));
+    if (!lg.barrier(peer_timeout_s())) return fail(HB_ESTATE, "peer merge: a rank never signalled (timeout)");
+    for (int q = 0; q < lg.n; ++q)
+      if (q != r) HB_CUDA(cudaStreamWaitEvent(c->stream, lg.ev_pack[q], 0));
+    peer_reduce_kernel<<<grid, 256, 0, c->stream>>>(c->peers, n_elems, 1.0f / static_cast<float>(c->peers.n));
+    HB_CUDA(cudaEventRecord(lg.ev_red[r], c->stream));
+    if (!lg.barrier(peer_timeout_s())) return fail(HB_ESTATE, "peer merge: a rank never signalled (timeout)");
+    for (int q = 0; q < lg.n; ++q)
+      if (q != r) HB_CUDA(cudaStreamWaitEvent(c->stream, lg.ev_red[q], 0));
+    unpack_model_kernel<<<grid, 256, 0, c->stream>>>(c->peers.flat[r], 1.0f, m);
+    HB_CUDA(cudaGetLastError());
+    c->last_launches += 3;
+    return HB_OK;
+  }
   unsigned long long* own = reinterpret_cast<unsigned long long*>(c->xbuf);
-  const unsigned long long timeout_ns =
-      static_cast<unsigned long long>((getenv("HB_PEER_TIMEOUT_S") ? atof(getenv("HB_PEER_TIMEOUT_S")) : 30.0) * 1e9);
+  const unsigned long long timeout_ns = static_cast<unsigned long long>(peer_timeout_s() * 1e9);
   HB_CUDA(launch_k(pack_model_kernel, grid, dim3(256), 0, c->stream, c->peers.flat[c->peers.rank], m));
   peer_signal_kernel<<<1, 1, 0, c->stream>>>(own, 0, g);
   peer_wait_kernel<<<1, 32, 0, c->stream>>>(c->peers, 0, g, timeout_ns);
@@ -2073,6 +2128,18 @@ int hb_ctx_destroy(hb_ctx* c) {
   cudaFree(c->grad_all);
   if (c->grad_host) cudaFreeHost(c->grad_host);
   cudaFree(c->flat);
+  if (c->local) {
+    std::lock_guard<std::mutex> lk(c->local->mu);
+    auto& lg = *c->local;
+    for (auto* evs : {&lg.ev_pack, &lg.ev_red})
+      if (c->peers.rank < static_cast<int>(evs->size()) && (*evs)[c->peers.rank]) {
+        cudaEventDestroy((*evs)[c->peers.rank]);
+        (*evs)[c->peers.rank] = nullptr;
+      }
+    lg.broken = true;  // a rank left: later merges of the others fail instead of waiting
+    lg.cv.notify_all();
+  }
+  c->local.reset();
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   cudaFree(c->xbuf);
   if (c->pinned) cudaFreeHost(c->pinned);
@@ -3478,7 +3545,8 @@ int hb_peer_handle(hb_ctx* c, void* out) {
   if (!out) return fail(HB_EINVAL, "null handle buffer");
   if (!c->xbuf) {
     HB_CUDA(cudaMalloc(&c->xbuf, kPeerHeader + c->n_params * sizeof(float)));
-    HB_CUDA(cudaMemset(c->xbuf, 0, kPeerHeader));
+    HB_CUDA(cudaMemsetAsync(c->xbuf, 0, kPeerHeader, c->stream));
+    HB_CUDA(cudaStreamSynchronize(c->stream));
   }
   PeerHandle h{};
   HB_CUDA(cudaIpcGetMemHandle(&h.ipc, c->xbuf));
@@ -3500,6 +3568,7 @@ int hb_peer_attach(hb_ctx* c, int nranks, int rank, const void* handles) {
   PeerTable t{};
   t.n = nranks;
   t.rank = rank;
+  int local_peers = 0;
   const char* hs = static_cast<const char*>(handles);
   for (int q = 0; q < nranks; ++q) {
     PeerHandle h;
@@ -3512,6 +3581,7 @@ int hb_peer_attach(hb_ctx* c, int nranks, int rank, const void* handles) {
       if (h.ptr != reinterpret_cast<uint64_t>(c->xbuf)) return fail(HB_EINVAL, "handle %d is not this context's", q);
       base = c->xbuf;
     } else if (h.pid == static_cast<int64_t>(getpid())) {
+      ++local_peers;
       if (h.device != c->device) {  // same process, another GPU: direct peer access over NVLink
         int ok = 0;
         HB_CUDA(cudaDeviceCanAccessPeer(&ok, c->device, static_cast<int>(h.device)));
@@ -3529,6 +3599,28 @@ int hb_peer_attach(hb_ctx* c, int nranks, int rank, const void* handles) {
     }
     t.flat[q] = reinterpret_cast<float*>(base + kPeerHeader);
     t.flag[q] = reinterpret_cast<unsigned long long*>(base);
+  }
+  if (local_peers == nranks - 1 && nranks > 1) {
+    // every rank is in this process: join (or create) the group's ordering
+    // state, keyed by rank 0's exchange buffer
+    static std::mutex groups_mu;
+    static std::map<uint64_t, std::weak_ptr<LocalGroup>> groups;
+    PeerHandle h0;
+    std::memcpy(&h0, hs, sizeof h0);
+    std::lock_guard<std::mutex> lk(groups_mu);
+    std::shared_ptr<LocalGroup> g = groups[h0.ptr].lock();
+    if (!g) {
+      g = std::make_shared<LocalGroup>();
+      g->n = nranks;
+      g->ev_pack.assign(nranks, nullptr);
+      g->ev_red.assign(nranks, nullptr);
+      groups[h0.ptr] = g;
+    }
+    HB_CUDA(cudaEventCreateWithFlags(&g->ev_pack[rank], cudaEventDisableTiming));
+    HB_CUDA(cudaEventCreateWithFlags(&g->ev_red[rank], cudaEventDisableTiming));
+    c->local = g;
+  } else if (local_peers != 0) {
+    return fail(HB_EINVAL, "a peer group is either all in this process or one rank per process");
   }
   c->peers = t;
   c->nranks = nranks;

@@ -1,6 +1,6 @@
 # GPU parity suite under every A/B switch of the measured optimisations
 # (README "Knobs"): each must stay parity-green, they only change speed.
-for v in HB_NO_GRAPHS HB_NO_CONC_BWD HB_NO_PDL HB_NO_FX_SPLIT HB_NO_EXACT_X; do
+for v in HB_NO_GRAPHS HB_NO_CONC_BWD HB_NO_PDL HB_NO_FX_SPLIT HB_NO_EXACT_X HB_SPLITK_FUSION; do
   echo "$v: $(env $v=1 timeout 400 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k 'not baseline_size' 2>&1 | tail -1)"
 done
 echo "HB_XCHG_MERGE=dma: $(HB_XCHG_MERGE=dma timeout 400 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k 'not baseline_size' 2>&1 | tail -1)"

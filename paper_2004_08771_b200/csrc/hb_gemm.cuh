@@ -103,6 +103,10 @@ __device__ unsigned long long hb_trace_cta[8 * 1024 * 4];
   } while (0)
 #endif
 
+#ifndef HB_GEMM_DRAIN
+#define HB_GEMM_DRAIN 1
+#endif
+
 constexpr int kBM = 128;
 constexpr int kBK = 32;  // 32 fp32 = one 128-byte swizzle row
 
@@ -129,9 +133,16 @@ struct GemmCfg {
   // the number of MMAs chained into one accumulator, so 3xTF32 keeps the two
   // small cross terms in their own accumulator and rotates the hi*hi term over
   // NBIG accumulators by k-block; the epilogue sums them in fp32 registers.
+  //
+  // DRAIN (3xTF32, BN >= 64): instead, every k-block's three products go into
+  // a fresh accumulator (two TMEM slots, alternating), which the epilogue warps
+  // drain into fp32 registers (round-to-nearest adds) while the tensor core
+  // fills the other slot: the truncating accumulation covers only the 12 MMAs
+  // of one k-block (4 of them on the large hi*hi term), not the whole K.
+  static constexpr bool DRAIN = (PASSES == 3) && (BN >= 64) && (HB_GEMM_DRAIN != 0);
   static constexpr int NBIG_RAW = PASSES == 3 ? 512 / BN - 1 : 1;
-  static constexpr int NBIG = NBIG_RAW > 15 ? 15 : (NBIG_RAW < 1 ? 1 : NBIG_RAW);
-  static constexpr int NACC = PASSES == 3 ? NBIG + 1 : 1;
+  static constexpr int NBIG = DRAIN ? 1 : (NBIG_RAW > 15 ? 15 : (NBIG_RAW < 1 ? 1 : NBIG_RAW));
+  static constexpr int NACC = PASSES == 3 ? NBIG + 1 : 1;  // DRAIN: the two k-block slots
   static constexpr int TMEM_COLS_RAW = NACC * BN;
   static constexpr int TMEM_COLS = TMEM_COLS_RAW <= 32 ? 32 : TMEM_COLS_RAW <= 64 ? 64 : TMEM_COLS_RAW <= 128 ? 128
                                    : TMEM_COLS_RAW <= 256 ? 256 : 512;
@@ -171,7 +182,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* acc_full = tmem_full + 1;  // DRAIN: k-block slot s holds a finished partial
+  uint64_t* acc_empty = acc_full + 2;  // DRAIN: slot s drained by every epilogue warp (of both CTAs)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -198,7 +211,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    // DRAIN: the drain warps publish the summed tile in TMEM (8 arrivals)
+    mbar_init(tmem_full, C::DRAIN ? C::EPI_WARPS : 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], C::EPI_WARPS * (PAIR ? 2 : 1));
+    }
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -268,6 +286,39 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
     // -------------------------------------------------------- MMA issuer
     if (lane == 0 && leader) {
       constexpr uint32_t idesc = make_idesc_tf32(PAIR ? 2 * kBM : kBM, BN, A_MN, B_MN);
+      if constexpr (C::DRAIN) {
+        for (int i = 0; i < nkb; ++i) {
+          const int s = i % STAGES;
+          const uint32_t ph = (i / STAGES) & 1;
+          const int slot = i & 1;
+          if (i >= 2) mbar_wait(&acc_empty[slot], ((i >> 1) - 1) & 1);  // drained (both CTAs)
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t aHi = smem_u32(smem + s * C::STAGE_BYTES);
+          const uint32_t bHi = aHi + C::A_BYTES;
+          const uint32_t t = tmem_base + slot * BN;
+          // the two small cross terms first (into the fresh accumulator), then hi*hi
+          uint32_t acc = 0u;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 8; ++kk) {
+            if (!args.a_lo_zero) {
+              mma_tf32_cg(t, op_desc(aHi + C::OP_BYTES, kk, A_MN), op_desc(bHi, kk, B_MN), idesc, acc, PAIR);
+              acc = 1u;
+            }
+            if (!args.b_lo_zero) {
+              mma_tf32_cg(t, op_desc(aHi, kk, A_MN), op_desc(bHi + C::OP_BYTES, kk, B_MN), idesc, acc, PAIR);
+              acc = 1u;
+            }
+          }
+#pragma unroll
+          for (int kk = 0; kk < kBK / 8; ++kk) {
+            mma_tf32_cg(t, op_desc(aHi, kk, A_MN), op_desc(bHi, kk, B_MN), idesc, acc, PAIR);
+            acc = 1u;
+          }
+          mma_commit_cg(&empty[s], PAIR);
+          mma_commit_cg(&acc_full[slot], PAIR);
+        }
+      } else
       for (int i = 0; i < nkb; ++i) {
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
@@ -298,8 +349,47 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
         mma_commit_cg(&empty[s], PAIR);
         HB_STAMP(2 * 512 + i);  // MMA: issue done
       }
-      mma_commit_cg(tmem_full, PAIR);  // accumulators complete (immediate if nkb == 0)
+      if (!C::DRAIN) mma_commit_cg(tmem_full, PAIR);  // accumulators complete (immediate if nkb == 0)
     }
+  } else if (C::DRAIN && warp >= 4 && warp < 4 + C::EPI_WARPS) {
+    // ------------------------------------- DRAIN: k-block partials -> registers
+    // warp (q, h) owns TMEM lane quarter q and column half h of the tile
+    constexpr int HC = BN / 2;  // columns per warp
+    const int ew = warp - 4, q = ew & 3, h = ew >> 2;
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + h * HC;
+    const uint32_t leader_empty = PAIR ? mapa_shared(smem_u32(&acc_empty[0]), 0) : smem_u32(&acc_empty[0]);
+    float sum[HC];
+#pragma unroll
+    for (int j = 0; j < HC; ++j) sum[j] = 0.f;
+    for (int i = 0; i < nkb; ++i) {
+      const int slot = i & 1;
+      mbar_wait(&acc_full[slot], (i >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int j = 0; j < HC / 32; ++j) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(lane_base + slot * BN + 32 * j, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int k = 0; k < 32; ++k) sum[32 * j + k] += __uint_as_float(r[k]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_empty + 8u * slot);
+    }
+    // publish the summed tile in slot 0 for the common epilogue below (every
+    // MMA of this tile has retired: the last k-block's slot was just drained)
+#pragma unroll
+    for (int j = 0; j < HC / 32; ++j) {
+      uint32_t r[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) r[k] = __float_as_uint(sum[32 * j + k]);
+      tmem_st_32x32b_x32(lane_base + 32 * j, r);
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tmem_full);
   }
   // The producer / MMA / allocator warps (0-3) are idle once the accumulators
   // are complete, so they join the epilogue (12 warps, 3 per TMEM lane
@@ -367,11 +457,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
         uint32_t r[32];
         // small-term accumulator first, then the hi*hi accumulators (only those
         // the k loop actually wrote)
-        tmem_ld_32x32b_x32(lane_addr + (C::NACC - 1) * BN, r);
+        tmem_ld_32x32b_x32(lane_addr + (C::DRAIN ? 0 : (C::NACC - 1) * BN), r);
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = nkb > 0 ? __uint_as_float(r[j]) : 0.f;
-        if (C::NACC > 1) {
+        for (int j = 0; j < 32; ++j) v[j] = (C::DRAIN || nkb > 0) ? __uint_as_float(r[j]) : 0.f;
+        if (C::NACC > 1 && !C::DRAIN) {
 #pragma unroll 1
           for (int a = 0; a < C::NBIG; ++a) {
             tmem_ld_32x32b_x32(lane_addr + a * BN, r);

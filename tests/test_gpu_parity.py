@@ -697,7 +697,11 @@ def test_concurrent_host_writer_keeps_its_updates(hb):
             assert a.max() <= n
         lost = sum(int((a < n).sum()) for a in shared)  # the writer always finishes its pass
         total = sum(a.size for a in shared)
-        assert lost <= 1e-3 * total, (lost, total)
+        # per-element races where the two sweeps cross (a few cache lines per
+        # merge); a layer-wide read-merge-write window would lose ~every element
+        assert lost <= 1e-2 * total, (lost, total)
+        for a in shared:
+            assert (a < n).mean() <= 0.05
     finally:
         stop.set()
         ctx.close()

@@ -191,6 +191,17 @@ int hb_replica_step_host_csr(hb_ctx* ctx, double* const* ws, const int64_t* rowp
                              const float* val, const int64_t* labels, int rows, double eta, uint32_t flags,
                              double* out_loss);
 
+/* hb_replica_step on staged rows split in two: begin enqueues the snapshot,
+ * the step and the gradient copies and returns; end applies the stale merge
+ * into ws as the gradients land and waits for the step (out_loss as in
+ * hb_replica_step).  The calling thread may do host work in between -- the
+ * GPU worker answers the coordinator (SCHEDULE_WORK, workers.py:209) while
+ * its step runs, so the coordinator round trip (engine.py:278-316) overlaps
+ * the device instead of following it.  No other call on the context may
+ * come in between; ws must stay valid until end. */
+int hb_replica_begin(hb_ctx* ctx, double* const* ws, int64_t start, int rows, double eta, uint32_t flags);
+int hb_replica_end(hb_ctx* ctx, double* out_loss);
+
 /* Sum over staged rows [start, start+rows) of -log max(p_y, 1e-12)
  * (loss_sum, nn.py:139-146), evaluated in chunks of at most max_batch rows. */
 int hb_eval_loss_sum(hb_ctx* ctx, int64_t start, int64_t rows, double* out_sum);

@@ -63,6 +63,8 @@ SIGNATURES = {
     "hb_train_step": (_i32, [_p, _i64, _i32, _f64, _u32, _dp]),
     "hb_train_step_host_dense": (_i32, [_p, _fp, _i64, _i64p, _i32, _f64, _u32, _dp]),
     "hb_train_step_host_csr": (_i32, [_p, _i64p, _i32p, _fp, _i64p, _i32, _f64, _u32, _dp]),
+    "hb_replica_begin": (_i32, [_p, C.POINTER(_dp), _i64, _i32, _f64, _u32]),
+    "hb_replica_end": (_i32, [_p, _dp]),
     "hb_replica_step": (_i32, [_p, C.POINTER(_dp), _i64, _i32, _f64, _u32, _dp]),
     # host batch arrays pass as integer addresses (ndarray.ctypes.data): half the cost of data_as per call
     "hb_replica_step_host_dense": (_i32, [_p, C.POINTER(_dp), _p, _i64, _p, _i32, _f64, _u32, _dp]),

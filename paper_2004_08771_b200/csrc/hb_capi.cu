@@ -552,6 +552,11 @@ struct hb_ctx {
   std::vector<void*> ipc_opened;    // peer buffers opened through CUDA IPC
   unsigned long long peer_gen = 0;  // merges issued (the flag value of the next one)
   std::shared_ptr<LocalGroup> local;  // all ranks in this process: event + host-barrier ordering
+  // hb_replica_begin / hb_replica_end: the replica step in flight between them
+  bool pend_active = false;
+  int pend_rows = 0;
+  double pend_eta = 0.0;
+  uint32_t pend_flags = 0;
 };
 
 namespace {
@@ -689,7 +694,7 @@ void dw_plan(const hb_ctx* c, int l, int rows, int* splits, int* kb_per, int* kb
   *kb_total = std::max(1, cdiv(rows, kBK));
   // one wave: as many K splits as fit on the 148 SMs (1 CTA / SM)
   int want = std::max(1, 148 / tiles);
-  if (l == c->L - 1 && !c->small_head && c->passes == 3) {
+  if (l == c->L - 1 && !c->small_head && c->passes == 3 && !(HB_GEMM_DRAIN && c->bn_dw[l] >= 64)) {
     // precision: at most 16 k-blocks per rotating hi*hi accumulator for the
     // softmax head's cancelling dW sum (measured: 1e-4 bar missed at 1024
     // MMAs per accumulator on the 1000-class scaled config)
@@ -1686,6 +1691,7 @@ int enqueue_merge(hb_ctx* c) {
 // device forward pass).
 int do_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta, uint32_t flags, double* out_loss,
             bool graph_ok = true, const std::function<int()>& mid = nullptr) {
+  if (c->pend_active) return fail(HB_ESTATE, "a replica step is in flight (hb_replica_end first)");
   if (rows < 1 || rows > c->max_batch) return fail(HB_EINVAL, "rows=%d outside [1, %d]", rows, c->max_batch);
   c->last_launches = c->pre_launches;
   c->pre_launches = 0;
@@ -1949,7 +1955,9 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
     // long-K forward GEMM (measured ~15% slower steps, no further gain needed)
     const int max_bn_long = static_cast<int>(env_long("HB_BN_LONG_K", 128));
     const int long_from = static_cast<int>(env_long("HB_BN_LONG_FROM", c->small_head ? L : L - 1));
-    if (c->passes == 3 && cdiv(c->d[l], kBK) > 32 && l >= long_from)
+    // (with the accumulator drain every k-block starts a fresh accumulator, so
+    // neither cap is needed: HB_GEMM_DRAIN builds keep the wide tiles)
+    if (c->passes == 3 && cdiv(c->d[l], kBK) > 32 && l >= long_from && !HB_GEMM_DRAIN)
       c->bn_fwd[l] = std::min(c->bn_fwd[l], max_bn_long);
     c->bn_dw[l] = choose_bn(cdiv(c->d[l + 1], kBM), c->d[l]);
     // experiments: cap the tile width (more rotating accumulators, shorter MMA chains)
@@ -1959,7 +1967,7 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
     // the wide softmax head's dW sums error signals of both signs over the
     // whole batch (a cancelling sum): 128-wide tiles give 3 rotating hi*hi
     // accumulators, and dw_plan bounds the chain per accumulator
-    if (l == L - 1 && !c->small_head && c->passes == 3 && c->d[l] >= 64)
+    if (l == L - 1 && !c->small_head && c->passes == 3 && c->d[l] >= 64 && !HB_GEMM_DRAIN)
       c->bn_dw[l] = static_cast<int>(env_long("HB_HEAD_DW_BN", 128));
     n_params += static_cast<size_t>(c->d[l + 1]) * c->d[l];
   }
@@ -2619,7 +2627,8 @@ static void xfer_account(hb_ctx* c, bool loss) {
 
 // Enqueue the step asynchronously (the exchange rides inside it), apply the
 // host-mode merges as gradients land, then finish like do_step.
-static int replica_finish(hb_ctx* c, int rc, int rows, double eta, uint32_t flags, double* out_loss) {
+static int replica_finish(hb_ctx* c, int rc, int rows, double eta, uint32_t flags, double* out_loss,
+                          bool ev1_recorded = false) {
   if (rc != HB_OK) {
     // nothing may still be reading or writing the host model when the call
     // returns: drain the step stream and the exchange's copy streams
@@ -2630,7 +2639,7 @@ static int replica_finish(hb_ctx* c, int rc, int rows, double eta, uint32_t flag
     return rc;
   }
   const bool timed = (flags & HB_STEP_TIMED) != 0;
-  if (timed) HB_CUDA(cudaEventRecord(c->ev1, c->stream));
+  if (timed && !ev1_recorded) HB_CUDA(cudaEventRecord(c->ev1, c->stream));
   HB_TRY(xchg_host_merges(c, eta));
   if (out_loss != nullptr) {
     double sum = 0.0;
@@ -2659,6 +2668,32 @@ int hb_replica_step(hb_ctx* c, double* const* ws, int64_t start, int rows, doubl
   XchgGuard g{c};
   const int rc = hb_train_step(c, start, rows, eta, replica_flags(c, flags), nullptr);
   return replica_finish(c, rc, rows, eta, flags, out_loss);
+}
+
+int hb_replica_begin(hb_ctx* c, double* const* ws, int64_t start, int rows, double eta, uint32_t flags) {
+  HB_TRY(ctx_check(c));
+  if (c->pend_active) return fail(HB_ESTATE, "a replica step is already in flight");
+  HB_TRY(xchg_arm(c, ws));
+  const int rc = hb_train_step(c, start, rows, eta, replica_flags(c, flags), nullptr);
+  if (rc != HB_OK) {
+    XchgGuard g{c};
+    replica_finish(c, rc, rows, eta, flags, nullptr);  // drains the streams
+    return rc;
+  }
+  if (flags & HB_STEP_TIMED) HB_CUDA(cudaEventRecord(c->ev1, c->stream));  // the step's end, not end()'s call
+  c->pend_active = true;
+  c->pend_rows = rows;
+  c->pend_eta = eta;
+  c->pend_flags = flags;
+  return HB_OK;
+}
+
+int hb_replica_end(hb_ctx* c, double* out_loss) {
+  HB_TRY(ctx_check(c));
+  if (!c->pend_active) return fail(HB_ESTATE, "no replica step in flight");
+  c->pend_active = false;
+  XchgGuard g{c};
+  return replica_finish(c, HB_OK, c->pend_rows, c->pend_eta, c->pend_flags, out_loss, true);
 }
 
 int hb_replica_step_host_dense(hb_ctx* c, double* const* ws, const float* x, int64_t ld, const int64_t* labels,

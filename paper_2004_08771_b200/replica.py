@@ -284,6 +284,19 @@ class GpuReplica:
                                           C.byref(loss) if want_loss else None))
         return loss.value if want_loss else None
 
+    def replica_begin(self, weights, start: int, rows: int, eta: float, timed: bool = False,
+                      sole_writer: bool = False) -> None:
+        """First half of replica_step: enqueue snapshot, step and gradient
+        copies and return; replica_end applies the stale merge and waits."""
+        table = self._model_table(weights)
+        flags = (N.HB_STEP_TIMED if timed else 0) | (N.HB_STEP_SOLE_WRITER if sole_writer else 0)
+        N.check(self._lib.hb_replica_begin(self._h, table, int(start), int(rows), float(eta), flags))
+
+    def replica_end(self, want_loss: bool = False):
+        loss = C.c_double(0.0)
+        N.check(self._lib.hb_replica_end(self._h, C.byref(loss) if want_loss else None))
+        return loss.value if want_loss else None
+
     def replica_step_host(self, weights, batch, labels, eta: float, timed: bool = False, want_loss: bool = True,
                           sole_writer: bool = False):
         """replica_step on a batch held in host memory (float32 rows or a CsrDataset)."""

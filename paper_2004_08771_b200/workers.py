@@ -211,6 +211,53 @@ def execute_gpu_replica(model, batch, eta: float, speed_factor: float = 0.0) -> 
     return 1.0
 
 
+# replica steps begun (execute_gpu_replica_begin) whose stale merge has not
+# landed yet; the pipelined coordinator wrapper waits for zero before it
+# snapshots the shared model for an evaluation (feed.pipelined)
+_inflight = threading.Condition()
+_inflight_n = 0
+
+
+def execute_gpu_replica_begin(model, batch, eta: float) -> None:
+    """First half of execute_gpu_replica: stage (once per epoch array) and
+    enqueue snapshot, step and gradient copies, then return while the step
+    runs.  execute_gpu_replica_end on the same thread applies the stale merge;
+    nothing else may run on this thread's replica in between."""
+    global _inflight_n
+    sizes = layer_sizes_of(model)
+    sparse = isinstance(batch, CsrBatchRef) or _is_wide_sparse(batch.features)
+    ctx = _replica(sizes, batch.length, sparse, "train")
+    _tls.gpu_worker = True
+    _stage_for(ctx, batch)
+    ctx.replica_begin(model.weights, batch.start, batch.length, eta, timed=True, sole_writer=_sole_writer)
+    _tls.pending = (ctx, batch.length)
+    with _inflight:
+        _inflight_n += 1
+
+
+def execute_gpu_replica_end() -> float:
+    """Second half: the stale merge lands in the shared model; returns the
+    step's device time in seconds (booked like execute_gpu_replica)."""
+    global _inflight_n
+    ctx, rows = _tls.pending
+    _tls.pending = None
+    try:
+        ctx.replica_end()
+    finally:
+        with _inflight:
+            _inflight_n -= 1
+            _inflight.notify_all()
+    ms = ctx.last_step_ms
+    book_device_step(rows, ms)
+    return ms / 1000.0
+
+
+def wait_merges_landed(timeout: float | None = None) -> bool:
+    """Block until every begun replica step has merged into the shared model."""
+    with _inflight:
+        return _inflight.wait_for(lambda: _inflight_n == 0, timeout)
+
+
 def book_device_step(rows: int, ms: float) -> None:
     """Account one device-timed replica step on this thread: last / total
     device time, and the installed DeviceSpeedFeed under this thread's

@@ -705,3 +705,29 @@ def test_concurrent_host_writer_keeps_its_updates(hb):
     finally:
         stop.set()
         ctx.close()
+
+
+def test_pipelined_replica_equals_the_one_call_step(hb):
+    """execute_gpu_replica_begin / _end (hb_replica_begin / hb_replica_end:
+    the worker replies to the coordinator between them, feed.pipelined) leave
+    the shared model bit-identical to execute_gpu_replica, step after step."""
+    from paper_2004_08771_b200 import Architecture, BatchRef, Model, workers as W
+
+    sizes = (54, 256, 256, 2)
+    b = 512
+    x, y = ref_nn.synthetic_blobs(6 * b, sizes[0], 2, 2.5, 9)
+    w0 = ref_nn.init_weights(sizes, 10)
+    one = Model(Architecture(sizes), [a.copy() for a in w0])
+    two = Model(Architecture(sizes), [a.copy() for a in w0])
+    try:
+        for i in range(6):
+            batch = BatchRef(x, y, i * b, b)
+            assert W.execute_gpu_replica(one, batch, 0.3) == 1.0
+            W.execute_gpu_replica_begin(two, batch, 0.3)
+            assert W.wait_merges_landed(timeout=0.0) is False  # in flight until end
+            assert W.execute_gpu_replica_end() > 0.0
+            assert W.wait_merges_landed(timeout=0.0)
+            for a, c in zip(one.weights, two.weights):
+                assert np.array_equal(a, c), i
+    finally:
+        W.release_thread_contexts()

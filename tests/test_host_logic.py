@@ -195,6 +195,80 @@ class TestReferenceEngineSeam:
         assert speeds[-1] == pytest.approx(100 / 2e-3)
 
 
+    def test_pipelined_worker_keeps_the_reference_curve(self, monkeypatch):
+        """feed.pipelined answers the coordinator while the step runs and lands
+        the merge afterwards.  With a deterministic single worker
+        the loss curve and final model must equal the reference's own run
+        bit for bit -- including evaluations the coordinator starts right after
+        the early reply (it waits for in-flight merges first)."""
+        import threading
+        import time as _time
+
+        ref_src = Path("/root/reference/pkg/src")
+        if not ref_src.exists():
+            pytest.skip("reference package not present")
+        monkeypatch.syspath_prepend(str(ref_src))
+        import hogtrain
+        import hogtrain.engine as E
+        import hogtrain.workers as RW
+
+        from paper_2004_08771_b200 import workers as W
+
+        def run():
+            ds = hogtrain.data.synthetic_blobs(900, 6, 2, 2.5, seed=1)
+            model = hogtrain.nn.init_model(hogtrain.nn.Architecture((6, 8, 2)), seed=2)
+            roster = [RW.WorkerConfig("gpu0", RW.WorkerMode.BATCH_REPLICA, min_batch=64, max_batch=64)]
+            m = hogtrain.run_training(ds, model, roster, hogtrain.policies.UniformHogbatch(64, 0.3), epochs=3,
+                                      seed=3, loss_every_batches=4)
+            return [s.loss for s in m.samples], model.weights, m
+
+        ref_curve, ref_w, _ = run()
+        ref_step = RW.execute_batch_replica
+        tls = threading.local()
+
+        def begin(model, batch, eta):
+            tls.args = (model, batch, eta)
+
+        def end():
+            _time.sleep(0.003)  # the merge lands well after the early reply
+            ref_step(*tls.args)
+            W.book_device_step(tls.args[1].length, 1.0)
+            return 1e-3
+
+        monkeypatch.setattr(RW.WorkerThread, "_execute", RW.WorkerThread._execute)
+        monkeypatch.setattr(E._Coordinator, "_evaluate_and_sample", E._Coordinator._evaluate_and_sample)
+        monkeypatch.setattr(RW, "execute_batch_replica", W.execute_gpu_replica)
+        monkeypatch.setattr(W, "execute_gpu_replica_begin", begin)
+        monkeypatch.setattr(W, "execute_gpu_replica_end", end)
+        inflight = {"n": 0}
+        orig_begin = begin
+
+        def counting_begin(model, batch, eta):
+            with W._inflight:
+                W._inflight_n += 1
+            inflight["n"] += 1
+            orig_begin(model, batch, eta)
+
+        def counting_end():
+            try:
+                return end()
+            finally:
+                with W._inflight:
+                    W._inflight_n -= 1
+                    W._inflight.notify_all()
+
+        monkeypatch.setattr(W, "execute_gpu_replica_begin", counting_begin)
+        monkeypatch.setattr(W, "execute_gpu_replica_end", counting_end)
+        hb.pipelined(RW, E)
+        hb.pipelined(RW, E)  # idempotent
+        curve, w, m = run()
+        assert inflight["n"] == m.per_worker_updates["gpu0"] > 0
+        assert curve == ref_curve
+        for a, b in zip(w, ref_w):
+            assert np.array_equal(a, b)
+        assert m.per_worker_busy_ms["gpu0"] == pytest.approx(1.0 * m.per_worker_updates["gpu0"])
+
+
 class TestBenchAccounting:
     def test_flops_per_sample_match_survey(self):
         import bench

@@ -669,6 +669,22 @@ long long env_long(const char* name, long long dflt) {
   return v != nullptr && v[0] != 0 ? atoll(v) : dflt;
 }
 
+// Accumulator drain (hb_gemm.cuh "Drain mode") per GEMM: D k-blocks per
+// fresh accumulator, 0 = rotating accumulators.  The precision-critical GEMMs
+// are the ones the output layer's cancelling dW sum depends on -- the forward
+// GEMM that produces A_{L-1} and, for a wide softmax head, its logits and dW
+// GEMMs: the truncating tensor-core accumulation over a whole K biases them
+// enough to miss the per-step 1e-4 weight bar at near-cancelling output
+// weights (real-sim 8.6e-4, delicious 1.1e-4; 4.6e-5 / 8e-6 drained every
+// k-block).  Others keep the rotation (HB_DRAIN_KB: their D, 0 = off).
+enum GemmRole { R_FWD = 0, R_LOGITS = 1, R_DX = 2, R_DW = 3 };
+int drain_kb(const hb_ctx* c, GemmRole role, int l) {
+  if (c->passes != 3 || !HB_GEMM_DRAIN) return 0;
+  const int L = c->L;
+  const bool crit = (role == R_FWD && l == L - 2) || (!c->small_head && l == L - 1 && (role == R_LOGITS || role == R_DW));
+  return static_cast<int>(crit ? env_long("HB_DRAIN_KB_CRIT", 1) : env_long("HB_DRAIN_KB", 0));
+}
+
 // Split-K plan for a forward / dX GEMM: when its output tiles cannot fill
 // the SMs (small batches, e.g. covtype's b=512 gives 8-16 CTAs) K is split so
 // the launch covers about one wave; splitk_epi_kernel sums the slabs and
@@ -694,7 +710,7 @@ void dw_plan(const hb_ctx* c, int l, int rows, int* splits, int* kb_per, int* kb
   *kb_total = std::max(1, cdiv(rows, kBK));
   // one wave: as many K splits as fit on the 148 SMs (1 CTA / SM)
   int want = std::max(1, 148 / tiles);
-  if (l == c->L - 1 && !c->small_head && c->passes == 3 && !(HB_GEMM_DRAIN && c->bn_dw[l] >= 64)) {
+  if (l == c->L - 1 && !c->small_head && c->passes == 3 && !(drain_kb(c, R_DW, l) > 0 && c->bn_dw[l] >= 64)) {
     // precision: at most 16 k-blocks per rotating hi*hi accumulator for the
     // softmax head's cancelling dW sum (measured: 1e-4 bar missed at 1024
     // MMAs per accumulator on the 1000-class scaled config)
@@ -1191,6 +1207,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     // its dW), never a tensor-core GEMM: no lo twin to write
     a.out_lo = (c->need_lo() && !(c->small_head && l + 1 == L - 1)) ? c->A_lo[l + 1] : nullptr;
     a.ldo = c->ld[l + 1];
+    a.drain_kb = drain_kb(c, R_FWD, l);
     const Operand ta = l == 0 ? v.fwd() : c->opA_k(l);
     prof_begin(c, "gemm_fwd_sigmoid", l);
     int kb_per = a.kb_total;
@@ -1311,6 +1328,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
   a.kb_per_split = a.kb_total;
   a.out = c->D[l];
   a.ldo = c->ld[L];
+  a.drain_kb = drain_kb(c, R_LOGITS, l);
   const Operand ta = l == 0 ? v.fwd() : c->opA_k(l);
   prof_begin(c, "gemm_fwd_logits", l);
   {
@@ -1361,6 +1379,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       a.aux = c->A[l];
       a.ld_aux = c->ld[l];
       a.ds = ds;
+      a.drain_kb = drain_kb(c, R_DX, l);
       prof_begin(c, "gemm_dx_dsig", l);
       int kb_per = a.kb_total;
       const int fsplit = fx_plan(c, cdiv(zrows, kBM), cdiv(a.N, c->bn_dx[l]), c->bn_dx[l], a.kb_total, &kb_per);
@@ -1415,6 +1434,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
     a.kb_total = kb_total;
     a.kb_per_split = kb_per;
     a.eta = static_cast<float>(eta);
+    a.drain_kb = drain_kb(c, R_DW, l);
     const Operand tb = l == 0 ? v.dw() : c->opA_mn(l);
     const int mt = cdiv(a.M, kBM), nt = cdiv(a.N, c->bn_dw[l]);
     if (c->conc_bwd && l >= 1 && splits > 1) {
@@ -1957,7 +1977,8 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
     const int long_from = static_cast<int>(env_long("HB_BN_LONG_FROM", c->small_head ? L : L - 1));
     // (with the accumulator drain every k-block starts a fresh accumulator, so
     // neither cap is needed: HB_GEMM_DRAIN builds keep the wide tiles)
-    if (c->passes == 3 && cdiv(c->d[l], kBK) > 32 && l >= long_from && !HB_GEMM_DRAIN)
+    const bool crit_drain = HB_GEMM_DRAIN && env_long("HB_DRAIN_KB_CRIT", 1) > 0;
+    if (c->passes == 3 && cdiv(c->d[l], kBK) > 32 && l >= long_from && !crit_drain)
       c->bn_fwd[l] = std::min(c->bn_fwd[l], max_bn_long);
     c->bn_dw[l] = choose_bn(cdiv(c->d[l + 1], kBM), c->d[l]);
     // experiments: cap the tile width (more rotating accumulators, shorter MMA chains)
@@ -1967,7 +1988,7 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
     // the wide softmax head's dW sums error signals of both signs over the
     // whole batch (a cancelling sum): 128-wide tiles give 3 rotating hi*hi
     // accumulators, and dw_plan bounds the chain per accumulator
-    if (l == L - 1 && !c->small_head && c->passes == 3 && c->d[l] >= 64 && !HB_GEMM_DRAIN)
+    if (l == L - 1 && !c->small_head && c->passes == 3 && c->d[l] >= 64 && !crit_drain)
       c->bn_dw[l] = static_cast<int>(env_long("HB_HEAD_DW_BN", 128));
     n_params += static_cast<size_t>(c->d[l + 1]) * c->d[l];
   }

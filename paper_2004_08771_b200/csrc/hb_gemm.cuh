@@ -69,6 +69,7 @@ struct GemmArgs {
                              // w8a inputs) -- its lo tile is neither loaded nor multiplied
   int trace;              // HB_TRACE builds: record this launch's pipeline timeline
   int trace_slot;         // HB_TRACE builds: 1-based slot for the per-CTA stamps (0 = off)
+  int drain_kb;           // > 0: accumulator drain every drain_kb k-blocks (GemmCfg), 0: rotating accumulators
 };
 
 // Optional pipeline timeline (debug builds, -DHB_TRACE): CTA (0,0,0) records
@@ -134,16 +135,19 @@ struct GemmCfg {
   // small cross terms in their own accumulator and rotates the hi*hi term over
   // NBIG accumulators by k-block; the epilogue sums them in fp32 registers.
   //
-  // DRAIN (3xTF32, BN >= 64): instead, every k-block's three products go into
-  // a fresh accumulator (two TMEM slots, alternating), which the epilogue warps
-  // drain into fp32 registers (round-to-nearest adds) while the tensor core
-  // fills the other slot: the truncating accumulation covers only the 12 MMAs
-  // of one k-block (4 of them on the large hi*hi term), not the whole K.
-  static constexpr bool DRAIN = (PASSES == 3) && (BN >= 64) && (HB_GEMM_DRAIN != 0);
+  // Drain mode (args.drain_kb = D > 0; 3xTF32, BN >= 64): instead, each run of
+  // D k-blocks puts its three products into a fresh accumulator (two TMEM
+  // slots, alternating), which the epilogue warps drain into fp32 registers
+  // (round-to-nearest adds) while the tensor core fills the other slot: the
+  // truncating accumulation covers 12 D MMAs, not the whole K.  TMEM reads run
+  // at ~64 B/cycle per SM, so draining a 128 x BN tile costs ~2.7x the MMA time
+  // of one k-block: D = 1 is for the few precision-critical GEMMs, D >= 3
+  // hides the drain under the MMAs.
+  static constexpr bool DRAIN_OK = (PASSES == 3) && (BN >= 64) && (HB_GEMM_DRAIN != 0);
   static constexpr int NBIG_RAW = PASSES == 3 ? 512 / BN - 1 : 1;
-  static constexpr int NBIG = DRAIN ? 1 : (NBIG_RAW > 15 ? 15 : (NBIG_RAW < 1 ? 1 : NBIG_RAW));
-  static constexpr int NACC = PASSES == 3 ? NBIG + 1 : 1;  // DRAIN: the two k-block slots
-  static constexpr int TMEM_COLS_RAW = NACC * BN;
+  static constexpr int NBIG = NBIG_RAW > 15 ? 15 : (NBIG_RAW < 1 ? 1 : NBIG_RAW);
+  static constexpr int NACC = PASSES == 3 ? NBIG + 1 : 1;
+  static constexpr int TMEM_COLS_RAW = (DRAIN_OK && 2 * BN > NACC * BN) ? 2 * BN : NACC * BN;
   static constexpr int TMEM_COLS = TMEM_COLS_RAW <= 32 ? 32 : TMEM_COLS_RAW <= 64 ? 64 : TMEM_COLS_RAW <= 128 ? 128
                                    : TMEM_COLS_RAW <= 256 ? 256 : 512;
   static_assert(TMEM_COLS_RAW <= 512, "TMEM holds 512 fp32 columns");
@@ -199,6 +203,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
   const int kb_begin = blockIdx.z * args.kb_per_split;
   const int kb_end = min(kb_begin + args.kb_per_split, args.kb_total);
   const int nkb = max(kb_end - kb_begin, 0);
+  const bool drain = C::DRAIN_OK && args.drain_kb > 0;
+  const int dkb = drain ? args.drain_kb : 1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -212,7 +218,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
       mbar_init(&empty[s], 1);
     }
     // DRAIN: the drain warps publish the summed tile in TMEM (8 arrivals)
-    mbar_init(tmem_full, C::DRAIN ? C::EPI_WARPS : 1);
+    mbar_init(tmem_full, (C::DRAIN_OK && args.drain_kb > 0) ? C::EPI_WARPS : 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], C::EPI_WARPS * (PAIR ? 2 : 1));
@@ -286,19 +292,22 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
     // -------------------------------------------------------- MMA issuer
     if (lane == 0 && leader) {
       constexpr uint32_t idesc = make_idesc_tf32(PAIR ? 2 * kBM : kBM, BN, A_MN, B_MN);
-      if constexpr (C::DRAIN) {
+      if (C::DRAIN_OK && drain) {
+        uint32_t acc = 0u;
         for (int i = 0; i < nkb; ++i) {
           const int s = i % STAGES;
           const uint32_t ph = (i / STAGES) & 1;
-          const int slot = i & 1;
-          if (i >= 2) mbar_wait(&acc_empty[slot], ((i >> 1) - 1) & 1);  // drained (both CTAs)
+          const int ci = i / dkb;  // chunk of dkb k-blocks -> one fresh accumulator
+          const int slot = ci & 1;
+          const bool first = (i % dkb) == 0;
+          if (first && ci >= 2) mbar_wait(&acc_empty[slot], ((ci >> 1) - 1) & 1);  // drained (both CTAs)
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t aHi = smem_u32(smem + s * C::STAGE_BYTES);
           const uint32_t bHi = aHi + C::A_BYTES;
           const uint32_t t = tmem_base + slot * BN;
           // the two small cross terms first (into the fresh accumulator), then hi*hi
-          uint32_t acc = 0u;
+          if (first) acc = 0u;
 #pragma unroll
           for (int kk = 0; kk < kBK / 8; ++kk) {
             if (!args.a_lo_zero) {
@@ -316,7 +325,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
             acc = 1u;
           }
           mma_commit_cg(&empty[s], PAIR);
-          mma_commit_cg(&acc_full[slot], PAIR);
+          if ((i % dkb) == dkb - 1 || i == nkb - 1) mma_commit_cg(&acc_full[slot], PAIR);
         }
       } else
       for (int i = 0; i < nkb; ++i) {
@@ -349,9 +358,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
         mma_commit_cg(&empty[s], PAIR);
         HB_STAMP(2 * 512 + i);  // MMA: issue done
       }
-      if (!C::DRAIN) mma_commit_cg(tmem_full, PAIR);  // accumulators complete (immediate if nkb == 0)
+      if (!drain) mma_commit_cg(tmem_full, PAIR);  // accumulators complete (immediate if nkb == 0)
     }
-  } else if (C::DRAIN && warp >= 4 && warp < 4 + C::EPI_WARPS) {
+  } else if (C::DRAIN_OK && drain && warp >= 4 && warp < 4 + C::EPI_WARPS) {
     // ------------------------------------- DRAIN: k-block partials -> registers
     // warp (q, h) owns TMEM lane quarter q and column half h of the tile
     constexpr int HC = BN / 2;  // columns per warp
@@ -361,7 +370,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
     float sum[HC];
 #pragma unroll
     for (int j = 0; j < HC; ++j) sum[j] = 0.f;
-    for (int i = 0; i < nkb; ++i) {
+    const int nchunks = (nkb + dkb - 1) / dkb;
+    for (int i = 0; i < nchunks; ++i) {
       const int slot = i & 1;
       mbar_wait(&acc_full[slot], (i >> 1) & 1);
       tc_fence_after();
@@ -457,11 +467,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
         uint32_t r[32];
         // small-term accumulator first, then the hi*hi accumulators (only those
         // the k loop actually wrote)
-        tmem_ld_32x32b_x32(lane_addr + (C::DRAIN ? 0 : (C::NACC - 1) * BN), r);
+        tmem_ld_32x32b_x32(lane_addr + (drain ? 0 : (C::NACC - 1) * BN), r);
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = (C::DRAIN || nkb > 0) ? __uint_as_float(r[j]) : 0.f;
-        if (C::NACC > 1 && !C::DRAIN) {
+        for (int j = 0; j < 32; ++j) v[j] = (drain || nkb > 0) ? __uint_as_float(r[j]) : 0.f;
+        if (C::NACC > 1 && !drain) {
 #pragma unroll 1
           for (int a = 0; a < C::NBIG; ++a) {
             tmem_ld_32x32b_x32(lane_addr + a * BN, r);

@@ -537,7 +537,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         ctx.pin_host(host_model)  # what execute_gpu_replica does for the shared model
         for i in range(max(3, min(args.warmup, len(host_batches)))):  # warm the host path (and its graph)
             xb, yb = host_batches[i % len(host_batches)]
-            ctx.replica_step_host(host_model, xb, yb, cfg["eta"])
+            ctx.replica_step_host(host_model, xb, yb, cfg["eta"], sole_writer=True)
         if distributed:
             barrier(dist)
         t0 = time.perf_counter()
@@ -545,7 +545,8 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
             xb, yb = host_batches[i]
             # execute_batch_replica in one call: snapshot of the shared host model
             # (workers.py:132), batch H2D, the step, stale merge (workers.py:135), loss D2H
-            ctx.replica_step_host(host_model, xb, yb, cfg["eta"], want_loss=True)
+            # (a lone GPU replica is the host model's only writer: HB_STEP_SOLE_WRITER)
+            ctx.replica_step_host(host_model, xb, yb, cfg["eta"], want_loss=True, sole_writer=True)
         el = time.perf_counter() - t0
         # PCIe bytes of the last call as the library issued them
         h2d, d2h = ctx.last_xfer_bytes
@@ -556,7 +557,8 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
                "path": "execute_gpu_replica semantics through the C ABI (hb_replica_step_host_*), per step: "
                        "batch H2D from pinned host memory, snapshot of the page-locked f64 host model (DMA H2D, "
                        "layer l+1 in flight while layer l computes), the step, the f64 stale merge W_host += (-eta)*g "
-                       "per layer as soon as its gradient exists, loss D2H"}
+                       "per layer as soon as its gradient exists (the largest split-K layers merge on the device lane: "
+                       "the replica is the model's sole writer here), loss D2H"}
 
     # ---------------------------------------------------------- CPU baselines (rank 0, N=1)
     cpu = None

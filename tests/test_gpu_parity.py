@@ -438,27 +438,27 @@ def test_two_worker_threads_merge_concurrently(hb):
         assert np.array_equal(a, s) and np.array_equal(b2, s)
 
 
-# Updated weights of the real-sim-width case: one output weight lands at
-# |W_new| ~ 9e-5 (W ~ 3e-2 minus 0.5 * g ~ 3e-2), below the metric's 1e-4
-# floor, so a 2e-6-relative gradient (fp32 data, 3xTF32) shows up as 1.15e-4
-# there; every gradient of that case is within 1.8e-6.  Measured, not tuned.
-REALSIM_WEIGHT_TOL = 2e-4
+BASELINE_SEEDS = (0, 1, 2, 3, 4)
 
 
+@pytest.mark.parametrize("seed", BASELINE_SEEDS)
 @pytest.mark.parametrize(
-    "sizes,b,sparse_nnz,eta,weight_tol",
+    "sizes,b,sparse_nnz,eta",
     [
-        ((300, 512, 512, 512, 2), 8192, 12, 0.5, STEP_TOL),  # w8a config, full GPU batch
-        ((500, 1024, 1024, 983), 8192, None, 0.5, STEP_TOL),  # delicious config, full GPU batch
-        ((20958, 1024, 1024, 2), 2048, 52, 0.5, REALSIM_WEIGHT_TOL),  # real-sim width (CSR kernels), 1/4 batch
-        ((1024, 4096, 4096, 4096, 1000), 8192, None, 0.1, STEP_TOL),  # scaled config, full GPU batch
+        ((54, 512, 512, 512, 2), 512, None, 0.5),  # covtype config, its batch
+        ((300, 512, 512, 512, 2), 8192, 12, 0.5),  # w8a config, full GPU batch
+        ((500, 1024, 1024, 983), 8192, None, 0.5),  # delicious config, full GPU batch
+        ((20958, 1024, 1024, 2), 8192, 52, 0.5),  # real-sim config (CSR kernels), full GPU batch
+        ((1024, 4096, 4096, 4096, 1000), 8192, None, 0.1),  # scaled config, full GPU batch
     ],
+    ids=["covtype", "w8a", "delicious", "realsim", "scaled"],
 )
-def test_oracle_step_at_baseline_size(hb, sizes, b, sparse_nnz, eta, weight_tol):
-    """Per-step parity at the BASELINE.json configurations' own sizes (the
-    float64 oracle runs them in seconds): gradients within 1e-4 under the
-    reference's floored metric, updated weights too (see REALSIM_WEIGHT_TOL)."""
-    w, x, y = oracle_case(sizes, b, seed=7 + b, sparse_nnz=sparse_nnz)
+def test_oracle_step_at_baseline_size(hb, sizes, b, sparse_nnz, eta, seed):
+    """Per-step parity at every BASELINE.json configuration's own sizes and
+    batch (the float64 oracle runs them in seconds), five seeds each:
+    gradients and updated weights within 1e-4 under the reference's floored
+    metric (helpers.py:29-35), no loosened bar."""
+    w, x, y = oracle_case(sizes, b, seed=1000 * seed + 7 + b, sparse_nnz=sparse_nnz)
     grads = ref_nn.backward(w, ref_nn.forward(w, x), y)
     upd = ref_nn.deep_copy(w)
     ref_nn.apply_update(upd, grads, eta)
@@ -466,7 +466,53 @@ def test_oracle_step_at_baseline_size(hb, sizes, b, sparse_nnz, eta, weight_tol)
     eg = max_relative_error(out["grads"], grads)
     ew = max_relative_error(out["weights"], upd)
     assert eg <= STEP_TOL, eg
-    assert ew <= weight_tol, ew
+    assert ew <= STEP_TOL, ew
+
+
+@pytest.mark.parametrize(
+    "sizes,n,b,eta,epochs,classes",
+    [
+        ((54, 512, 512, 512, 2), 20480, 512, 0.5, 2, 2),  # covtype config on a 20K-row subset
+        ((500, 1024, 1024, 983), 16105, 2048, 2.0, 2, 983),  # delicious config, whole dataset
+    ],
+    ids=["covtype", "delicious"],
+)
+def test_loss_curve_at_baseline_shape(hb, sizes, n, b, eta, epochs, classes):
+    """Loss-vs-epoch curve of the deterministic single-worker schedule
+    (tests/helpers.py:54-74 == engine.py with one replica worker) at BASELINE
+    shapes: within 1% of the float64 oracle at every sample."""
+    x, y = ref_nn.synthetic_blobs(n, sizes[0], classes, 2.5, 42)
+    w = ref_nn.init_weights(sizes, 42)
+    want = ref_nn.sequential_minibatch_sgd(x, y, ref_nn.deep_copy(w), b, eta, epochs, 42)
+    model = hb.Model(hb.Architecture(sizes), [a.copy() for a in w])
+    res = hb.train_gpu(hb.Dataset(x, y), model, b, eta, epochs, 42)
+    rel = np.abs(np.array(res.curve) - want) / np.abs(want)
+    assert rel.max() <= CURVE_TOL, (rel.max(), res.curve, want)
+    assert want[-1] < want[0]  # it trains
+
+
+def test_sigmoid_epilogue_keeps_subnormals(hb):
+    """sigmoid(-100) stays a positive (subnormal) float (test_linalg.py:67-70)
+    through the tensor-core GEMM's fused sigmoid epilogue, sigmoid(100) == 1."""
+    sizes = (32, 64, 2)
+    w = [np.zeros((64, 32)), np.zeros((2, 64))]
+    w[0][0, 0], w[0][1, 0], w[0][2, 0] = -100.0, 100.0, -80.0
+    x = np.zeros((4, 32))
+    x[:, 0] = 1.0
+    y = np.zeros(4, dtype=np.int64)
+    ctx = hb.GpuReplica(sizes, 4)
+    try:
+        ctx.set_weights(w)
+        ctx.stage(x, y)
+        ctx.forward(0, 4)
+        a = ctx.activation(1, 4)
+    finally:
+        ctx.close()
+    want = np.float32(1.0 / (1.0 + np.exp(100.0)))  # 3.72e-44, subnormal in fp32
+    assert np.all(a[:, 0] > 0) and np.all(np.abs(a[:, 0] - want) <= 8 * np.float32(1.4e-45)), a[:, 0]
+    assert np.all(a[:, 1] == 1.0)
+    assert np.allclose(a[:, 2], 1.0 / (1.0 + np.exp(80.0)), rtol=1e-5)
+    assert np.all(a[:, 3:] == 0.5)
 
 
 def test_shared_host_model_outlives_one_context(hb):
@@ -562,6 +608,14 @@ def test_edge_batches(hb, sizes, b, kind):
         for a, n, w0, g in zip(got, upd, w, grads):
             assert float(np.abs(a - n).max()) <= 1e-6 * float((np.abs(w0) + 0.5 * np.abs(g)).max()), kind
         assert max_relative_error(got, upd) <= CANCEL_WEIGHT_TOL, kind
+    # Why 1e-4 is out of reach here for any fp32 gradient: the exact gradient,
+    # rounded once to fp32 and merged in float64 exactly like the drop-in path
+    # (w + (-eta) * g, linalg.py:79), already misses it at the cancelling
+    # weights -- and the drop-in result is within a small factor of that floor.
+    g32 = [gl.astype(np.float32).astype(np.float64) for gl in grads]
+    floor = max_relative_error([w0 + (-0.5) * g for w0, g in zip(w, g32)], upd)
+    if floor > STEP_TOL:
+        assert max_relative_error(model.weights, upd) <= 8 * floor, (kind, floor)
 
 
 def test_replica_step_reports_its_pcie_bytes(hb):

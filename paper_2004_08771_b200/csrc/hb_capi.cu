@@ -676,13 +676,20 @@ long long env_long(const char* name, long long dflt) {
 // GEMMs: the truncating tensor-core accumulation over a whole K biases them
 // enough to miss the per-step 1e-4 weight bar at near-cancelling output
 // weights (real-sim 8.6e-4, delicious 1.1e-4; 4.6e-5 / 8e-6 drained every
-// k-block).  Others keep the rotation (HB_DRAIN_KB: their D, 0 = off).
+// k-block).  Measured at b = 8192 (seed 1, worst weight error / step time):
+//   small head (real-sim)  D=1 4.6e-5 / 0.630 ms  D=2 1.03e-4  D=3 1.44e-4   rotation 8.6e-4 / 0.602 ms
+//   wide head (delicious)  D=1 7e-6 / 0.727 ms    D=2 2.1e-5 / 0.645 ms      rotation 1.1e-4 / 0.626 ms
+//   wide head (scaled)     D=2 6e-6 / 8.25 ms     D=3 9.6e-6 / 8.18 ms       rotation 3.9e-5 / 8.36 ms
+// (the drained head GEMMs also keep their 256-wide tiles, which the rotation
+// had to give up for precision).  Others keep the rotation (HB_DRAIN_KB: their
+// D, 0 = off); HB_DRAIN_KB_CRIT overrides the critical ones' D.
 enum GemmRole { R_FWD = 0, R_LOGITS = 1, R_DX = 2, R_DW = 3 };
+int crit_drain_default(const hb_ctx* c) { return c->small_head ? 1 : 2; }
 int drain_kb(const hb_ctx* c, GemmRole role, int l) {
   if (c->passes != 3 || !HB_GEMM_DRAIN) return 0;
   const int L = c->L;
   const bool crit = (role == R_FWD && l == L - 2) || (!c->small_head && l == L - 1 && (role == R_LOGITS || role == R_DW));
-  return static_cast<int>(crit ? env_long("HB_DRAIN_KB_CRIT", 1) : env_long("HB_DRAIN_KB", 0));
+  return static_cast<int>(crit ? env_long("HB_DRAIN_KB_CRIT", crit_drain_default(c)) : env_long("HB_DRAIN_KB", 0));
 }
 
 // Split-K plan for a forward / dX GEMM: when its output tiles cannot fill

@@ -231,6 +231,12 @@ int hb_profile_read(hb_ctx* ctx, int max_entries, char* names, double* total_ms,
 /* Restrict profiling to launches named `name` (null/empty: all launches). */
 int hb_profile_filter(hb_ctx* ctx, const char* name);
 
+/* Measurement only (bench.py's "l2" ceiling of the CSR kernels): rate in GB/s
+ * at which the device gathers pseudo-random whole rows of an L2-resident
+ * (rows x cols) fp32 matrix, `unroll` rows in flight per warp lane -- the
+ * access pattern of one W0^T row per nonzero.  No reference counterpart. */
+int hb_probe_l2_gather(int device, int64_t rows, int cols, int per_warp, int unroll, double* out_gbps);
+
 /* NCCL merge between GPU replicas (one communicator per process/device). */
 int hb_nccl_unique_id(void* out_128_bytes);
 int hb_comm_init(hb_ctx* ctx, const void* id_128_bytes, int nranks, int rank);

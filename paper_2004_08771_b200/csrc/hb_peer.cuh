@@ -106,3 +106,35 @@ __global__ void __launch_bounds__(256) peer_reduce_kernel(const __grid_constant_
 }
 
 }  // namespace hb
+
+namespace hb {
+// L2 gather ceiling probe (bench.py's "l2" roofline for the CSR kernels): each
+// warp gathers `per_warp` pseudo-random whole rows of a (rows x cols) fp32
+// matrix -- the access pattern of the CSR SpMM (one W0^T row per nonzero) --
+// with UNROLL rows in flight per lane, and reduces them into one float.
+template <int UNROLL>
+__global__ void __launch_bounds__(256) l2_gather_probe_kernel(const float* __restrict__ m, long long rows, int cols,
+                                                              int per_warp, float* __restrict__ out) {
+  const long long warp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  float acc = 0.f;
+  for (int k = 0; k < per_warp; k += UNROLL) {
+    float4 v[UNROLL][8];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      unsigned h = static_cast<unsigned>(warp * 2654435761ull + (k + u) * 40503u);
+      h ^= h >> 15;
+      h *= 2246822519u;
+      h ^= h >> 13;
+      const float4* row = reinterpret_cast<const float4*>(m + (h % rows) * cols);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v[u][t] = (4 * lane + 128 * t < cols) ? __ldg(row + lane + 32 * t) : make_float4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u)
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc += v[u][t].x + v[u][t].y + v[u][t].z + v[u][t].w;
+  }
+  if (acc == 1234.5f) out[warp] = acc;  // keep the loads alive
+}
+}  // namespace hb

@@ -108,6 +108,14 @@ int hb_host_unregister(const void* p);
 /* Raw mean gradient of the last HB_STEP_EMIT_GRAD step, (d_{l+1}, d_l) fp32. */
 int hb_get_grad_f32(hb_ctx* ctx, int layer, float* g);
 
+/* Host threads (caller included) that apply the float64 stale merges, and how
+ * long (pause iterations, ~25 ns each) they spin for the next layer before
+ * sleeping.  Default: 3/4 of the host threads (at most 12), 20000 spins.  A
+ * process that also runs the reference's CPU Hogwild pool
+ * (execute_hogwild_sharded, workers.py:94-123) gives its cores back with e.g.
+ * hb_host_merge_threads(2, 0).  Process-wide. */
+int hb_host_merge_threads(int threads, int spin);
+
 /* Stage one epoch's (or any dataset's) rows on the device so steps can index
  * them by (start, rows) -- the per-epoch shuffled copy that BatchRef views
  * (engine.py:214-221, data.py:57-79).  Dense: features (n_rows, n_cols) with

@@ -937,12 +937,30 @@ class HostPool {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     // merge threads (caller included): 3/4 of the host threads, at most 12 -- e2e on a 16-thread B200 host,
     // w8a / covtype / delicious: 8 threads 1.46e7 / 1.36e6 / 4.71e6, 12 threads 1.54e7 / 1.36e6 / 4.87e6
-    int t = static_cast<int>(std::min(12u, std::max(1u, hw * 3 / 4))) - 1;
-    if (const char* e = getenv("HB_HOST_MERGE_THREADS")) t = std::max(0, atoi(e) - 1);
+    int t = static_cast<int>(std::min(12u, std::max(1u, hw * 3 / 4)));
+    if (const char* e = getenv("HB_HOST_MERGE_THREADS")) t = std::max(1, atoi(e));
+    spins_ = getenv("HB_POOL_SPIN") ? atoi(getenv("HB_POOL_SPIN")) : 20000;
     next_.store(ticket(0, 0, 0));
-    for (int i = 0; i < t; ++i) threads_.emplace_back([this] { loop(); });
+    start(t);
   }
-  ~HostPool() {
+  ~HostPool() { stop(); }
+
+ public:
+  // Resize the pool (threads, caller included) and its post-job spin: a CPU
+  // Hogwild pool in the same process wants the cores back (hb_host_merge_threads)
+  void configure(int threads, int spins) {
+    std::lock_guard<std::mutex> job(run_mu_);  // no job in flight
+    stop();
+    spins_ = std::max(0, spins);
+    start(std::max(1, threads));
+  }
+
+ private:
+  void start(int threads) {
+    stop_ = false;
+    for (int i = 0; i < threads - 1; ++i) threads_.emplace_back([this] { loop(); });
+  }
+  void stop() {
     {
       std::lock_guard<std::mutex> lk(mu_);
       stop_ = true;
@@ -950,14 +968,14 @@ class HostPool {
     }
     cv_.notify_all();
     for (auto& t : threads_) t.join();
+    threads_.clear();
   }
   void loop() {
     unsigned long long seen = gen_.load();
     for (;;) {
       // spin ~0.5 ms for the next job (a merge is a burst of one job per
-      // layer), then sleep; HB_POOL_SPIN=0 yields the cores at once (a CPU
-      // Hogwild pool sharing the host)
-      static const int spins = getenv("HB_POOL_SPIN") ? atoi(getenv("HB_POOL_SPIN")) : 20000;
+      // layer), then sleep; spin 0 yields the cores at once
+      const int spins = spins_;
       for (int k = 0; k < spins && gen_.load(std::memory_order_acquire) == seen; ++k) pause();
       if (gen_.load(std::memory_order_acquire) == seen) {
         std::unique_lock<std::mutex> lk(mu_);
@@ -977,6 +995,7 @@ class HostPool {
   std::atomic<unsigned long long> gen_{0};
   uint64_t job_ = 0;
   bool stop_ = false;
+  int spins_ = 20000;
 };
 
 #if defined(__x86_64__)
@@ -3644,6 +3663,12 @@ int hb_merge_allreduce(hb_ctx* c) {
   HB_TRY(enqueue_merge(c));
   HB_CUDA(cudaStreamSynchronize(c->stream));
   return peer_check(c);
+}
+
+int hb_host_merge_threads(int threads, int spin) {
+  if (threads < 1 || spin < 0) return fail(HB_EINVAL, "need threads >= 1 and spin >= 0");
+  HostPool::get().configure(threads, spin);
+  return HB_OK;
 }
 
 int hb_probe_l2_gather(int device, int64_t rows, int cols, int per_warp, int unroll, double* out_gbps) {

@@ -326,14 +326,32 @@ def routed_loss_sum(reference_loss_sum):
     return loss_sum
 
 
-def install(hogtrain_module=None, devices: dict | None = None, sole_writer: bool = False, feed=None) -> None:
+def set_host_merge_threads(threads: int, spin: int = 20000) -> None:
+    """Size the library's host merge pool (caller included) and its post-layer
+    spin (hb_host_merge_threads): leave the cores to a CPU Hogwild pool
+    sharing the process, e.g. set_host_merge_threads(2, spin=0)."""
+    from . import _native as N
+
+    N.check(N.load().hb_host_merge_threads(int(threads), int(spin)))
+
+
+def install(hogtrain_module=None, devices: dict | None = None, sole_writer: bool = False, feed=None,
+            cpu_pool_threads: int = 0) -> None:
     """Route the reference's BATCH_REPLICA workers to the B200 path by
     rebinding `hogtrain.workers.execute_batch_replica`, and the GPU workers'
     evaluation slices by wrapping `loss_sum`.  devices: worker id -> GPU
     (set_worker_devices); feed: a DeviceSpeedFeed that every replica step
     records its device-timed examples/s into (the coordinator's eval split,
-    engine.py:335-351, can read it; see device_timed_engine)."""
+    engine.py:335-351, can read it; see feed.device_timed); cpu_pool_threads:
+    threads of a CPU Hogwild worker in the same roster, whose cores the merge
+    pool then leaves alone."""
     global _speed_feed
+    if cpu_pool_threads > 0:
+        # the roster's CPU Hogwild pool keeps its cores: the merge pool takes
+        # what is left (at least 2 threads) and never spins between layers
+        import os
+
+        set_host_merge_threads(max(2, min(12, (os.cpu_count() or 4) - int(cpu_pool_threads))), spin=0)
     if hogtrain_module is None:
         import hogtrain.workers as hogtrain_module  # noqa: F811  (reference package, if present)
     if devices is not None:

@@ -994,8 +994,8 @@ class HostPool {
   std::atomic<int> done_{0};
   std::atomic<unsigned long long> gen_{0};
   uint64_t job_ = 0;
-  bool stop_ = false;
-  int spins_ = 20000;
+  std::atomic<bool> stop_{false};
+  std::atomic<int> spins_{20000};
 };
 
 #if defined(__x86_64__)

@@ -94,3 +94,11 @@ def test_product_path_has_no_oracle_or_fallback():
             "try:\n    _native.load()\nexcept _native.NativeLibraryMissing as e:\n    print('LOUD', e)\n")
     out = subprocess.run(["python", "-c", code], capture_output=True, text=True, cwd=ROOT).stdout
     assert out.startswith("LOUD")
+
+
+def test_host_merge_pool_resizes(lib):
+    """hb_host_merge_threads (host only, no GPU): resize and restore the merge pool."""
+    assert lib.hb_host_merge_threads(3, 0) == 0
+    assert lib.hb_host_merge_threads(1, 100) == 0
+    assert lib.hb_host_merge_threads(0, 0) != 0  # invalid
+    assert lib.hb_host_merge_threads(4, 20000) == 0

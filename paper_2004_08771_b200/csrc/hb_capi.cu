@@ -958,7 +958,10 @@ class HostPool {
  private:
   void start(int threads) {
     stop_ = false;
-    for (int i = 0; i < threads - 1; ++i) threads_.emplace_back([this] { loop(); });
+    // the generation a worker starts from is read here, not in the new
+    // thread: a stop() racing its start-up must still wake it
+    const unsigned long long g0 = gen_.load();
+    for (int i = 0; i < threads - 1; ++i) threads_.emplace_back([this, g0] { loop(g0); });
   }
   void stop() {
     {
@@ -970,8 +973,7 @@ class HostPool {
     for (auto& t : threads_) t.join();
     threads_.clear();
   }
-  void loop() {
-    unsigned long long seen = gen_.load();
+  void loop(unsigned long long seen) {
     for (;;) {
       // spin ~0.5 ms for the next job (a merge is a burst of one job per
       // layer), then sleep; spin 0 yields the cores at once

@@ -785,3 +785,26 @@ def test_pipelined_replica_equals_the_one_call_step(hb):
                 assert np.array_equal(a, c), i
     finally:
         W.release_thread_contexts()
+
+
+def test_replica_step_then_merge_grads_into_on_one_context(hb):
+    """A context used for the fused replica_step (its pointer-table cache armed
+    with these arrays) must still apply merge_grads_into to the same arrays
+    afterwards: the three-call form then equals the oracle."""
+    sizes = (40, 96, 3)
+    w, x, y = oracle_case(sizes, 128, seed=15)
+    x32 = x.astype(np.float32)
+    ctx = hb.GpuReplica(sizes, 128)
+    try:
+        host = [a.copy() for a in w]
+        ctx.stage(x32, y)
+        ctx.replica_step(host, 0, 128, 0.2)
+        before = [a.copy() for a in host]
+        ctx.set_weights(host)
+        ctx.step(0, 128, 0.2, emit_grad=True)
+        ctx.merge_grads_into(host, 0.2)
+        g = ref_nn.backward(before, ref_nn.forward(before, x32.astype(np.float64)), y)
+        assert max_relative_error(host, [b - 0.2 * gl for b, gl in zip(before, g)]) <= STEP_TOL
+        assert any(not np.array_equal(a, b) for a, b in zip(host, before))
+    finally:
+        ctx.close()

@@ -142,7 +142,7 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
-// launch_k with an L2 access-policy window: [base, base + bytes) is kept
+// launch_k with an optional L2 access-policy window: [base, base + bytes) is kept
 // resident (persisting) in L2 while the kernel runs -- the operand a gather
 // kernel re-reads row by row (W0^T for the CSR SpMM: every nonzero pulls one
 // 4 KB row, 426 K rows per real-sim batch against 86 MB of unique bytes).
@@ -150,7 +150,9 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k_l2(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                         const void* base, size_t bytes, Args&&... args) {
-  static const bool off = getenv("HB_NO_L2_WINDOW") && getenv("HB_NO_L2_WINDOW")[0] == '1';
+  // measured on real-sim (b = 8192): no faster (0.655 vs 0.625 ms/step, the
+  // carve-out shrinks the L2 every other kernel sees), so opt-in: HB_L2_WINDOW=1
+  static const bool off = !(getenv("HB_L2_WINDOW") && getenv("HB_L2_WINDOW")[0] == '1');
   static size_t carve[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -553,6 +555,16 @@ struct hb_ctx {
   // W_host -= eta*g_l as a chunked DMA read-modify-write (H2D on xh2d, update
   // + D2H on xmrg) as soon as layer l's gradient exists.
   std::vector<double*> xw;          // armed host model (page-locked); empty: no exchange
+  // Resident mirror (sole-writer calls): after a HB_STEP_SOLE_WRITER call the
+  // f64 staging buffer holds exactly the host model (the device applies the
+  // same f64 merge, rounding like np.add), so the next sole-writer call on the
+  // same arrays skips the snapshot DMA -- unless a sampled fingerprint of the
+  // host model shows another write in between.
+  bool mirror_valid = false;   // stage_all == host model (as of the last call)
+  long long mirror_gen = 0;    // pointer-set key the mirror belongs to
+  bool xmirror = false;        // the call being enqueued uses (and keeps) the mirror
+  bool xsole = false;          // the call being enqueued is a sole-writer call
+  std::vector<double> fp_vals; // sampled host values after the last sole-writer call
   std::vector<double*> xw_prev;     // pointer set of the last armed call (graph key)
   long long xgen = 0;               // graph key of the armed pointer set (hash)
   cudaStream_t xh2d = nullptr, xmrg = nullptr;
@@ -1063,8 +1075,9 @@ int xchg_begin(hb_ctx* c) {
   HB_CUDA(cudaStreamWaitEvent(c->xh2d, c->xstart_ev, 0));  // earlier users of the staging buffer are done
   for (int l = 0; l < c->L; ++l) {
     const size_t n = static_cast<size_t>(c->d[l + 1]) * c->d[l];
-    HB_CUDA(cudaMemcpyAsync(c->stage_all + layer_offset(c, l), c->xw[l], n * sizeof(double), cudaMemcpyHostToDevice,
-                            c->xh2d));
+    if (!c->xmirror)  // resident mirror: the staging buffer already holds the host model
+      HB_CUDA(cudaMemcpyAsync(c->stage_all + layer_offset(c, l), c->xw[l], n * sizeof(double),
+                              cudaMemcpyHostToDevice, c->xh2d));
     HB_CUDA(cudaEventRecord(c->xsnap_ev[l], c->xh2d));
     xtl(c, c->xh2d, "h2d: snapshot layer %d landed", l);
   }
@@ -1129,6 +1142,14 @@ int xchg_merge(hb_ctx* c, int l, double eta, const DevStep* ds, cudaStream_t src
     }
     HB_CUDA(cudaMemcpyAsync(c->xgrad_host + off, src, n * sizeof(float), cudaMemcpyDeviceToHost, c->xmrg));
     HB_CUDA(cudaMemcpyAsync(c->xseq_host + 1 + l, c->d_xseq, sizeof(int32_t), cudaMemcpyDeviceToHost, c->xmrg));
+    if (c->xsole) {
+      // the same f64 merge on the device copy (w + (-eta) * g, product and sum
+      // rounded like the host's): the staging buffer stays equal to the host model
+      merge_host_f64_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 4)), 256, 0, c->xmrg>>>(
+          c->stage_all + off, c->G[l], tr ? c->ldw[0] : cols, rows, cols, tr ? 1 : 0, eta, ds);
+      HB_CUDA(cudaGetLastError());
+      c->last_launches++;
+    }
     xtl(c, c->xmrg, "mrg: gradient %d on host", l);
     return HB_OK;
   }
@@ -1542,8 +1563,9 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       if (dev_lane) {
         c->xdma_used[l] = 1;
         HB_CUDA(cudaStreamWaitEvent(c->xh2d, c->bev[2 * l], 0));
-        HB_CUDA(cudaMemcpyAsync(host_rows, c->xw[l], static_cast<size_t>(a.M) * a.N * sizeof(double),
-                                cudaMemcpyHostToDevice, c->xh2d));
+        if (!c->xmirror)  // (a resident mirror already holds these rows)
+          HB_CUDA(cudaMemcpyAsync(host_rows, c->xw[l], static_cast<size_t>(a.M) * a.N * sizeof(double),
+                                  cudaMemcpyHostToDevice, c->xh2d));
         HB_CUDA(cudaEventRecord(c->xread_ev[l], c->xh2d));
       }
       c->prof_st = c->side;
@@ -1650,7 +1672,7 @@ int run_phase(hb_ctx* c, const DataView& v, long long start, int rows, uint32_t 
 int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta, uint32_t flags, bool graph_ok,
                  int phase = 0) {
   const uint32_t gflags = (flags & (HB_STEP_EMIT_GRAD | HB_STEP_SOLE_WRITER)) | (static_cast<uint32_t>(phase) << 8) |
-                          (v.x_lo_zero ? (1u << 16) : 0u);
+                          (v.x_lo_zero ? (1u << 16) : 0u) | (c->xmirror ? (1u << 17) : 0u);
   const bool view_epoch = (&v == &c->epoch);
   if (!c->use_graphs || !graph_ok) return run_phase(c, v, start, rows, flags, eta, nullptr, phase);
   const auto key = std::make_tuple(rows, gflags, view_epoch ? c->view_gen : -c->view_gen, c->prof_on,
@@ -2453,6 +2475,7 @@ int hb_set_weights_all_f64(hb_ctx* c, const double* const* ws) {
   HB_TRY(ctx_check(c));
   if (!ws) return fail(HB_EINVAL, "null weight array");
   HB_TRY(ensure_stage_all(c));
+  c->mirror_valid = false;  // the staging buffer is reused below
   XferClock clk("snapshot");
   for (int l = 0; l < c->L; ++l)
     if (!ws[l]) return fail(HB_EINVAL, "null weights for layer %d", l);
@@ -2493,6 +2516,7 @@ int hb_merge_grads_all_into_f64(hb_ctx* c, double* const* ws, double eta) {
   if (!ws) return fail(HB_EINVAL, "null weight array");
   if (!c->grads_valid) return fail(HB_ESTATE, "no gradient kept: run a step with HB_STEP_EMIT_GRAD first");
   HB_TRY(ensure_stage_all(c));
+  c->mirror_valid = false;  // the staging buffer is reused below
   bool mapped = true;
   std::vector<double*> dws(c->L);
   for (int l = 0; l < c->L; ++l) {
@@ -2652,7 +2676,20 @@ static void xchg_plan_lanes_impl(hb_ctx* c) {
   }
 }
 
-static int xchg_arm(hb_ctx* c, double* const* ws) {
+// host-model fingerprint for the resident mirror: 64 evenly spaced values per layer
+static void mirror_sample(const hb_ctx* c, double* const* ws, std::vector<double>& out) {
+  constexpr int K = 64;
+  out.clear();
+  for (int l = 0; l < c->L; ++l) {
+    const size_t n = static_cast<size_t>(c->d[l + 1]) * c->d[l];
+    for (int k = 0; k < K; ++k) {
+      const double v = reinterpret_cast<volatile const double*>(ws[l])[(n - 1) * k / (K - 1)];
+      out.push_back(v);
+    }
+  }
+}
+
+static int xchg_arm(hb_ctx* c, double* const* ws, uint32_t flags) {
   g_call_t0 = std::chrono::steady_clock::now();
   if (!ws) return fail(HB_EINVAL, "null weight array");
   for (int l = 0; l < c->L; ++l) {
@@ -2693,6 +2730,18 @@ static int xchg_arm(hb_ctx* c, double* const* ws) {
     c->xgen = static_cast<long long>(h >> 1) | 1;  // never 0 (0 = no exchange armed)
   }
   c->xw = cur;
+  // resident mirror: a sole-writer call right after a sole-writer call on the
+  // same arrays, and nobody touched the sampled host values in between
+  c->xsole = (flags & HB_STEP_SOLE_WRITER) != 0 && c->xmode == 0 &&
+             !(getenv("HB_NO_MIRROR") && getenv("HB_NO_MIRROR")[0] == '1');
+  c->xmirror = false;
+  if (c->xsole && c->mirror_valid && c->mirror_gen == c->xgen) {
+    std::vector<double> now;
+    mirror_sample(c, ws, now);
+    c->xmirror = now.size() == c->fp_vals.size() &&
+                 std::memcmp(now.data(), c->fp_vals.data(), now.size() * sizeof(double)) == 0;
+  }
+  c->mirror_valid = false;  // until this call completes
   c->xseq = c->xseq == 0x7fffffff ? 1 : c->xseq + 1;
   *reinterpret_cast<volatile int32_t*>(c->xseq_host) = c->xseq;
   return HB_OK;
@@ -2713,10 +2762,10 @@ static void xfer_account(hb_ctx* c, bool loss) {
   if (c->xmode == 0) h2d += sizeof(int32_t);  // the sequence number the layer flags carry
   for (int l = 0; l < c->L; ++l) {
     const long long n = static_cast<long long>(c->d[l + 1]) * c->d[l];
-    h2d += n * 8;  // snapshot (deep_copy, workers.py:132)
+    if (!c->xmirror) h2d += n * 8;  // snapshot (deep_copy, workers.py:132)
     const bool dev = c->xmode != 0 || (l < static_cast<int>(c->xdma_used.size()) && c->xdma_used[l]);
     if (dev) {
-      h2d += n * 8;  // merge read of the host rows
+      if (!c->xmirror) h2d += n * 8;  // merge read of the host rows
       d2h += n * 8;  // merged rows written back
     } else {
       d2h += n * 4 + static_cast<long long>(sizeof(int32_t));  // fp32 gradient + the layer's flag
@@ -2752,6 +2801,11 @@ static int replica_finish(hb_ctx* c, int rc, int rows, double eta, uint32_t flag
   }
   if (timed) HB_CUDA(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
   xfer_account(c, out_loss != nullptr);
+  if (c->xsole) {  // the staging buffer now equals the host model
+    c->mirror_valid = true;
+    c->mirror_gen = c->xgen;
+    mirror_sample(c, c->xw.data(), c->fp_vals);
+  }
   xmark("done");
   return HB_OK;
 }
@@ -2765,7 +2819,7 @@ static uint32_t replica_flags(hb_ctx* c, uint32_t flags) {
 int hb_replica_step(hb_ctx* c, double* const* ws, int64_t start, int rows, double eta, uint32_t flags,
                     double* out_loss) {
   HB_TRY(ctx_check(c));
-  HB_TRY(xchg_arm(c, ws));
+  HB_TRY(xchg_arm(c, ws, flags));
   XchgGuard g{c};
   const int rc = hb_train_step(c, start, rows, eta, replica_flags(c, flags), nullptr);
   return replica_finish(c, rc, rows, eta, flags, out_loss);
@@ -2774,7 +2828,7 @@ int hb_replica_step(hb_ctx* c, double* const* ws, int64_t start, int rows, doubl
 int hb_replica_begin(hb_ctx* c, double* const* ws, int64_t start, int rows, double eta, uint32_t flags) {
   HB_TRY(ctx_check(c));
   if (c->pend_active) return fail(HB_ESTATE, "a replica step is already in flight");
-  HB_TRY(xchg_arm(c, ws));
+  HB_TRY(xchg_arm(c, ws, flags));
   const int rc = hb_train_step(c, start, rows, eta, replica_flags(c, flags), nullptr);
   if (rc != HB_OK) {
     XchgGuard g{c};
@@ -2800,7 +2854,7 @@ int hb_replica_end(hb_ctx* c, double* out_loss) {
 int hb_replica_step_host_dense(hb_ctx* c, double* const* ws, const float* x, int64_t ld, const int64_t* labels,
                                int rows, double eta, uint32_t flags, double* out_loss) {
   HB_TRY(ctx_check(c));
-  HB_TRY(xchg_arm(c, ws));
+  HB_TRY(xchg_arm(c, ws, flags));
   XchgGuard g{c};
   const int rc = hb_train_step_host_dense(c, x, ld, labels, rows, eta, replica_flags(c, flags), nullptr);
   return replica_finish(c, rc, rows, eta, flags, out_loss);
@@ -2810,7 +2864,7 @@ int hb_replica_step_host_csr(hb_ctx* c, double* const* ws, const int64_t* rowptr
                              const float* val, const int64_t* labels, int rows, double eta, uint32_t flags,
                              double* out_loss) {
   HB_TRY(ctx_check(c));
-  HB_TRY(xchg_arm(c, ws));
+  HB_TRY(xchg_arm(c, ws, flags));
   XchgGuard g{c};
   const int rc =
       hb_train_step_host_csr(c, rowptr, col, val, labels, rows, eta, replica_flags(c, flags), nullptr);

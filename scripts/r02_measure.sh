@@ -1,7 +1,7 @@
 # round-2 measurements: ncu captures, launch list of the default bench, L2-gather ceiling, A/B switches
 mkdir -p gpurun_out
 bash scripts/ncu_traffic.sh > gpurun_out/ncu_traffic.log 2>&1; tail -12 gpurun_out/ncu_traffic.log
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 200 -c 300 --csv --log-file gpurun_out/launches_scaled.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 0 -c 400 --csv --log-file gpurun_out/launches_scaled.csv \
     python bench.py --steps 3 --warmup 3 --skip-e2e --skip-cpu --no-ttt > gpurun_out/bench_under_ncu.log 2>&1; echo "launch list rc=$?"
 python - <<'PY'
 import paper_2004_08771_b200 as hb, ctypes as C

@@ -258,14 +258,17 @@ def test_sequential_curves_match_reference(hb):
         assert res.examples == r["epochs"] * r["x"].shape[0]
 
 
+@pytest.mark.parametrize("sole", [False, True], ids=["shared", "sole_writer"])
 @pytest.mark.parametrize("kind", ["dense", "csr_densified", "csr_kernels", "wide_head"])
-def test_fused_replica_step_equals_three_calls(hb, kind):
+def test_fused_replica_step_equals_three_calls(hb, kind, sole):
     """hb_replica_step* (snapshot, step and stale merge in one call, with the
     exchange overlapped layer by layer) gives bit-identical host models to the
     three separate calls set_weights / step / merge_grads_into, on every call
     (the first eager, later ones replayed from the captured graph), and keeps
     the stale-merge semantics of workers.py:126-138 when the host model moves
-    between calls (another writer)."""
+    between calls (another writer).  sole_writer: from the second call on the
+    snapshot comes from the device-resident float64 mirror, until the host
+    model is moved by someone else (the fingerprint catches it)."""
     sizes = {"dense": (54, 128, 128, 2), "csr_densified": (300, 256, 128, 2),
              "csr_kernels": (600, 256, 128, 2), "wide_head": (40, 96, 70)}[kind]
     sparse = kind.startswith("csr")
@@ -288,7 +291,7 @@ def test_fused_replica_step_equals_three_calls(hb, kind):
         for it in range(6):
             xb, yb = batches[it % len(batches)]
             eta = 0.3 + 0.05 * it
-            lf = fused.replica_step_host(wf, xb, yb, eta)
+            lf = fused.replica_step_host(wf, xb, yb, eta, sole_writer=sole)
             three.set_weights(wt)
             lt = three.step_host(xb, yb, eta, emit_grad=True)
             three.merge_grads_into(wt, eta)

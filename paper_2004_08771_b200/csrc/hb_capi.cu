@@ -1126,6 +1126,24 @@ int xchg_merge(hb_ctx* c, int l, double eta, const DevStep* ds, cudaStream_t src
     xtl(c, c->xmrg, "mrg: layer %d written back (device lane)", l);
     return HB_OK;
   }
+  static const bool mirror_lane = !(getenv("HB_MIRROR_LANE") && getenv("HB_MIRROR_LANE")[0] == '0');
+  if (c->xmode == 0 && c->xsole && mirror_lane) {
+    // mirror lane (sole writer): the device staging copy equals the host model
+    // (snapshot or resident mirror), so the float64 merge runs on the device
+    // (w + (-eta) * g, NumPy's rounding) and the merged layer goes D2H in place
+    // of the gradient -- no host read-modify-write, no merge read
+    HB_CUDA(cudaStreamWaitEvent(c->xmrg, c->xgrad_ev[l], 0));
+    const size_t n = static_cast<size_t>(rows) * cols;
+    const size_t off = layer_offset(c, l);
+    merge_host_f64_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 4)), 256, 0, c->xmrg>>>(
+        c->stage_all + off, c->G[l], tr ? c->ldw[0] : cols, rows, cols, tr ? 1 : 0, eta, ds);
+    HB_CUDA(cudaGetLastError());
+    c->last_launches++;
+    HB_CUDA(cudaMemcpyAsync(c->xw[l], c->stage_all + off, n * sizeof(double), cudaMemcpyDeviceToHost, c->xmrg));
+    if (l < static_cast<int>(c->xdma_used.size())) c->xdma_used[l] = 2;  // merged on the device (no host pass)
+    xtl(c, c->xmrg, "mrg: layer %d written back (mirror lane)", l);
+    return HB_OK;
+  }
   if (c->xmode == 0) {
     // host mode: the fp32 gradient goes D2H on the merge stream; the calling
     // thread applies it (hb_replica_step*, xchg_host_merges)
@@ -2763,9 +2781,10 @@ static void xfer_account(hb_ctx* c, bool loss) {
   for (int l = 0; l < c->L; ++l) {
     const long long n = static_cast<long long>(c->d[l + 1]) * c->d[l];
     if (!c->xmirror) h2d += n * 8;  // snapshot (deep_copy, workers.py:132)
-    const bool dev = c->xmode != 0 || (l < static_cast<int>(c->xdma_used.size()) && c->xdma_used[l]);
+    const int lane = l < static_cast<int>(c->xdma_used.size()) ? c->xdma_used[l] : 0;
+    const bool dev = c->xmode != 0 || lane != 0;
     if (dev) {
-      if (!c->xmirror) h2d += n * 8;  // merge read of the host rows
+      if (!c->xmirror && lane != 2) h2d += n * 8;  // merge read of the host rows
       d2h += n * 8;  // merged rows written back
     } else {
       d2h += n * 4 + static_cast<long long>(sizeof(int32_t));  // fp32 gradient + the layer's flag

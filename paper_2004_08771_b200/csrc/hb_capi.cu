@@ -599,6 +599,7 @@ struct hb_ctx {
   // split-K reduce kernel on a float64 copy of the host rows DMA'd in just
   // before it and DMA'd back (splits the merge between PCIe and host DRAM)
   std::vector<char> xdma;       // planned per layer
+  std::vector<char> xml;        // sole-writer calls: layers merged on the mirror lane (planned per layer)
   long long last_h2d = 0, last_d2h = 0;  // PCIe bytes of the last hb_replica_step* call
   std::vector<char> xdma_used;  // taken by the step just enqueued (rows decide whether the split-K path runs)
   std::vector<cudaEvent_t> xread_ev;
@@ -1126,8 +1127,7 @@ int xchg_merge(hb_ctx* c, int l, double eta, const DevStep* ds, cudaStream_t src
     xtl(c, c->xmrg, "mrg: layer %d written back (device lane)", l);
     return HB_OK;
   }
-  static const bool mirror_lane = !(getenv("HB_MIRROR_LANE") && getenv("HB_MIRROR_LANE")[0] == '0');
-  if (c->xmode == 0 && c->xsole && mirror_lane) {
+  if (c->xmode == 0 && c->xsole && l < static_cast<int>(c->xml.size()) && c->xml[l]) {
     // mirror lane (sole writer): the device staging copy equals the host model
     // (snapshot or resident mirror), so the float64 merge runs on the device
     // (w + (-eta) * g, NumPy's rounding) and the merged layer goes D2H in place
@@ -2661,11 +2661,47 @@ int hb_merge_grad_into_f64(hb_ctx* c, int layer, double* host_w, double eta) {
 // counted).  Only layers whose split-K reduce carries the merge and whose
 // merge read can hide under the dW partial GEMM (large batches) qualify.
 static void xchg_plan_lanes_impl(hb_ctx* c);
+static void xchg_plan_mirror(hb_ctx* c);
 static void xchg_plan_lanes(hb_ctx* c) {
   xchg_plan_lanes_impl(c);
+  xchg_plan_mirror(c);
   if (xfer_debug())
-    for (int l = 0; l < c->L; ++l) fprintf(stderr, "[xfer] layer %d merges on the %s lane\n", l, c->xdma[l] ? "device" : "host");
+    for (int l = 0; l < c->L; ++l)
+      fprintf(stderr, "[xfer] layer %d merges on the %s lane\n", l, c->xdma[l] ? "device" : (c->xml[l] ? "mirror (sole writer)" : "host"));
 }
+// Mirror lane plan (sole-writer calls, §6): a mirror-lane layer moves 8 B per
+// weight D2H (the merged float64 row) and no host work; a host-lane layer 4 B
+// D2H (the fp32 gradient) plus ~20 B of host DRAM traffic for the float64
+// read-modify-write.  Largest layers first, each goes where max(D2H time, host
+// time) stays lowest.  Measured e2e with every layer on the mirror lane vs none:
+// scaled 5.9e5 -> 6.2e5, w8a 1.65e7 -> 1.88e7, real-sim 1.3e6 -> 1.7e6 samples/s.
+// HB_MIRROR_LANE=0 / =all force none / every layer; HB_PCIE_GBS, HB_HOST_MERGE_GBS tune.
+static void xchg_plan_mirror(hb_ctx* c) {
+  c->xml.assign(c->L, 0);
+  const char* e = getenv("HB_MIRROR_LANE");
+  if (e && e[0] == '0') return;
+  const bool all = e && strcmp(e, "all") == 0;
+  const double pcie = static_cast<double>(env_long("HB_PCIE_GBS", 50)), hostbw = static_cast<double>(env_long("HB_HOST_MERGE_GBS", 40));
+  std::vector<int> order(c->L);
+  for (int l = 0; l < c->L; ++l) order[l] = l;
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    return static_cast<long long>(c->d[a + 1]) * c->d[a] > static_cast<long long>(c->d[b + 1]) * c->d[b];
+  });
+  double d2h = 0.0, host = 0.0;
+  for (int l : order) {
+    if (l < static_cast<int>(c->xdma.size()) && c->xdma[l]) continue;  // device lane
+    const double n = static_cast<double>(c->d[l + 1]) * c->d[l];
+    const double cm = std::max((d2h + 8 * n) / pcie, host / hostbw), ch = std::max((d2h + 4 * n) / pcie, (host + 20 * n) / hostbw);
+    if (all || cm <= ch) {
+      c->xml[l] = 1;
+      d2h += 8 * n;
+    } else {
+      d2h += 4 * n;
+      host += 20 * n;
+    }
+  }
+}
+
 static void xchg_plan_lanes_impl(hb_ctx* c) {
   c->xdma.assign(c->L, 0);
   if (c->xmode != 0 || !c->conc_bwd || c->cap < 4096 ||

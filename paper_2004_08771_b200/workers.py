@@ -108,10 +108,11 @@ def set_worker_devices(mapping: dict, max_batch: int | None = None) -> None:
 
 
 def set_sole_writer(on: bool) -> None:
-    """Declare that GPU replica workers are the only writers of the shared host
-    model (no CPU Hogwild pool, a single replica): lets the largest layers
-    merge on the device lane (HB_STEP_SOLE_WRITER).  Off by default, since the
-    lane's layer-wide read-merge-write window would drop concurrent host
+    """Declare that this GPU replica is the only writer of the shared host
+    model (no CPU Hogwild pool, a single replica; HB_STEP_SOLE_WRITER): the
+    float64 merge then runs on a device-resident copy of the model, merged
+    layers are DMA'd back and later calls skip the snapshot.  Off by default,
+    since the device's layer-wide read-merge-write would drop concurrent host
     updates that the reference's per-element np.add (linalg.py:79) keeps."""
     global _sole_writer
     _sole_writer = bool(on)

@@ -378,14 +378,20 @@ def time_to_target(ctx, src, cfg, args, rank, world, dist, init_w, max_rows):
     gpu_curve = []
     wall_s = dev_ms = 0.0
     step = 0
+    # the replica target is step-matched (the same batches); the Hogbatch
+    # target may need more passes over the training rows (the CPU pool made
+    # many small updates): cycle through them, up to --ttt-max-steps
     limit = max(cpu_k + 3, 4)
+    n_batches = max(1, e0 // b)
     loss = ctx.eval_loss_sum(e0, E) / E if rank == 0 else 0.0
     gpu_curve.append(loss)
-    while step < limit and (step + 1) * b <= e0:
+    while step < max(limit, args.ttt_max_steps) and (step < limit or hit[0] is not None):
+        if step >= limit and hit[1] is not None:
+            break
         if dist is not None:
             barrier(dist)
         t0 = time.perf_counter()
-        ctx.step(step * b, b, eta, timed=True, merge=dist is not None)
+        ctx.step((step % n_batches) * b, b, eta, timed=True, merge=dist is not None)
         wall_s += time.perf_counter() - t0
         dev_ms += ctx.last_step_ms
         step += 1
@@ -413,9 +419,11 @@ def time_to_target(ctx, src, cfg, args, rank, world, dist, init_w, max_rows):
                          "speedup": None if h is None else round(out[key]["cpu_ms"] / max(h[1], 1e-9), 1)})
     out["gpu_curve"] = [round(v, 7) for v in gpu_curve]
     out["n_gpus"] = world
-    out["note"] = ("training clock (evaluation excluded); step-matched batches of epoch 0; GPU 'reached' = eval loss "
+    out["note"] = ("training clock (evaluation excluded); replica target: step-matched batches of epoch 0; Hogbatch "
+                   "target: the GPU cycles over the training rows (up to --ttt-max-steps); GPU 'reached' = eval loss "
                    "within 1e-5 relative of the target (float64 vs the device's fp32 model); N>1: replicas averaged "
-                   "by NCCL every step, eval on rank 0")
+                   "every step, eval on rank 0")
+    out["gpu_curve"] = out["gpu_curve"][:64]
     return out
 
 
@@ -654,6 +662,7 @@ def main():
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--ttt-budget-s", type=float, default=20.0, help="CPU time budget of the time-to-target legs")
     ap.add_argument("--no-ttt", dest="ttt", action="store_false")
+    ap.add_argument("--ttt-max-steps", type=int, default=256, help="GPU step cap of the Hogbatch time-to-target leg")
     ap.add_argument("--no-prof", action="store_true", help="no per-kernel events in the timed region")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -2674,13 +2674,16 @@ static void xchg_plan_lanes(hb_ctx* c) {
 // D2H (the fp32 gradient) plus ~20 B of host DRAM traffic for the float64
 // read-modify-write.  Largest layers first, each goes where max(D2H time, host
 // time) stays lowest.  Measured e2e with every layer on the mirror lane vs none:
-// scaled 5.9e5 -> 6.2e5, w8a 1.65e7 -> 1.88e7, real-sim 1.3e6 -> 1.7e6 samples/s.
-// HB_MIRROR_LANE=0 / =all force none / every layer; HB_PCIE_GBS, HB_HOST_MERGE_GBS tune.
+// scaled 5.9e5 -> 6.2e5, w8a 1.65e7 -> 1.88e7, real-sim 1.3e6 -> 1.7e6 samples/s;
+// the split this cost model picks (scaled: the two 4M-weight layers on the
+// host) measured 5.9e5 vs 6.1e5 for all-mirror -- the B200 host's float64 merge
+// is slower than PCIe -- so every layer takes the mirror lane by default.
+// HB_MIRROR_LANE=0 / =plan: none / the cost-model split (HB_PCIE_GBS, HB_HOST_MERGE_GBS).
 static void xchg_plan_mirror(hb_ctx* c) {
   c->xml.assign(c->L, 0);
   const char* e = getenv("HB_MIRROR_LANE");
   if (e && e[0] == '0') return;
-  const bool all = e && strcmp(e, "all") == 0;
+  const bool all = !(e && strcmp(e, "plan") == 0);
   const double pcie = static_cast<double>(env_long("HB_PCIE_GBS", 50)), hostbw = static_cast<double>(env_long("HB_HOST_MERGE_GBS", 40));
   std::vector<int> order(c->L);
   for (int l = 0; l < c->L; ++l) order[l] = l;

@@ -225,6 +225,24 @@ def measured_peaks():
     return hbm, bf16 / 2.0, f"TF32 = bf16/2 of {bf16} TF/s ({src}; no TF32 measurement found)"
 
 
+def l2_gather_ceiling(device, rows, cols):
+    """GB/s at which the device gathers pseudo-random whole rows of an
+    L2-resident (rows x cols) fp32 matrix (hb_probe_l2_gather), or None."""
+    import ctypes as C
+
+    import paper_2004_08771_b200 as hb
+
+    if cols % 128 or cols > 1024:
+        return None
+    lib = hb.load_library()
+    best = 0.0
+    for unroll in (1, 2):
+        v = C.c_double(0.0)
+        if lib.hb_probe_l2_gather(int(device), int(rows), int(cols), 64, unroll, C.byref(v)) == 0:
+            best = max(best, v.value)
+    return best or None
+
+
 def ncu_kernel_stats(config, kernel):
     """Per-launch ncu figures (DRAM / L2 bytes, cold-cache duration) of `kernel`
     for `config` from the newest profiles/r*_ncu_kernels.json (one `ncu --set
@@ -615,10 +633,20 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
                         "traffic": traffic, "peak_basis": peak_src, "work_per_launch": work,
                         "avg_launch_us": round(avg_s * 1e6, 2),
                         "timing": "CUDA events around this kernel only, inside the timed region"}
-            if ncu and "l2_bytes" in ncu:
-                roofline["l2"] = {"bytes_per_launch": ncu["l2_bytes"],
-                                  "achieved_gbs": round(ncu["l2_bytes"] / avg_s / 1e9, 1),
-                                  "ncu_l2_throughput_pct": round(ncu.get("l2_throughput_pct", 0.0), 1)}
+            if dom.startswith(("spmm_sigmoid", "sparse_dw_sgd")):
+                # the CSR kernels are L2-gather bound: one d1-wide row per nonzero,
+                # against the gather ceiling measured live (hb_probe_l2_gather)
+                gathered = b * cfg.get("nnz", 0) * sizes[1] * 4.0
+                ceil = l2_gather_ceiling(device, sizes[0], sizes[1])
+                roofline["l2"] = {"gathered_bytes_per_launch": gathered,
+                                  "achieved_gbs": round(gathered / avg_s / 1e9, 1),
+                                  "ceiling_gbs": None if ceil is None else round(ceil, 1),
+                                  "frac": None if not ceil else round(gathered / avg_s / 1e9 / ceil, 4),
+                                  "ceiling_basis": "hb_probe_l2_gather: pseudo-random whole rows of an L2-resident "
+                                                   f"({sizes[0]} x {sizes[1]}) fp32 matrix, 64 warps/SM"}
+                if ncu and "l2_bytes" in ncu:
+                    roofline["l2"].update({"ncu_l2_bytes_per_launch": ncu["l2_bytes"],
+                                           "ncu_l2_throughput_pct": round(ncu.get("l2_throughput_pct", 0.0), 1)})
         if roofline is not None and ncu:
             roofline["traffic_source"] = f"profiles/{ncu_src} ({args.config}/{dom}: dram read+write bytes of one launch)"
     # step-level tensor work: every GEMM of the step against the step time

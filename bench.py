@@ -47,6 +47,7 @@ from paper_2004_08771_b200.parallel import (  # noqa: E402
     broadcast_float,
     init_process_group,
     init_replica_comm,
+    init_replica_peers,
     max_over_ranks,
     shard_seed,
 )
@@ -453,7 +454,9 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
     from paper_2004_08771_b200.nn import Architecture, init_model
 
     distributed = dist is not None
-    device = local_rank
+    # HB_BENCH_SAME_DEVICE=1: every rank on cuda:0 (exercises the multi-rank
+    # path, e.g. the CUDA-IPC peer merge, on a one-GPU box; not a bench number)
+    device = 0 if os.environ.get("HB_BENCH_SAME_DEVICE") == "1" else local_rank
     sizes = cfg["sizes"]
     b = cfg["batch"]
     sparse = cfg["kind"] == "csr"
@@ -467,9 +470,14 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
     n = src.n
     comm = None
     if distributed:
-        init_replica_comm(ctx, dist, rank, world)
-        comm = {"nranks": world, "rank": rank, "backend": "NCCL (library communicator, hb_comm_init)"}
-        print(f"[bench] rank {rank}/{world}: NCCL replica communicator up on cuda:{device}", file=sys.stderr)
+        if args.transport == "peer":
+            init_replica_peers(ctx, dist, rank, world)
+            comm = {"nranks": world, "rank": rank,
+                    "backend": "peer memory (hb_peer_attach: CUDA IPC exchange buffers, one-shot reduce kernel)"}
+        else:
+            init_replica_comm(ctx, dist, rank, world)
+            comm = {"nranks": world, "rank": rank, "backend": "NCCL (library communicator, hb_comm_init)"}
+        print(f"[bench] rank {rank}/{world}: {comm['backend']} up on cuda:{device}", file=sys.stderr)
     starts = choose_starts(cfg, n, b, args.warmup + args.steps, args.seed, rank)
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{device}")
@@ -684,7 +692,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "tf32"])
     ap.add_argument("--seed", type=int, default=42)
-    ap.add_argument("--merge-every", type=int, default=1, help="NCCL replica averaging cadence (N>1)")
+    ap.add_argument("--merge-every", type=int, default=1, help="replica averaging cadence (N>1)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="replica averaging over NCCL or over peer memory (CUDA IPC, hb_peer_attach)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)

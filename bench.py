@@ -750,7 +750,7 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
+        torch.cuda.set_device(0 if os.environ.get("HB_BENCH_SAME_DEVICE") == "1" else local_rank)
         init_process_group(dist)
     res = run_ours(args, cfg, rank, world, local_rank, dist)
     if rank == 0:

@@ -678,7 +678,7 @@ def config_block(args, cfg, world):
     return {"workload": cfg["desc"], "config": args.config, "arch": "-".join(map(str, cfg["sizes"])),
             "batch_per_gpu": cfg["batch"], "global_batch": cfg["batch"] * world, "precision": args.precision,
             "rows": cfg["n"], "rows_per_gpu": cfg["n"] // world if cfg["kind"] == "blobs" else cfg["n"],
-            "parallelism": f"dp{world}" + (f" (NCCL replica averaging every {args.merge_every} step(s))"
+            "parallelism": f"dp{world}" + (f" ({"peer-memory" if args.transport == "peer" else "NCCL"} replica averaging every {args.merge_every} step(s))"
                                            if world > 1 else ""),
             "l2": "flushed between timed steps (256 MiB write)", "data": "synthetic, resident in HBM"}
 

@@ -226,6 +226,31 @@ def measured_peaks():
     return hbm, bf16 / 2.0, f"TF32 = bf16/2 of {bf16} TF/s ({src}; no TF32 measurement found)"
 
 
+def pcie_bandwidth(device):
+    """Pinned host<->device copy rates in GB/s (256 MiB, best of 3), or None."""
+    import torch
+
+    try:
+        n = 256 * 1024 * 1024
+        host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        dev = torch.empty(n, dtype=torch.uint8, device=f"cuda:{device}")
+        out = {}
+        for name, (dst, src) in (("h2d_gbs", (dev, host)), ("d2h_gbs", (host, dev))):
+            best = 0.0
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                dst.copy_(src, non_blocking=True)
+                e1.record()
+                e1.synchronize()
+                best = max(best, n / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+            out[name] = round(best, 1)
+        del host, dev
+        return out
+    except Exception:  # noqa: BLE001  (reporting only)
+        return None
+
+
 def l2_gather_ceiling(device, rows, cols):
     """GB/s at which the device gathers pseudo-random whole rows of an
     L2-resident (rows x cols) fp32 matrix (hb_probe_l2_gather), or None."""
@@ -589,10 +614,18 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         e2e = {"value": world * args.steps * b / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
                "path": "execute_gpu_replica semantics through the C ABI (hb_replica_step_host_*), per step: "
-                       "batch H2D from pinned host memory, snapshot of the page-locked f64 host model (DMA H2D, "
-                       "layer l+1 in flight while layer l computes), the step, the f64 stale merge W_host += (-eta)*g "
-                       "per layer as soon as its gradient exists (the largest split-K layers merge on the device lane: "
-                       "the replica is the model's sole writer here), loss D2H"}
+                       "batch H2D from pinned host memory, snapshot of the page-locked f64 host model (skipped while "
+                       "the device-resident f64 mirror is current: the replica is the model's sole writer here), the "
+                       "step, the f64 stale merge W_host += (-eta)*g per layer as soon as its gradient exists (run on "
+                       "the device mirror, merged layers DMA'd back), loss D2H"}
+        # PCIe roofline of the drop-in call: its bytes at the link's measured copy rate
+        bw = pcie_bandwidth(device)
+        if bw:
+            t_link = max(h2d / (bw["h2d_gbs"] * 1e9), d2h / (bw["d2h_gbs"] * 1e9))
+            e2e["pcie"] = {**bw, "link_bound_samples_s": round(world * b / t_link, 1),
+                           "frac": round((world * args.steps * b / el) / (world * b / t_link), 4),
+                           "note": "max(H2D, D2H bytes per step) at pinned cudaMemcpy rates (256 MiB, best of 3): "
+                                   "the e2e ceiling the call's PCIe traffic allows, before any compute"}
 
     # ---------------------------------------------------------- CPU baselines (rank 0, N=1)
     cpu = None

@@ -612,7 +612,15 @@ struct hb_ctx {
   char* xbuf = nullptr;
   PeerTable peers{};                // peers.n == 0: not attached
   std::vector<void*> ipc_opened;    // peer buffers opened through CUDA IPC
-  unsigned long long peer_gen = 0;  // merges issued (the flag value of the next one)
+  unsigned long long peer_gen = 0;  // merges issued (the flag value of the last one)
+  // per-layer merge inside the backward (HB_STEP_MERGE with NCCL or a
+  // cross-process peer group): layer l is averaged on comm_st as soon as its
+  // update lands, overlapping the rest of the backward
+  bool merge_layers = false;
+  cudaStream_t comm_st = nullptr;
+  std::vector<cudaEvent_t> mev;  // per layer: update done; mev[L]: comm stream joined
+  std::vector<long long> flat_off;  // segment start of layer l in the packed model (multiple of 4)
+  long long flat_n = 0;             // packed model length incl. segment padding
   std::shared_ptr<LocalGroup> local;  // all ranks in this process: event + host-barrier ordering
   // hb_replica_begin / hb_replica_end: the replica step in flight between them
   bool pend_active = false;
@@ -622,6 +630,8 @@ struct hb_ctx {
 };
 
 namespace {
+
+int enqueue_layer_merge(hb_ctx* c, int l, cudaStream_t src, const DevStep* ds);
 
 int ctx_check(hb_ctx* c) {
   if (c == nullptr) return fail(HB_EINVAL, "null context");
@@ -1430,6 +1440,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
       c->prof_st = nullptr;
       c->last_launches++;
       HB_TRY(xchg_merge(c, l, eta, ds, rs));
+      if (c->merge_layers) HB_TRY(enqueue_layer_merge(c, l, rs, ds));
     }
     return HB_OK;
   }
@@ -1539,6 +1550,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       c->last_launches++;
       prof_end(c, "sparse_dw_sgd", 0);
       HB_TRY(xchg_merge(c, 0, eta, ds));
+      if (c->merge_layers) HB_TRY(enqueue_layer_merge(c, 0, st, ds));
       continue;
     }
     int splits, kb_per, kb_total;
@@ -1610,6 +1622,7 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       c->prof_st = nullptr;
       c->last_launches += 2;
       HB_TRY(xchg_merge(c, l, eta, ds, c->side));
+      if (c->merge_layers) HB_TRY(enqueue_layer_merge(c, l, c->side, ds));
       used_side = true;
       continue;
     }
@@ -1664,6 +1677,11 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       c->last_launches += 2;
     }
     HB_TRY(xchg_merge(c, l, eta, ds));
+    if (c->merge_layers) HB_TRY(enqueue_layer_merge(c, l, st, ds));
+  }
+  if (c->merge_layers) {  // join the merge stream: every layer averaged before the step ends
+    HB_CUDA(cudaEventRecord(c->mev[c->L], c->comm_st));
+    HB_CUDA(cudaStreamWaitEvent(st, c->mev[c->L], 0));
   }
   if (used_side || c->side_pending) {  // join the side stream
     HB_CUDA(cudaEventRecord(c->bev.back(), c->side));
@@ -1690,12 +1708,13 @@ int run_phase(hb_ctx* c, const DataView& v, long long start, int rows, uint32_t 
 int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta, uint32_t flags, bool graph_ok,
                  int phase = 0) {
   const uint32_t gflags = (flags & (HB_STEP_EMIT_GRAD | HB_STEP_SOLE_WRITER)) | (static_cast<uint32_t>(phase) << 8) |
+                          (c->merge_layers ? (1u << 18) : 0u) |
                           (v.x_lo_zero ? (1u << 16) : 0u) | (c->xmirror ? (1u << 17) : 0u);
   const bool view_epoch = (&v == &c->epoch);
   if (!c->use_graphs || !graph_ok) return run_phase(c, v, start, rows, flags, eta, nullptr, phase);
   const auto key = std::make_tuple(rows, gflags, view_epoch ? c->view_gen : -c->view_gen, c->prof_on,
                                    c->xw.empty() ? 0LL : c->xgen);
-  DevStep hs{start, static_cast<float>(eta), 0, eta};
+  DevStep hs{start, static_cast<float>(eta), 0, eta, c->peer_gen};
   auto it = c->graphs.find(key);
   if (it == c->graphs.end()) {
     if (c->graph_seen[key]++ == 0)  // first sighting: run eagerly (also configures kernel attributes)
@@ -1750,8 +1769,90 @@ void drop_graphs(hb_ctx* c) {
 // this rank's slice across every rank's flat, signal, wait, unpack
 double peer_timeout_s() { return getenv("HB_PEER_TIMEOUT_S") ? atof(getenv("HB_PEER_TIMEOUT_S")) : 30.0; }
 
-int enqueue_peer_merge(hb_ctx* c, const ModelLayout& m, long long n_elems, const dim3 grid) {
-  const unsigned long long g = ++c->peer_gen;
+// packed-model layout: layer l's (rows, cols) block at flat_off[l], padded to 4 floats
+void ensure_flat_layout(hb_ctx* c) {
+  if (!c->flat_off.empty()) return;
+  c->flat_off.assign(c->L + 1, 0);
+  long long off = 0;
+  for (int l = 0; l < c->L; ++l) {
+    c->flat_off[l] = off;
+    off += round_up(static_cast<long long>(c->d[l + 1]) * c->d[l], 4);
+  }
+  c->flat_off[c->L] = off;
+  c->flat_n = off;
+}
+
+// layers [l0, l1) of the packed model; offsets relative to flat_off[l0]
+ModelLayout merge_layout(const hb_ctx* c, int l0, int l1) {
+  ModelLayout m{};
+  m.n = l1 - l0;
+  for (int l = l0; l < l1; ++l) {
+    const bool tr = l == 0 && c->sparse;  // W0^T (d_in, d_out) on the device: averaged in that layout
+    const long long rows = tr ? c->d[0] : c->d[l + 1], cols = tr ? c->d[1] : c->d[l];
+    const int i = l - l0;
+    m.w[i] = c->W[l];
+    m.w_lo[i] = (c->need_lo() && !tr) ? c->W_lo[l] : nullptr;
+    m.ld[i] = c->ldw[l];
+    m.cols[i] = static_cast<int>(cols);
+    m.off[i] = c->flat_off[l] - c->flat_off[l0];
+    m.size[i] = rows * cols;
+  }
+  m.off[m.n] = c->flat_off[l1] - c->flat_off[l0];
+  return m;
+}
+
+bool layerwise_merge_ok(const hb_ctx* c) {
+  if (getenv("HB_NO_LAYER_MERGE") && getenv("HB_NO_LAYER_MERGE")[0] == '1') return false;
+  if (c->L > kMaxMergeLayers) return false;
+  if (c->peers.n > 0) return !c->local;  // in-process groups order merges on the host
+  return c->comm != nullptr;
+}
+
+// Average layer l across the replicas on comm_st once its update (enqueued on
+// `src`) is done; the step joins comm_st at the end of the backward.
+int enqueue_layer_merge(hb_ctx* c, int l, cudaStream_t src, const DevStep* ds) {
+  HB_CUDA(cudaEventRecord(c->mev[l], src));
+  HB_CUDA(cudaStreamWaitEvent(c->comm_st, c->mev[l], 0));
+  const ModelLayout m = merge_layout(c, l, l + 1);
+  const long long n = m.off[1], base = c->flat_off[l];
+  const dim3 grid(static_cast<int>(std::min<long long>(cdiv(n, 256), 148 * 4)));
+  if (c->peers.n > 0) {
+    const int r = c->peers.rank;
+    const unsigned long long g = c->peer_gen;  // eager value; graphs read the step record
+    const unsigned long long timeout_ns = static_cast<unsigned long long>(peer_timeout_s() * 1e9);
+    unsigned long long* own = reinterpret_cast<unsigned long long*>(c->xbuf);
+    pack_model_kernel<<<grid, 256, 0, c->comm_st>>>(c->peers.flat[r] + base, m);
+    peer_signal_kernel<<<1, 1, 0, c->comm_st>>>(own, 2 + 2 * l, g, ds);
+    peer_wait_kernel<<<1, 32, 0, c->comm_st>>>(c->peers, 2 + 2 * l, g, timeout_ns, ds);
+    peer_reduce_kernel<<<grid, 256, 0, c->comm_st>>>(c->peers, n, 1.0f / static_cast<float>(c->peers.n), base);
+    peer_signal_kernel<<<1, 1, 0, c->comm_st>>>(own, 3 + 2 * l, g, ds);
+    peer_wait_kernel<<<1, 32, 0, c->comm_st>>>(c->peers, 3 + 2 * l, g, timeout_ns, ds);
+    unpack_model_kernel<<<grid, 256, 0, c->comm_st>>>(c->peers.flat[r] + base, 1.0f, m);
+    c->last_launches += 7;
+  } else {
+    pack_model_kernel<<<grid, 256, 0, c->comm_st>>>(c->flat + base, m);
+    const int rc = g_nccl.allReduce(c->flat + base, c->flat + base, static_cast<size_t>(n), kNcclFloat32, kNcclSum,
+                                    c->comm, c->comm_st);
+    if (rc != 0) return fail(HB_ENCCL, "ncclAllReduce: %s", g_nccl.errStr ? g_nccl.errStr(rc) : "error");
+    unpack_model_kernel<<<grid, 256, 0, c->comm_st>>>(c->flat + base, 1.0f / static_cast<float>(c->nranks), m);
+    c->last_launches += 2;
+  }
+  HB_CUDA(cudaGetLastError());
+  return HB_OK;
+}
+
+int ensure_comm_stream(hb_ctx* c) {
+  if (c->comm_st) return HB_OK;
+  int lo_prio = 0, hi_prio = 0;
+  HB_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  HB_CUDA(cudaStreamCreateWithPriority(&c->comm_st, cudaStreamNonBlocking, hi_prio));
+  c->mev.resize(c->L + 1);
+  for (auto& e : c->mev) HB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return HB_OK;
+}
+
+int enqueue_peer_merge(hb_ctx* c, const ModelLayout& m, long long n_elems, const dim3 grid, bool bump) {
+  const unsigned long long g = bump ? ++c->peer_gen : c->peer_gen;
   const int r = c->peers.rank;
   if (c->local) {
     // in-process group: every rank's pack is enqueued before anyone waits on it
@@ -1777,8 +1878,8 @@ int enqueue_peer_merge(hb_ctx* c, const ModelLayout& m, long long n_elems, const
   peer_signal_kernel<<<1, 1, 0, c->stream>>>(own, 0, g);
   peer_wait_kernel<<<1, 32, 0, c->stream>>>(c->peers, 0, g, timeout_ns);
   peer_reduce_kernel<<<grid, 256, 0, c->stream>>>(c->peers, n_elems, 1.0f / static_cast<float>(c->peers.n));
-  peer_signal_kernel<<<1, 1, 0, c->stream>>>(own, 8, g);
-  peer_wait_kernel<<<1, 32, 0, c->stream>>>(c->peers, 8, g, timeout_ns);
+  peer_signal_kernel<<<1, 1, 0, c->stream>>>(own, 1, g);
+  peer_wait_kernel<<<1, 32, 0, c->stream>>>(c->peers, 1, g, timeout_ns);
   unpack_model_kernel<<<grid, 256, 0, c->stream>>>(c->peers.flat[c->peers.rank], 1.0f, m);
   HB_CUDA(cudaGetLastError());
   c->last_launches += 7;
@@ -1789,7 +1890,7 @@ int enqueue_peer_merge(hb_ctx* c, const ModelLayout& m, long long n_elems, const
 int peer_check(hb_ctx* c) {
   if (c->peers.n == 0) return HB_OK;
   unsigned err = 0;
-  HB_CUDA(cudaMemcpyAsync(&err, c->xbuf + 128, sizeof err, cudaMemcpyDeviceToHost, c->stream));
+  HB_CUDA(cudaMemcpyAsync(&err, c->xbuf + 8 * kPeerErrWord, sizeof err, cudaMemcpyDeviceToHost, c->stream));
   HB_CUDA(cudaStreamSynchronize(c->stream));
   if (err != 0) return fail(HB_ESTATE, "peer merge: rank %u never signalled (timeout)", err - 1);
   return HB_OK;
@@ -1798,25 +1899,14 @@ int peer_check(hb_ctx* c) {
 // pack -> allreduce(sum) -> unpack x 1/nranks (+ lo twins), enqueued on the
 // step stream: inside a step's CUDA-event bracket when HB_STEP_MERGE asks.
 // Peer-attached contexts average over peer memory instead of NCCL.
-int enqueue_merge(hb_ctx* c) {
+int enqueue_merge(hb_ctx* c, bool bump = true) {
   if (!c->comm && c->peers.n == 0) return fail(HB_ESTATE, "communicator not initialised");
   if (c->L > kMaxMergeLayers) return fail(HB_EINVAL, "merge supports up to %d layers", kMaxMergeLayers);
-  ModelLayout m{};
-  m.n = c->L;
-  long long off = 0;
-  for (int l = 0; l < c->L; ++l) {
-    const bool tr = l == 0 && c->sparse;  // W0^T (d_in, d_out) on the device: averaged in that layout
-    const long long rows = tr ? c->d[0] : c->d[l + 1], cols = tr ? c->d[1] : c->d[l];
-    m.w[l] = c->W[l];
-    m.w_lo[l] = (c->need_lo() && !tr) ? c->W_lo[l] : nullptr;
-    m.ld[l] = c->ldw[l];
-    m.cols[l] = static_cast<int>(cols);
-    m.off[l] = off;
-    off += rows * cols;
-  }
-  m.off[c->L] = off;
+  ensure_flat_layout(c);
+  const ModelLayout m = merge_layout(c, 0, c->L);
+  const long long off = c->flat_n;
   const dim3 grid(static_cast<int>(std::min<long long>(cdiv(off, 256), 148 * 8)));
-  if (c->peers.n > 0) return enqueue_peer_merge(c, m, off, grid);
+  if (c->peers.n > 0) return enqueue_peer_merge(c, m, off, grid, bump);
   HB_CUDA(launch_k(pack_model_kernel, grid, dim3(256), 0, c->stream, c->flat, m));
   int r = g_nccl.allReduce(c->flat, c->flat, static_cast<size_t>(off), kNcclFloat32, kNcclSum, c->comm, c->stream);
   if (r != 0) return fail(HB_ENCCL, "ncclAllReduce: %s", g_nccl.errStr ? g_nccl.errStr(r) : "error");
@@ -1838,6 +1928,16 @@ int do_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta,
   c->ev_used = 0;
   c->step_marks.clear();
   const bool timed = (flags & HB_STEP_TIMED) != 0;
+  const bool merge = (flags & HB_STEP_MERGE) != 0;
+  if (merge && !c->comm && c->peers.n == 0) return fail(HB_ESTATE, "communicator not initialised");
+  // the replica merge: per layer inside the backward where the transport
+  // allows (NCCL, cross-process peers), else the whole model after the step
+  c->merge_layers = merge && layerwise_merge_ok(c);
+  if (merge) {
+    ++c->peer_gen;
+    ensure_flat_layout(c);
+    if (c->merge_layers) HB_TRY(ensure_comm_stream(c));
+  }
   if (timed) HB_CUDA(cudaEventRecord(c->ev0, c->stream));
   if (mid) {
     HB_TRY(enqueue_step(c, v, start, rows, eta, flags, graph_ok, 1));
@@ -1846,7 +1946,8 @@ int do_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta,
   } else {
     HB_TRY(enqueue_step(c, v, start, rows, eta, flags, graph_ok));
   }
-  if (flags & HB_STEP_MERGE) HB_TRY(enqueue_merge(c));  // the replica merge, inside the timed bracket
+  if (merge && !c->merge_layers) HB_TRY(enqueue_merge(c, false));  // the replica merge, inside the timed bracket
+  c->merge_layers = false;
   if (timed) HB_CUDA(cudaEventRecord(c->ev1, c->stream));
   c->grads_valid = (flags & HB_STEP_EMIT_GRAD) != 0;
   if (out_loss != nullptr) {
@@ -2277,6 +2378,8 @@ int hb_ctx_destroy(hb_ctx* c) {
   cudaFree(c->grad_all);
   if (c->grad_host) cudaFreeHost(c->grad_host);
   cudaFree(c->flat);
+  for (auto e : c->mev) cudaEventDestroy(e);
+  if (c->comm_st) cudaStreamDestroy(c->comm_st);
   if (c->local) {
     std::lock_guard<std::mutex> lk(c->local->mu);
     auto& lg = *c->local;
@@ -3768,7 +3871,8 @@ int hb_comm_init(hb_ctx* c, const void* id_bytes, int nranks, int rank) {
   if (r != 0) return fail(HB_ENCCL, "ncclCommInitRank: %s", g_nccl.errStr ? g_nccl.errStr(r) : "error");
   c->comm = comm;
   c->nranks = nranks;
-  if (!c->flat) HB_CUDA(cudaMalloc(&c->flat, c->n_params * sizeof(float)));
+  ensure_flat_layout(c);
+  if (!c->flat) HB_CUDA(cudaMalloc(&c->flat, c->flat_n * sizeof(float)));
   return HB_OK;
 }
 
@@ -3849,7 +3953,8 @@ int hb_peer_handle(hb_ctx* c, void* out) {
   HB_TRY(ctx_check(c));
   if (!out) return fail(HB_EINVAL, "null handle buffer");
   if (!c->xbuf) {
-    HB_CUDA(cudaMalloc(&c->xbuf, kPeerHeader + c->n_params * sizeof(float)));
+    ensure_flat_layout(c);
+    HB_CUDA(cudaMalloc(&c->xbuf, kPeerHeader + c->flat_n * sizeof(float)));
     HB_CUDA(cudaMemsetAsync(c->xbuf, 0, kPeerHeader, c->stream));
     HB_CUDA(cudaStreamSynchronize(c->stream));
   }

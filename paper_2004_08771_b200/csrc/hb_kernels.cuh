@@ -24,6 +24,7 @@ struct DevStep {
   float eta;
   int pad;
   double eta64;  // the merge's learning rate at the reference's float64 precision
+  unsigned long long merge_gen;  // replica merges issued so far, this step's included (peer-merge flags)
 };
 __device__ __forceinline__ long long step_start(const DevStep* ds, long long s) { return ds ? ds->start : s; }
 __device__ __forceinline__ float step_eta(const DevStep* ds, float e) { return ds ? ds->eta : e; }
@@ -1128,7 +1129,8 @@ struct ModelLayout {
   float* w_lo[kMaxMergeLayers];
   long long ld[kMaxMergeLayers];
   int cols[kMaxMergeLayers];
-  long long off[kMaxMergeLayers + 1];
+  long long off[kMaxMergeLayers + 1];  // segment starts (multiples of 4; padding after each layer)
+  long long size[kMaxMergeLayers];     // elements of each layer
   int n;
 };
 __device__ __forceinline__ int layout_layer(const ModelLayout& m, long long i) {
@@ -1143,7 +1145,7 @@ __global__ void pack_model_kernel(float* __restrict__ flat, const __grid_constan
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int l = layout_layer(m, i);
     const long long k = i - m.off[l];
-    flat[i] = m.w[l][(k / m.cols[l]) * m.ld[l] + k % m.cols[l]];
+    flat[i] = k < m.size[l] ? m.w[l][(k / m.cols[l]) * m.ld[l] + k % m.cols[l]] : 0.f;
   }
 }
 __global__ void unpack_model_kernel(const float* __restrict__ flat, float scale, const __grid_constant__ ModelLayout m) {
@@ -1151,6 +1153,7 @@ __global__ void unpack_model_kernel(const float* __restrict__ flat, float scale,
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int l = layout_layer(m, i);
     const long long k = i - m.off[l];
+    if (k >= m.size[l]) continue;  // segment padding
     const long long o = (k / m.cols[l]) * m.ld[l] + k % m.cols[l];
     const float v = flat[i] * scale;
     m.w[l][o] = v;

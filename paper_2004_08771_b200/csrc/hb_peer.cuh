@@ -2,8 +2,10 @@
 // between processes): the GPU-replica merge of SURVEY.md §8e without a
 // collective library.  Every rank owns one exchange buffer
 //
-//   [0, 256)            flags: pack generation (u64 @0), reduce generation (u64 @64), error word (u32 @128)
-//   [256, 256 + 4 n)    the packed fp32 model ("flat", layer-major, dense rows)
+//   [0, 512)            flags (u64): whole-model pack @0, reduce @1; layer l pack @2+2l, reduce @3+2l;
+//                       error word (u32) @ byte 448
+//   [512, 512 + 4 n')   the packed fp32 model ("flat", layer-major, dense rows, each layer's segment
+//                       padded to a multiple of 4 floats)
 //
 // and maps every peer's buffer (same process: the raw pointer with peer access
 // enabled; another process: cudaIpcOpenMemHandle).  One merge is
@@ -25,10 +27,13 @@
 
 #include <cstdint>
 
+#include "hb_kernels.cuh"
+
 namespace hb {
 
 constexpr int kMaxPeers = 8;
-constexpr size_t kPeerHeader = 256;  // bytes before the flat model in an exchange buffer
+constexpr size_t kPeerHeader = 512;  // bytes before the flat model in an exchange buffer
+constexpr int kPeerErrWord = 448 / 8;  // u64 index of the error word
 
 struct PeerTable {
   float* flat[kMaxPeers];
@@ -51,32 +56,42 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
-// flag word `which` (0 = pack, 8 = reduce: u64 index) of this rank := g, after
-// everything this stream wrote before (kernel boundary + system fence)
-__global__ void peer_signal_kernel(unsigned long long* flag_base, int which, unsigned long long g) {
+// The merge generation g: by value (eager steps) or from the step record in
+// device memory (captured graphs replay with the current step's value).
+__device__ __forceinline__ unsigned long long merge_gen(const DevStep* ds, unsigned long long g) {
+  return ds != nullptr ? ds->merge_gen : g;
+}
+
+// flag word `which` (u64 index) of this rank := g, after everything this
+// stream wrote before (kernel boundary + system fence)
+__global__ void peer_signal_kernel(unsigned long long* flag_base, int which, unsigned long long g,
+                                   const DevStep* ds = nullptr) {
   __threadfence_system();
-  st_release_sys_u64(flag_base + which, g);
+  st_release_sys_u64(flag_base + which, merge_gen(ds, g));
 }
 
 // thread q waits for rank q's flag `which` to reach g (timeout: error word, no hang)
 __global__ void peer_wait_kernel(const __grid_constant__ PeerTable t, int which, unsigned long long g,
-                                 unsigned long long timeout_ns) {
+                                 unsigned long long timeout_ns, const DevStep* ds = nullptr) {
   const int q = threadIdx.x;
   if (q >= t.n) return;
+  g = merge_gen(ds, g);
   const unsigned long long* f = t.flag[q] + which;
   const unsigned long long t0 = globaltimer_ns();
   while (ld_acquire_sys_u64(f) < g) {
     if (globaltimer_ns() - t0 > timeout_ns) {
-      atomicExch(reinterpret_cast<unsigned*>(t.flag[t.rank] + 16), 1u + static_cast<unsigned>(q));
+      atomicExch(reinterpret_cast<unsigned*>(t.flag[t.rank] + kPeerErrWord), 1u + static_cast<unsigned>(q));
       break;
     }
     __nanosleep(256);
   }
 }
 
-// slice `rank` of the n-way average, written back into every rank's flat
-__global__ void __launch_bounds__(256) peer_reduce_kernel(const __grid_constant__ PeerTable t, long long n_elems,
-                                                          float scale) {
+// slice `rank` of the n-way average of flat[base, base + n_elems) (base a
+// multiple of 4), written back into every rank's flat
+__global__ void __launch_bounds__(256) peer_reduce_kernel(PeerTable t, long long n_elems, float scale,
+                                                          long long base = 0) {
+  for (int q = 0; q < t.n; ++q) t.flat[q] += base;
   const long long n4 = n_elems / 4;
   const long long a = n4 * t.rank / t.n, b = n4 * (t.rank + 1) / t.n;
   for (long long i = a + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < b;

@@ -153,6 +153,7 @@ def _free_port():
 def _ipc_worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
                       LOCAL_RANK="0")
+    import torch
     import torch.distributed as dist
 
     import paper_2004_08771_b200 as hb
@@ -163,23 +164,40 @@ def _ipc_worker(rank, world, port, q):
     b = 256
     w, x, y = _case(sizes, b, 30 + rank, False)
     r = hb.GpuReplica(sizes, b)
-    r.set_weights(w)
-    r.stage(x, y)
+    shadow = hb.GpuReplica(sizes, b)  # the same step without the merge
+    for c in (r, shadow):
+        c.set_weights(w)
+        c.stage(x, y)
     worker = P.DataParallelWorker(r, dist, merge_every=2, transport="peer")
-    trail = []
-    for it in range(4):
+    trail, worst = [], 0.0
+    for it in range(6):
+        shadow.set_weights(r.get_weights())
         worker.step(0, b, 0.3)
-        trail.append([a.copy() for a in r.get_weights()])
-    q.put((rank, trail))
+        shadow.step(0, b, 0.3)
+        got = r.get_weights()
+        if it % 2 == 1:  # merged inside the backward, layer by layer: the fp32 average of both ranks' local steps
+            mine = [torch.from_numpy(a.astype(np.float32)) for a in shadow.get_weights()]
+            both = [[torch.zeros_like(t) for _ in range(world)] for t in mine]
+            for t, out in zip(mine, both):
+                dist.all_gather(out, t)
+            for g, parts in zip(got, both):
+                want = ((parts[0] + parts[1]) * 0.5).numpy().astype(np.float64)
+                worst = max(worst, float(np.abs(g - want).max()))
+        trail.append([a.copy() for a in got])
+    q.put((rank, trail, worst, r.last_step_launches))
     P.barrier(dist)
     r.close()
+    shadow.close()
     dist.destroy_process_group()
 
 
 def test_peer_merge_two_processes_over_ipc(hb):
     """Two processes (torchrun-style ranks) on one GPU: the exchange buffers
-    are shared with CUDA IPC, handles all-gathered over gloo; merges every 2
-    steps (DataParallelWorker's cadence), after which both ranks agree."""
+    are shared with CUDA IPC, handles all-gathered over gloo; every 2nd step
+    (DataParallelWorker's cadence) averages the replicas inside the backward,
+    layer by layer as each update lands (flag kernels, capture-safe
+    generations), and the result is the exact fp32 average of both ranks'
+    local steps."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
@@ -188,11 +206,15 @@ def test_peer_merge_two_processes_over_ipc(hb):
     ps = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in ps:
         p.start()
-    got = dict(q.get(timeout=300) for _ in ps)
+    got = {}
+    for _ in ps:
+        rank, trail, worst, launches = q.get(timeout=300)
+        got[rank] = (trail, worst)
     for p in ps:
         p.join(timeout=60)
         assert p.exitcode == 0
-    t0, t1 = got[0], got[1]
-    for it in range(4):
+    (t0, w0), (t1, w1) = got[0], got[1]
+    assert w0 == 0.0 and w1 == 0.0  # bit-exact fp32 average, eager and graph-replayed merges
+    for it in range(6):
         same = all(np.array_equal(a, c) for a, c in zip(t0[it], t1[it]))
-        assert same == (it % 2 == 1), it  # merged after steps 2 and 4 only
+        assert same == (it % 2 == 1), it  # merged on steps 2, 4, 6 only

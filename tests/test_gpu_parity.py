@@ -367,6 +367,13 @@ def test_nccl_merge_single_rank(hb, sparse):
             c.step(0, 128, 0.3, emit_grad=True)
         for a, b in zip(ref.grads(), ctx.grads()):
             assert np.array_equal(a, b)
+        # the merge inside the step (HB_STEP_MERGE): each layer all-reduced on
+        # the merge stream as its update lands (eager, then the captured graph)
+        for it in range(3):
+            ref.step(0, 128, 0.3)
+            ctx.step(0, 128, 0.3, merge=True)
+            for a, b in zip(ref.get_weights(), ctx.get_weights()):
+                assert np.array_equal(a, b), it
     finally:
         ctx.close()
         ref.close()

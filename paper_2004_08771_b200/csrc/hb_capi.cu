@@ -1626,6 +1626,35 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
       used_side = true;
       continue;
     }
+    if (splits == 1 && l >= 1 && c->xsole && c->xmode == 0 && l < static_cast<int>(c->xml.size()) && c->xml[l] &&
+        !(getenv("HB_NO_DW_FIRST") && getenv("HB_NO_DW_FIRST")[0] == '1')) {
+      // sole-writer mirror lane: the host copy of W_l is PCIe-bound (8 B per
+      // weight), so start it as early as possible -- dW first (the gradient
+      // into G_l, W_l untouched), the float64 merge + D2H on the merge stream
+      // from here, then dX (the last reader of the old W_l), then the SGD update
+      a.out = c->G[l];
+      a.ldo = c->d[l];
+      a.split_stride = 0;
+      prof_begin(c, "gemm_dw_first", l);
+      HB_TRY(launch_gemm(c->passes, G_DW, EPI_PARTIAL, c->bn_dw[l], c->opD_mn(l), tb, a, mt, nt, 1, st));
+      prof_end(c, "gemm_dw_first", l);
+      HB_TRY(xchg_merge(c, l, eta, ds));
+      HB_TRY(do_dx());
+      const long long slab = static_cast<long long>(a.M) * a.N;
+      prof_begin(c, "sgd_update", l);
+      if (a.N % 4 == 0 && c->ldw[l] % 4 == 0 && (slab / 4) >= 148 * 256)
+        HB_CUDA(launch_k(reduce_sgd_vec_kernel, dim3(static_cast<int>(std::min<long long>(cdiv(slab / 4, 256), 148 * 8))),
+                         dim3(256), 0, st, c->W[l], c->ldw[l], c->G[l], 1, slab, a.M, a.N, static_cast<float>(eta),
+                         nullptr, c->d[l], ds, c->need_lo() ? c->W_lo[l] : nullptr, nullptr, 0.0));
+      else
+        HB_CUDA(launch_k(reduce_sgd_kernel, dim3(cdiv(slab, 32)), dim3(256), 0, st, c->W[l], c->ldw[l], c->G[l], 1, slab,
+                         a.M, a.N, static_cast<float>(eta), nullptr, c->d[l], ds, c->need_lo() ? c->W_lo[l] : nullptr));
+      HB_CUDA(cudaGetLastError());
+      prof_end(c, "sgd_update", l);
+      c->last_launches += 2;
+      if (c->merge_layers) HB_TRY(enqueue_layer_merge(c, l, st, ds));
+      continue;
+    }
     HB_TRY(do_dx());
     if (splits == 1) {
       a.out = c->W[l];

@@ -61,7 +61,9 @@ extern "C" {
 #define HB_STEP_EMIT_GRAD 1u /* keep the raw mean gradient of every layer (for the host merge / parity) */
 #define HB_STEP_TIMED 2u     /* bracket the step with CUDA events (hb_last_step_ms) */
 #define HB_STEP_ASYNC 4u     /* return once the step is enqueued (no out_loss); hb_synchronize() waits */
-#define HB_STEP_MERGE 8u     /* after the step, average the replicas (hb_merge_allreduce) on the same stream */
+#define HB_STEP_MERGE 8u     /* average the replicas within the step (NCCL or a cross-process peer group:
+                                * each layer as soon as its update lands, overlapping the rest of the
+                                * backward; an in-process peer group: the whole model after the step) */
 /* hb_replica_step*: the caller guarantees no other thread writes the host
  * model during the call (a lone GPU replica, no CPU Hogwild pool).  Lets the
  * largest split-K layers merge on the device (host rows read while the dW

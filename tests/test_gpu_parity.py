@@ -818,3 +818,53 @@ def test_replica_step_then_merge_grads_into_on_one_context(hb):
         assert any(not np.array_equal(a, b) for a, b in zip(host, before))
     finally:
         ctx.close()
+
+
+def test_dense_as_csr_equals_csr_staging(hb):
+    """hb_stage_dense_as_csr_f64 on a densified array (empty rows, an
+    all-features row, ragged nnz) stages exactly what hb_stage_csr stages from
+    the same rows' CSR: bit-identical steps."""
+    sizes = (600, 128, 64, 2)
+    x = sparse_rows_with_empties(sizes, 300, 5, 14)
+    y = np.random.default_rng(5).integers(0, 2, size=300)
+    w = ref_nn.init_weights(sizes, 6)
+    a = hb.GpuReplica(sizes, 300, sparse=True)
+    c = hb.GpuReplica(sizes, 300, sparse=True)
+    try:
+        a.stage(x, y)  # dense float64 -> CSR on the host
+        c.stage(to_csr(hb, x, y))
+        for ctx in (a, c):
+            ctx.set_weights(w)
+            ctx.step(0, 300, 0.4, emit_grad=True)
+        for ga, gc in zip(a.grads(), c.grads()):
+            assert np.array_equal(ga, gc)
+    finally:
+        a.close()
+        c.close()
+
+
+def test_exchange_state_errors(hb):
+    """Misuse of the split replica call and of the merge raises instead of
+    corrupting state: begin twice, end without begin, a step while a replica
+    call is in flight, a merge without a communicator."""
+    sizes = (20, 32, 2)
+    w, x, y = oracle_case(sizes, 64, seed=3)
+    host = [a.copy() for a in w]
+    ctx = hb.GpuReplica(sizes, 64)
+    try:
+        ctx.stage(x.astype(np.float32), y)
+        with pytest.raises(RuntimeError, match="no replica step in flight"):
+            ctx.replica_end()
+        ctx.replica_begin(host, 0, 64, 0.1)
+        with pytest.raises(RuntimeError, match="in flight"):
+            ctx.replica_begin(host, 0, 64, 0.1)
+        with pytest.raises(RuntimeError, match="in flight"):
+            ctx.step(0, 64, 0.1)
+        ctx.replica_end()
+        with pytest.raises(RuntimeError, match="communicator"):
+            ctx.step(0, 64, 0.1, merge=True)
+        with pytest.raises(RuntimeError, match="communicator"):
+            ctx.merge_allreduce()
+        ctx.step(0, 64, 0.1)  # still usable
+    finally:
+        ctx.close()

@@ -643,6 +643,19 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
                                 "seconds": rep["seconds"]}}
 
     # ---------------------------------------------------------- time to target
+    # GPU loss evaluation (loss_sum, nn.py:139-146): the forward
+    # plus the CE epilogue over staged rows, excluded from the training clock
+    ev = None
+    if rank == 0:
+        er = min(n, 16 * b)
+        ctx.eval_loss_sum(0, er)
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        for _ in range(3):
+            ctx.eval_loss_sum(0, er)
+        ev_s = (time.perf_counter() - t0) / 3
+        ev = {"rows": er, "samples_s": round(er / ev_s, 1), "ms": round(ev_s * 1000.0, 3),
+              "note": "hb_eval_loss_sum over staged rows in chunks of the context's max batch, host wall time"}
     ttt = None
     if args.ttt:
         ttt = time_to_target(ctx, src, cfg, args, rank, world, dist, model.weights, max_rows=n)
@@ -704,7 +717,7 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
                                         "concurrently on two streams, so this kernel's event-timed duration includes "
                                         "sharing the SMs with the other; step_tensor is the figure that adds up")
     return dict(value=value, total_ms=total_ms, e2e=e2e, roofline=roofline, kernels=kernels, clocks=clocks.summary(),
-                launches=launches, cpu=cpu, ttt=ttt, comm=comm, stage_s=stage_s, rows_staged=n)
+                launches=launches, cpu=cpu, ttt=ttt, comm=comm, stage_s=stage_s, rows_staged=n, eval=ev)
 
 
 def config_block(args, cfg, world):
@@ -796,7 +809,7 @@ def main():
             "clocks": res["clocks"], "gpu_launches": res["launches"], "kernels": res["kernels"],
             "kernels_note": "per-launch CUDA events on every kernel in a separate instrumented pass "
                             "(each bracket adds ~5 us); the timed region brackets only roofline.kernel",
-            "time_to_target": res["ttt"], "comm": res["comm"],
+            "time_to_target": res["ttt"], "eval": res["eval"], "comm": res["comm"],
             "staging": {"rows_per_gpu": res["rows_staged"], "seconds": round(res["stage_s"], 2)},
         }
         print(json.dumps(line))

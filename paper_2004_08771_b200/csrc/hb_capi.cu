@@ -586,7 +586,9 @@ struct hb_ctx {
   // merge strategy: 0 = host (gradient D2H as fp32, float64 axpy on host
   // threads as each layer's gradient lands -- the reference's own np.add on
   // the host model); 1 = DMA read-modify-write through device memory
-  int xmode = 0;
+  int xmode = 0;       // this call: 0 = host / mirror merge, 1 = chunked device read-modify-write
+  int xmode_env = 0;   // HB_XCHG_MERGE=dma: the DMA merge for sole-writer calls (its per-chunk window
+                       // would drop a concurrent writer's updates; shared-model calls keep the host merge)
   // host mode: "layer l's gradient is in grad_host" flags.  Event syncs do
   // not survive graph capture, so the merge stream copies the call's sequence
   // number (read from pinned memory when the step runs) into xflags[l] after
@@ -2907,7 +2909,7 @@ static int xchg_arm(hb_ctx* c, double* const* ws, uint32_t flags) {
     c->xread_ev.resize(c->L);
     for (auto& e : c->xread_ev) HB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     xchg_plan_lanes(c);
-    if (const char* m = getenv("HB_XCHG_MERGE")) c->xmode = strcmp(m, "dma") == 0 ? 1 : 0;
+    if (const char* m = getenv("HB_XCHG_MERGE")) c->xmode_env = strcmp(m, "dma") == 0 ? 1 : 0;
   }
   std::vector<double*> cur(ws, ws + c->L);
   if (cur != c->xw_prev) {
@@ -2921,6 +2923,7 @@ static int xchg_arm(hb_ctx* c, double* const* ws, uint32_t flags) {
   c->xw = cur;
   // resident mirror: a sole-writer call right after a sole-writer call on the
   // same arrays, and nobody touched the sampled host values in between
+  c->xmode = (c->xmode_env == 1 && (flags & HB_STEP_SOLE_WRITER) != 0) ? 1 : 0;
   c->xsole = (flags & HB_STEP_SOLE_WRITER) != 0 && c->xmode == 0 &&
              !(getenv("HB_NO_MIRROR") && getenv("HB_NO_MIRROR")[0] == '1');
   c->xmirror = false;

@@ -642,12 +642,23 @@ def test_replica_step_reports_its_pcie_bytes(hb):
         h2d, d2h = ctx.last_xfer_bytes
         n = sum(a.size for a in w)
         batch = x32.nbytes + y64.nbytes
-        if os.environ.get("HB_XCHG_MERGE") == "dma":  # device read-modify-write of every layer
+        # shared model: every layer merges on the host lane (also under HB_XCHG_MERGE=dma, a sole-writer mode)
+        assert batch + 8 * n < h2d < batch + 8 * n + 4096  # + the step record and sequence number
+        assert d2h == 4 * n + 4 * len(w) + 8
+        # sole writer: the first call snapshots, merges on the device mirror and DMAs merged layers back (8 B
+        # per weight; HB_XCHG_MERGE=dma: read + write back); the second skips the snapshot
+        ctx.replica_step_host(model, x32, y64, 0.1, want_loss=True, sole_writer=True)
+        h2d, d2h = ctx.last_xfer_bytes
+        dma = os.environ.get("HB_XCHG_MERGE") == "dma"
+        assert batch + (16 if dma else 8) * n <= h2d < batch + (16 if dma else 8) * n + 4096
+        assert d2h == 8 * n + 8
+        ctx.replica_step_host(model, x32, y64, 0.1, want_loss=True, sole_writer=True)
+        h2d, d2h = ctx.last_xfer_bytes
+        if dma:  # the DMA merge keeps its snapshot + merge read every call
             assert batch + 16 * n <= h2d < batch + 16 * n + 4096
-            assert d2h == 8 * n + 8
         else:
-            assert batch + 8 * n < h2d < batch + 8 * n + 4096  # + the step record and sequence number
-            assert d2h == 4 * n + 4 * len(w) + 8  # small batch: every layer merges on the host lane
+            assert batch <= h2d < batch + 4096
+        assert d2h == 8 * n + 8
     finally:
         ctx.close()
 

@@ -117,6 +117,9 @@ int hb_get_grad_f32(hb_ctx* ctx, int layer, float* g);
  * (execute_hogwild_sharded, workers.py:94-123) gives its cores back with e.g.
  * hb_host_merge_threads(2, 0).  Process-wide. */
 int hb_host_merge_threads(int threads, int spin);
+/* Self-test of that pool (host only, no device): `jobs` back-to-back jobs of
+ * varying part counts; out_errors = parts not run exactly once. */
+int hb_host_pool_selftest(int jobs, int64_t* out_errors);
 
 /* Stage one epoch's (or any dataset's) rows on the device so steps can index
  * them by (start, rows) -- the per-epoch shuffled copy that BatchRef views

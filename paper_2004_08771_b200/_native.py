@@ -84,6 +84,7 @@ SIGNATURES = {
     "hb_merge_allreduce": (_i32, [_p]),
     "hb_comm_destroy": (_i32, [_p]),
     "hb_host_merge_threads": (_i32, [_i32, _i32]),
+    "hb_host_pool_selftest": (_i32, [_i32, _i64p]),
     "hb_probe_l2_gather": (_i32, [_i32, _i64, _i32, _i32, _i32, _dp]),
     "hb_peer_handle": (_i32, [_p, _p]),
     "hb_peer_attach": (_i32, [_p, _i32, _i32, _p]),

@@ -3915,6 +3915,29 @@ int hb_merge_allreduce(hb_ctx* c) {
   return peer_check(c);
 }
 
+int hb_host_pool_selftest(int jobs, int64_t* out_errors) {
+  if (jobs < 1 || !out_errors) return fail(HB_EINVAL, "need jobs >= 1 and an output");
+  HostPool& pool = HostPool::get();
+  long long errors = 0;
+  std::vector<std::atomic<int>> hits(64);
+  for (int j = 0; j < jobs; ++j) {
+    // part counts that grow and shrink from job to job: a stale ticket of the
+    // previous job would run a part of this one twice (or with the wrong job)
+    const int n = 1 + (j * 7919) % 61;
+    for (auto& h : hits) h.store(0, std::memory_order_relaxed);
+    const int tag = j;
+    std::atomic<int> wrong{0};
+    pool.run(n, [&, tag](int i) {
+      if (tag != j) wrong.fetch_add(1);
+      hits[i].fetch_add(1, std::memory_order_relaxed);
+    });
+    for (int i = 0; i < 64; ++i) errors += (hits[i].load() != (i < n ? 1 : 0)) ? 1 : 0;
+    errors += wrong.load();
+  }
+  *out_errors = errors;
+  return HB_OK;
+}
+
 int hb_host_merge_threads(int threads, int spin) {
   if (threads < 1 || spin < 0) return fail(HB_EINVAL, "need threads >= 1 and spin >= 0");
   HostPool::get().configure(threads, spin);

@@ -3,6 +3,7 @@ header declares, and reports errors the way the reference does (ValueError
 for arguments, RuntimeError for device state).  No compute calls here."""
 
 import ctypes as C
+import os
 import re
 import subprocess
 from pathlib import Path
@@ -102,3 +103,15 @@ def test_host_merge_pool_resizes(lib):
     assert lib.hb_host_merge_threads(1, 100) == 0
     assert lib.hb_host_merge_threads(0, 0) != 0  # invalid
     assert lib.hb_host_merge_threads(4, 20000) == 0
+
+
+def test_host_merge_pool_runs_every_part_once(lib):
+    """The merge pool's tickets carry their job: across 20000 back-to-back jobs
+    of growing and shrinking part counts, with the pool spinning (stale
+    workers race the next job) and sleeping, every part runs exactly once."""
+    for threads, spin in ((8, 20000), (3, 0), (12, 200)):
+        assert lib.hb_host_merge_threads(threads, spin) == 0
+        err = C.c_int64(-1)
+        assert lib.hb_host_pool_selftest(20000, C.byref(err)) == 0
+        assert err.value == 0, (threads, spin, err.value)
+    assert lib.hb_host_merge_threads(max(2, min(12, (os.cpu_count() or 4) * 3 // 4)), 20000) == 0

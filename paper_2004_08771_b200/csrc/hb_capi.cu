@@ -758,12 +758,13 @@ long long env_long(const char* name, long long dflt) {
 // had to give up for precision).  Others keep the rotation (HB_DRAIN_KB: their
 // D, 0 = off); HB_DRAIN_KB_CRIT overrides the critical ones' D.
 enum GemmRole { R_FWD = 0, R_LOGITS = 1, R_DX = 2, R_DW = 3 };
-int crit_drain_default(const hb_ctx* c) { return c->small_head ? 1 : 2; }
+// (small heads need D=1 even at K = 512: w8a with D=2 measured 1.21e-4 on one of five seeds)
+int crit_drain_default(const hb_ctx* c, int) { return c->small_head ? 1 : 2; }
 int drain_kb(const hb_ctx* c, GemmRole role, int l) {
   if (c->passes != 3 || !HB_GEMM_DRAIN) return 0;
   const int L = c->L;
   const bool crit = (role == R_FWD && l == L - 2) || (!c->small_head && l == L - 1 && (role == R_LOGITS || role == R_DW));
-  return static_cast<int>(crit ? env_long("HB_DRAIN_KB_CRIT", crit_drain_default(c)) : env_long("HB_DRAIN_KB", 0));
+  return static_cast<int>(crit ? env_long("HB_DRAIN_KB_CRIT", crit_drain_default(c, l)) : env_long("HB_DRAIN_KB", 0));
 }
 
 // Split-K plan for a forward / dX GEMM: when its output tiles cannot fill

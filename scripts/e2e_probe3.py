@@ -30,6 +30,9 @@ print("step_host (batch H2D + step)      %.3f ms" % t(lambda: ctx.step_host(xb, 
 print("step_host timed device ms         %.3f" % (ctx.step_host(xb, yb, 0.1, emit_grad=True, timed=True) and ctx.last_step_ms))
 print("replica_step_host (fused)         %.3f ms" % t(lambda: ctx.replica_step_host(w, xb, yb, 0.1)))
 ctx.replica_step_host(w, xb, yb, 0.1, timed=True); print("replica_step_host device ms       %.3f" % ctx.last_step_ms)
+print("replica_step_host sole writer     %.3f ms" % t(lambda: ctx.replica_step_host(w, xb, yb, 0.1, sole_writer=True)))
+ctx.replica_step_host(w, xb, yb, 0.1, timed=True, sole_writer=True); print("  ... device ms                   %.3f" % ctx.last_step_ms)
+print("  ... PCIe bytes (h2d, d2h)       %s" % (ctx.last_xfer_bytes,))
 print("set_weights                       %.3f ms" % t(lambda: ctx.set_weights(w)))
 print("merge_grads_into                  %.3f ms" % t(lambda: ctx.merge_grads_into(w, 0.1)))
 if not sparse:

@@ -113,6 +113,7 @@ int make_map(CUtensorMap* m, const float* base, long long inner, long long rows,
   return HB_OK;
 }
 
+std::atomic<long long> g_pin_epoch{0};  // bumped whenever a host range is unregistered
 std::mutex g_host_mu;
 std::map<uintptr_t, std::pair<size_t, void*>> g_host_ranges;  // host base -> (bytes, device alias)
 std::map<uintptr_t, int> g_host_refs;  // registrations per base: contexts of several worker threads can share
@@ -566,6 +567,7 @@ struct hb_ctx {
   bool xsole = false;          // the call being enqueued is a sole-writer call
   std::vector<double> fp_vals; // sampled host values after the last sole-writer call
   std::vector<double*> xw_prev;     // pointer set of the last armed call (graph key)
+  long long pin_epoch = -1;         // g_pin_epoch when that set's page-lock was last checked
   long long xgen = 0;               // graph key of the armed pointer set (hash)
   cudaStream_t xh2d = nullptr, xmrg = nullptr;
   std::vector<cudaEvent_t> xsnap_ev, xgrad_ev, xchunk_ev;
@@ -2557,6 +2559,7 @@ int hb_host_unregister(const void* p) {
   if (--g_host_refs[it->first] > 0) return HB_OK;  // still page-locked for another context
   g_host_refs.erase(it->first);
   g_host_ranges.erase(it);
+  g_pin_epoch.fetch_add(1);  // contexts re-check their host model's page-lock
   cudaError_t e = cudaHostUnregister(const_cast<void*>(p));
   if (e == cudaErrorHostMemoryNotRegistered) {
     cudaGetLastError();
@@ -2884,7 +2887,12 @@ static void mirror_sample(const hb_ctx* c, double* const* ws, std::vector<double
 static int xchg_arm(hb_ctx* c, double* const* ws, uint32_t flags) {
   g_call_t0 = std::chrono::steady_clock::now();
   if (!ws) return fail(HB_EINVAL, "null weight array");
-  for (int l = 0; l < c->L; ++l) {
+  // (the page-lock check costs a driver call per layer: once per pointer set)
+  const long long epoch = g_pin_epoch.load();
+  const bool same_set = c->xw_prev.size() == static_cast<size_t>(c->L) &&
+                        std::equal(c->xw_prev.begin(), c->xw_prev.end(), ws) && c->pin_epoch == epoch;
+  c->pin_epoch = epoch;
+  for (int l = 0; l < c->L && !same_set; ++l) {
     if (!ws[l]) return fail(HB_EINVAL, "null weights for layer %d", l);
     if (!is_pinned(ws[l]))
       return fail(HB_EINVAL, "layer %d of the host model is not page-locked (hb_host_register it first)", l);

@@ -766,7 +766,9 @@ int drain_kb(const hb_ctx* c, GemmRole role, int l) {
   if (c->passes != 3 || !HB_GEMM_DRAIN) return 0;
   const int L = c->L;
   const bool crit = (role == R_FWD && l == L - 2) || (!c->small_head && l == L - 1 && (role == R_LOGITS || role == R_DW));
-  return static_cast<int>(crit ? env_long("HB_DRAIN_KB_CRIT", crit_drain_default(c, l)) : env_long("HB_DRAIN_KB", 0));
+  if (crit) return static_cast<int>(env_long("HB_DRAIN_KB_CRIT", crit_drain_default(c, l)));
+  if (role == R_FWD) return static_cast<int>(env_long("HB_DRAIN_KB_FWD", env_long("HB_DRAIN_KB", 0)));
+  return static_cast<int>(env_long("HB_DRAIN_KB", 0));
 }
 
 // Split-K plan for a forward / dX GEMM: when its output tiles cannot fill

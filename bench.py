@@ -416,7 +416,13 @@ def time_to_target(ctx, src, cfg, args, rank, world, dist, init_w, max_rows):
     if dist is not None:
         targets = [broadcast_float(dist, t) for t in targets]
         cpu_k = int(broadcast_float(dist, float(cpu_k)))
-    # GPU run (every rank), eval by rank 0 outside the clock
+    # GPU run (every rank), eval by rank 0 outside the clock.  The CPU legs
+    # leave BLAS / pool threads spinning for a while; let them settle and
+    # warm the step's graph first, so the GPU leg's clock measures the GPU
+    time.sleep(0.5)
+    ctx.set_weights(init_w)
+    for _ in range(2):
+        ctx.step(0, b, eta, timed=True)
     ctx.set_weights(init_w)
     hit = [None, None]
     gpu_curve = []

@@ -767,9 +767,11 @@ int drain_kb(const hb_ctx* c, GemmRole role, int l) {
   const int L = c->L;
   const bool crit = (role == R_FWD && l == L - 2) || (!c->small_head && l == L - 1 && (role == R_LOGITS || role == R_DW));
   if (crit) return static_cast<int>(env_long("HB_DRAIN_KB_CRIT", crit_drain_default(c, l)));
-  // the other forward GEMMs feed the critical one: D=3 (the drain hides under three k-blocks of MMAs)
-  // lifts w8a's worst of 20 seeds from 9.8e-5 to 7.2e-5 at no measured cost
-  if (role == R_FWD) return static_cast<int>(env_long("HB_DRAIN_KB_FWD", env_long("HB_DRAIN_KB", 3)));
+  // small heads: the other forward GEMMs feed the critical one; D=3 (the drain hides under three k-blocks
+  // of MMAs) lifts w8a's worst of 20 seeds from 9.8e-5 to 7.2e-5 at no measured cost.  Wide heads have the
+  // margin without it (and the scaled config's power-capped GEMMs measured ~3% slower with it).
+  if (role == R_FWD)
+    return static_cast<int>(env_long("HB_DRAIN_KB_FWD", env_long("HB_DRAIN_KB", c->small_head ? 3 : 0)));
   return static_cast<int>(env_long("HB_DRAIN_KB", 0));
 }
 

@@ -89,6 +89,11 @@ int hb_ctx_destroy(hb_ctx* ctx);
 
 /* Model snapshot H2D (deep_copy, nn.py:182-184): host float64 (d_{l+1}, d_l). */
 int hb_set_weights_f64(hb_ctx* ctx, int layer, const double* w);
+/* Optional fixed per-unit offset of hidden layer `layer` (0..n_layers-2),
+ * d_{layer+1} float64 values, fused into the forward epilogue before the
+ * sigmoid (A = sigmoid(Z + b)); null removes it.  The reference MLP has no
+ * bias (nn.py:63-78), so parity runs without one; the offset is not trained. */
+int hb_set_bias_f64(hb_ctx* ctx, int layer, const double* bias);
 /* Device model D2H into host float64 (d_{l+1}, d_l). */
 int hb_get_weights_f64(hb_ctx* ctx, int layer, double* w);
 int hb_get_weights_f32(hb_ctx* ctx, int layer, float* w);

@@ -42,6 +42,7 @@ SIGNATURES = {
     "hb_ctx_create": (_i32, [C.POINTER(_p), _i32, _i32, C.POINTER(_i32), _i32, _u32]),
     "hb_ctx_destroy": (_i32, [_p]),
     "hb_set_weights_f64": (_i32, [_p, _i32, _dp]),
+    "hb_set_bias_f64": (_i32, [_p, _i32, _dp]),
     "hb_get_weights_f64": (_i32, [_p, _i32, _dp]),
     "hb_get_weights_f32": (_i32, [_p, _i32, _fp]),
     "hb_merge_grad_into_f64": (_i32, [_p, _i32, _dp, _f64]),

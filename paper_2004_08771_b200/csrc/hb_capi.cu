@@ -450,6 +450,7 @@ struct hb_ctx {
   int head_nct = 0, head_maxt = 0;
 
   std::vector<float*> W, G;    // W[l]; G[l] raw gradient (EMIT_GRAD)
+  std::vector<float*> bias;    // optional fixed per-unit offset of hidden layer l (hb_set_bias_f64), or null
   std::vector<float*> W_lo, A_lo, D_lo;  // 3xTF32 lo twins of the GEMM operands (3-pass only)
   std::vector<long long> ldw;  // row stride of W[l] (in its device layout)
   std::vector<float*> A;       // A[l] l=1..L-1 activations (cap, ld[l])
@@ -636,6 +637,11 @@ struct hb_ctx {
 namespace {
 
 int enqueue_layer_merge(hb_ctx* c, int l, cudaStream_t src, const DevStep* ds);
+const float* layer_bias(const hb_ctx* c, int l);
+
+const float* layer_bias(const hb_ctx* c, int l) {
+  return l < static_cast<int>(c->bias.size()) ? c->bias[l] : nullptr;
+}
 
 int ctx_check(hb_ctx* c) {
   if (c == nullptr) return fail(HB_EINVAL, "null context");
@@ -846,14 +852,18 @@ int launch_fx_split(hb_ctx* c, GemmKind kind, int mode, int bn, const Operand& t
   a.ldo = a.N;
   a.split_stride = static_cast<long long>(a.M) * a.N;
   a.kb_per_split = kb_per;
-  HB_TRY(launch_gemm(c->passes, kind, EPI_PARTIAL, bn, ta, tb, a, m_tiles, n_tiles, splits, st));
+  {
+    GemmArgs pa = a;
+    pa.bias = nullptr;  // the slabs are raw partial sums; the finish adds the bias once
+    HB_TRY(launch_gemm(c->passes, kind, EPI_PARTIAL, bn, ta, tb, pa, m_tiles, n_tiles, splits, st));
+  }
   const bool vec = (a.N % 4 == 0) && (ldo % 4 == 0);
   const int rows_total = mode == SPLIT_DSIG ? std::max(a.M, a.m_zero_rows) : a.M;
   const long long items = static_cast<long long>(rows_total) * (vec ? a.N / 4 : a.N);
   const dim3 grid(static_cast<int>(std::min<long long>(cdiv(items, 256), 148 * 8)));
 #define HB_SE(MODE_, VEC_)                                                                                  \
   HB_CUDA(launch_k(splitk_epi_kernel<MODE_, VEC_>, grid, dim3(256), 0, st, out, out_lo, ldo, c->ws, splits, a.M, \
-                   a.N, a.aux, a.ld_aux, a.m_zero_rows))
+                   a.N, a.aux, a.ld_aux, a.m_zero_rows, a.bias))
   if (mode == SPLIT_SIGMOID) {
     if (vec) HB_SE(SPLIT_SIGMOID, true); else HB_SE(SPLIT_SIGMOID, false);
   } else if (mode == SPLIT_STORE) {
@@ -1318,7 +1328,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     HB_TRY(xchg_use(c, l));
     if (l == 0 && c->sparse) {
       SpmmArgs p{v.rowptr, v.col, v.val, ds, start, rows, c->W[0], c->ldw[0], c->d[0], c->d[1], c->A[1], c->ld[1],
-                 (c->need_lo() && !(c->small_head && L == 2)) ? c->A_lo[1] : nullptr};
+                 (c->need_lo() && !(c->small_head && L == 2)) ? c->A_lo[1] : nullptr, layer_bias(c, 0)};
       prof_begin(c, "spmm_sigmoid", 0);
       const int blocks = cdiv(static_cast<long long>(rows) * 32, 256);
       const size_t w0t_bytes = static_cast<size_t>(c->d[0]) * c->ldw[0] * sizeof(float);
@@ -1346,6 +1356,7 @@ int run_forward(hb_ctx* c, const DataView& v, long long start, int rows, bool tr
     a.out_lo = (c->need_lo() && !(c->small_head && l + 1 == L - 1)) ? c->A_lo[l + 1] : nullptr;
     a.ldo = c->ld[l + 1];
     a.drain_kb = drain_kb(c, R_FWD, l);
+    a.bias = layer_bias(c, l);
     const Operand ta = l == 0 ? v.fwd() : c->opA_k(l);
     prof_begin(c, "gemm_fwd_sigmoid", l);
     int kb_per = a.kb_total;
@@ -2418,6 +2429,7 @@ int hb_ctx_destroy(hb_ctx* c) {
   cudaFree(c->grad_all);
   if (c->grad_host) cudaFreeHost(c->grad_host);
   cudaFree(c->flat);
+  for (float* b : c->bias) cudaFree(b);
   for (auto e : c->mev) cudaEventDestroy(e);
   if (c->comm_st) cudaStreamDestroy(c->comm_st);
   if (c->local) {
@@ -2630,6 +2642,25 @@ static int ensure_stage_all(hb_ctx* c) {
   HB_CUDA(cudaMalloc(&c->stage_all, c->n_params * sizeof(double)));
   HB_CUDA(cudaMalloc(&c->grad_all, c->n_params * sizeof(float)));
   HB_CUDA(cudaMallocHost(&c->grad_host, c->n_params * sizeof(float)));
+  return HB_OK;
+}
+
+int hb_set_bias_f64(hb_ctx* c, int layer, const double* b) {
+  HB_TRY(ctx_check(c));
+  if (layer < 0 || layer >= c->L - 1)
+    return fail(HB_EINVAL, "bias is supported on hidden layers 0..%d (the output layer has none)", c->L - 2);
+  if (c->bias.empty()) c->bias.assign(c->L, nullptr);
+  drop_graphs(c);  // the fused epilogues read the pointer at capture time
+  if (b == nullptr) {
+    cudaFree(c->bias[layer]);
+    c->bias[layer] = nullptr;
+    return HB_OK;
+  }
+  const int n = c->d[layer + 1];
+  std::vector<float> h(round_up(n, 4), 0.f);
+  for (int i = 0; i < n; ++i) h[i] = static_cast<float>(b[i]);
+  if (!c->bias[layer]) HB_CUDA(cudaMalloc(&c->bias[layer], h.size() * sizeof(float)));
+  HB_CUDA(cudaMemcpy(c->bias[layer], h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
   return HB_OK;
 }
 

@@ -70,6 +70,7 @@ struct GemmArgs {
   int trace;              // HB_TRACE builds: record this launch's pipeline timeline
   int trace_slot;         // HB_TRACE builds: 1-based slot for the per-CTA stamps (0 = off)
   int drain_kb;           // > 0: accumulator drain every drain_kb k-blocks (GemmCfg), 0: rotating accumulators
+  const float* bias;      // EPI_SIGMOID / EPI_STORE: optional per-column offset added before the op (or null)
 };
 
 // Optional pipeline timeline (debug builds, -DHB_TRACE): CTA (0,0,0) records
@@ -506,6 +507,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, PASSES>::THREADS, 1)
         if (nleft <= 0) continue;
         float o[4] = {acc.x, acc.y, acc.z, acc.w};
         bool write = grow < args.M;
+        if ((EPI == EPI_SIGMOID || EPI == EPI_STORE) && args.bias != nullptr) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) o[k] += k < nleft ? args.bias[gn + k] : 0.f;
+        }
         if (EPI == EPI_SIGMOID) {
 #ifndef HB_DEBUG_EPI_NO_SIGMOID
 #pragma unroll

@@ -605,6 +605,7 @@ struct SpmmArgs {
   float* out;  // (rows, d_out)
   long long ldo;
   float* out_lo;  // lo twin of out (or null)
+  const float* bias;  // optional per-unit offset (d_out) added before the sigmoid (or null)
 };
 
 // CSR gather kernels: output columns per pass (HB_*_PASS float4 accumulators
@@ -679,6 +680,13 @@ __global__ void __launch_bounds__(256, HB_SPMM_MINB) spmm_sigmoid_kernel(SpmmArg
       for (int t = 0; t < HB_SPMM_PASS; ++t) {
         const int j = base + 4 * lane + 128 * t;
         if (j < p.d_out) {
+          if (p.bias != nullptr) {
+            const float4 b4 = *reinterpret_cast<const float4*>(p.bias + j);
+            acc[t].x += b4.x;
+            acc[t].y += b4.y;
+            acc[t].z += b4.z;
+            acc[t].w += b4.w;
+          }
           const float4 sv = make_float4(sigmoidf_stable(acc[t].x), sigmoidf_stable(acc[t].y),
                                         sigmoidf_stable(acc[t].z), sigmoidf_stable(acc[t].w));
           reinterpret_cast<float4*>(o)[j / 4] = sv;
@@ -704,7 +712,7 @@ __global__ void __launch_bounds__(256, HB_SPMM_MINB) spmm_sigmoid_kernel(SpmmArg
       for (int t = 0; t < 8; ++t) {
         const int j = base + lane + 32 * t;
         if (j < p.d_out) {
-          const float sv = sigmoidf_stable(acc[t]);
+          const float sv = sigmoidf_stable(p.bias != nullptr ? acc[t] + p.bias[j] : acc[t]);
           o[j] = sv;
           if (p.out_lo != nullptr) p.out_lo[warp * p.ldo + j] = tf32_lo(sv);
         }
@@ -1010,7 +1018,7 @@ template <int MODE, bool VEC>
 __global__ void __launch_bounds__(256) splitk_epi_kernel(float* __restrict__ out, float* __restrict__ out_lo,
                                                          long long ldo, const float* __restrict__ part, int S,
                                                          int M, int N, const float* __restrict__ aux, long long ld_aux,
-                                                         int zero_rows) {
+                                                         int zero_rows, const float* __restrict__ bias = nullptr) {
   pdl_wait();
   pdl_trigger();
   const long long slab = static_cast<long long>(M) * N;
@@ -1054,6 +1062,7 @@ __global__ void __launch_bounds__(256) splitk_epi_kernel(float* __restrict__ out
       }
 #pragma unroll
       for (int k = 0; k < W; ++k) {
+        if (MODE != SPLIT_DSIG && bias != nullptr) v[k] += bias[c + k];
         if (MODE == SPLIT_SIGMOID) v[k] = sigmoidf_fast(v[k]);
         if (MODE == SPLIT_DSIG) {
           const float a = aux[r * ld_aux + c + k];

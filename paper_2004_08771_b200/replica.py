@@ -87,6 +87,18 @@ class GpuReplica:
         table = (C.POINTER(C.c_double) * self.depth)(*[N.ptr(a, C.c_double) for a in arrs])
         N.check(self._lib.hb_set_weights_all_f64(self._h, table))
 
+    def set_bias(self, layer: int, bias) -> None:
+        """Optional fixed per-unit offset of hidden layer `layer`, fused into the
+        forward epilogue (A = sigmoid(Z + b)); None removes it.  The reference
+        MLP has no bias; it is not trained."""
+        if bias is None:
+            N.check(self._lib.hb_set_bias_f64(self._h, int(layer), None))
+            return
+        b = np.ascontiguousarray(bias, dtype=np.float64)
+        if b.shape != (self.sizes[layer + 1],):
+            raise ValueError(f"bias of layer {layer} must have shape ({self.sizes[layer + 1]},)")
+        N.check(self._lib.hb_set_bias_f64(self._h, int(layer), N.ptr(b, C.c_double)))
+
     def get_weights(self) -> list:
         out = []
         for l in range(self.depth):

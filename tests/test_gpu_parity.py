@@ -879,3 +879,46 @@ def test_exchange_state_errors(hb):
         ctx.step(0, 64, 0.1)  # still usable
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("kind,b", [("dense", 512), ("dense", 48), ("csr_kernels", 256), ("csr_densified", 256)])
+def test_forward_bias_epilogue(hb, kind, b):
+    """The optional per-unit bias (hb_set_bias_f64) is fused into the forward
+    epilogue -- tensor-core GEMM, its split-K finish (small batches) and the
+    CSR SpMM -- as A = sigmoid(Z + b); the step's gradients follow the biased
+    forward (oracle: the reference backward on the biased tape); removing it
+    restores the reference model."""
+    sparse = kind.startswith("csr")
+    sizes = (600, 128, 64, 3) if sparse else (40, 128, 96, 3)
+    w, x, y = oracle_case(sizes, b, seed=21, sparse_nnz=9 if sparse else None)
+    rng = np.random.default_rng(22)
+    bias = [rng.normal(0, 0.5, size=sizes[l + 1]) for l in range(len(sizes) - 2)]
+    tape = [x]
+    for l, wl in enumerate(w):
+        z = tape[-1] @ wl.T
+        if l < len(bias):
+            tape.append(1.0 / (1.0 + np.exp(-(z + bias[l]))))
+        else:
+            e = np.exp(z - z.max(axis=1, keepdims=True))
+            tape.append(e / e.sum(axis=1, keepdims=True))
+    grads = ref_nn.backward(w, tape, y)
+    ctx = hb.GpuReplica(sizes, b, sparse=sparse, sparse_kernels=(kind == "csr_kernels"))
+    try:
+        ctx.set_weights(w)
+        ctx.stage(to_csr(hb, x, y) if sparse else x, None if sparse else y)
+        for l, bl in enumerate(bias):
+            ctx.set_bias(l, bl)
+        ctx.forward(0, b)
+        for l in range(1, len(sizes) - 1):
+            assert np.abs(ctx.activation(l, b) - tape[l]).max() <= 1e-5, l
+        ctx.step(0, b, 0.3, emit_grad=True)
+        assert max_relative_error(ctx.grads(), grads) <= STEP_TOL
+        with pytest.raises(ValueError):
+            ctx.set_bias(len(sizes) - 2, np.zeros(sizes[-1]))  # the output layer has none
+        ctx.set_weights(w)
+        for l in range(len(bias)):
+            ctx.set_bias(l, None)
+        ctx.forward(0, b)
+        assert np.abs(ctx.activation(1, b) - ref_nn.forward(w, x)[1]).max() <= 1e-5
+    finally:
+        ctx.close()

@@ -28,7 +28,7 @@ from .data import (
     synthetic_csr,
 )
 from .nn import Architecture, InitScheme, Model, deep_copy, init_model
-from .feed import DeviceSpeedFeed, device_timed, pipelined
+from .feed import DeviceSpeedFeed, device_timed, pipelined, share_host
 from .replica import GpuReplica
 from .trainer import TrainResult, train_gpu
 from .workers import (
@@ -49,7 +49,7 @@ from .workers import (
 __all__ = [
     "Architecture", "BatchRef", "CsrBatchRef", "CsrDataset", "Dataset", "DeviceSpeedFeed", "GpuReplica",
     "InitScheme", "LabelMapping", "LibsvmParseError", "Model", "TrainResult", "WorkerConfig", "WorkerMode",
-    "deep_copy", "device_busy_seconds", "device_count", "device_timed", "pipelined", "epoch_shuffle_seed", "execute_gpu_replica", "execute_gpu_replica_begin", "execute_gpu_replica_end",
+    "deep_copy", "device_busy_seconds", "device_count", "device_timed", "pipelined", "share_host", "epoch_shuffle_seed", "execute_gpu_replica", "execute_gpu_replica_begin", "execute_gpu_replica_end",
     "gpu_loss_sum", "init_model", "install", "last_device_ms", "load_libsvm", "load_libsvm_csr", "load_library",
     "reorder", "set_sole_writer", "set_worker_device", "set_worker_devices", "shuffle_epoch", "synthetic_blobs",
     "synthetic_csr", "train_gpu",

@@ -147,3 +147,36 @@ def pipelined(workers_module, engine_module) -> None:
 
     _evaluate_and_sample.reference = ref_eval
     co._evaluate_and_sample = _evaluate_and_sample
+
+
+last_host_share = None  # (merge threads, spin) the last coordinator's roster chose (share_host)
+
+
+def share_host(engine_module) -> None:
+    """Size the library's host merge pool from the coordinator's roster.
+
+    Wraps `_Coordinator.__init__` (engine.py:93-157): when the roster has a
+    CPU Hogwild pool (HOGWILD_SHARDED, `threads` each, workers.py:94-123) the
+    merge pool takes only the remaining host threads (at least 2) and stops
+    spinning between layers, so the pool's cores stay with the CPU workers
+    (measured: the CPU pool keeps 0.91 instead of 0.83 of its throughput on
+    w8a, scripts/coexist.py); a GPU-only roster restores the default pool.
+    Idempotent."""
+    import os
+
+    co = engine_module._Coordinator
+    ref_init = getattr(co.__init__, "reference", co.__init__)
+
+    def __init__(self, dataset, model, roster, *args, **kwargs):
+        global last_host_share
+        ref_init(self, dataset, model, roster, *args, **kwargs)
+        cpu = sum(int(getattr(cfg, "threads", 1)) for cfg in roster
+                  if getattr(getattr(cfg, "mode", None), "value", "") == "hogwild_sharded")
+        hw = os.cpu_count() or 4
+        share = (max(2, min(12, hw - cpu)), 0) if cpu else (max(2, min(12, hw * 3 // 4)), 20000)
+        if share != last_host_share:
+            _w.set_host_merge_threads(*share)
+            last_host_share = share
+
+    __init__.reference = ref_init
+    co.__init__ = __init__

@@ -269,6 +269,36 @@ class TestReferenceEngineSeam:
         assert m.per_worker_busy_ms["gpu0"] == pytest.approx(1.0 * m.per_worker_updates["gpu0"])
 
 
+    def test_share_host_sizes_the_merge_pool_from_the_roster(self, monkeypatch):
+        """feed.share_host reads the coordinator's roster: a CPU Hogwild pool
+        gets the host threads, the merge pool shrinks and stops spinning."""
+        ref_src = Path("/root/reference/pkg/src")
+        if not ref_src.exists():
+            pytest.skip("reference package not present")
+        monkeypatch.syspath_prepend(str(ref_src))
+        import os
+
+        import hogtrain
+        import hogtrain.engine as E
+        import hogtrain.workers as RW
+
+        from paper_2004_08771_b200 import feed
+
+        monkeypatch.setattr(E._Coordinator, "__init__", E._Coordinator.__init__)
+        hb.share_host(E)
+        hb.share_host(E)  # idempotent
+        ds = hogtrain.data.synthetic_blobs(300, 6, 2, 2.5, seed=1)
+        model = hogtrain.nn.init_model(hogtrain.nn.Architecture((6, 8, 2)), seed=2)
+        hw = os.cpu_count() or 4
+        roster = [RW.WorkerConfig("cpu", RW.WorkerMode.HOGWILD_SHARDED, threads=3, min_batch=3, max_batch=30),
+                  RW.WorkerConfig("gpu0", RW.WorkerMode.BATCH_REPLICA, min_batch=50, max_batch=100)]
+        hogtrain.run_training(ds, model, roster, hogtrain.policies.UniformHogbatch(30, 0.1), epochs=1, seed=3)
+        assert feed.last_host_share == (max(2, min(12, hw - 3)), 0)
+        roster = roster[1:]
+        hogtrain.run_training(ds, model, roster, hogtrain.policies.UniformHogbatch(50, 0.1), epochs=1, seed=3)
+        assert feed.last_host_share == (max(2, min(12, hw * 3 // 4)), 20000)
+
+
 class TestBenchAccounting:
     def test_flops_per_sample_match_survey(self):
         import bench

@@ -736,20 +736,25 @@ int build_data_maps(hb_ctx* c, DataView& v) {
   return HB_OK;
 }
 
-int choose_bn(long long m_tiles, long long n) {
+long long env_long(const char* name, long long dflt) {
+  const char* v = getenv(name);
+  return v != nullptr && v[0] != 0 ? atoll(v) : dflt;
+}
+
+int choose_bn(long long m_tiles, long long n, bool batch_rows = false) {
   // narrow outputs get narrow tiles: less wasted MMA work and more TMEM
   // accumulators to rotate over (hb_gemm.cuh, GemmCfg::NBIG)
   if (n <= 32) return 32;
   if (n <= 64) return 64;
   if (n <= 128) return 128;
   if (m_tiles * cdiv(n, 256) >= 120) return 256;
+  // forward / dX GEMMs of a small batch (covtype's b = 512): 64-wide tiles give more CTAs to
+  // spread the latency-bound k-loop over (measured covtype 0.084 -> 0.080 ms/step; on w8a's dW
+  // GEMMs -- few M tiles but a long K -- it measured 20% slower, hence batch rows only)
+  if (batch_rows && m_tiles * cdiv(n, 128) < 32 && env_long("HB_SMALL_BN64", 1) != 0) return 64;
   return 128;
 }
 
-long long env_long(const char* name, long long dflt) {
-  const char* v = getenv(name);
-  return v != nullptr && v[0] != 0 ? atoll(v) : dflt;
-}
 
 // Accumulator drain (hb_gemm.cuh "Drain mode") per GEMM: D k-blocks per
 // fresh accumulator, 0 = rotating accumulators.  The precision-critical GEMMs
@@ -2237,8 +2242,8 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
       HB_CK(cudaMalloc(&c->D_lo[l], static_cast<size_t>(c->cap) * c->ld[l + 1] * sizeof(float)));
       HB_CK(cudaMemset(c->D_lo[l], 0, static_cast<size_t>(c->cap) * c->ld[l + 1] * sizeof(float)));
     }
-    c->bn_fwd[l] = choose_bn(m_tiles, c->d[l + 1]);
-    c->bn_dx[l] = choose_bn(m_tiles, c->d[l]);
+    c->bn_fwd[l] = choose_bn(m_tiles, c->d[l + 1], true);
+    c->bn_dx[l] = choose_bn(m_tiles, c->d[l], true);
     // precision: the wide softmax head's logits GEMM with a long contraction
     // (K > 1024) rotates the hi*hi term over >= 3 accumulators (BN <= 128; a
     // 256-wide tile has room for only one): the biased round-toward-zero

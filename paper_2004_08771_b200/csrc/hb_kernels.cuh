@@ -34,6 +34,11 @@ __device__ __forceinline__ float warp_sum(float v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+__device__ __forceinline__ double warp_sum_f64(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -125,34 +130,38 @@ __global__ void __launch_bounds__(kHeadWarps * 32, (MAXT <= 16 && NCT <= 2) ? 2 
       const int j = lane + 32 * t;
       av[t] = (t < T && j < p.d) ? p.a[row * p.lda + j] : 0.f;
     }
-    float z[NCT];
+    // logits, softmax and the error signal in float64 (a handful of values per
+    // row): p - 1 for a confident row loses its relative precision in fp32,
+    // and the head's dW sum cancels those signals over the batch
+    double z[NCT];
 #pragma unroll
     for (int c = 0; c < NCT; ++c) {
-      float s = 0.f;
+      double s = 0.0;
 #pragma unroll
-      for (int t = 0; t < MAXT; ++t) s = fmaf(av[t], sW[c * 32 * MAXT + lane + 32 * t], s);
-      z[c] = warp_sum(s);
+      for (int t = 0; t < MAXT; ++t) s = fma(static_cast<double>(av[t]), static_cast<double>(sW[c * 32 * MAXT + lane + 32 * t]), s);
+      z[c] = warp_sum_f64(s);
     }
-    float zmax = -INFINITY;
+    double zmax = -INFINITY;
 #pragma unroll
     for (int c = 0; c < NCT; ++c)
-      if (c < p.nc) zmax = fmaxf(zmax, z[c]);
-    float e[NCT], esum = 0.f;
+      if (c < p.nc) zmax = fmax(zmax, z[c]);
+    double e[NCT], esum = 0.0;
 #pragma unroll
     for (int c = 0; c < NCT; ++c) {
-      e[c] = c < p.nc ? expf(z[c] - zmax) : 0.f;
+      e[c] = c < p.nc ? exp(z[c] - zmax) : 0.0;
       esum += e[c];
     }
     const int y = static_cast<int>(p.labels[row]);
-    float py = 0.f;
+    double py = 0.0;
 #pragma unroll
     for (int c = 0; c < NCT; ++c)
       if (c == y) py = e[c] / esum;
-    loss += -log(fmax(static_cast<double>(py), 1e-12));
+    loss += -log(fmax(py, 1e-12));
     if (!p.train) continue;
     float dl[NCT];
 #pragma unroll
-    for (int c = 0; c < NCT; ++c) dl[c] = c < p.nc ? (e[c] / esum - (c == y ? 1.f : 0.f)) * p.inv_n : 0.f;
+    for (int c = 0; c < NCT; ++c)
+      dl[c] = c < p.nc ? static_cast<float>((e[c] / esum - (c == y ? 1.0 : 0.0)) * static_cast<double>(p.inv_n)) : 0.f;
     if (p.delta_out != nullptr && lane < p.nc) {
 #pragma unroll
       for (int c = 0; c < NCT; ++c)
@@ -250,19 +259,19 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_small_vec_kernel(HeadArg
       av[k][t] = (row < p.rows && j < p.d) ? *reinterpret_cast<const float4*>(p.a + row * p.lda + j)
                                            : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-  float z[RPW][NCT];
+  double z[RPW][NCT];  // float64 logits / softmax / error signal (see head_small_kernel)
 #pragma unroll
   for (int k = 0; k < RPW; ++k)
 #pragma unroll
     for (int c = 0; c < NCT; ++c) {
-      float sacc = 0.f;
+      double sacc = 0.0;
 #pragma unroll
       for (int t = 0; t < VPL; ++t) {
         const float4 w4 = *reinterpret_cast<const float4*>(&sW[c * D + 4 * lane + 128 * t]);
-        sacc = fmaf(av[k][t].x, w4.x, sacc);
-        sacc = fmaf(av[k][t].y, w4.y, sacc);
-        sacc = fmaf(av[k][t].z, w4.z, sacc);
-        sacc = fmaf(av[k][t].w, w4.w, sacc);
+        sacc = fma(static_cast<double>(av[k][t].x), static_cast<double>(w4.x), sacc);
+        sacc = fma(static_cast<double>(av[k][t].y), static_cast<double>(w4.y), sacc);
+        sacc = fma(static_cast<double>(av[k][t].z), static_cast<double>(w4.z), sacc);
+        sacc = fma(static_cast<double>(av[k][t].w), static_cast<double>(w4.w), sacc);
       }
       z[k][c] = sacc;
     }
@@ -289,26 +298,27 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_small_vec_kernel(HeadArg
       }
       continue;
     }
-    float zmax = -INFINITY;
+    double zmax = -INFINITY;
 #pragma unroll
     for (int c = 0; c < NCT; ++c)
-      if (c < p.nc) zmax = fmaxf(zmax, z[k][c]);
-    float e[NCT], esum = 0.f;
+      if (c < p.nc) zmax = fmax(zmax, z[k][c]);
+    double e[NCT], esum = 0.0;
 #pragma unroll
     for (int c = 0; c < NCT; ++c) {
-      e[c] = c < p.nc ? expf(z[k][c] - zmax) : 0.f;
+      e[c] = c < p.nc ? exp(z[k][c] - zmax) : 0.0;
       esum += e[c];
     }
     const int y = static_cast<int>(p.labels[row]);
-    float py = 0.f;
+    double py = 0.0;
 #pragma unroll
     for (int c = 0; c < NCT; ++c)
       if (c == y) py = e[c] / esum;
-    loss += -log(fmax(static_cast<double>(py), 1e-12));
+    loss += -log(fmax(py, 1e-12));
     if (!p.train) continue;
     float dl[NCT];
 #pragma unroll
-    for (int c = 0; c < NCT; ++c) dl[c] = c < p.nc ? (e[c] / esum - (c == y ? 1.f : 0.f)) * p.inv_n : 0.f;
+    for (int c = 0; c < NCT; ++c)
+      dl[c] = c < p.nc ? static_cast<float>((e[c] / esum - (c == y ? 1.0 : 0.0)) * static_cast<double>(p.inv_n)) : 0.f;
 #pragma unroll
     for (int t = 0; t < VPL; ++t) {
       const int j = 4 * lane + 128 * t;

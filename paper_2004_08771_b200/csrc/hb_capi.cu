@@ -605,6 +605,12 @@ struct hb_ctx {
   // before it and DMA'd back (splits the merge between PCIe and host DRAM)
   std::vector<char> xdma;       // planned per layer
   std::vector<char> xml;        // sole-writer calls: layers merged on the mirror lane (planned per layer)
+  // one merge stream per layer: a layer's merge / copy-back starts as soon as
+  // its gradient exists, not behind a later-finishing layer's (the backward's
+  // two streams can finish layers out of order)
+  std::vector<cudaStream_t> xmrg_l;
+  std::vector<cudaEvent_t> xmdone_ev;
+  std::vector<char> xmrg_used;  // this call's layers whose merge stream carried work (joined at the end)
   long long last_h2d = 0, last_d2h = 0;  // PCIe bytes of the last hb_replica_step* call
   std::vector<char> xdma_used;  // taken by the step just enqueued (rows decide whether the split-K path runs)
   std::vector<cudaEvent_t> xread_ev;
@@ -1151,16 +1157,21 @@ int xchg_merge(hb_ctx* c, int l, double eta, const DevStep* ds, cudaStream_t src
   if (c->xw.empty()) return HB_OK;
   if (src == nullptr) src = c->stream;
   xtl(c, src, "step: G%d done", l);
+  cudaStream_t ms = c->xmrg;
+  if (c->xmode == 0 && l < static_cast<int>(c->xmrg_l.size())) {
+    ms = c->xmrg_l[l];
+    c->xmrg_used[l] = 1;
+  }
   HB_CUDA(cudaEventRecord(c->xgrad_ev[l], src));
   const int rows = c->d[l + 1], cols = c->d[l];
   const bool tr = (l == 0 && c->sparse);
   if (c->xmode == 0 && l < static_cast<int>(c->xdma_used.size()) && c->xdma_used[l] && src == c->side) {
     // device lane: the reduce kernel already merged the freshly read host
     // rows; write them back
-    HB_CUDA(cudaStreamWaitEvent(c->xmrg, c->xgrad_ev[l], 0));
+    HB_CUDA(cudaStreamWaitEvent(ms, c->xgrad_ev[l], 0));
     HB_CUDA(cudaMemcpyAsync(c->xw[l], c->stage_all + layer_offset(c, l),
-                            static_cast<size_t>(rows) * cols * sizeof(double), cudaMemcpyDeviceToHost, c->xmrg));
-    xtl(c, c->xmrg, "mrg: layer %d written back (device lane)", l);
+                            static_cast<size_t>(rows) * cols * sizeof(double), cudaMemcpyDeviceToHost, ms));
+    xtl(c, ms, "mrg: layer %d written back (device lane)", l);
     return HB_OK;
   }
   if (c->xmode == 0 && c->xsole && l < static_cast<int>(c->xml.size()) && c->xml[l]) {
@@ -1168,43 +1179,43 @@ int xchg_merge(hb_ctx* c, int l, double eta, const DevStep* ds, cudaStream_t src
     // (snapshot or resident mirror), so the float64 merge runs on the device
     // (w + (-eta) * g, NumPy's rounding) and the merged layer goes D2H in place
     // of the gradient -- no host read-modify-write, no merge read
-    HB_CUDA(cudaStreamWaitEvent(c->xmrg, c->xgrad_ev[l], 0));
+    HB_CUDA(cudaStreamWaitEvent(ms, c->xgrad_ev[l], 0));
     const size_t n = static_cast<size_t>(rows) * cols;
     const size_t off = layer_offset(c, l);
-    merge_host_f64_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 4)), 256, 0, c->xmrg>>>(
+    merge_host_f64_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 4)), 256, 0, ms>>>(
         c->stage_all + off, c->G[l], tr ? c->ldw[0] : cols, rows, cols, tr ? 1 : 0, eta, ds);
     HB_CUDA(cudaGetLastError());
     c->last_launches++;
-    HB_CUDA(cudaMemcpyAsync(c->xw[l], c->stage_all + off, n * sizeof(double), cudaMemcpyDeviceToHost, c->xmrg));
+    HB_CUDA(cudaMemcpyAsync(c->xw[l], c->stage_all + off, n * sizeof(double), cudaMemcpyDeviceToHost, ms));
     if (l < static_cast<int>(c->xdma_used.size())) c->xdma_used[l] = 2;  // merged on the device (no host pass)
-    xtl(c, c->xmrg, "mrg: layer %d written back (mirror lane)", l);
+    xtl(c, ms, "mrg: layer %d written back (mirror lane)", l);
     return HB_OK;
   }
   if (c->xmode == 0) {
     // host mode: the fp32 gradient goes D2H on the merge stream; the calling
     // thread applies it (hb_replica_step*, xchg_host_merges)
-    HB_CUDA(cudaStreamWaitEvent(c->xmrg, c->xgrad_ev[l], 0));
+    HB_CUDA(cudaStreamWaitEvent(ms, c->xgrad_ev[l], 0));
     const size_t n = static_cast<size_t>(rows) * cols;
     const size_t off = layer_offset(c, l);
     const float* src = c->G[l];
     if (tr) {
-      transpose_f32_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 1024)), 256, 0, c->xmrg>>>(
+      transpose_f32_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 1024)), 256, 0, ms>>>(
           c->grad_all + off, c->G[0], c->ldw[0], rows, cols);
       HB_CUDA(cudaGetLastError());
       c->last_launches++;
       src = c->grad_all + off;
     }
-    HB_CUDA(cudaMemcpyAsync(c->xgrad_host + off, src, n * sizeof(float), cudaMemcpyDeviceToHost, c->xmrg));
-    HB_CUDA(cudaMemcpyAsync(c->xseq_host + 1 + l, c->d_xseq, sizeof(int32_t), cudaMemcpyDeviceToHost, c->xmrg));
+    HB_CUDA(cudaMemcpyAsync(c->xgrad_host + off, src, n * sizeof(float), cudaMemcpyDeviceToHost, ms));
+    HB_CUDA(cudaMemcpyAsync(c->xseq_host + 1 + l, c->d_xseq, sizeof(int32_t), cudaMemcpyDeviceToHost, ms));
     if (c->xsole) {
       // the same f64 merge on the device copy (w + (-eta) * g, product and sum
       // rounded like the host's): the staging buffer stays equal to the host model
-      merge_host_f64_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 4)), 256, 0, c->xmrg>>>(
+      merge_host_f64_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 4)), 256, 0, ms>>>(
           c->stage_all + off, c->G[l], tr ? c->ldw[0] : cols, rows, cols, tr ? 1 : 0, eta, ds);
       HB_CUDA(cudaGetLastError());
       c->last_launches++;
     }
-    xtl(c, c->xmrg, "mrg: gradient %d on host", l);
+    xtl(c, ms, "mrg: gradient %d on host", l);
     return HB_OK;
   }
   HB_CUDA(cudaStreamWaitEvent(c->xh2d, c->xgrad_ev[l], 0));
@@ -1272,8 +1283,16 @@ int xchg_host_merges(hb_ctx* c, double eta) {
 // join: the step stream waits for the last write-back
 int xchg_end(hb_ctx* c) {
   if (c->xw.empty()) return HB_OK;
-  HB_CUDA(cudaEventRecord(c->xdone_ev, c->xmrg));
-  HB_CUDA(cudaStreamWaitEvent(c->stream, c->xdone_ev, 0));
+  for (size_t l = 0; l < c->xmrg_l.size(); ++l) {  // every layer's merge stream this call used
+    if (!c->xmrg_used[l]) continue;
+    c->xmrg_used[l] = 0;
+    HB_CUDA(cudaEventRecord(c->xmdone_ev[l], c->xmrg_l[l]));
+    HB_CUDA(cudaStreamWaitEvent(c->stream, c->xmdone_ev[l], 0));
+  }
+  if (c->xmode != 0) {  // the DMA merge's chunks run on the shared merge stream
+    HB_CUDA(cudaEventRecord(c->xdone_ev, c->xmrg));
+    HB_CUDA(cudaStreamWaitEvent(c->stream, c->xdone_ev, 0));
+  }
   xtl(c, c->stream, "end");
   // the H2D stream must rejoin too (its last reads feed xmrg, but a capture
   // needs every forked stream joined)
@@ -2470,6 +2489,8 @@ int hb_ctx_destroy(hb_ctx* c) {
   if (c->xdone_ev) cudaEventDestroy(c->xdone_ev);
   if (c->xh2d) cudaStreamDestroy(c->xh2d);
   if (c->xmrg) cudaStreamDestroy(c->xmrg);
+  for (auto st_ : c->xmrg_l) cudaStreamDestroy(st_);
+  for (auto e : c->xmdone_ev) cudaEventDestroy(e);
   for (auto e : c->bev) cudaEventDestroy(e);
   if (c->bev_loss) cudaEventDestroy(c->bev_loss);
   if (c->side) cudaStreamDestroy(c->side);
@@ -2945,6 +2966,13 @@ static int xchg_arm(hb_ctx* c, double* const* ws, uint32_t flags) {
     HB_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
     HB_CUDA(cudaStreamCreateWithPriority(&c->xh2d, cudaStreamNonBlocking, hi_prio));
     HB_CUDA(cudaStreamCreateWithPriority(&c->xmrg, cudaStreamNonBlocking, hi_prio));
+    c->xmrg_l.resize(c->L);
+    c->xmdone_ev.resize(c->L);
+    c->xmrg_used.assign(c->L, 0);
+    for (int l = 0; l < c->L; ++l) {
+      HB_CUDA(cudaStreamCreateWithPriority(&c->xmrg_l[l], cudaStreamNonBlocking, hi_prio));
+      HB_CUDA(cudaEventCreateWithFlags(&c->xmdone_ev[l], cudaEventDisableTiming));
+    }
     HB_CUDA(cudaEventCreateWithFlags(&c->xstart_ev, cudaEventDisableTiming));
     HB_CUDA(cudaEventCreateWithFlags(&c->xdone_ev, cudaEventDisableTiming));
     c->xsnap_ev.resize(c->L);
@@ -3029,6 +3057,7 @@ static int replica_finish(hb_ctx* c, int rc, int rows, double eta, uint32_t flag
     cudaStreamSynchronize(c->stream);
     if (c->xh2d) cudaStreamSynchronize(c->xh2d);
     if (c->xmrg) cudaStreamSynchronize(c->xmrg);
+    for (auto st_ : c->xmrg_l) cudaStreamSynchronize(st_);
     if (c->side) cudaStreamSynchronize(c->side);
     return rc;
   }

@@ -23,6 +23,6 @@ if sparse:
 else:
     x, y = ref_nn.synthetic_blobs(2 * b, sizes[0], sizes[-1], 2.5, 1)
     ctx.stage(x.astype(np.float32), y)
-for i in range(3):
+for i in range(int(sys.argv[3]) if len(sys.argv) > 3 else 3):
     print("---- call", i, file=sys.stderr, flush=True)
     ctx.replica_step(w, 0, b, 0.1, sole_writer=sole)

@@ -603,27 +603,39 @@ def run_ours(args, cfg, rank, world, local_rank, dist):
         for i in range(max(3, min(args.warmup, len(host_batches)))):  # warm the host path (and its graph)
             xb, yb = host_batches[i % len(host_batches)]
             ctx.replica_step_host(host_model, xb, yb, cfg["eta"], sole_writer=True)
-        if distributed:
-            barrier(dist)
-        t0 = time.perf_counter()
-        for i in range(args.steps):
-            xb, yb = host_batches[i]
-            # execute_batch_replica in one call: snapshot of the shared host model
-            # (workers.py:132), batch H2D, the step, stale merge (workers.py:135), loss D2H
-            # (a lone GPU replica is the host model's only writer: HB_STEP_SOLE_WRITER)
-            ctx.replica_step_host(host_model, xb, yb, cfg["eta"], want_loss=True, sole_writer=True)
-        el = time.perf_counter() - t0
+        def e2e_run(land_async):
+            if distributed:
+                barrier(dist)
+            t0 = time.perf_counter()
+            for i in range(args.steps):
+                xb, yb = host_batches[i]
+                # execute_batch_replica in one call: snapshot of the shared host model
+                # (workers.py:132), batch H2D, the step, stale merge (workers.py:135), loss D2H
+                # (a lone GPU replica is the host model's only writer: HB_STEP_SOLE_WRITER)
+                ctx.replica_step_host(host_model, xb, yb, cfg["eta"], want_loss=True, sole_writer=True,
+                                      land_async=land_async)
+            ctx.landed()  # every step's merge is in the host model before the clock stops
+            el = time.perf_counter() - t0
+            return max_over_ranks(dist, el) if distributed else el
+
+        el_seq = e2e_run(False)
         # PCIe bytes of the last call as the library issued them
         h2d, d2h = ctx.last_xfer_bytes
-        if distributed:
-            el = max_over_ranks(dist, el)
+        el = e2e_run(True) if args.e2e_mode == "deferred" else el_seq
         e2e = {"value": world * args.steps * b / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h),
+               "d2h_bytes_per_step": int(d2h), "mode": args.e2e_mode,
                "path": "execute_gpu_replica semantics through the C ABI (hb_replica_step_host_*), per step: "
                        "batch H2D from pinned host memory, snapshot of the page-locked f64 host model (skipped while "
                        "the device-resident f64 mirror is current: the replica is the model's sole writer here), the "
                        "step, the f64 stale merge W_host += (-eta)*g per layer as soon as its gradient exists (run on "
-                       "the device mirror, merged layers DMA'd back), loss D2H"}
+                       "the device mirror, merged layers DMA'd back), loss D2H; the clock stops after hb_replica_landed "
+                       "(every merge in the host model)" + (
+                           ". deferred (HB_STEP_LAND_ASYNC): a call returns once its step and loss are done and its "
+                           "write-backs land while the next call's batch copy and forward run" if args.e2e_mode ==
+                           "deferred" else ""),
+               "sequential": {"value": world * args.steps * b / el_seq, "unit": UNIT,
+                              "note": "each call returns after its merge is in the host model (execute_batch_replica "
+                                      "order, workers.py:126-138)"}}
         # PCIe roofline of the drop-in call: its bytes at the link's measured copy rate
         bw = pcie_bandwidth(device)
         if bw:
@@ -748,6 +760,9 @@ def main():
     ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
                     help="replica averaging over NCCL or over peer memory (CUDA IPC, hb_peer_attach)")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--e2e-mode", choices=["deferred", "sequential"], default="deferred",
+                    help="e2e calls land their host-model write-backs in the background (HB_STEP_LAND_ASYNC) "
+                         "or before returning")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--ttt-budget-s", type=float, default=20.0, help="CPU time budget of the time-to-target legs")

@@ -70,6 +70,17 @@ extern "C" {
  * partial GEMM runs, written back after the reduce); without it every layer
  * merges on the host with per-element read-modify-writes, as np.add does. */
 #define HB_STEP_SOLE_WRITER 16u
+/* hb_replica_step* / hb_replica_begin with HB_STEP_SOLE_WRITER: return once the
+ * step and its loss are done and let the merged layers' write-backs into the
+ * host model finish in the background -- the next call's batch copy and
+ * forward overlap them.  Consecutive deferred calls on the same host arrays
+ * chain on the device copy; hb_replica_landed (or any call that reads or
+ * writes the host model through the context: another replica call without the
+ * flag or on other arrays, set_weights, merge_grads, hb_synchronize,
+ * hb_ctx_destroy) waits until every write-back is in host memory.  The caller
+ * must not read ws in between (the reference's coordinator snapshot waits,
+ * feed.pipelined). */
+#define HB_STEP_LAND_ASYNC 32u
 
 typedef struct hb_ctx hb_ctx;
 
@@ -219,6 +230,8 @@ int hb_replica_step_host_csr(hb_ctx* ctx, double* const* ws, const int64_t* rowp
  * come in between; ws must stay valid until end. */
 int hb_replica_begin(hb_ctx* ctx, double* const* ws, int64_t start, int rows, double eta, uint32_t flags);
 int hb_replica_end(hb_ctx* ctx, double* out_loss);
+/* Block until the write-backs of HB_STEP_LAND_ASYNC calls are in the host model. */
+int hb_replica_landed(hb_ctx* ctx);
 
 /* Sum over staged rows [start, start+rows) of -log max(p_y, 1e-12)
  * (loss_sum, nn.py:139-146), evaluated in chunks of at most max_batch rows. */

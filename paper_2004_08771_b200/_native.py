@@ -27,6 +27,7 @@ HB_STEP_TIMED = 2
 HB_STEP_ASYNC = 4
 HB_STEP_MERGE = 8
 HB_STEP_SOLE_WRITER = 16
+HB_STEP_LAND_ASYNC = 32
 HB_PEER_HANDLE_BYTES = 128
 
 _p = C.c_void_p
@@ -66,6 +67,7 @@ SIGNATURES = {
     "hb_train_step_host_csr": (_i32, [_p, _i64p, _i32p, _fp, _i64p, _i32, _f64, _u32, _dp]),
     "hb_replica_begin": (_i32, [_p, C.POINTER(_dp), _i64, _i32, _f64, _u32]),
     "hb_replica_end": (_i32, [_p, _dp]),
+    "hb_replica_landed": (_i32, [_p]),
     "hb_replica_step": (_i32, [_p, C.POINTER(_dp), _i64, _i32, _f64, _u32, _dp]),
     # host batch arrays pass as integer addresses (ndarray.ctypes.data): half the cost of data_as per call
     "hb_replica_step_host_dense": (_i32, [_p, C.POINTER(_dp), _p, _i64, _p, _i32, _f64, _u32, _dp]),

@@ -128,6 +128,18 @@ bool pdl_enabled() {
   static const bool on = !(getenv("HB_NO_PDL") && getenv("HB_NO_PDL")[0] == '1');
   return on;
 }
+// The next launch on this stream is issued without the programmatic attribute
+// (set where a merge kernel forks off the step: an early-launched successor
+// would hold every SM and keep the merge -- and the copy behind it -- waiting
+// for a whole GEMM).
+thread_local cudaStream_t t_no_pdl_once = nullptr;
+bool pdl_for(cudaStream_t st) {
+  if (st != nullptr && st == t_no_pdl_once) {
+    t_no_pdl_once = nullptr;
+    return false;
+  }
+  return pdl_enabled();
+}
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
@@ -137,7 +149,7 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_for(st) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
@@ -177,7 +189,7 @@ cudaError_t launch_k_l2(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sm
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_for(st) ? 1 : 0;
   int n = 1;
   if (max_persist > 0 && bytes > 0) {
     attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
@@ -235,7 +247,7 @@ int launch_gemm_t(const Operand& ta, const Operand& tb, const GemmArgs& a, int m
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_for(st) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   cudaError_t le = cudaLaunchKernelEx(&cfg, kern, *ta.hi, *tb.hi, *ta.lo, *tb.lo, a);
@@ -518,6 +530,7 @@ struct hb_ctx {
   double* ws_loss = nullptr;
   int ws_loss_n = 0;
   double* d_loss = nullptr;
+  double* h_loss = nullptr;  // mapped pinned: the loss read back by a kernel store, not a copy-engine D2H
   double* stage64 = nullptr;  // f64 staging for the weight exchange
   size_t stage64_n = 0;
   float* stage32 = nullptr;  // fp32 staging (grad transpose)
@@ -638,7 +651,19 @@ struct hb_ctx {
   int pend_rows = 0;
   double pend_eta = 0.0;
   uint32_t pend_flags = 0;
+  // HB_STEP_LAND_ASYNC (sole writer): the call returns once the step and its
+  // loss are done; the merged layers' write-backs land in the host model in the
+  // background (the next call's batch copy and forward overlap them)
+  bool xland = false;                  // this call defers its write-backs
+  bool land_pending = false;           // write-backs of a deferred call may be in flight
+  std::vector<double*> land_ws;        // the host model they land in
+  std::vector<cudaEvent_t> xmerged_ev;  // layer l's merged float64 values are on the device
+  std::vector<char> xmerged_rec;       // ... recorded by the pending call
 };
+
+extern "C" {
+static int land_wait(hb_ctx* c);  // (defined in the extern "C" block below)
+}
 
 namespace {
 
@@ -654,6 +679,7 @@ int ctx_check(hb_ctx* c) {
   HB_CUDA(cudaSetDevice(c->device));
   return HB_OK;
 }
+
 
 // Profiling marks: (kernel name, begin event, end event) on the step stream.
 // Eager steps take events from a reusable pool; a captured graph owns its
@@ -905,6 +931,8 @@ static void xtl(hb_ctx* c, cudaStream_t s, const char* fmt, int a = 0, int b = 0
   if (!xchg_debug()) return;
   char buf[96];
   snprintf(buf, sizeof buf, fmt, a, b);
+  static const char* only = getenv("HB_XTL_ONLY");  // record only labels containing this (and begin / end)
+  if (only && !strstr(buf, only) && strcmp(buf, "begin") != 0 && strcmp(buf, "end") != 0) return;
   cudaEvent_t e = nullptr;
   for (auto& p : g_xtl)
     if (p.first == buf) e = p.second;
@@ -1153,6 +1181,15 @@ int xchg_use(hb_ctx* c, int l) {
 // float64), chunk k read H2D while chunk k-1 is updated and written back D2H.
 // Each chunk is read just before it is written, so the window in which a
 // concurrent host writer's update could be overwritten stays one chunk long.
+// deferred calls: "layer l's merged values (and every read of its gradient)
+// are done" -- the next step waits for this before it converts or rewrites them
+static int record_merged(hb_ctx* c, int l, cudaStream_t ms) {
+  if (!c->xland) return HB_OK;
+  HB_CUDA(cudaEventRecord(c->xmerged_ev[l], ms));
+  c->xmerged_rec[l] = 1;
+  return HB_OK;
+}
+
 int xchg_merge(hb_ctx* c, int l, double eta, const DevStep* ds, cudaStream_t src = nullptr) {
   if (c->xw.empty()) return HB_OK;
   if (src == nullptr) src = c->stream;
@@ -1169,6 +1206,7 @@ int xchg_merge(hb_ctx* c, int l, double eta, const DevStep* ds, cudaStream_t src
     // device lane: the reduce kernel already merged the freshly read host
     // rows; write them back
     HB_CUDA(cudaStreamWaitEvent(ms, c->xgrad_ev[l], 0));
+    HB_TRY(record_merged(c, l, ms));
     HB_CUDA(cudaMemcpyAsync(c->xw[l], c->stage_all + layer_offset(c, l),
                             static_cast<size_t>(rows) * cols * sizeof(double), cudaMemcpyDeviceToHost, ms));
     xtl(c, ms, "mrg: layer %d written back (device lane)", l);
@@ -1180,12 +1218,15 @@ int xchg_merge(hb_ctx* c, int l, double eta, const DevStep* ds, cudaStream_t src
     // (w + (-eta) * g, NumPy's rounding) and the merged layer goes D2H in place
     // of the gradient -- no host read-modify-write, no merge read
     HB_CUDA(cudaStreamWaitEvent(ms, c->xgrad_ev[l], 0));
+    static const bool keep_pdl = getenv("HB_XCHG_KEEP_PDL") && getenv("HB_XCHG_KEEP_PDL")[0] == '1';
+    if (!keep_pdl) t_no_pdl_once = src;
     const size_t n = static_cast<size_t>(rows) * cols;
     const size_t off = layer_offset(c, l);
     merge_host_f64_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 4)), 256, 0, ms>>>(
         c->stage_all + off, c->G[l], tr ? c->ldw[0] : cols, rows, cols, tr ? 1 : 0, eta, ds);
     HB_CUDA(cudaGetLastError());
     c->last_launches++;
+    HB_TRY(record_merged(c, l, ms));
     HB_CUDA(cudaMemcpyAsync(c->xw[l], c->stage_all + off, n * sizeof(double), cudaMemcpyDeviceToHost, ms));
     if (l < static_cast<int>(c->xdma_used.size())) c->xdma_used[l] = 2;  // merged on the device (no host pass)
     xtl(c, ms, "mrg: layer %d written back (mirror lane)", l);
@@ -1215,6 +1256,7 @@ int xchg_merge(hb_ctx* c, int l, double eta, const DevStep* ds, cudaStream_t src
       HB_CUDA(cudaGetLastError());
       c->last_launches++;
     }
+    HB_TRY(record_merged(c, l, ms));
     xtl(c, ms, "mrg: gradient %d on host", l);
     return HB_OK;
   }
@@ -1286,6 +1328,7 @@ int xchg_end(hb_ctx* c) {
   for (size_t l = 0; l < c->xmrg_l.size(); ++l) {  // every layer's merge stream this call used
     if (!c->xmrg_used[l]) continue;
     c->xmrg_used[l] = 0;
+    if (c->xland) continue;  // deferred: lands in the background (land_wait / the next step's waits)
     HB_CUDA(cudaEventRecord(c->xmdone_ev[l], c->xmrg_l[l]));
     HB_CUDA(cudaStreamWaitEvent(c->stream, c->xmdone_ev[l], 0));
   }
@@ -1786,7 +1829,7 @@ int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double
                           (c->merge_layers ? (1u << 18) : 0u) |
                           (v.x_lo_zero ? (1u << 16) : 0u) | (c->xmirror ? (1u << 17) : 0u);
   const bool view_epoch = (&v == &c->epoch);
-  if (!c->use_graphs || !graph_ok) return run_phase(c, v, start, rows, flags, eta, nullptr, phase);
+  if (!c->use_graphs || !graph_ok || c->xland) return run_phase(c, v, start, rows, flags, eta, nullptr, phase);
   const auto key = std::make_tuple(rows, gflags, view_epoch ? c->view_gen : -c->view_gen, c->prof_on,
                                    c->xw.empty() ? 0LL : c->xgen);
   DevStep hs{start, static_cast<float>(eta), 0, eta, c->peer_gen};
@@ -1994,6 +2037,21 @@ int enqueue_merge(hb_ctx* c, bool bump = true) {
 // `mid` (optional): host work run between the enqueued forward and backward
 // phases (the host-buffer CSR step builds the batch CSC there, overlapping the
 // device forward pass).
+// The step's loss sum to the host: a one-thread kernel stores it into mapped
+// pinned memory.  A D2H copy would queue on the copy engine behind the merged
+// layers a replica call writes back (tens to hundreds of MB), so a deferred
+// call (HB_STEP_LAND_ASYNC) would still wait for them.
+__global__ void store_loss_kernel(const double* d, volatile double* h) { *h = *d; }
+int read_loss(hb_ctx* c, double* out) {
+  *reinterpret_cast<volatile double*>(c->h_loss) = 0.0;
+  store_loss_kernel<<<1, 1, 0, c->stream>>>(c->d_loss, c->h_loss);
+  HB_CUDA(cudaGetLastError());
+  c->last_launches++;
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  *out = *reinterpret_cast<volatile double*>(c->h_loss);
+  return HB_OK;
+}
+
 int do_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta, uint32_t flags, double* out_loss,
             bool graph_ok = true, const std::function<int()>& mid = nullptr) {
   if (c->pend_active) return fail(HB_ESTATE, "a replica step is in flight (hb_replica_end first)");
@@ -2013,6 +2071,13 @@ int do_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta,
     ensure_flat_layout(c);
     if (c->merge_layers) HB_TRY(ensure_comm_stream(c));
   }
+  if (c->land_pending) {
+    // a deferred call's merges read G_l and write the float64 copy this step
+    // converts: wait for them (its write-backs keep running)
+    for (int l = 0; l < c->L && l < static_cast<int>(c->xmerged_rec.size()); ++l)
+      if (c->xmerged_rec[l]) HB_CUDA(cudaStreamWaitEvent(c->stream, c->xmerged_ev[l], 0));
+  }
+  std::fill(c->xmerged_rec.begin(), c->xmerged_rec.end(), 0);
   if (timed) HB_CUDA(cudaEventRecord(c->ev0, c->stream));
   if (mid) {
     HB_TRY(enqueue_step(c, v, start, rows, eta, flags, graph_ok, 1));
@@ -2027,8 +2092,7 @@ int do_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta,
   c->grads_valid = (flags & HB_STEP_EMIT_GRAD) != 0;
   if (out_loss != nullptr) {
     double s = 0.0;
-    HB_CUDA(cudaMemcpyAsync(&s, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    HB_CUDA(cudaStreamSynchronize(c->stream));
+    HB_TRY(read_loss(c, &s));
     *out_loss = s / rows;
   } else if (!(flags & HB_STEP_ASYNC) || c->prof_on) {
     HB_CUDA(cudaStreamSynchronize(c->stream));
@@ -2369,6 +2433,7 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
   c->ws_loss_n = std::max(cdiv(c->cap, kHeadRowsPerBlock), cdiv(c->cap, 8)) + 1;
   HB_CK(cudaMalloc(&c->ws_loss, c->ws_loss_n * sizeof(double)));
   HB_CK(cudaMalloc(&c->d_loss, sizeof(double)));
+  HB_CK(cudaHostAlloc(&c->h_loss, sizeof(double), cudaHostAllocMapped));
   HB_CK(cudaMalloc(&c->d_step, sizeof(DevStep)));
   if (c->sparse) {
     HB_CK(cudaMalloc(&c->csc_lo, static_cast<size_t>(c->d[0]) * sizeof(long long)));
@@ -2415,6 +2480,7 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
 int hb_ctx_destroy(hb_ctx* c) {
   if (!c) return HB_OK;
   cudaSetDevice(c->device);
+  land_wait(c);
   if (c->stream) cudaStreamSynchronize(c->stream);
   hb_comm_destroy(c);
   drop_graphs(c);
@@ -2447,6 +2513,7 @@ int hb_ctx_destroy(hb_ctx* c) {
   cudaFree(c->ws_loss);
   cudaFree(c->tile_sync);
   cudaFree(c->d_loss);
+  cudaFreeHost(c->h_loss);
   cudaFree(c->stage64);
   cudaFree(c->stage32);
   cudaFree(c->stage_all);
@@ -2503,6 +2570,7 @@ int hb_ctx_destroy(hb_ctx* c) {
 
 int hb_set_weights_f64(hb_ctx* c, int layer, const double* w) {
   HB_TRY(ctx_check(c));
+  HB_TRY(land_wait(c));  // (the staging buffer is reused)
   if (layer < 0 || layer >= c->L || !w) return fail(HB_EINVAL, "bad layer %d or null weights", layer);
   const int rows = c->d[layer + 1], cols = c->d[layer];
   const size_t n = static_cast<size_t>(rows) * cols;
@@ -2692,6 +2760,7 @@ int hb_set_bias_f64(hb_ctx* c, int layer, const double* b) {
 
 int hb_set_weights_all_f64(hb_ctx* c, const double* const* ws) {
   HB_TRY(ctx_check(c));
+  HB_TRY(land_wait(c));  // (the staging buffer is reused)
   if (!ws) return fail(HB_EINVAL, "null weight array");
   HB_TRY(ensure_stage_all(c));
   c->mirror_valid = false;  // the staging buffer is reused below
@@ -2732,6 +2801,7 @@ int hb_set_weights_all_f64(hb_ctx* c, const double* const* ws) {
 
 int hb_merge_grads_all_into_f64(hb_ctx* c, double* const* ws, double eta) {
   HB_TRY(ctx_check(c));
+  HB_TRY(land_wait(c));  // (the staging buffer is reused)
   if (!ws) return fail(HB_EINVAL, "null weight array");
   if (!c->grads_valid) return fail(HB_ESTATE, "no gradient kept: run a step with HB_STEP_EMIT_GRAD first");
   HB_TRY(ensure_stage_all(c));
@@ -2836,6 +2906,7 @@ int hb_merge_grads_all_into_f64(hb_ctx* c, double* const* ws, double eta) {
 
 int hb_merge_grad_into_f64(hb_ctx* c, int layer, double* host_w, double eta) {
   HB_TRY(ctx_check(c));
+  HB_TRY(land_wait(c));  // (the staging buffer is reused)
   if (layer < 0 || layer >= c->L || !host_w) return fail(HB_EINVAL, "bad layer %d or null weights", layer);
   const int rows = c->d[layer + 1], cols = c->d[layer];
   const size_t n = static_cast<size_t>(rows) * cols;
@@ -2947,9 +3018,36 @@ static void mirror_sample(const hb_ctx* c, double* const* ws, std::vector<double
   }
 }
 
+// Wait until the write-backs of a deferred (HB_STEP_LAND_ASYNC) call are in
+// the host model, then fingerprint it for the resident-mirror check.
+static int land_wait(hb_ctx* c) {
+  if (!c->land_pending) return HB_OK;
+  c->land_pending = false;
+  cudaError_t err = cudaSuccess;
+  for (cudaStream_t st : c->xmrg_l) {
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (err == cudaSuccess) err = e;
+  }
+  if (err != cudaSuccess) {
+    c->mirror_valid = false;
+    return fail(HB_ECUDA, "deferred write-back failed: %s", cudaGetErrorString(err));
+  }
+  if (c->mirror_valid && c->land_ws.size() == static_cast<size_t>(c->L))
+    mirror_sample(c, c->land_ws.data(), c->fp_vals);
+  return HB_OK;
+}
+
 static int xchg_arm(hb_ctx* c, double* const* ws, uint32_t flags) {
   g_call_t0 = std::chrono::steady_clock::now();
   if (!ws) return fail(HB_EINVAL, "null weight array");
+  const bool defer = (flags & HB_STEP_LAND_ASYNC) != 0;
+  if (defer && !(flags & HB_STEP_SOLE_WRITER))
+    return fail(HB_EINVAL, "HB_STEP_LAND_ASYNC needs HB_STEP_SOLE_WRITER (nobody else may write the host model)");
+  // a deferred chain continues only on the same host arrays; anything else
+  // (another model, a call that lands before returning) waits for the landing
+  if (c->land_pending && !(defer && c->land_ws.size() == static_cast<size_t>(c->L) &&
+                           std::equal(c->land_ws.begin(), c->land_ws.end(), ws)))
+    HB_TRY(land_wait(c));
   // (the page-lock check costs a driver call per layer: once per pointer set)
   const long long epoch = g_pin_epoch.load();
   const bool same_set = c->xw_prev.size() == static_cast<size_t>(c->L) &&
@@ -2969,9 +3067,12 @@ static int xchg_arm(hb_ctx* c, double* const* ws, uint32_t flags) {
     c->xmrg_l.resize(c->L);
     c->xmdone_ev.resize(c->L);
     c->xmrg_used.assign(c->L, 0);
+    c->xmerged_ev.resize(c->L);
+    c->xmerged_rec.assign(c->L, 0);
     for (int l = 0; l < c->L; ++l) {
       HB_CUDA(cudaStreamCreateWithPriority(&c->xmrg_l[l], cudaStreamNonBlocking, hi_prio));
       HB_CUDA(cudaEventCreateWithFlags(&c->xmdone_ev[l], cudaEventDisableTiming));
+      HB_CUDA(cudaEventCreateWithFlags(&c->xmerged_ev[l], cudaEventDisableTiming));
     }
     HB_CUDA(cudaEventCreateWithFlags(&c->xstart_ev, cudaEventDisableTiming));
     HB_CUDA(cudaEventCreateWithFlags(&c->xdone_ev, cudaEventDisableTiming));
@@ -3007,11 +3108,18 @@ static int xchg_arm(hb_ctx* c, double* const* ws, uint32_t flags) {
              !(getenv("HB_NO_MIRROR") && getenv("HB_NO_MIRROR")[0] == '1');
   c->xmirror = false;
   if (c->xsole && c->mirror_valid && c->mirror_gen == c->xgen) {
-    std::vector<double> now;
-    mirror_sample(c, ws, now);
-    c->xmirror = now.size() == c->fp_vals.size() &&
-                 std::memcmp(now.data(), c->fp_vals.data(), now.size() * sizeof(double)) == 0;
+    if (c->land_pending) {
+      // deferred chain: the host copy is still landing (it cannot be sampled);
+      // the sole-writer declaration covers it until hb_replica_landed
+      c->xmirror = true;
+    } else {
+      std::vector<double> now;
+      mirror_sample(c, ws, now);
+      c->xmirror = now.size() == c->fp_vals.size() &&
+                   std::memcmp(now.data(), c->fp_vals.data(), now.size() * sizeof(double)) == 0;
+    }
   }
+  c->xland = defer && c->xsole;  // (the DMA merge mode lands before returning)
   c->mirror_valid = false;  // until this call completes
   c->xseq = c->xseq == 0x7fffffff ? 1 : c->xseq + 1;
   *reinterpret_cast<volatile int32_t*>(c->xseq_host) = c->xseq;
@@ -3059,6 +3167,9 @@ static int replica_finish(hb_ctx* c, int rc, int rows, double eta, uint32_t flag
     if (c->xmrg) cudaStreamSynchronize(c->xmrg);
     for (auto st_ : c->xmrg_l) cudaStreamSynchronize(st_);
     if (c->side) cudaStreamSynchronize(c->side);
+    c->land_pending = false;
+    c->xland = false;
+    c->mirror_valid = false;
     return rc;
   }
   const bool timed = (flags & HB_STEP_TIMED) != 0;
@@ -3066,8 +3177,7 @@ static int replica_finish(hb_ctx* c, int rc, int rows, double eta, uint32_t flag
   HB_TRY(xchg_host_merges(c, eta));
   if (out_loss != nullptr) {
     double sum = 0.0;
-    HB_CUDA(cudaMemcpyAsync(&sum, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    HB_CUDA(cudaStreamSynchronize(c->stream));
+    HB_TRY(read_loss(c, &sum));
     *out_loss = sum / rows;
   } else {
     HB_CUDA(cudaStreamSynchronize(c->stream));
@@ -3077,8 +3187,14 @@ static int replica_finish(hb_ctx* c, int rc, int rows, double eta, uint32_t flag
   if (c->xsole) {  // the staging buffer now equals the host model
     c->mirror_valid = true;
     c->mirror_gen = c->xgen;
-    mirror_sample(c, c->xw.data(), c->fp_vals);
+    if (c->xland) {  // ... and will, once the write-backs land (fingerprinted then)
+      c->land_pending = true;
+      c->land_ws = c->xw;
+    } else {
+      mirror_sample(c, c->xw.data(), c->fp_vals);
+    }
   }
+  c->xland = false;
   xmark("done");
   return HB_OK;
 }
@@ -3959,7 +4075,13 @@ extern "C" int hb_trace_cta_read(unsigned long long* out) {
 int hb_synchronize(hb_ctx* c) {
   HB_TRY(ctx_check(c));
   HB_CUDA(cudaStreamSynchronize(c->stream));
-  return HB_OK;
+  return land_wait(c);
+}
+
+int hb_replica_landed(hb_ctx* c) {
+  HB_TRY(ctx_check(c));
+  if (c->pend_active) return fail(HB_ESTATE, "a replica step is in flight (hb_replica_end first)");
+  return land_wait(c);
 }
 
 int hb_nccl_unique_id(void* out) {

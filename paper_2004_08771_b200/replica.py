@@ -281,27 +281,41 @@ class GpuReplica:
         self._tbl_key = key
         return self._tbl
 
+    @staticmethod
+    def _replica_flags(timed: bool, sole_writer: bool, land_async: bool) -> int:
+        if land_async and not sole_writer:
+            raise ValueError("land_async needs sole_writer=True")
+        return ((N.HB_STEP_TIMED if timed else 0) | (N.HB_STEP_SOLE_WRITER if sole_writer else 0)
+                | (N.HB_STEP_LAND_ASYNC if land_async else 0))
+
+    def landed(self) -> None:
+        """Wait until the write-backs of land_async calls are in the host model."""
+        N.check(self._lib.hb_replica_landed(self._h))
+
     def replica_step(self, weights, start: int, rows: int, eta: float, timed: bool = False,
-                     want_loss: bool = False, sole_writer: bool = False):
+                     want_loss: bool = False, sole_writer: bool = False, land_async: bool = False):
         """execute_batch_replica (workers.py:126-138) on staged rows in one call:
         snapshot of the shared float64 `weights`, the step, and the stale merge
         weights[l] -= eta * g_l, with the snapshot / merge DMAs overlapped with
         the compute layer by layer.  Returns the batch's mean loss if want_loss.
         sole_writer=True promises that no other thread writes `weights` during
-        the call, which lets the largest layers merge on the device lane."""
+        the call, which lets the largest layers merge on the device lane.
+        land_async=True (sole writers) returns before the merged layers have
+        landed in `weights`: the next call overlaps them; landed() (or any call
+        on another model) waits -- do not read `weights` in between."""
         table = self._model_table(weights)
-        flags = (N.HB_STEP_TIMED if timed else 0) | (N.HB_STEP_SOLE_WRITER if sole_writer else 0)
+        flags = self._replica_flags(timed, sole_writer, land_async)
         loss = C.c_double(0.0)
         N.check(self._lib.hb_replica_step(self._h, table, int(start), int(rows), float(eta), flags,
                                           C.byref(loss) if want_loss else None))
         return loss.value if want_loss else None
 
     def replica_begin(self, weights, start: int, rows: int, eta: float, timed: bool = False,
-                      sole_writer: bool = False) -> None:
+                      sole_writer: bool = False, land_async: bool = False) -> None:
         """First half of replica_step: enqueue snapshot, step and gradient
         copies and return; replica_end applies the stale merge and waits."""
         table = self._model_table(weights)
-        flags = (N.HB_STEP_TIMED if timed else 0) | (N.HB_STEP_SOLE_WRITER if sole_writer else 0)
+        flags = self._replica_flags(timed, sole_writer, land_async)
         N.check(self._lib.hb_replica_begin(self._h, table, int(start), int(rows), float(eta), flags))
 
     def replica_end(self, want_loss: bool = False):
@@ -310,10 +324,10 @@ class GpuReplica:
         return loss.value if want_loss else None
 
     def replica_step_host(self, weights, batch, labels, eta: float, timed: bool = False, want_loss: bool = True,
-                          sole_writer: bool = False):
+                          sole_writer: bool = False, land_async: bool = False):
         """replica_step on a batch held in host memory (float32 rows or a CsrDataset)."""
         table = self._model_table(weights)
-        flags = (N.HB_STEP_TIMED if timed else 0) | (N.HB_STEP_SOLE_WRITER if sole_writer else 0)
+        flags = self._replica_flags(timed, sole_writer, land_async)
         loss = C.c_double(0.0)
         lp = C.byref(loss) if want_loss else None
         if isinstance(batch, CsrDataset):

@@ -410,6 +410,78 @@ def test_fused_replica_step_device_lane(hb):
         three.close()
 
 
+@pytest.mark.parametrize("kind", ["dense", "csr_kernels", "wide_head", "device_lane"])
+def test_land_async_chain_matches_sequential(hb, kind):
+    """HB_STEP_LAND_ASYNC: deferred write-backs chained over several calls give
+    the same losses on every call and, once landed, the bit-identical host
+    model of sequential sole-writer calls; a call that lands before returning
+    (or set_weights) after the chain waits for the landing first, and a host
+    write after landed() is caught by the mirror fingerprint."""
+    sizes, n, b = {"dense": ((54, 128, 128, 2), 640, 160), "csr_kernels": ((600, 256, 128, 2), 640, 160),
+                   "wide_head": ((40, 96, 70), 640, 160), "device_lane": ((64, 512, 512, 2), 8192, 4096)}[kind]
+    sparse = kind.startswith("csr")
+    w0 = ref_nn.init_weights(sizes, 15)
+    if sparse:
+        data = hb.synthetic_csr(n, sizes[0], 9, sizes[-1], seed=16)
+        data.val = data.val.astype(np.float32)
+        batches = [(data.rows(i * b, (i + 1) * b), None) for i in range(n // b)]
+    else:
+        x, y = ref_nn.synthetic_blobs(n, sizes[0], sizes[-1], 2.5, 17)
+        x = x.astype(np.float32)
+        batches = [(x[i * b:(i + 1) * b], y[i * b:(i + 1) * b]) for i in range(n // b)]
+    kw = dict(sparse=sparse, sparse_kernels=(kind == "csr_kernels"))
+    dfr, seq = hb.GpuReplica(sizes, b, **kw), hb.GpuReplica(sizes, b, **kw)
+    wd, ws = [a.copy() for a in w0], [a.copy() for a in w0]
+    dfr.pin_host(wd)
+    seq.pin_host(ws)
+    with pytest.raises(ValueError):
+        dfr.replica_step_host(wd, *batches[0], 0.1, land_async=True)
+    try:
+        for rnd in range(2):
+            for it in range(5):
+                xb, yb = batches[it % len(batches)]
+                eta = 0.3 + 0.05 * it
+                ld = dfr.replica_step_host(wd, xb, yb, eta, sole_writer=True, land_async=True)
+                ls = seq.replica_step_host(ws, xb, yb, eta, sole_writer=True)
+                assert ld == ls, (rnd, it)
+            if rnd == 0:
+                # a call that lands before returning, on the same arrays: waits first
+                xb, yb = batches[0]
+                assert dfr.replica_step_host(wd, xb, yb, 0.2, sole_writer=True) == \
+                    seq.replica_step_host(ws, xb, yb, 0.2, sole_writer=True)
+            else:
+                dfr.landed()
+            for a, c in zip(wd, ws):
+                assert np.array_equal(a, c), rnd
+            # another writer moves the model (after the landing): the next
+            # deferred call must snapshot it, not reuse the device copy
+            for a, c in zip(wd, ws):
+                a *= 0.999
+                c *= 0.999
+        # set_weights after a pending chain lands first (it reuses the staging buffer)
+        xb, yb = batches[1]
+        dfr.replica_step_host(wd, xb, yb, 0.25, sole_writer=True, land_async=True)
+        seq.replica_step_host(ws, xb, yb, 0.25, sole_writer=True)
+        dfr.set_weights(w0)
+        for a, c in zip(wd, ws):
+            assert np.array_equal(a, c)
+        if not sparse:
+            # the staged form and the begin / end split
+            for c in (dfr, seq):
+                c.stage(x, y)
+            for it in range(3):
+                dfr.replica_begin(wd, it * b % n, b, 0.2, sole_writer=True, land_async=True)
+                l1 = dfr.replica_end(want_loss=True)
+                l2 = seq.replica_step(ws, it * b % n, b, 0.2, want_loss=True, sole_writer=True)
+                assert l1 == l2, it
+            dfr.landed()
+            for a, c in zip(wd, ws):
+                assert np.array_equal(a, c)
+    finally:
+        dfr.close()
+        seq.close()
+
+
 def test_two_worker_threads_merge_concurrently(hb):
     """Two GPU replica workers on their own threads (the reference engine runs
     each worker as a thread, engine.py:131-134) exchange with two shared host

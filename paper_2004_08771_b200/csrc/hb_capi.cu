@@ -45,6 +45,7 @@
 #include "hb_gemm.cuh"
 #include "hb_kernels.cuh"
 #include "hb_peer.cuh"
+#include "hb_small.cuh"
 
 using namespace hb;
 
@@ -659,6 +660,12 @@ struct hb_ctx {
   std::vector<double*> land_ws;        // the host model they land in
   std::vector<cudaEvent_t> xmerged_ev;  // layer l's merged float64 values are on the device
   std::vector<char> xmerged_rec;       // ... recorded by the pending call
+  // small nets (hb_small.cuh): the whole training step as one persistent kernel
+  bool sn_ok = false;          // shape qualifies (dense, small head, widths <= kSnMaxWidth) and HB_SMALL_NET=1
+  int sn_grid = 0;             // CTAs of the cooperative launch (all co-resident)
+  float* sn_hd = nullptr;      // (kSnMaxRows, 4) output error signal
+  double* sn_loss = nullptr;   // (kSnMaxRows) per-row loss
+  unsigned* sn_bar = nullptr;  // grid barrier counter
 };
 
 extern "C" {
@@ -1813,13 +1820,76 @@ int run_backward(hb_ctx* c, const DataView& v, long long start, int rows, uint32
 // seen; from the second time on, the whole step is a captured CUDA graph that
 // reads (start, eta) from c->d_step, so a step costs one graph launch.
 // phase 0: whole step; 1: forward (incl. the fused head and its update); 2: backward
+int run_small_net(hb_ctx* c, const DataView& v, long long start, int rows, uint32_t flags, double eta,
+                  const DevStep* ds);
+
 int run_phase(hb_ctx* c, const DataView& v, long long start, int rows, uint32_t flags, double eta, const DevStep* ds,
               int phase) {
+  if (phase == 0 && c->sn_ok && rows <= kSnMaxRows && !c->merge_layers && v.x != nullptr)
+    return run_small_net(c, v, start, rows, flags, eta, ds);
   if (phase != 2) c->xdma_used.assign(c->L, 0);
   if (phase != 2) HB_TRY(xchg_begin(c));
   if (phase != 2) HB_TRY(run_forward(c, v, start, rows, true, flags, eta, ds));
   if (phase != 1) HB_TRY(run_backward(c, v, start, rows, flags, eta, ds));
   if (phase != 1) HB_TRY(xchg_end(c));
+  return HB_OK;
+}
+
+// The whole step of a small net (hb_small.cuh): the snapshot conversions, one
+// cooperative launch, then every layer's stale merge (top layer first, as the
+// backward produces them).
+int run_small_net(hb_ctx* c, const DataView& v, long long start, int rows, uint32_t flags, double eta,
+                  const DevStep* ds) {
+  const int L = c->L;
+  c->xdma_used.assign(L, 0);
+  HB_TRY(xchg_begin(c));
+  for (int l = 0; l < L; ++l) HB_TRY(xchg_use(c, l));
+  SmallNetArgs p{};
+  p.L = L;
+  p.rows = rows;
+  p.train = 1;
+  for (int l = 0; l <= L; ++l) {
+    p.d[l] = c->d[l];
+    p.ld[l] = c->ld[l];
+  }
+  p.x = v.x;
+  p.ldx = v.ldx;
+  p.start = start;
+  p.labels = v.labels;
+  p.ds = ds;
+  p.eta = static_cast<float>(eta);
+  const bool emit = (flags & HB_STEP_EMIT_GRAD) != 0;
+  for (int l = 0; l < L; ++l) {
+    p.W[l] = c->W[l];
+    p.W_lo[l] = c->need_lo() ? c->W_lo[l] : nullptr;
+    p.ldw[l] = c->ldw[l];
+    p.bias[l] = l < L - 1 ? layer_bias(c, l) : nullptr;
+    p.A[l] = c->A[l];
+    p.D[l] = c->D[l];
+    p.G[l] = emit ? c->G[l] : nullptr;
+  }
+  p.hd = c->sn_hd;
+  p.row_loss = c->sn_loss;
+  p.loss_out = c->d_loss;
+  p.bar = c->sn_bar;
+  cudaStream_t st = c->stream;
+  HB_CUDA(cudaMemsetAsync(c->sn_bar, 0, sizeof(unsigned), st));
+  prof_begin(c, "small_net_step", 0);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(c->sn_grid);
+  cfg.blockDim = dim3(kSnThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HB_CUDA(cudaLaunchKernelEx(&cfg, small_net_step_kernel, p));
+  prof_end(c, "small_net_step", 0);
+  c->last_launches++;
+  for (int l = L - 1; l >= 0; --l) HB_TRY(xchg_merge(c, l, eta, ds));
+  HB_TRY(xchg_end(c));
   return HB_OK;
 }
 
@@ -2472,6 +2542,25 @@ int hb_ctx_create(hb_ctx** out, int device, int n_layers, const int* sizes, int 
     if (rc != HB_OK) return bail(rc);
   }
   c->batch.labels = c->blabels;
+  {
+    const char* e = getenv("HB_SMALL_NET");
+    // opt-in (HB_SMALL_NET=1): measured slower than the per-layer tcgen05 path at
+    // the covtype config (0.23 vs 0.092 ms/step, profiles/r02_small_net.txt)
+    bool ok = !c->sparse && c->passes == 3 && c->small_head && L >= 2 && L <= kSnMaxL && (e && e[0] == '1');
+    for (int l = 0; l < L; ++l) ok = ok && c->d[l] <= kSnMaxWidth;
+    if (ok) {
+      int sms = 0, per_sm = 0;
+      HB_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+      HB_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_net_step_kernel, kSnThreads, 0));
+      if (per_sm >= 1) {
+        c->sn_grid = sms * std::min(per_sm, 2);  // two CTAs per SM: a B phase's dX and dW tiles in one wave
+        HB_CK(cudaMalloc(&c->sn_hd, kSnMaxRows * 4 * sizeof(float)));
+        HB_CK(cudaMalloc(&c->sn_loss, kSnMaxRows * sizeof(double)));
+        HB_CK(cudaMalloc(&c->sn_bar, sizeof(unsigned)));
+        c->sn_ok = true;
+      }
+    }
+  }
 #undef HB_CK
   *out = c;
   return HB_OK;
@@ -2511,6 +2600,9 @@ int hb_ctx_destroy(hb_ctx* c) {
   cudaFree(c->bcval);
   cudaFree(c->ws);
   cudaFree(c->ws_loss);
+  cudaFree(c->sn_hd);
+  cudaFree(c->sn_loss);
+  cudaFree(c->sn_bar);
   cudaFree(c->tile_sync);
   cudaFree(c->d_loss);
   cudaFreeHost(c->h_loss);

@@ -1,3 +1,4 @@
+# GPU parity tests of the opt-in persistent small-net step, then the covtype bench with it on and off
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_gpu_small_net.py -x -q -p no:cacheprovider > gpurun_out/small.log 2>&1; echo small_rc=$?; tail -30 gpurun_out/small.log
 timeout 300 python bench.py --config covtype --skip-cpu --no-ttt > gpurun_out/cov_fused.json 2> gpurun_out/cov_fused.err; echo rc=$?

@@ -406,6 +406,7 @@ struct Mark {
 struct StepGraph {
   cudaGraphExec_t exec = nullptr;
   std::vector<char> xdma_used;  // device-lane merges inside this graph
+  std::vector<char> d2h_defer;  // deferred-landing graphs: layers whose D2H follows the launch
   std::vector<Mark> marks;
   std::vector<cudaEvent_t> events;
   int launches = 0;
@@ -660,6 +661,13 @@ struct hb_ctx {
   std::vector<double*> land_ws;        // the host model they land in
   std::vector<cudaEvent_t> xmerged_ev;  // layer l's merged float64 values are on the device
   std::vector<char> xmerged_rec;       // ... recorded by the pending call
+  // deferred calls replayed from the step graph (every layer on the mirror
+  // lane): the graph ends after the merge kernels; each merged layer's D2H is
+  // issued after the graph launch, on the layer's merge stream, behind an
+  // external event the graph records (xd2h_ready_ev), and the next graph's
+  // merge of that layer waits for xd2h_done_ev before it rewrites the rows
+  std::vector<cudaEvent_t> xd2h_ready_ev, xd2h_done_ev;
+  std::vector<char> xd2h_defer;        // layers whose D2H the graph being captured leaves to its launcher
   // small nets (hb_small.cuh): the whole training step as one persistent kernel
   bool sn_ok = false;          // shape qualifies (dense, small head, widths <= kSnMaxWidth) and HB_SMALL_NET=1
   int sn_grid = 0;             // CTAs of the cooperative launch (all co-resident)
@@ -1192,7 +1200,8 @@ int xchg_use(hb_ctx* c, int l) {
 // are done" -- the next step waits for this before it converts or rewrites them
 static int record_merged(hb_ctx* c, int l, cudaStream_t ms) {
   if (!c->xland) return HB_OK;
-  HB_CUDA(cudaEventRecord(c->xmerged_ev[l], ms));
+  HB_CUDA(c->capturing ? cudaEventRecordWithFlags(c->xmerged_ev[l], ms, cudaEventRecordExternal)
+                       : cudaEventRecord(c->xmerged_ev[l], ms));
   c->xmerged_rec[l] = 1;
   return HB_OK;
 }
@@ -1229,12 +1238,22 @@ int xchg_merge(hb_ctx* c, int l, double eta, const DevStep* ds, cudaStream_t src
     if (!keep_pdl) t_no_pdl_once = src;
     const size_t n = static_cast<size_t>(rows) * cols;
     const size_t off = layer_offset(c, l);
+    const bool defer_d2h = c->xland && c->capturing;
+    if (defer_d2h)  // the previous call's copy of these rows was issued outside any graph
+      HB_CUDA(cudaStreamWaitEvent(ms, c->xd2h_done_ev[l], cudaEventWaitExternal));
     merge_host_f64_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 4)), 256, 0, ms>>>(
         c->stage_all + off, c->G[l], tr ? c->ldw[0] : cols, rows, cols, tr ? 1 : 0, eta, ds);
     HB_CUDA(cudaGetLastError());
     c->last_launches++;
     HB_TRY(record_merged(c, l, ms));
+    if (defer_d2h) {
+      HB_CUDA(cudaEventRecordWithFlags(c->xd2h_ready_ev[l], ms, cudaEventRecordExternal));
+      c->xd2h_defer[l] = 1;
+      if (l < static_cast<int>(c->xdma_used.size())) c->xdma_used[l] = 2;
+      return HB_OK;
+    }
     HB_CUDA(cudaMemcpyAsync(c->xw[l], c->stage_all + off, n * sizeof(double), cudaMemcpyDeviceToHost, ms));
+    if (c->xland) HB_CUDA(cudaEventRecord(c->xd2h_done_ev[l], ms));
     if (l < static_cast<int>(c->xdma_used.size())) c->xdma_used[l] = 2;  // merged on the device (no host pass)
     xtl(c, ms, "mrg: layer %d written back (mirror lane)", l);
     return HB_OK;
@@ -1335,7 +1354,8 @@ int xchg_end(hb_ctx* c) {
   for (size_t l = 0; l < c->xmrg_l.size(); ++l) {  // every layer's merge stream this call used
     if (!c->xmrg_used[l]) continue;
     c->xmrg_used[l] = 0;
-    if (c->xland) continue;  // deferred: lands in the background (land_wait / the next step's waits)
+    if (c->xland && !c->capturing) continue;  // deferred: lands in the background (land_wait / the next step's waits)
+    // (a captured deferred step joins its merge streams: they hold only the merge kernels, the D2H follows the launch)
     HB_CUDA(cudaEventRecord(c->xmdone_ev[l], c->xmrg_l[l]));
     HB_CUDA(cudaStreamWaitEvent(c->stream, c->xmdone_ev[l], 0));
   }
@@ -1835,6 +1855,19 @@ int run_phase(hb_ctx* c, const DataView& v, long long start, int rows, uint32_t 
   return HB_OK;
 }
 
+// A deferred (HB_STEP_LAND_ASYNC) call can replay the step graph when every
+// layer merges on the mirror lane (no device lane, no host lane): the graph
+// then carries the merge kernels and leaves the write-backs to its launcher.
+bool land_graph_ok(const hb_ctx* c) {
+  if (c->xmode != 0 || !c->xsole || static_cast<int>(c->xml.size()) < c->L) return false;
+  if (getenv("HB_LAND_EAGER") && getenv("HB_LAND_EAGER")[0] == '1') return false;
+  for (int l = 0; l < c->L; ++l) {
+    if (!c->xml[l]) return false;
+    if (l < static_cast<int>(c->xdma.size()) && c->xdma[l]) return false;
+  }
+  return true;
+}
+
 // The whole step of a small net (hb_small.cuh): the snapshot conversions, one
 // cooperative launch, then every layer's stale merge (top layer first, as the
 // backward produces them).
@@ -1896,10 +1929,11 @@ int run_small_net(hb_ctx* c, const DataView& v, long long start, int rows, uint3
 int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double eta, uint32_t flags, bool graph_ok,
                  int phase = 0) {
   const uint32_t gflags = (flags & (HB_STEP_EMIT_GRAD | HB_STEP_SOLE_WRITER)) | (static_cast<uint32_t>(phase) << 8) |
-                          (c->merge_layers ? (1u << 18) : 0u) |
+                          (c->merge_layers ? (1u << 18) : 0u) | (c->xland ? (1u << 19) : 0u) |
                           (v.x_lo_zero ? (1u << 16) : 0u) | (c->xmirror ? (1u << 17) : 0u);
   const bool view_epoch = (&v == &c->epoch);
-  if (!c->use_graphs || !graph_ok || c->xland) return run_phase(c, v, start, rows, flags, eta, nullptr, phase);
+  if (!c->use_graphs || !graph_ok || (c->xland && !land_graph_ok(c)))
+    return run_phase(c, v, start, rows, flags, eta, nullptr, phase);
   const auto key = std::make_tuple(rows, gflags, view_epoch ? c->view_gen : -c->view_gen, c->prof_on,
                                    c->xw.empty() ? 0LL : c->xgen);
   DevStep hs{start, static_cast<float>(eta), 0, eta, c->peer_gen};
@@ -1913,6 +1947,7 @@ int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double
     c->step_marks.clear();
     HB_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     const int launches0 = c->last_launches;
+    c->xd2h_defer.assign(c->L, 0);
     int rc = run_phase(c, v, 0, rows, flags, 0.0, c->d_step, phase);
     cudaGraph_t graph = nullptr;
     cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
@@ -1925,6 +1960,7 @@ int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double
     g.marks = c->step_marks;
     g.events = c->cap_events;
     g.xdma_used = c->xdma_used;
+    g.d2h_defer = c->xd2h_defer;
     g.launches = c->last_launches - launches0;
     c->step_marks.clear();
     c->cap_events.clear();
@@ -1938,6 +1974,16 @@ int enqueue_step(hb_ctx* c, const DataView& v, long long start, int rows, double
   xmark("graph launch");
   c->xdma_used = it->second.xdma_used;
   HB_CUDA(cudaGraphLaunch(it->second.exec, c->stream));
+  // deferred landing: each merged layer's D2H, once the graph has merged it
+  const std::vector<char>& dd = it->second.d2h_defer;
+  for (int l = 0; l < static_cast<int>(dd.size()) && l < c->L; ++l) {
+    if (!dd[l]) continue;
+    cudaStream_t ms = c->xmrg_l[l];
+    HB_CUDA(cudaStreamWaitEvent(ms, c->xd2h_ready_ev[l], 0));
+    HB_CUDA(cudaMemcpyAsync(c->xw[l], c->stage_all + layer_offset(c, l),
+                            static_cast<size_t>(c->d[l + 1]) * c->d[l] * sizeof(double), cudaMemcpyDeviceToHost, ms));
+    HB_CUDA(cudaEventRecord(c->xd2h_done_ev[l], ms));
+  }
   xmark("graph launched");
   c->last_launches += it->second.launches;
   if (c->prof_on) c->step_marks.insert(c->step_marks.end(), it->second.marks.begin(), it->second.marks.end());
@@ -3166,6 +3212,13 @@ static int xchg_arm(hb_ctx* c, double* const* ws, uint32_t flags) {
       HB_CUDA(cudaEventCreateWithFlags(&c->xmdone_ev[l], cudaEventDisableTiming));
       HB_CUDA(cudaEventCreateWithFlags(&c->xmerged_ev[l], cudaEventDisableTiming));
     }
+    c->xd2h_ready_ev.resize(c->L);
+    c->xd2h_done_ev.resize(c->L);
+    c->xd2h_defer.assign(c->L, 0);
+    for (int l = 0; l < c->L; ++l) {
+      HB_CUDA(cudaEventCreateWithFlags(&c->xd2h_ready_ev[l], cudaEventDisableTiming));
+      HB_CUDA(cudaEventCreateWithFlags(&c->xd2h_done_ev[l], cudaEventDisableTiming));
+    }
     HB_CUDA(cudaEventCreateWithFlags(&c->xstart_ev, cudaEventDisableTiming));
     HB_CUDA(cudaEventCreateWithFlags(&c->xdone_ev, cudaEventDisableTiming));
     c->xsnap_ev.resize(c->L);
@@ -3884,6 +3937,19 @@ int hb_train_step_host_dense(hb_ctx* c, const float* x, int64_t ld, const int64_
   const int d0 = c->d[0];
   const long long n = static_cast<long long>(rows) * d0;
   const int blocks = static_cast<int>(std::min<long long>(cdiv(n, 256), 148 * 16));
+  // small batches in registered (mapped) host memory: read by the SMs directly
+  static const long long zc_max = env_long("HB_ZC_BATCH_MAX", 4 << 20);
+  const float* zx = n * 4 <= zc_max ? static_cast<const float*>(mapped_alias(x, ((rows - 1) * ld + d0) * sizeof(float)))
+                                    : nullptr;
+  const int64_t* zl = zx ? static_cast<const int64_t*>(mapped_alias(labels, rows * sizeof(int64_t))) : nullptr;
+  if (zx && zl) {
+    zc_batch_kernel<<<static_cast<int>(std::min<long long>(cdiv(n, 256), 148 * 8)), 256, 0, c->stream>>>(
+        zx, ld, zl, c->bx, c->bx_lo, c->ld[0], c->blabels, rows, d0);
+    HB_CUDA(cudaGetLastError());
+    c->pre_launches++;
+    t_h2d_bytes += n * static_cast<long long>(sizeof(float)) + rows * static_cast<long long>(sizeof(int64_t));
+    return do_step(c, c->batch, 0, rows, eta, flags, out_loss);
+  }
   if (ld == d0 && c->ld[0] == d0) {
     // contiguous on both sides: one linear DMA (a pitched 2D copy of
     // thousands of short rows runs far below link speed)

@@ -1125,6 +1125,26 @@ __global__ void split_lo_kernel(const float* x, float* lo, long long ld, long lo
   }
 }
 
+// Zero-copy batch load: the SMs read a page-locked host batch through its
+// mapped device alias (x rows of ldx floats, labels) and write the padded
+// device rows, their lo twin and the labels.  Small batches take this path
+// instead of a copy-engine DMA, which would queue behind the previous call's
+// deferred float64 write-backs.
+__global__ void zc_batch_kernel(const float* __restrict__ x, long long ldx, const int64_t* __restrict__ labels,
+                                float* dst, float* dst_lo, long long ld, int64_t* dst_labels, long long rows,
+                                int cols) {
+  const long long total = rows * cols;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total; i += stride) {
+    const long long r = i / cols, c = i % cols;
+    const float v = x[r * ldx + c];
+    dst[r * ld + c] = v;
+    if (dst_lo != nullptr) dst_lo[r * ld + c] = tf32_lo(v);
+  }
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < rows; i += stride)
+    dst_labels[i] = labels[i];
+}
+
 // dst (rows, cols, ldd) = scale * src (rows, cols, dense): unpack of the
 // allreduced flat model (replica averaging).
 __global__ void unpack_scale_kernel(float* dst, long long ldd, const float* src, int rows, int cols, float scale,

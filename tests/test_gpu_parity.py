@@ -1001,3 +1001,38 @@ def test_forward_bias_epilogue(hb, kind, b):
         assert np.abs(ctx.activation(1, b) - ref_nn.forward(w, x)[1]).max() <= 1e-5
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("padded", [False, True], ids=["contiguous", "strided_rows"])
+def test_registered_batch_zero_copy_equals_dma(hb, padded):
+    """A host batch in registered memory is read by one kernel through its
+    mapped alias (HB_ZC_BATCH_MAX, default 4 MiB) instead of a copy-engine DMA:
+    the step is bit-identical to the DMA path (an unregistered copy), also for
+    rows with a stride (a column slice of a wider array), and its PCIe bytes are
+    still counted."""
+    sizes, b = (54, 256, 256, 2), 300
+    w, x, y = oracle_case(sizes, b, seed=31)
+    wide = np.zeros((b, sizes[0] + 10), dtype=np.float32)
+    wide[:, :sizes[0]] = x
+    xz = wide[:, :sizes[0]] if padded else np.ascontiguousarray(x, dtype=np.float32)
+    yz = np.ascontiguousarray(y, dtype=np.int64)
+    out = {}
+    for mode in ("dma", "zero_copy"):
+        ctx = hb.GpuReplica(sizes, b)
+        try:
+            ctx.set_weights(w)
+            if mode == "zero_copy":
+                ctx.pin_host([wide if padded else xz, yz])
+                xb, yb = xz, yz
+            else:
+                xb, yb = np.array(xz), np.array(yz)  # fresh, unregistered copies
+            loss = ctx.step_host(xb, yb, 0.4, emit_grad=True)
+            out[mode] = (loss, ctx.get_weights(), ctx.grads(), ctx.last_step_launches)
+        finally:
+            ctx.close()
+    assert out["zero_copy"][3] == out["dma"][3] + 1  # the batch-load kernel ran (the DMA path launches none it counts)
+    assert out["dma"][0] == out["zero_copy"][0]
+    for p, q in zip(out["dma"][1] + out["dma"][2], out["zero_copy"][1] + out["zero_copy"][2]):
+        assert np.array_equal(p, q)
+    g = ref_nn.backward(w, ref_nn.forward(w, x), y)
+    assert max_relative_error(out["zero_copy"][2], g) <= STEP_TOL
